@@ -1,0 +1,335 @@
+"""TEST INFRASTRUCTURE ONLY: ctypes handle on the UNMODIFIED reference library.
+
+oracle/_ref/libhybridref.so is compiled by oracle/Makefile from the reference
+sources where they lie (/root/reference/proj/src) plus oracle/ref_shim.cpp.
+Only tests/, __graft_entry__.smoke() and bench.py's CPU baseline use this.
+"""
+import ctypes as C
+import os
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "_ref", "libhybridref.so")
+_L = None
+
+TOK_MINIMAL, TOK_STOPWORD, TOK_FULL, TOK_PORTER = 0, 1, 2, 3
+
+
+def available():
+    return os.path.exists(LIB_PATH)
+
+
+def lib():
+    global _L
+    if _L is not None:
+        return _L
+    if not available():
+        raise ImportError(f"{LIB_PATH} missing: run `make -C oracle` where /root/reference exists")
+    L = C.CDLL(LIB_PATH)
+    vp, u64, u32, i64, dbl = C.c_void_p, C.c_uint64, C.c_uint32, C.c_int64, C.c_double
+    P = C.POINTER
+    L.ref_last_error.restype = C.c_char_p
+    L.ref_gen_corpus.argtypes = [u64, u64, u32, dbl, u32, u32, i64, P(vp)]
+    L.ref_corpus_size.argtypes = [vp]
+    L.ref_corpus_size.restype = u64
+    L.ref_corpus_text_bytes.argtypes = [vp]
+    L.ref_corpus_text_bytes.restype = u64
+    L.ref_corpus_export.argtypes = [vp, P(u64), P(i64), C.c_char_p]
+    L.ref_corpus_free.argtypes = [vp]
+    L.ref_gen_queries.argtypes = [vp, u64, u32, u32, u64, P(vp)]
+    L.ref_queries_size.argtypes = [vp]
+    L.ref_queries_size.restype = u64
+    L.ref_queries_text_bytes.argtypes = [vp]
+    L.ref_queries_text_bytes.restype = u64
+    L.ref_queries_export.argtypes = [vp, P(u32), P(u64), P(i64), C.c_char_p]
+    L.ref_queries_free.argtypes = [vp]
+    L.ref_build_index_texts.argtypes = [u64, P(u64), P(C.c_char_p), C.c_int, dbl, dbl, P(vp)]
+    L.ref_build_index_corpus.argtypes = [vp, C.c_int, dbl, dbl, P(vp)]
+    L.ref_index_from_arrays.argtypes = [u32, P(C.c_char_p), P(u64), P(u32), P(dbl), P(dbl),
+                                        P(dbl), P(dbl), u32, P(u32), P(u64), dbl, dbl, dbl, P(vp)]
+    L.ref_index_free.argtypes = [vp]
+    L.ref_index_sizes.argtypes = [vp, P(u64)]
+    L.ref_index_export.argtypes = [vp, C.c_char_p, P(u64), P(u32), P(dbl), P(dbl), P(dbl),
+                                   P(dbl), P(u32), P(u64), P(dbl)]
+    L.ref_search.argtypes = [vp, P(C.c_char_p), u32, u64, dbl, dbl, C.c_int, P(u64), P(dbl),
+                             P(u32), P(u64)]
+    L.ref_search_batch.argtypes = [vp, u32, P(u32), P(C.c_char_p), u64, dbl, dbl, C.c_int,
+                                   C.c_uint, C.c_uint, P(u64), P(dbl), P(u32), P(u64), P(dbl),
+                                   P(dbl)]
+    L.ref_build_temporal.argtypes = [u64, P(u64), P(i64), P(C.c_char_p), i64, dbl, dbl, u32,
+                                     C.c_int, dbl, dbl, P(vp)]
+    L.ref_build_temporal_corpus.argtypes = [vp, i64, dbl, dbl, u32, C.c_int, dbl, dbl, P(vp)]
+    L.ref_temporal_free.argtypes = [vp]
+    L.ref_temporal_num_partitions.argtypes = [vp]
+    L.ref_temporal_num_partitions.restype = u32
+    L.ref_temporal_partitions.argtypes = [vp, P(i64), P(i64), P(u32)]
+    L.ref_temporal_topk.argtypes = [vp, P(C.c_char_p), u32, u64, dbl, dbl, C.c_int, P(u64),
+                                    P(dbl), P(u32), P(u32), P(u64)]
+    L.ref_temporal_batch.argtypes = [vp, u32, P(u32), P(C.c_char_p), u64, dbl, dbl, C.c_uint,
+                                     P(u64), P(dbl), P(u32), P(dbl)]
+    L.ref_bm25_score.argtypes = [dbl] * 6
+    L.ref_bm25_score.restype = dbl
+    L.ref_confidence.argtypes = [P(dbl), u32, C.c_int, dbl, P(dbl)]
+    L.ref_k_star.argtypes = [dbl, dbl, P(u32)]
+    L.ref_ndcg.argtypes = [P(u64), P(dbl), u32, P(u64), P(u32), u32, u64, C.c_int, P(dbl)]
+    L.ref_twophase_batch.argtypes = [u64, C.c_int, u32, u32, P(dbl), u64, P(u64), P(dbl), P(u32)]
+    _L = L
+    return L
+
+
+def _chk(rc):
+    if rc != 0:
+        raise RuntimeError(lib().ref_last_error().decode())
+
+
+def _p(a, ct):
+    return a.ctypes.data_as(C.POINTER(ct))
+
+
+def _cstrs(strs):
+    arr = (C.c_char_p * max(1, len(strs)))()
+    arr[:len(strs)] = [s.encode() for s in strs]
+    return arr
+
+
+def _split(buf, n):
+    parts = bytes(buf).split(b"\0")
+    return [p.decode() for p in parts[:n]]
+
+
+class RefCorpus:
+    def __init__(self, n_records, seed=42, vocab_size=5000, zipf_s=1.1, min_tok=5, max_tok=30,
+                 time_span_ms=0):
+        h = C.c_void_p()
+        _chk(lib().ref_gen_corpus(n_records, seed, vocab_size, zipf_s, min_tok, max_tok,
+                                  time_span_ms, C.byref(h)))
+        self.h = h
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            lib().ref_corpus_free(self.h)
+
+    def export(self):
+        L = lib()
+        n = L.ref_corpus_size(self.h)
+        ids = np.zeros(n, np.uint64)
+        ts = np.zeros(n, np.int64)
+        buf = C.create_string_buffer(int(L.ref_corpus_text_bytes(self.h)))
+        L.ref_corpus_export(self.h, _p(ids, C.c_uint64), _p(ts, C.c_int64), buf)
+        return ids, ts, _split(buf.raw, n)
+
+
+class RefQueries:
+    def __init__(self, corpus, n_queries=1000, min_terms=3, max_terms=6, seed=42):
+        h = C.c_void_p()
+        _chk(lib().ref_gen_queries(corpus.h, n_queries, min_terms, max_terms, seed, C.byref(h)))
+        L = lib()
+        n = L.ref_queries_size(h)
+        nt = np.zeros(n, np.uint32)
+        gold = np.zeros(n, np.uint64)
+        ts = np.zeros(n, np.int64)
+        buf = C.create_string_buffer(int(L.ref_queries_text_bytes(h)) + 1)
+        L.ref_queries_export(h, _p(nt, C.c_uint32), _p(gold, C.c_uint64), _p(ts, C.c_int64), buf)
+        flat = _split(buf.raw, int(nt.sum()))
+        off = np.concatenate([[0], np.cumsum(nt)]).astype(np.int64)
+        self.terms = [flat[off[i]:off[i + 1]] for i in range(n)]
+        self.gold, self.ts = gold, ts
+        L.ref_queries_free(h)
+
+
+class RefIndex:
+    """A reference hybrid::CsrIndex (built by the reference or adopted from arrays)."""
+
+    def __init__(self, h):
+        self.h = h
+
+    @classmethod
+    def from_texts(cls, docs, tok_mode=TOK_MINIMAL, k1=1.2, b=0.75):
+        ids = np.array([d for d, _ in docs], dtype=np.uint64)
+        texts = _cstrs([t for _, t in docs])
+        h = C.c_void_p()
+        _chk(lib().ref_build_index_texts(len(docs), _p(ids, C.c_uint64), texts, tok_mode, k1, b,
+                                         C.byref(h)))
+        return cls(h)
+
+    @classmethod
+    def from_corpus(cls, corpus, tok_mode=TOK_STOPWORD, k1=1.2, b=0.75):
+        h = C.c_void_p()
+        _chk(lib().ref_build_index_corpus(corpus.h, tok_mode, k1, b, C.byref(h)))
+        return cls(h)
+
+    @classmethod
+    def from_arrays(cls, terms, term_offsets, posting_rows, posting_weights, idf, maxscore,
+                    order_key, doc_lens, doc_ids, avgdl, k1=1.2, b=0.75):
+        keep = [np.ascontiguousarray(term_offsets, np.uint64),
+                np.ascontiguousarray(posting_rows, np.uint32),
+                np.ascontiguousarray(posting_weights, np.float64),
+                np.ascontiguousarray(idf, np.float64), np.ascontiguousarray(maxscore, np.float64),
+                np.ascontiguousarray(order_key, np.float64),
+                np.ascontiguousarray(doc_lens, np.uint32), np.ascontiguousarray(doc_ids, np.uint64)]
+        h = C.c_void_p()
+        _chk(lib().ref_index_from_arrays(
+            len(terms), _cstrs(terms), _p(keep[0], C.c_uint64), _p(keep[1], C.c_uint32),
+            _p(keep[2], C.c_double), _p(keep[3], C.c_double), _p(keep[4], C.c_double),
+            _p(keep[5], C.c_double), len(doc_ids), _p(keep[6], C.c_uint32),
+            _p(keep[7], C.c_uint64), avgdl, k1, b, C.byref(h)))
+        return cls(h)
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            lib().ref_index_free(self.h)
+
+    def export(self):
+        L = lib()
+        s = np.zeros(4, np.uint64)
+        L.ref_index_sizes(self.h, _p(s, C.c_uint64))
+        nt, npst, nd, tb = (int(x) for x in s)
+        out = dict(term_offsets=np.zeros(nt + 1, np.uint64), posting_rows=np.zeros(npst, np.uint32),
+                   posting_weights=np.zeros(npst, np.float64), idf=np.zeros(nt, np.float64),
+                   maxscore=np.zeros(nt, np.float64), order_key=np.zeros(nt, np.float64),
+                   doc_lens=np.zeros(nd, np.uint32), doc_ids=np.zeros(nd, np.uint64))
+        buf = C.create_string_buffer(tb + 1)
+        avg = C.c_double()
+        L.ref_index_export(self.h, buf, _p(out["term_offsets"], C.c_uint64),
+                           _p(out["posting_rows"], C.c_uint32),
+                           _p(out["posting_weights"], C.c_double), _p(out["idf"], C.c_double),
+                           _p(out["maxscore"], C.c_double), _p(out["order_key"], C.c_double),
+                           _p(out["doc_lens"], C.c_uint32), _p(out["doc_ids"], C.c_uint64),
+                           C.byref(avg))
+        out["terms"] = _split(buf.raw, nt)
+        out["avgdl"] = avg.value
+        return out
+
+    def search(self, terms, k, k1=1.2, b=0.75, maxscore=False):
+        """-> (ids, scores, postings_touched)"""
+        cap = max(int(k), 1)
+        ids = np.zeros(cap, np.uint64)
+        sc = np.zeros(cap, np.float64)
+        n = C.c_uint32()
+        post = C.c_uint64()
+        _chk(lib().ref_search(self.h, _cstrs(terms), len(terms), k, k1, b, 1 if maxscore else 0,
+                              _p(ids, C.c_uint64), _p(sc, C.c_double), C.byref(n), C.byref(post)))
+        return ids[:n.value].copy(), sc[:n.value].copy(), post.value
+
+    def search_batch(self, queries, k, k1=1.2, b=0.75, maxscore=False, workers=1, warmup=0):
+        """CLI-shaped parallel batch (hybridmem.cpp:58-71, 305-313).
+        -> dict(ids[nq,k], scores[nq,k], n[nq], postings[nq], lat_ms[nq], wall_ms)"""
+        nq = len(queries)
+        flat = [t for q in queries for t in q]
+        off = np.zeros(nq + 1, np.uint32)
+        off[1:] = np.cumsum([len(q) for q in queries])
+        ids = np.zeros((nq, k), np.uint64)
+        sc = np.zeros((nq, k), np.float64)
+        n = np.zeros(nq, np.uint32)
+        post = np.zeros(nq, np.uint64)
+        lat = np.zeros(nq, np.float64)
+        wall = C.c_double()
+        _chk(lib().ref_search_batch(self.h, nq, _p(off, C.c_uint32), _cstrs(flat), k, k1, b,
+                                    1 if maxscore else 0, workers, warmup, _p(ids, C.c_uint64),
+                                    _p(sc, C.c_double), _p(n, C.c_uint32), _p(post, C.c_uint64),
+                                    _p(lat, C.c_double), C.byref(wall)))
+        return dict(ids=ids, scores=sc, n=n, postings=post, lat_ms=lat, wall_ms=wall.value)
+
+
+class RefTemporal:
+    def __init__(self, h):
+        self.h = h
+
+    @classmethod
+    def from_records(cls, ids, ts, texts, window_ms=7 * 24 * 3600 * 1000, epsilon=0.05,
+                     lambda_hat=1.4, k_max=4, tok_mode=TOK_MINIMAL, k1=1.2, b=0.75):
+        ids = np.ascontiguousarray(ids, np.uint64)
+        ts = np.ascontiguousarray(ts, np.int64)
+        h = C.c_void_p()
+        _chk(lib().ref_build_temporal(len(ids), _p(ids, C.c_uint64), _p(ts, C.c_int64),
+                                      _cstrs(texts), window_ms, epsilon, lambda_hat, k_max,
+                                      tok_mode, k1, b, C.byref(h)))
+        return cls(h)
+
+    @classmethod
+    def from_corpus(cls, corpus, window_ms=7 * 24 * 3600 * 1000, epsilon=0.05, lambda_hat=1.4,
+                    k_max=4, tok_mode=TOK_STOPWORD, k1=1.2, b=0.75):
+        h = C.c_void_p()
+        _chk(lib().ref_build_temporal_corpus(corpus.h, window_ms, epsilon, lambda_hat, k_max,
+                                             tok_mode, k1, b, C.byref(h)))
+        return cls(h)
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            lib().ref_temporal_free(self.h)
+
+    def partitions(self):
+        K = lib().ref_temporal_num_partitions(self.h)
+        ws = np.zeros(K, np.int64)
+        we = np.zeros(K, np.int64)
+        nd = np.zeros(K, np.uint32)
+        lib().ref_temporal_partitions(self.h, _p(ws, C.c_int64), _p(we, C.c_int64),
+                                      _p(nd, C.c_uint32))
+        return ws, we, nd
+
+    def topk(self, terms, k, k1=1.2, b=0.75, use_ub_stop=True):
+        cap = max(int(k), 1)
+        ids = np.zeros(cap, np.uint64)
+        sc = np.zeros(cap, np.float64)
+        n = C.c_uint32()
+        srch = C.c_uint32()
+        post = C.c_uint64()
+        _chk(lib().ref_temporal_topk(self.h, _cstrs(terms), len(terms), k, k1, b,
+                                     1 if use_ub_stop else 0, _p(ids, C.c_uint64),
+                                     _p(sc, C.c_double), C.byref(n), C.byref(srch), C.byref(post)))
+        return ids[:n.value].copy(), sc[:n.value].copy(), srch.value, post.value
+
+    def topk_batch(self, queries, k, k1=1.2, b=0.75, workers=1):
+        nq = len(queries)
+        flat = [t for q in queries for t in q]
+        off = np.zeros(nq + 1, np.uint32)
+        off[1:] = np.cumsum([len(q) for q in queries])
+        ids = np.zeros((nq, k), np.uint64)
+        sc = np.zeros((nq, k), np.float64)
+        n = np.zeros(nq, np.uint32)
+        wall = C.c_double()
+        _chk(lib().ref_temporal_batch(self.h, nq, _p(off, C.c_uint32), _cstrs(flat), k, k1, b,
+                                      workers, _p(ids, C.c_uint64), _p(sc, C.c_double),
+                                      _p(n, C.c_uint32), C.byref(wall)))
+        return dict(ids=ids, scores=sc, n=n, wall_ms=wall.value)
+
+
+def bm25_score(tf, idf, dl, avgdl, k1=1.2, b=0.75):
+    return lib().ref_bm25_score(tf, idf, dl, avgdl, k1, b)
+
+
+def confidence(scores, proxy=0, eps=1e-9):
+    s = np.ascontiguousarray(scores, np.float64)
+    out = C.c_double()
+    _chk(lib().ref_confidence(_p(s, C.c_double), len(s), proxy, eps, C.byref(out)))
+    return out.value
+
+
+def k_star(eps, lam):
+    out = C.c_uint32()
+    _chk(lib().ref_k_star(eps, lam, C.byref(out)))
+    return out.value
+
+
+def ndcg(ids, rels, k, linear=False):
+    ids = np.ascontiguousarray(ids, np.uint64)
+    sc = np.zeros(len(ids), np.float64)
+    rd = np.array(list(rels.keys()), np.uint64)
+    rg = np.array(list(rels.values()), np.uint32)
+    out = C.c_double()
+    _chk(lib().ref_ndcg(_p(ids, C.c_uint64), _p(sc, C.c_double), len(ids), _p(rd, C.c_uint64),
+                        _p(rg, C.c_uint32), len(rd), k, 1 if linear else 0, C.byref(out)))
+    return out.value
+
+
+def twophase_batch(rows, k, capacity, reset_sentinel=True):
+    rows = np.ascontiguousarray(rows, np.float64)
+    r, n = rows.shape
+    ids = np.zeros((r, k), np.uint64)
+    sc = np.zeros((r, k), np.float64)
+    cnt = np.zeros(r, np.uint32)
+    _chk(lib().ref_twophase_batch(capacity, 1 if reset_sentinel else 0, r, n,
+                                  _p(rows, C.c_double), k, _p(ids, C.c_uint64), _p(sc, C.c_double),
+                                  _p(cnt, C.c_uint32)))
+    return ids, sc, cnt
