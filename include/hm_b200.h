@@ -1,0 +1,143 @@
+/* include/hm_b200.h -- C ABI of the B200-native BM25 search path.
+ *
+ * This is the drop-in boundary under the reference's C++ search API.  The
+ * reference has no FFI of its own: its boundary is the C++
+ * API in /root/reference/proj/include/hybrid/.  Each entry point below names
+ * the reference interface it replaces; include/hybrid/ (this repo) keeps
+ * those C++ declarations and implements them on top of this ABI, and
+ * INTEGRATION.md shows the bindings (C++, ctypes) a maintainer would add.
+ *
+ * Conventions: plain pointers and sizes only; every function returns
+ * HM_OK (0) or a nonzero hm_status, with a thread-local message in
+ * hm_last_error().  Host buffers are borrowed for the duration of the call.
+ * An index is immutable after creation and hm_search_batch is re-entrant:
+ * concurrent calls from many threads on one index are allowed (the
+ * reference's concurrent const readers, tools/hybridmem.cpp:309)
+ * and results do not depend on concurrency or batch composition.
+ */
+#ifndef HM_B200_H
+#define HM_B200_H
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    HM_OK = 0,
+    HM_ERR_INVALID = 1,    /* std::invalid_argument in the reference */
+    HM_ERR_RUNTIME = 2,    /* std::runtime_error (CUDA/NCCL failures map here) */
+    HM_ERR_RANGE = 3,      /* std::out_of_range */
+    HM_ERR_NO_DEVICE = 4   /* no usable sm_100 device: there is no CPU fallback */
+} hm_status;
+
+typedef struct hm_index hm_index;
+
+/* Borrowed view of a hybrid::CsrIndex (proj/include/hybrid/csr_index.hpp:44-60).
+ * Exactly one of posting_weights (the reference's raw-tf doubles) or
+ * posting_tf must be non-NULL.  Rows must be strictly increasing per term. */
+typedef struct {
+    uint32_t n_terms;
+    const uint64_t* term_offsets;     /* [n_terms + 1] */
+    const uint32_t* posting_rows;     /* [P] */
+    const double* posting_weights;    /* [P] raw tf as double, or NULL */
+    const uint32_t* posting_tf;       /* [P] raw tf, or NULL */
+    const double* term_idfs;          /* [n_terms] */
+    const double* term_order_keys;    /* [n_terms] canonical accumulation order */
+    uint32_t n_docs;
+    const uint32_t* doc_lens;         /* [n_docs] */
+    const uint64_t* doc_ids;          /* [n_docs] external DocId of each row */
+    double avgdl;
+} hm_csr_view;
+
+/* Upload an index to `device` (HBM-resident until destroy).
+ * Replaces: the in-memory CsrIndex produced by hybrid::build_index /
+ * hybrid::load_index (src/csr_index.cpp:232-324, src/io.cpp:229-232). */
+int hm_index_create(const hm_csr_view* view, int device, hm_index** out);
+int hm_index_destroy(hm_index* index);
+
+/* Device bytes held by the index (postings, tf, tables, per-doc arrays). */
+uint64_t hm_index_device_bytes(const hm_index* index);
+/* Packed posting format: bits of the row field and of the impact code. */
+int hm_index_format(const hm_index* index, uint32_t* row_bits, uint32_t* code_bits,
+                    uint32_t* n_codes, uint64_t* n_escaped);
+
+/* One batch of queries.  Query i owns q_tid[q_off[i] .. q_off[i+1]):
+ * vocabulary-resolved term ids in query order, duplicates allowed (they
+ * become the plan multiplicity), 0xFFFFFFFF for an unknown term (dropped, as
+ * in make_plan, src/csr_index.cpp:31-48).  Scoring is restricted to rows in
+ * [row_lo, row_hi) (row_hi = 0 means n_docs): the temporal index's recency
+ * window and doc-range shards use this. */
+typedef struct {
+    uint32_t n_queries;
+    const uint32_t* q_off;     /* [n_queries + 1] */
+    const uint32_t* q_tid;     /* [q_off[n_queries]] */
+    uint32_t k;                /* top-k; 0 gives empty results */
+    double k1, b;              /* hybrid::Bm25Params */
+    const double* tau;         /* [n_queries] per-query skip threshold, or NULL */
+    double tau_default;        /* CascadeConfig::conf_threshold (0.10) */
+    double epsilon_guard;      /* CascadeConfig::epsilon_guard (1e-9) */
+    uint32_t row_lo, row_hi;
+    uint32_t flags;            /* HM_FLAG_* */
+} hm_query_batch;
+
+#define HM_FLAG_FORCE_EXACT 1u   /* run every query on the exact fp64 kernel */
+#define HM_FLAG_DEBUG_NO_RESET 2u /* test-only: skip the per-query sentinel reset
+                                    of the candidate state (pitfall-3 witness,
+                                    src/twophase.cpp:24-27) */
+
+/* Results, caller-allocated.  Row i of ids/scores has stride k; out_n[i] <= k
+ * entries ranked by (score desc, DocId asc), zero scores never emitted
+ * (RankedList::better / sort_and_truncate, include/hybrid/types.hpp:21-30;
+ * collect_topk, src/csr_index.cpp:50-59).  conf = Margin confidence
+ * (src/cascade.cpp:15-21); skip = conf >= tau (src/cascade.cpp:79-84);
+ * postings = SearchStats::postings_touched of the exhaustive path
+ * (src/csr_index.cpp:100-102; postings inside the row window). */
+typedef struct {
+    uint64_t* ids;       /* [n_queries * k] */
+    double* scores;      /* [n_queries * k] */
+    uint32_t* n;         /* [n_queries] */
+    double* conf;        /* [n_queries], may be NULL */
+    uint8_t* skip;       /* [n_queries], may be NULL */
+    uint64_t* postings;  /* [n_queries], may be NULL */
+} hm_results;
+
+/* Batch search with HOST buffers (synchronous).
+ * Replaces: per-query CsrIndex::bm25_topk / bm25_topk_maxscore
+ * (include/hybrid/csr_index.hpp:72-79, src/csr_index.cpp:77-207) driven by
+ * hybridmem's parallel_for batch loop (tools/hybridmem.cpp:227-313), plus
+ * cascade::confidence + the skip decision (src/cascade.cpp:10-21, 67-92). */
+int hm_search_batch(hm_index* index, const hm_query_batch* batch, hm_results* out);
+
+/* Same with DEVICE buffers (batch arrays and results on the index's device),
+ * enqueued on `stream` (a cudaStream_t, NULL = legacy default) without host
+ * synchronisation.  `n_queries` etc. are read from the host struct. */
+int hm_search_batch_device(hm_index* index, const hm_query_batch* batch_dev,
+                           hm_results* out_dev, void* stream);
+
+/* Statistics of the last batch on this thread: queries that fell back to the
+ * exact fp64 kernel (candidate overflow or non-positive impacts), kernel
+ * launches issued. */
+int hm_last_batch_stats(uint32_t* n_exact_fallback, uint32_t* n_launches);
+
+/* Doc-sharded multi-GPU merge (the step after the all-gather of k candidates
+ * per query): shard_ids/shard_scores/shard_n hold G blocks of per-shard exact
+ * top-k results ([G][n_queries][k], [G][n_queries]).  Produces the global
+ * top-k, Margin confidence and skip per query.  DEVICE pointers, on `stream`.
+ * New in this framework (the reference has no sharded path; precedent:
+ * SharedStats, csr_index.hpp:28-35). */
+int hm_merge_shards_device(uint32_t n_shards, uint32_t n_queries, uint32_t k,
+                           const uint64_t* shard_ids, const double* shard_scores,
+                           const uint32_t* shard_n, const double* tau, double tau_default,
+                           double epsilon_guard, hm_results* out_dev, void* stream);
+
+/* Margin confidence over a ranked score list (src/cascade.cpp:10-21). */
+double hm_margin(const double* scores, uint32_t n, double epsilon_guard);
+
+const char* hm_last_error(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

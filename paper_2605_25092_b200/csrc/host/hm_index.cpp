@@ -1,0 +1,680 @@
+// C-ABI implementation (include/hm_b200.h): device index build/upload, the
+// per-call workspace pool, batch orchestration and error mapping.
+//
+// Index build (once, at hm_index_create):
+//   * raw tf per posting (from the reference's posting_weights doubles or a
+//     u32 array) and doc length per row define a (tf, len) pair; the 2^cb - 1
+//     most frequent pairs get codes, the rest use the escape code;
+//   * packed posting = (row << cb) | code  (cb = min(8, 32 - row_bits));
+//   * long terms (df > 32 * n_tiles) get a tile-boundary table;
+//   * everything is uploaded once and stays resident in HBM.
+// Search (per batch): upload query tids, plan kernel, LPT sort, persistent
+// selection kernel, persistent exact kernel (takes only flagged queries),
+// download results.  No CPU scoring path exists.
+#include <algorithm>
+#include <atomic>
+#include <cmath>
+#include <cstring>
+#include <mutex>
+#include <stdexcept>
+#include <string>
+#include <thread>
+#include <unordered_map>
+#include <vector>
+
+#include <cuda_runtime.h>
+
+#include "hm_b200.h"
+#include "hm_launch.h"
+
+namespace {
+
+thread_local std::string g_err;
+thread_local uint32_t g_last_exact = 0, g_last_launches = 0;
+
+struct no_device_error : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+
+void ck(cudaError_t e, const char* what) {
+    if (e != cudaSuccess)
+        throw std::runtime_error(std::string("CUDA error in ") + what + ": " + cudaGetErrorString(e));
+}
+
+template <typename F>
+int guard(F&& f) {
+    try {
+        f();
+        return HM_OK;
+    } catch (const no_device_error& e) {
+        g_err = e.what();
+        return HM_ERR_NO_DEVICE;
+    } catch (const std::invalid_argument& e) {
+        g_err = e.what();
+        return HM_ERR_INVALID;
+    } catch (const std::out_of_range& e) {
+        g_err = e.what();
+        return HM_ERR_RANGE;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return HM_ERR_RUNTIME;
+    } catch (...) {
+        g_err = "unknown error";
+        return HM_ERR_RUNTIME;
+    }
+}
+
+int hw_threads() {
+    unsigned h = std::thread::hardware_concurrency();
+    return h ? static_cast<int>(std::min(h, 64u)) : 1;
+}
+
+template <typename F>
+void par_for(uint64_t n, F&& f) {
+    int T = static_cast<int>(std::min<uint64_t>(hw_threads(), std::max<uint64_t>(n / 65536, 1)));
+    if (T <= 1) {
+        f(0, 0, n);
+        return;
+    }
+    std::vector<std::thread> pool;
+    for (int t = 0; t < T; ++t)
+        pool.emplace_back([&, t] { f(t, n * t / T, n * (t + 1) / T); });
+    for (auto& th : pool) th.join();
+}
+
+template <typename T>
+T* dev_upload(const T* host, uint64_t n, std::vector<void*>& allocs, uint64_t& bytes) {
+    void* p = nullptr;
+    uint64_t sz = std::max<uint64_t>(n, 1) * sizeof(T);
+    ck(cudaMalloc(&p, sz), "cudaMalloc(index)");
+    allocs.push_back(p);
+    bytes += sz;
+    if (n) ck(cudaMemcpy(p, host, n * sizeof(T), cudaMemcpyHostToDevice), "cudaMemcpy(index)");
+    return static_cast<T*>(p);
+}
+
+// device scratch + stream + pinned staging for one in-flight batch
+struct Workspace {
+    cudaStream_t stream = nullptr;
+    uint32_t nq_cap = 0, tid_cap = 0, k_cap = 0;
+    size_t sort_bytes = 0;
+    // device
+    uint32_t *q_off = nullptr, *q_tid = nullptr, *plan_tid = nullptr, *plan_mult = nullptr,
+             *plan_len = nullptr, *order_in = nullptr, *order = nullptr, *counters = nullptr,
+             *exact_list = nullptr, *out_n = nullptr;
+    uint64_t *cost = nullptr, *cost_sorted = nullptr, *out_ids = nullptr, *out_post = nullptr;
+    double *tau = nullptr, *out_scores = nullptr, *out_conf = nullptr;
+    float* w32 = nullptr;
+    uint8_t* out_skip = nullptr;
+    void* sort_tmp = nullptr;
+    // pinned host staging
+    unsigned char* pin = nullptr;
+    size_t pin_bytes = 0;
+
+    void free_dev() {
+        void* ps[] = {q_off, q_tid, plan_tid, plan_mult, plan_len, order_in, order, counters,
+                      exact_list, out_n, cost, cost_sorted, out_ids, out_post, tau, out_scores,
+                      out_conf, w32, out_skip, sort_tmp};
+        for (void* p : ps)
+            if (p) cudaFree(p);
+        q_off = q_tid = plan_tid = plan_mult = plan_len = order_in = order = counters = exact_list =
+            out_n = nullptr;
+        cost = cost_sorted = out_ids = out_post = nullptr;
+        tau = out_scores = out_conf = nullptr;
+        w32 = nullptr;
+        out_skip = nullptr;
+        sort_tmp = nullptr;
+    }
+    ~Workspace() {
+        free_dev();
+        if (pin) cudaFreeHost(pin);
+        if (stream) cudaStreamDestroy(stream);
+    }
+};
+
+template <typename T>
+void dalloc(T*& p, uint64_t n) {
+    void* v = nullptr;
+    ck(cudaMalloc(&v, std::max<uint64_t>(n, 1) * sizeof(T)), "cudaMalloc(workspace)");
+    p = static_cast<T*>(v);
+}
+
+}  // namespace
+
+struct hm_index {
+    int device = 0;
+    hm::DevIndex dev{};
+    std::vector<void*> allocs;
+    uint64_t bytes = 0;
+    uint32_t row_bits = 0, code_bits = 0, n_codes = 0;
+    uint64_t n_escaped = 0;
+    std::vector<uint32_t> code_tf, code_len;
+    int grid_search = 0, grid_exact = 0;
+    std::mutex mu;
+    std::vector<Workspace*> pool;
+
+    ~hm_index() {
+        int prev = 0;
+        cudaGetDevice(&prev);
+        cudaSetDevice(device);
+        for (auto* w : pool) delete w;
+        for (void* p : allocs) cudaFree(p);
+        cudaSetDevice(prev);
+    }
+};
+
+namespace {
+
+void use_device(int device) {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0)
+        throw no_device_error("no CUDA device available (the B200 path has no CPU fallback)");
+    if (device < 0 || device >= n) throw std::invalid_argument("device ordinal out of range");
+    ck(cudaSetDevice(device), "cudaSetDevice");
+}
+
+void build_index(const hm_csr_view* v, hm_index* X) {
+    const uint32_t V = v->n_terms, N = v->n_docs;
+    if (!v->term_offsets) throw std::invalid_argument("term_offsets is required");
+    const uint64_t P = v->term_offsets[V];
+    if ((P && !v->posting_rows) || (N && (!v->doc_lens || !v->doc_ids)) ||
+        (V && (!v->term_idfs || !v->term_order_keys)))
+        throw std::invalid_argument("hm_csr_view: missing array");
+    if (P && !v->posting_weights == !v->posting_tf)
+        throw std::invalid_argument("exactly one of posting_weights / posting_tf must be set");
+    // packed row width
+    uint32_t row_bits = N <= 1 ? 1 : 32 - __builtin_clz(N - 1);
+    if (row_bits > 28)
+        throw std::invalid_argument("more than 2^28 rows per index: shard the corpus across devices");
+    uint32_t cb = std::min<uint32_t>(8, 32 - row_bits);
+    uint32_t esc = (1u << cb) - 1;
+    X->row_bits = row_bits;
+    X->code_bits = cb;
+    // raw tf per posting (BM25 mode: integral, >= 1)
+    std::vector<uint32_t> tf(P);
+    std::atomic<int> bad{0};
+    par_for(P, [&](int, uint64_t a, uint64_t b) {
+        for (uint64_t i = a; i < b; ++i) {
+            uint32_t t;
+            if (v->posting_tf) {
+                t = v->posting_tf[i];
+            } else {
+                double w = v->posting_weights[i];
+                if (!(w >= 1.0 && w < 4294967296.0) || w != std::floor(w)) {
+                    bad = 1;
+                    t = 1;
+                } else {
+                    t = static_cast<uint32_t>(w);
+                }
+            }
+            if (t == 0) bad = 1;
+            if (v->posting_rows[i] >= N) bad = 2;
+            tf[i] = t;
+        }
+    });
+    if (bad == 1)
+        throw std::runtime_error("BM25 scoring requires a BM25-mode index (raw integral tf weights)");
+    if (bad == 2) throw std::out_of_range("posting row out of range");
+    // rows strictly increasing per term
+    par_for(V, [&](int, uint64_t a, uint64_t b) {
+        for (uint64_t t = a; t < b; ++t) {
+            uint64_t lo = v->term_offsets[t], hi = v->term_offsets[t + 1];
+            if (hi < lo || hi > P) {
+                bad = 3;
+                return;
+            }
+            for (uint64_t i = lo + 1; i < hi; ++i)
+                if (v->posting_rows[i] <= v->posting_rows[i - 1]) bad = 4;
+        }
+    });
+    if (bad == 3) throw std::invalid_argument("term_offsets not monotone");
+    if (bad == 4) throw std::invalid_argument("posting rows must be strictly increasing per term");
+    // (tf, len) pair histogram: dense for small pairs, hashed otherwise
+    constexpr uint32_t kTfD = 64, kLenD = 4096;
+    const int T = hw_threads();
+    std::vector<std::vector<uint64_t>> dense(T);
+    std::vector<std::unordered_map<uint64_t, uint64_t>> sparse(T);
+    auto key = [](uint64_t t, uint64_t l) { return (t << 32) | l; };
+    {
+        std::vector<std::thread> pool;
+        for (int t = 0; t < T; ++t)
+            pool.emplace_back([&, t] {
+                dense[t].assign(static_cast<size_t>(kTfD) * kLenD, 0);
+                uint64_t a = P * t / T, b = P * (t + 1) / T;
+                for (uint64_t i = a; i < b; ++i) {
+                    uint32_t f = tf[i], l = v->doc_lens[v->posting_rows[i]];
+                    if (f < kTfD && l < kLenD) ++dense[t][static_cast<size_t>(f) * kLenD + l];
+                    else ++sparse[t][key(f, l)];
+                }
+            });
+        for (auto& th : pool) th.join();
+    }
+    std::vector<std::pair<uint64_t, uint64_t>> pairs;  // (count, key)
+    {
+        std::vector<uint64_t> dsum(static_cast<size_t>(kTfD) * kLenD, 0);
+        std::unordered_map<uint64_t, uint64_t> ssum;
+        for (int t = 0; t < T; ++t) {
+            for (size_t i = 0; i < dsum.size(); ++i) dsum[i] += dense[t][i];
+            for (auto& kv : sparse[t]) ssum[kv.first] += kv.second;
+            std::vector<uint64_t>().swap(dense[t]);
+        }
+        for (size_t i = 0; i < dsum.size(); ++i)
+            if (dsum[i]) pairs.emplace_back(dsum[i], key(i / kLenD, i % kLenD));
+        for (auto& kv : ssum) pairs.emplace_back(kv.second, kv.first);
+    }
+    std::sort(pairs.begin(), pairs.end(), [](const auto& x, const auto& y) {
+        if (x.first != y.first) return x.first > y.first;
+        return x.second < y.second;
+    });
+    const uint32_t n_codes = static_cast<uint32_t>(std::min<size_t>(pairs.size(), esc));
+    X->n_codes = n_codes;
+    X->code_tf.assign(hm::kMaxCodes, 0);
+    X->code_len.assign(hm::kMaxCodes, 0);
+    std::vector<uint16_t> dense_code(static_cast<size_t>(kTfD) * kLenD, static_cast<uint16_t>(esc));
+    std::unordered_map<uint64_t, uint32_t> sparse_code;
+    uint64_t escaped = 0;
+    for (uint32_t c = 0; c < n_codes; ++c) {
+        uint64_t kk = pairs[c].second;
+        uint32_t f = static_cast<uint32_t>(kk >> 32), l = static_cast<uint32_t>(kk);
+        X->code_tf[c] = f;
+        X->code_len[c] = l;
+        if (f < kTfD && l < kLenD) dense_code[static_cast<size_t>(f) * kLenD + l] = static_cast<uint16_t>(c);
+        else sparse_code[kk] = c;
+    }
+    for (size_t c = n_codes; c < pairs.size(); ++c) escaped += pairs[c].first;
+    X->n_escaped = escaped;
+    // packed postings
+    std::vector<uint32_t> packed(P);
+    par_for(P, [&](int, uint64_t a, uint64_t b) {
+        for (uint64_t i = a; i < b; ++i) {
+            uint32_t r = v->posting_rows[i], f = tf[i], l = v->doc_lens[r];
+            uint32_t code = esc;
+            if (f < kTfD && l < kLenD) {
+                code = dense_code[static_cast<size_t>(f) * kLenD + l];
+            } else {
+                auto it = sparse_code.find(key(f, l));
+                if (it != sparse_code.end()) code = it->second;
+            }
+            packed[i] = (r << cb) | code;
+        }
+    });
+    // long-term tile tables
+    const uint32_t n_tiles = std::max<uint32_t>(1, (N + hm::kTile - 1) / hm::kTile);
+    std::vector<int32_t> slot(V, -1);
+    std::vector<uint32_t> long_terms;
+    for (uint32_t t = 0; t < V; ++t) {
+        uint64_t df = v->term_offsets[t + 1] - v->term_offsets[t];
+        if (df > static_cast<uint64_t>(hm::kLongFactor) * n_tiles) {
+            slot[t] = static_cast<int32_t>(long_terms.size());
+            long_terms.push_back(t);
+        }
+    }
+    std::vector<uint32_t> tab(long_terms.size() * (static_cast<uint64_t>(n_tiles) + 1));
+    par_for(long_terms.size(), [&](int, uint64_t a, uint64_t b) {
+        for (uint64_t s = a; s < b; ++s) {
+            uint32_t t = long_terms[s];
+            uint64_t lo = v->term_offsets[t], hi = v->term_offsets[t + 1];
+            uint32_t* row = tab.data() + s * (n_tiles + 1);
+            uint64_t i = lo;
+            for (uint32_t j = 0; j <= n_tiles; ++j) {
+                uint64_t lim = static_cast<uint64_t>(j) * hm::kTile;
+                while (i < hi && v->posting_rows[i] < lim) ++i;
+                row[j] = static_cast<uint32_t>(i - lo);
+            }
+            row[n_tiles] = static_cast<uint32_t>(hi - lo);
+        }
+    });
+    std::vector<float> idf32(V);
+    for (uint32_t t = 0; t < V; ++t) idf32[t] = static_cast<float>(v->term_idfs[t]);
+    // upload
+    auto& A = X->allocs;
+    auto& B = X->bytes;
+    hm::DevIndex& d = X->dev;
+    d.post = dev_upload(packed.data(), P, A, B);
+    std::vector<uint32_t>().swap(packed);
+    d.tf = dev_upload(tf.data(), P, A, B);
+    std::vector<uint32_t>().swap(tf);
+    d.term_off = dev_upload(v->term_offsets, static_cast<uint64_t>(V) + 1, A, B);
+    d.idf = dev_upload(v->term_idfs, V, A, B);
+    d.idf32 = dev_upload(idf32.data(), V, A, B);
+    d.order_key = dev_upload(v->term_order_keys, V, A, B);
+    d.long_slot = dev_upload(slot.data(), V, A, B);
+    d.tile_tab = dev_upload(tab.data(), tab.size(), A, B);
+    d.doc_lens = dev_upload(v->doc_lens, N, A, B);
+    d.doc_ids = dev_upload(v->doc_ids, N, A, B);
+    d.code_tf = dev_upload(X->code_tf.data(), hm::kMaxCodes, A, B);
+    d.code_len = dev_upload(X->code_len.data(), hm::kMaxCodes, A, B);
+    d.n_terms = V;
+    d.n_docs = N;
+    d.n_tiles = n_tiles;
+    d.code_bits = cb;
+    d.n_codes = n_codes;
+    d.esc = esc;
+    d.avgdl = v->avgdl;
+    int sb = 0, eb = 0, sms = 0;
+    ck(hm::search_occupancy(&sb, &eb), "occupancy");
+    ck(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, X->device), "SM count");
+    if (sb < 1 || eb < 1) throw std::runtime_error("search kernels do not fit on this device");
+    X->grid_search = sb * sms;
+    X->grid_exact = eb * sms;
+}
+
+Workspace* acquire(hm_index* X) {
+    {
+        std::lock_guard<std::mutex> lk(X->mu);
+        if (!X->pool.empty()) {
+            Workspace* w = X->pool.back();
+            X->pool.pop_back();
+            return w;
+        }
+    }
+    auto* w = new Workspace();
+    ck(cudaStreamCreateWithFlags(&w->stream, cudaStreamNonBlocking), "cudaStreamCreate");
+    return w;
+}
+
+void release(hm_index* X, Workspace* w) {
+    std::lock_guard<std::mutex> lk(X->mu);
+    X->pool.push_back(w);
+}
+
+void ensure(Workspace* w, uint32_t nq, uint32_t ntid, uint32_t k, bool need_io) {
+    if (nq > w->nq_cap || ntid > w->tid_cap || k > w->k_cap || !w->counters) {
+        cudaStreamSynchronize(w->stream);
+        w->free_dev();
+        uint32_t NQ = std::max(nq, std::max(w->nq_cap, 1u));
+        uint32_t NT = std::max(ntid, std::max(w->tid_cap, 1u));
+        uint32_t K = std::max(k, std::max(w->k_cap, 1u));
+        dalloc(w->q_off, NQ + 1ull);
+        dalloc(w->q_tid, NT);
+        dalloc(w->plan_tid, NT);
+        dalloc(w->plan_mult, NT);
+        dalloc(w->plan_len, NQ);
+        dalloc(w->order_in, NQ);
+        dalloc(w->order, NQ);
+        dalloc(w->counters, 4);
+        dalloc(w->exact_list, NQ);
+        dalloc(w->cost, NQ);
+        dalloc(w->cost_sorted, NQ);
+        dalloc(w->tau, NQ);
+        dalloc(w->w32, hm::kMaxCodes);
+        dalloc(w->out_ids, static_cast<uint64_t>(NQ) * K);
+        dalloc(w->out_scores, static_cast<uint64_t>(NQ) * K);
+        dalloc(w->out_n, NQ);
+        dalloc(w->out_conf, NQ);
+        dalloc(w->out_skip, NQ);
+        dalloc(w->out_post, NQ);
+        ck(hm::lpt_sort_bytes(NQ, &w->sort_bytes), "cub sort sizing");
+        void* t = nullptr;
+        ck(cudaMalloc(&t, std::max<size_t>(w->sort_bytes, 16)), "cudaMalloc(sort)");
+        w->sort_tmp = t;
+        w->nq_cap = NQ;
+        w->tid_cap = NT;
+        w->k_cap = K;
+    }
+    // pinned staging: inputs (q_off, q_tid, tau, w32) + outputs
+    size_t need = 1024 + hm::kMaxCodes * 4;
+    if (need_io)
+        need += (nq + 1ull) * 4 + ntid * 4ull + nq * 8ull +
+                static_cast<size_t>(nq) * k * 16 + nq * (4ull + 8 + 1 + 8) + 64;
+    if (need > w->pin_bytes) {
+        cudaStreamSynchronize(w->stream);
+        if (w->pin) cudaFreeHost(w->pin);
+        w->pin = nullptr;
+        ck(cudaMallocHost(&w->pin, need * 2), "cudaMallocHost");
+        w->pin_bytes = need * 2;
+    }
+}
+
+bool needs_exact(double k1, double b) { return !(k1 >= 0.0 && b >= 0.0 && b <= 1.0); }
+
+// impact table of the codes for (k1, b): tf*(k1+1)/(tf + k1*(1-b+b*len/avgdl))
+void fill_w32(const hm_index* X, double k1, double b, float* w) {
+    const double avgdl = X->dev.avgdl;
+    for (uint32_t c = 0; c < hm::kMaxCodes; ++c) {
+        if (c >= X->n_codes) {
+            w[c] = 0.f;
+            continue;
+        }
+        double tf = X->code_tf[c], dl = X->code_len[c];
+        double norm = avgdl > 0.0 ? dl / avgdl : 1.0;
+        double denom = tf + k1 * (1.0 - b + b * norm);
+        w[c] = static_cast<float>(tf * (k1 + 1.0) / denom);
+    }
+}
+
+// enqueue the whole batch on w->stream; batch arrays already on the device
+void run_batch(hm_index* X, Workspace* w, const hm_query_batch& hb, const uint32_t* d_off,
+               const uint32_t* d_tid, const double* d_tau, const hm_results& out, float* pin_w32) {
+    const uint32_t nq = hb.n_queries;
+    hm::BatchArgs a{};
+    a.nq = nq;
+    a.k = hb.k;
+    a.q_off = d_off;
+    a.q_tid = d_tid;
+    a.k1 = hb.k1;
+    a.b = hb.b;
+    a.tau = d_tau;
+    a.tau_default = hb.tau_default;
+    a.eps = hb.epsilon_guard;
+    a.row_lo = hb.row_lo;
+    a.row_hi = hb.row_hi == 0 ? X->dev.n_docs : std::min(hb.row_hi, X->dev.n_docs);
+    a.flags = hb.flags | (needs_exact(hb.k1, hb.b) ? HM_FLAG_FORCE_EXACT : 0u);
+    a.w32 = w->w32;
+    a.plan_tid = w->plan_tid;
+    a.plan_mult = w->plan_mult;
+    a.plan_len = w->plan_len;
+    a.cost = w->cost;
+    a.order = w->order;
+    a.counters = w->counters;
+    a.exact_list = w->exact_list;
+    a.out_ids = out.ids;
+    a.out_scores = out.scores;
+    a.out_n = out.n;
+    a.out_conf = out.conf;
+    a.out_skip = out.skip;
+    a.out_post = out.postings;
+    fill_w32(X, hb.k1, hb.b, pin_w32);
+    cudaStream_t st = w->stream;
+    ck(cudaMemcpyAsync(w->w32, pin_w32, hm::kMaxCodes * sizeof(float), cudaMemcpyHostToDevice, st),
+       "upload w32");
+    ck(cudaMemsetAsync(w->counters, 0, 4 * sizeof(uint32_t), st), "memset counters");
+    ck(hm::launch_plan(X->dev, a, w->order_in, st), "plan kernel");
+    ck(hm::launch_lpt_sort(w->sort_tmp, w->sort_bytes, a, w->cost_sorted, w->order_in, st),
+       "lpt sort");
+    ck(hm::launch_search(X->dev, a, X->grid_search, st), "search kernel");
+    ck(hm::launch_exact(X->dev, a, X->grid_exact, st), "exact kernel");
+    g_last_launches = 5;  // plan, cub sort (upsweep/scan/downsweep passes count as 1), search, exact, memset
+}
+
+void validate(const hm_index* X, const hm_query_batch* b) {
+    if (!b) throw std::invalid_argument("null batch");
+    if (b->k > static_cast<uint32_t>(hm::kMaxK))
+        throw std::invalid_argument("k exceeds the supported maximum of 256");
+    if (b->n_queries && (!b->q_off)) throw std::invalid_argument("q_off is required");
+    (void)X;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* hm_last_error(void) { return g_err.c_str(); }
+
+int hm_index_create(const hm_csr_view* view, int device, hm_index** out) {
+    return guard([&] {
+        if (!view || !out) throw std::invalid_argument("null argument");
+        use_device(device);
+        auto* X = new hm_index();
+        X->device = device;
+        try {
+            build_index(view, X);
+        } catch (...) {
+            delete X;
+            throw;
+        }
+        *out = X;
+    });
+}
+
+int hm_index_destroy(hm_index* index) {
+    return guard([&] { delete index; });
+}
+
+uint64_t hm_index_device_bytes(const hm_index* index) { return index ? index->bytes : 0; }
+
+int hm_index_format(const hm_index* X, uint32_t* row_bits, uint32_t* code_bits, uint32_t* n_codes,
+                    uint64_t* n_escaped) {
+    return guard([&] {
+        if (!X) throw std::invalid_argument("null index");
+        if (row_bits) *row_bits = X->row_bits;
+        if (code_bits) *code_bits = X->code_bits;
+        if (n_codes) *n_codes = X->n_codes;
+        if (n_escaped) *n_escaped = X->n_escaped;
+    });
+}
+
+int hm_search_batch(hm_index* X, const hm_query_batch* b, hm_results* out) {
+    return guard([&] {
+        if (!X || !out) throw std::invalid_argument("null argument");
+        validate(X, b);
+        const uint32_t nq = b->n_queries;
+        if (nq == 0) return;
+        if (!out->ids || !out->scores || !out->n) throw std::invalid_argument("null result buffer");
+        const uint32_t ntid = b->q_off[nq];
+        for (uint32_t i = 0; i < nq; ++i)
+            if (b->q_off[i + 1] < b->q_off[i]) throw std::invalid_argument("q_off not monotone");
+        if (ntid && !b->q_tid) throw std::invalid_argument("q_tid is required");
+        for (uint32_t i = 0; i < ntid; ++i)
+            if (b->q_tid[i] != hm::kNoTerm && b->q_tid[i] >= X->dev.n_terms)
+                throw std::out_of_range("term id out of range");
+        ck(cudaSetDevice(X->device), "cudaSetDevice");
+        Workspace* w = acquire(X);
+        try {
+            const uint32_t k = std::max(b->k, 1u);
+            ensure(w, nq, std::max(ntid, 1u), k, true);
+            unsigned char* p = w->pin;
+            auto take = [&](size_t bytes) {
+                unsigned char* r = p;
+                p += (bytes + 15) & ~size_t(15);
+                return r;
+            };
+            float* pw = reinterpret_cast<float*>(take(hm::kMaxCodes * 4));
+            uint32_t* poff = reinterpret_cast<uint32_t*>(take((nq + 1ull) * 4));
+            uint32_t* ptid = reinterpret_cast<uint32_t*>(take(ntid * 4ull));
+            double* ptau = reinterpret_cast<double*>(take(nq * 8ull));
+            uint64_t* rids = reinterpret_cast<uint64_t*>(take(static_cast<size_t>(nq) * k * 8));
+            double* rsc = reinterpret_cast<double*>(take(static_cast<size_t>(nq) * k * 8));
+            uint32_t* rn = reinterpret_cast<uint32_t*>(take(nq * 4ull));
+            double* rconf = reinterpret_cast<double*>(take(nq * 8ull));
+            uint8_t* rskip = take(nq);
+            uint64_t* rpost = reinterpret_cast<uint64_t*>(take(nq * 8ull));
+            uint32_t* rcnt = reinterpret_cast<uint32_t*>(take(16));
+            std::memcpy(poff, b->q_off, (nq + 1ull) * 4);
+            if (ntid) std::memcpy(ptid, b->q_tid, ntid * 4ull);
+            if (b->tau) std::memcpy(ptau, b->tau, nq * 8ull);
+            cudaStream_t st = w->stream;
+            ck(cudaMemcpyAsync(w->q_off, poff, (nq + 1ull) * 4, cudaMemcpyHostToDevice, st), "H2D");
+            if (ntid) ck(cudaMemcpyAsync(w->q_tid, ptid, ntid * 4ull, cudaMemcpyHostToDevice, st), "H2D");
+            if (b->tau) ck(cudaMemcpyAsync(w->tau, ptau, nq * 8ull, cudaMemcpyHostToDevice, st), "H2D");
+            hm_query_batch hb = *b;
+            hm_results dout{w->out_ids, w->out_scores, w->out_n, w->out_conf, w->out_skip, w->out_post};
+            // the k used on device must match the output stride
+            run_batch(X, w, hb, w->q_off, w->q_tid, b->tau ? w->tau : nullptr, dout, pw);
+            const size_t kk = b->k;
+            if (kk) {
+                ck(cudaMemcpyAsync(rids, w->out_ids, nq * kk * 8, cudaMemcpyDeviceToHost, st), "D2H");
+                ck(cudaMemcpyAsync(rsc, w->out_scores, nq * kk * 8, cudaMemcpyDeviceToHost, st), "D2H");
+            }
+            ck(cudaMemcpyAsync(rn, w->out_n, nq * 4ull, cudaMemcpyDeviceToHost, st), "D2H");
+            ck(cudaMemcpyAsync(rconf, w->out_conf, nq * 8ull, cudaMemcpyDeviceToHost, st), "D2H");
+            ck(cudaMemcpyAsync(rskip, w->out_skip, nq, cudaMemcpyDeviceToHost, st), "D2H");
+            ck(cudaMemcpyAsync(rpost, w->out_post, nq * 8ull, cudaMemcpyDeviceToHost, st), "D2H");
+            ck(cudaMemcpyAsync(rcnt, w->counters, 16, cudaMemcpyDeviceToHost, st), "D2H");
+            ck(cudaStreamSynchronize(st), "batch");
+            g_last_exact = rcnt[1];
+            if (rcnt[3] & hm::kErrTooManyTerms)
+                throw std::invalid_argument("a query has more than 256 distinct terms");
+            if (rcnt[3] & 2u) throw std::runtime_error("exact kernel failed to converge");
+            for (uint32_t i = 0; i < nq; ++i) {
+                out->n[i] = rn[i];
+                for (uint32_t j = 0; j < rn[i]; ++j) {
+                    out->ids[i * kk + j] = rids[i * kk + j];
+                    out->scores[i * kk + j] = rsc[i * kk + j];
+                }
+            }
+            if (out->conf) std::memcpy(out->conf, rconf, nq * 8ull);
+            if (out->skip) std::memcpy(out->skip, rskip, nq);
+            if (out->postings) std::memcpy(out->postings, rpost, nq * 8ull);
+        } catch (...) {
+            cudaStreamSynchronize(w->stream);
+            release(X, w);
+            throw;
+        }
+        release(X, w);
+    });
+}
+
+int hm_search_batch_device(hm_index* X, const hm_query_batch* b, hm_results* out, void* stream) {
+    return guard([&] {
+        if (!X || !out) throw std::invalid_argument("null argument");
+        validate(X, b);
+        const uint32_t nq = b->n_queries;
+        if (nq == 0) return;
+        ck(cudaSetDevice(X->device), "cudaSetDevice");
+        // the batch's tid count is unknown on the host: plan scratch is sized
+        // from q_off[nq] read back once (a 4-byte D2H on the caller's stream)
+        cudaStream_t ust = static_cast<cudaStream_t>(stream);
+        uint32_t ntid = 0;
+        ck(cudaMemcpyAsync(&ntid, b->q_off + nq, 4, cudaMemcpyDeviceToHost, ust), "D2H q_off");
+        ck(cudaStreamSynchronize(ust), "sync");
+        Workspace* w = acquire(X);
+        try {
+            ensure(w, nq, std::max(ntid, 1u), std::max(b->k, 1u), false);
+            // order the workspace stream after the caller's stream and back
+            cudaEvent_t ev;
+            ck(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming), "event");
+            ck(cudaEventRecord(ev, ust), "event record");
+            ck(cudaStreamWaitEvent(w->stream, ev, 0), "wait");
+            run_batch(X, w, *b, b->q_off, b->q_tid, b->tau, *out, reinterpret_cast<float*>(w->pin));
+            ck(cudaEventRecord(ev, w->stream), "event record");
+            ck(cudaStreamWaitEvent(ust, ev, 0), "wait");
+            // pinned w32 staging is reused by the next call on this workspace:
+            // make sure the async upload finished before handing it back
+            ck(cudaStreamSynchronize(w->stream), "sync");
+            cudaEventDestroy(ev);
+        } catch (...) {
+            cudaStreamSynchronize(w->stream);
+            release(X, w);
+            throw;
+        }
+        release(X, w);
+    });
+}
+
+int hm_last_batch_stats(uint32_t* n_exact, uint32_t* n_launches) {
+    if (n_exact) *n_exact = g_last_exact;
+    if (n_launches) *n_launches = g_last_launches;
+    return HM_OK;
+}
+
+int hm_merge_shards_device(uint32_t G, uint32_t nq, uint32_t k, const uint64_t* ids,
+                           const double* scores, const uint32_t* n, const double* tau,
+                           double tau_default, double eps, hm_results* out, void* stream) {
+    return guard([&] {
+        if (!out) throw std::invalid_argument("null result");
+        if (static_cast<uint64_t>(G) * k > 2048)
+            throw std::invalid_argument("n_shards * k must be <= 2048");
+        ck(hm::launch_merge(G, nq, k, ids, scores, n, tau, tau_default, eps, out->ids, out->scores,
+                            out->n, out->conf, out->skip, static_cast<cudaStream_t>(stream)),
+           "merge kernel");
+    });
+}
+
+double hm_margin(const double* s, uint32_t n, double eps) {
+    if (n == 0 || s[0] <= 0.0) return 0.0;  // src/cascade.cpp:14
+    if (n < 2) return 0.0;
+    return (s[0] - s[1]) / std::max(s[0], eps);
+}
+
+}  // extern "C"

@@ -1,0 +1,32 @@
+// Host-visible launchers of the sm_100a search kernels (kernels/bm25_search.cu).
+#pragma once
+#include <cstddef>
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "hm_types.h"
+
+namespace hm {
+
+// one thread per query: make_plan (src/csr_index.cpp:31-48) + LPT cost
+cudaError_t launch_plan(const DevIndex& ix, const BatchArgs& a, uint32_t* order_in,
+                        cudaStream_t st);
+// LPT order: queries sorted by descending posting cost (CUB radix sort)
+cudaError_t lpt_sort_bytes(uint32_t nq, size_t* bytes);
+cudaError_t launch_lpt_sort(void* temp, size_t bytes, const BatchArgs& a,
+                            uint64_t* cost_sorted, const uint32_t* order_in,
+                            cudaStream_t st);
+// persistent fused kernel: TAAT scoring + selection + exact rescoring + margin
+cudaError_t launch_search(const DevIndex& ix, const BatchArgs& a, int grid, cudaStream_t st);
+// persistent exact fp64 kernel for the queries in a.exact_list
+cudaError_t launch_exact(const DevIndex& ix, const BatchArgs& a, int grid, cudaStream_t st);
+// merge of per-shard exact top-k lists (after the all-gather)
+cudaError_t launch_merge(uint32_t n_shards, uint32_t nq, uint32_t k, const uint64_t* ids,
+                         const double* scores, const uint32_t* n, const double* tau,
+                         double tau_default, double eps, uint64_t* out_ids,
+                         double* out_scores, uint32_t* out_n, double* out_conf,
+                         uint8_t* out_skip, cudaStream_t st);
+// resident CTAs per SM of the two persistent kernels
+cudaError_t search_occupancy(int* search_blocks_per_sm, int* exact_blocks_per_sm);
+
+}  // namespace hm

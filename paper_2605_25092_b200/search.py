@@ -1,0 +1,367 @@
+"""Python mirror of the reference search API over the B200 C ABI (hm_b200.h).
+
+Reference interfaces mirrored (paths under /root/reference/proj):
+  Bm25Params                      include/hybrid/csr_index.hpp:15-18
+  SearchStats                     include/hybrid/csr_index.hpp:37-39
+  CsrIndex.bm25_topk / _maxscore  include/hybrid/csr_index.hpp:72-79
+  TemporalIndex.topk              include/hybrid/temporal_index.hpp:63-66
+  confidence (Margin)             include/hybrid/cascade.hpp:29-34
+  the cmd_search batch loop       tools/hybridmem.cpp:227-313  -> search_batch
+
+Every search runs on the GPU through libhm_b200.so; there is no CPU path.
+Errors map to the reference's exception types (RuntimeError for
+std::runtime_error, ValueError for std::invalid_argument, IndexError for
+std::out_of_range).
+"""
+import ctypes as C
+import math
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib
+
+HM_FLAG_FORCE_EXACT = 1
+HM_FLAG_DEBUG_NO_RESET = 2
+NO_TERM = 0xFFFFFFFF
+MAX_K = 256
+
+_L = None
+
+
+class CsrView(C.Structure):
+    _fields_ = [("n_terms", C.c_uint32), ("term_offsets", C.c_void_p),
+                ("posting_rows", C.c_void_p), ("posting_weights", C.c_void_p),
+                ("posting_tf", C.c_void_p), ("term_idfs", C.c_void_p),
+                ("term_order_keys", C.c_void_p), ("n_docs", C.c_uint32),
+                ("doc_lens", C.c_void_p), ("doc_ids", C.c_void_p), ("avgdl", C.c_double)]
+
+
+class QueryBatch(C.Structure):
+    _fields_ = [("n_queries", C.c_uint32), ("q_off", C.c_void_p), ("q_tid", C.c_void_p),
+                ("k", C.c_uint32), ("k1", C.c_double), ("b", C.c_double),
+                ("tau", C.c_void_p), ("tau_default", C.c_double),
+                ("epsilon_guard", C.c_double), ("row_lo", C.c_uint32),
+                ("row_hi", C.c_uint32), ("flags", C.c_uint32)]
+
+
+class Results(C.Structure):
+    _fields_ = [("ids", C.c_void_p), ("scores", C.c_void_p), ("n", C.c_void_p),
+                ("conf", C.c_void_p), ("skip", C.c_void_p), ("postings", C.c_void_p)]
+
+
+EXPORTS = ["hm_index_create", "hm_index_destroy", "hm_index_device_bytes", "hm_index_format",
+           "hm_search_batch", "hm_search_batch_device", "hm_last_batch_stats",
+           "hm_merge_shards_device", "hm_margin", "hm_last_error"]
+
+
+def lib():
+    global _L
+    if _L is not None:
+        return _L
+    L = _lib.load("libhm_b200.so")
+    P = C.POINTER
+    L.hm_last_error.restype = C.c_char_p
+    L.hm_index_create.argtypes = [P(CsrView), C.c_int, P(C.c_void_p)]
+    L.hm_index_destroy.argtypes = [C.c_void_p]
+    L.hm_index_device_bytes.argtypes = [C.c_void_p]
+    L.hm_index_device_bytes.restype = C.c_uint64
+    L.hm_index_format.argtypes = [C.c_void_p, P(C.c_uint32), P(C.c_uint32), P(C.c_uint32),
+                                  P(C.c_uint64)]
+    L.hm_search_batch.argtypes = [C.c_void_p, P(QueryBatch), P(Results)]
+    L.hm_search_batch_device.argtypes = [C.c_void_p, P(QueryBatch), P(Results), C.c_void_p]
+    L.hm_last_batch_stats.argtypes = [P(C.c_uint32), P(C.c_uint32)]
+    L.hm_merge_shards_device.argtypes = [C.c_uint32, C.c_uint32, C.c_uint32, C.c_void_p,
+                                         C.c_void_p, C.c_void_p, C.c_void_p, C.c_double,
+                                         C.c_double, P(Results), C.c_void_p]
+    L.hm_margin.argtypes = [P(C.c_double), C.c_uint32, C.c_double]
+    L.hm_margin.restype = C.c_double
+    _L = L
+    return L
+
+
+def _check(rc):
+    if rc == 0:
+        return
+    msg = lib().hm_last_error().decode()
+    if rc == 1:
+        raise ValueError(msg)
+    if rc == 3:
+        raise IndexError(msg)
+    raise RuntimeError(msg)
+
+
+def _ptr(a):
+    return None if a is None else a.ctypes.data
+
+
+@dataclass
+class Bm25Params:
+    """hybrid::Bm25Params (csr_index.hpp:15-18)."""
+    k1: float = 1.2
+    b: float = 0.75
+
+
+@dataclass
+class SearchStats:
+    """hybrid::SearchStats (csr_index.hpp:37-39); accumulates like the reference."""
+    postings_touched: int = 0
+
+
+class DeviceIndex:
+    """An HBM-resident index (hm_index).  Arrays follow hybrid::CsrIndex."""
+
+    def __init__(self, term_offsets, posting_rows, idf, order_key, doc_lens, doc_ids, avgdl,
+                 posting_tf=None, posting_weights=None, device=0):
+        self._keep = dict(
+            term_offsets=np.ascontiguousarray(term_offsets, np.uint64),
+            posting_rows=np.ascontiguousarray(posting_rows, np.uint32),
+            idf=np.ascontiguousarray(idf, np.float64),
+            order_key=np.ascontiguousarray(order_key, np.float64),
+            doc_lens=np.ascontiguousarray(doc_lens, np.uint32),
+            doc_ids=np.ascontiguousarray(doc_ids, np.uint64))
+        if posting_tf is not None:
+            self._keep["tf"] = np.ascontiguousarray(posting_tf, np.uint32)
+        if posting_weights is not None:
+            self._keep["w"] = np.ascontiguousarray(posting_weights, np.float64)
+        k = self._keep
+        v = CsrView(len(k["idf"]), _ptr(k["term_offsets"]), _ptr(k["posting_rows"]),
+                    _ptr(k.get("w")), _ptr(k.get("tf")), _ptr(k["idf"]), _ptr(k["order_key"]),
+                    len(k["doc_ids"]), _ptr(k["doc_lens"]), _ptr(k["doc_ids"]), float(avgdl))
+        h = C.c_void_p()
+        _check(lib().hm_index_create(C.byref(v), device, C.byref(h)))
+        self._h = h
+        self.device = device
+        self.n_terms = len(k["idf"])
+        self.n_docs = len(k["doc_ids"])
+        self.df = np.diff(k["term_offsets"].astype(np.int64))
+        self._keep = None  # borrowed only for the duration of create
+
+    @classmethod
+    def from_host(cls, hx, device=0):
+        """From a paper_2605_25092_b200.synth.HostIndex."""
+        return cls(hx.term_offsets, hx.posting_rows, hx.idf, hx.order_key, hx.doc_lens,
+                   hx.doc_ids, hx.avgdl, posting_tf=hx.posting_tf, device=device)
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib().hm_index_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        self.close()
+
+    @property
+    def device_bytes(self):
+        return lib().hm_index_device_bytes(self._h)
+
+    def format(self):
+        rb, cb, nc = C.c_uint32(), C.c_uint32(), C.c_uint32()
+        ne = C.c_uint64()
+        _check(lib().hm_index_format(self._h, C.byref(rb), C.byref(cb), C.byref(nc), C.byref(ne)))
+        return dict(row_bits=rb.value, code_bits=cb.value, n_codes=nc.value, n_escaped=ne.value)
+
+    # ------------------------------------------------------------ batch API
+    def search_batch(self, q_off, q_tid, k, k1=1.2, b=0.75, tau=None, tau_default=0.10,
+                     epsilon_guard=1e-9, row_lo=0, row_hi=0, flags=0):
+        """Host-buffer batch search (hm_search_batch).  q_off[nq+1], q_tid resolved term
+        ids (NO_TERM for unknown).  Returns dict(ids[nq,k], scores[nq,k], n[nq],
+        conf[nq], skip[nq], postings[nq], n_exact)."""
+        q_off = np.ascontiguousarray(q_off, np.uint32)
+        q_tid = np.ascontiguousarray(q_tid, np.uint32)
+        nq = len(q_off) - 1
+        kk = max(int(k), 1)
+        out = dict(ids=np.zeros((nq, kk), np.uint64), scores=np.zeros((nq, kk), np.float64),
+                   n=np.zeros(nq, np.uint32), conf=np.zeros(nq, np.float64),
+                   skip=np.zeros(nq, np.uint8), postings=np.zeros(nq, np.uint64))
+        tau_a = None if tau is None else np.ascontiguousarray(tau, np.float64)
+        qb = QueryBatch(nq, _ptr(q_off), _ptr(q_tid) if len(q_tid) else None, int(k), k1, b,
+                        _ptr(tau_a), tau_default, epsilon_guard, row_lo, row_hi, flags)
+        r = Results(_ptr(out["ids"]), _ptr(out["scores"]), _ptr(out["n"]), _ptr(out["conf"]),
+                    _ptr(out["skip"]), _ptr(out["postings"]))
+        _check(lib().hm_search_batch(self._h, C.byref(qb), C.byref(r)))
+        ne, nl = C.c_uint32(), C.c_uint32()
+        lib().hm_last_batch_stats(C.byref(ne), C.byref(nl))
+        out["n_exact"] = ne.value
+        if k == 0:
+            out["ids"] = out["ids"][:, :0]
+            out["scores"] = out["scores"][:, :0]
+        return out
+
+    def search_lists(self, tid_lists, k, **kw):
+        off = np.zeros(len(tid_lists) + 1, np.uint32)
+        off[1:] = np.cumsum([len(t) for t in tid_lists])
+        tids = (np.concatenate([np.asarray(t, np.uint32) for t in tid_lists])
+                if tid_lists and off[-1] else np.zeros(0, np.uint32))
+        return self.search_batch(off, tids, k, **kw)
+
+    def search_batch_device(self, q_off, q_tid, out, k, k1=1.2, b=0.75, tau=None,
+                            tau_default=0.10, epsilon_guard=1e-9, row_lo=0, row_hi=0, flags=0,
+                            stream=None):
+        """Device-resident batch (torch CUDA tensors), enqueued on `stream`
+        (default: torch's current stream).  `out` is a dict of torch tensors
+        (ids[nq,k] int64, scores[nq,k] f64, n[nq] int32, conf[nq] f64,
+        skip[nq] uint8, postings[nq] int64)."""
+        import torch
+        nq = q_off.numel() - 1
+        st = stream if stream is not None else torch.cuda.current_stream(q_off.device)
+        qb = QueryBatch(nq, q_off.data_ptr(), q_tid.data_ptr(), int(k), k1, b,
+                        None if tau is None else tau.data_ptr(), tau_default, epsilon_guard,
+                        row_lo, row_hi, flags)
+        r = Results(out["ids"].data_ptr(), out["scores"].data_ptr(), out["n"].data_ptr(),
+                    out["conf"].data_ptr(), out["skip"].data_ptr(), out["postings"].data_ptr())
+        _check(lib().hm_search_batch_device(self._h, C.byref(qb), C.byref(r), st.cuda_stream))
+
+
+def merge_shards_device(shard_ids, shard_scores, shard_n, out, k, tau=None, tau_default=0.10,
+                        epsilon_guard=1e-9, stream=None):
+    """hm_merge_shards_device over torch CUDA tensors [G,nq,k] / [G,nq]."""
+    import torch
+    G, nq = shard_n.shape
+    st = stream if stream is not None else torch.cuda.current_stream(shard_n.device)
+    r = Results(out["ids"].data_ptr(), out["scores"].data_ptr(), out["n"].data_ptr(),
+                out["conf"].data_ptr(), out["skip"].data_ptr(), None)
+    _check(lib().hm_merge_shards_device(G, nq, k, shard_ids.data_ptr(), shard_scores.data_ptr(),
+                                        shard_n.data_ptr(),
+                                        None if tau is None else tau.data_ptr(), tau_default,
+                                        epsilon_guard, C.byref(r), st.cuda_stream))
+
+
+def margin(scores, epsilon_guard=1e-9):
+    """Margin confidence (src/cascade.cpp:15-21)."""
+    s = np.ascontiguousarray(scores, np.float64)
+    return lib().hm_margin(s.ctypes.data_as(C.POINTER(C.c_double)), len(s), epsilon_guard)
+
+
+# ---------------------------------------------------------------- reference-shaped API
+class CsrIndex:
+    """Mirror of hybrid::CsrIndex (csr_index.hpp:44-87) whose searches run on the GPU.
+
+    `terms` (alphabetical; tid = position) and the CSR arrays are the reference's
+    fields; the device copy is created lazily on first search and cached."""
+
+    def __init__(self, terms, term_offsets, posting_rows, posting_weights, term_idfs,
+                 term_order_keys, doc_lens, doc_ids, avgdl, build_params=None, device=0):
+        self.terms = list(terms)
+        self.vocab = {t: i for i, t in enumerate(self.terms)}
+        self.term_offsets = np.asarray(term_offsets, np.uint64)
+        self.posting_rows = np.asarray(posting_rows, np.uint32)
+        self.posting_weights = np.asarray(posting_weights, np.float64)
+        self.term_idfs = np.asarray(term_idfs, np.float64)
+        self.term_order_keys = np.asarray(term_order_keys, np.float64)
+        self.doc_lens = np.asarray(doc_lens, np.uint32)
+        self.doc_ids = np.asarray(doc_ids, np.uint64)
+        self.avgdl = float(avgdl)
+        self.build_params = build_params or Bm25Params()
+        self.device = device
+        self._dev = None
+
+    @classmethod
+    def from_host(cls, hx, device=0):
+        idx = cls(hx.term_strings(), hx.term_offsets, hx.posting_rows,
+                  hx.posting_tf.astype(np.float64), hx.idf, hx.order_key, hx.doc_lens,
+                  hx.doc_ids, hx.avgdl, Bm25Params(hx.build_k1, hx.build_b), device)
+        return idx
+
+    def num_docs(self):
+        return len(self.doc_ids)
+
+    def num_postings(self):
+        return len(self.posting_rows)
+
+    def dev(self):
+        if self._dev is None:
+            self._dev = DeviceIndex(self.term_offsets, self.posting_rows, self.term_idfs,
+                                    self.term_order_keys, self.doc_lens, self.doc_ids,
+                                    self.avgdl, posting_weights=self.posting_weights,
+                                    device=self.device)
+        return self._dev
+
+    def resolve(self, query_terms):
+        return [self.vocab.get(t, NO_TERM) for t in query_terms]
+
+    def bm25_topk(self, query_terms, k, p=None, stats=None):
+        """-> list[(doc_id, score)] ranked (score desc, id asc) (csr_index.cpp:77-104)."""
+        p = p or Bm25Params()
+        r = self.dev().search_lists([self.resolve(query_terms)], k, k1=p.k1, b=p.b)
+        if stats is not None:
+            stats.postings_touched += int(r["postings"][0])
+        n = int(r["n"][0])
+        return [(int(r["ids"][0, i]), float(r["scores"][0, i])) for i in range(n)]
+
+    # MaxScore's output is identical to the exhaustive path (csr_index.hpp:77-79,
+    # acceptance.cpp:144-171); the GPU path serves both with the same kernel.
+    bm25_topk_maxscore = bm25_topk
+
+    def search_batch(self, queries, k, p=None, tau=None, tau_default=0.10, row_lo=0, row_hi=0,
+                     flags=0):
+        """Batch of string queries (the cmd_search loop, hybridmem.cpp:227-313)."""
+        p = p or Bm25Params()
+        return self.dev().search_lists([self.resolve(q) for q in queries], k, k1=p.k1, b=p.b,
+                                       tau=tau, tau_default=tau_default, row_lo=row_lo,
+                                       row_hi=row_hi, flags=flags)
+
+
+def k_star(epsilon, lam):
+    """temporal_index.cpp:9-17."""
+    if not (0.0 < epsilon < 1.0):
+        raise ValueError("epsilon must be in (0,1)")
+    if not lam > 0.0:
+        raise ValueError("lambda must be > 0")
+    return max(1, int(math.ceil(math.log(1.0 / epsilon) / lam)))
+
+
+@dataclass
+class TemporalParams:
+    """hybrid::TemporalParams (temporal_index.hpp:12-17)."""
+    window_ms: int = 7 * 24 * 3600 * 1000
+    epsilon: float = 0.05
+    lambda_hat: float = 1.4
+    k_max_partitions: int = 4
+
+
+class TemporalIndex:
+    """Time-partitioned index on one device (temporal_index.hpp:40-72).
+
+    Rows are laid out partition by partition (oldest first, insertion order
+    inside a partition) and every partition shares the flat corpus statistics
+    (temporal_index.cpp:136-142), so the newest `budget` partitions are a row
+    suffix and scoring them is the flat kernel restricted to that row window.
+    The result equals the reference's greedy most-recent-first merge
+    (temporal_index.cpp:72-123)."""
+
+    def __init__(self, flat_dev, part_row, params=None):
+        self.dev = flat_dev
+        self.part_row = np.asarray(part_row, np.uint32)
+        self.params = params or TemporalParams()
+
+    def num_partitions(self):
+        return len(self.part_row) - 1
+
+    def budget(self):
+        K = self.num_partitions()
+        if K == 0:
+            return 0
+        p = self.params
+        return min(k_star(p.epsilon, p.lambda_hat), p.k_max_partitions, K)
+
+    def window(self):
+        K = self.num_partitions()
+        first = K - self.budget()
+        return int(self.part_row[first]), int(self.part_row[K])
+
+    def topk_batch(self, q_off, q_tid, k, k1=1.2, b=0.75, **kw):
+        if self.num_partitions() == 0 or k == 0:
+            nq = len(q_off) - 1
+            return dict(ids=np.zeros((nq, 0), np.uint64), scores=np.zeros((nq, 0)),
+                        n=np.zeros(nq, np.uint32), conf=np.zeros(nq), skip=np.zeros(nq, np.uint8),
+                        postings=np.zeros(nq, np.uint64), n_exact=0)
+        lo, hi = self.window()
+        if hi <= lo:  # newest partitions are empty: nothing to score
+            nq = len(q_off) - 1
+            return dict(ids=np.zeros((nq, max(k, 1)), np.uint64),
+                        scores=np.zeros((nq, max(k, 1))), n=np.zeros(nq, np.uint32),
+                        conf=np.zeros(nq), skip=(np.zeros(nq) >= kw.get("tau_default", 0.10)
+                                                 ).astype(np.uint8),
+                        postings=np.zeros(nq, np.uint64), n_exact=0)
+        return self.dev.search_batch(q_off, q_tid, k, k1=k1, b=b, row_lo=lo, row_hi=hi, **kw)

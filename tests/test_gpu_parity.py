@@ -1,0 +1,186 @@
+"""GPU parity: the CUDA path through the C ABI vs the oracle / the reference.
+
+Bar: bit-identical ids, score bits, counts, Margin confidence, skip decision
+and postings_touched (stricter than north_star's 1e-5 relative tolerance).
+Mirrors proj/tests/test_csr.cpp, test_cascade.cpp and acceptance.cpp:144-208.
+"""
+import threading
+
+import numpy as np
+import pytest
+
+from _util import (assert_same, check_batch, export_to_csr, random_instance, ref, restate,
+                   search, synth_setup, toy_docs)
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def c1(gpu):
+    """BASELINE config 1: 100K Zipf docs (V=5000, 5-30 tokens), 1K queries, k=10."""
+    corpus, queries, hx, tids = synth_setup(100000, 5000, 5, 30, 1000)
+    dev = search.DeviceIndex.from_host(hx)
+    orc = restate.OracleIndex.from_host(hx)
+    return dict(corpus=corpus, queries=queries, hx=hx, tids=tids, dev=dev, orc=orc)
+
+
+def test_c1_bit_identical_to_oracle(c1):
+    got = c1["dev"].search_lists(c1["tids"], 10)
+    ids, sc, n, post = c1["orc"].topk(c1["tids"], 10)
+    check_batch(got, ids, sc, n, post, what="C1")
+    # nDCG@10 (exponential gain, qrels = gold) identical -> within 0.0002
+    q = c1["queries"]
+    d_got = np.mean([restate.ndcg(got["ids"][i, :got["n"][i]], {int(q.gold[i]): 1}, 10)
+                     for i in range(len(q))])
+    d_orc = np.mean([restate.ndcg(ids[i, :n[i]], {int(q.gold[i]): 1}, 10) for i in range(len(q))])
+    assert abs(d_got - d_orc) <= 2e-4
+
+
+def test_c1_matches_reference_library(c1):
+    """Against the reference's own bm25_topk and bm25_topk_maxscore on the same index."""
+    hx, q = c1["hx"], c1["queries"]
+    ri = ref.RefIndex.from_arrays(hx.term_strings(), hx.term_offsets, hx.posting_rows,
+                                  hx.posting_tf.astype(np.float64), hx.idf, hx.maxscore,
+                                  hx.order_key, hx.doc_lens, hx.doc_ids, hx.avgdl)
+    sub = list(range(0, len(q), 7))
+    got = c1["dev"].search_lists([c1["tids"][i] for i in sub], 10)
+    for j, i in enumerate(sub):
+        for ms in (False, True):
+            ids, sc, post = ri.search(q.terms(i), 10, maxscore=ms)
+            m = got["n"][j]
+            assert_same(got["ids"][j, :m], got["scores"][j, :m], ids, sc, f"ref q{i} ms={ms}")
+            if not ms:
+                assert got["postings"][j] == post
+
+
+@pytest.mark.parametrize("k", [1, 3, 100, 256])
+def test_c1_other_k(c1, k):
+    tids = c1["tids"][:300]
+    got = c1["dev"].search_lists(tids, k)
+    ids, sc, n, post = c1["orc"].topk(tids, k)
+    check_batch(got, ids, sc, n, post, what=f"k={k}")
+
+
+@pytest.mark.parametrize("k1,b", [(0.9, 0.4), (2.0, 1.0), (1.2, 0.0), (0.0, 0.75)])
+def test_c1_other_params(c1, k1, b):
+    tids = c1["tids"][:200]
+    got = c1["dev"].search_lists(tids, 10, k1=k1, b=b)
+    ids, sc, n, post = c1["orc"].topk(tids, 10, k1=k1, b=b)
+    check_batch(got, ids, sc, n, post, what=f"k1={k1} b={b}")
+
+
+@pytest.mark.parametrize("k1,b", [(1.2, 1.5), (1.2, -0.5)])
+def test_params_outside_unit_b_use_exact_kernel(c1, k1, b):
+    tids = c1["tids"][:64]
+    got = c1["dev"].search_lists(tids, 10, k1=k1, b=b)
+    assert got["n_exact"] == len(tids)
+    ids, sc, n, post = c1["orc"].topk(tids, 10, k1=k1, b=b)
+    check_batch(got, ids, sc, n, post, what=f"exact k1={k1} b={b}")
+
+
+def test_forced_exact_kernel_identical(c1):
+    tids = c1["tids"][:300]
+    fast = c1["dev"].search_lists(tids, 10)
+    exact = c1["dev"].search_lists(tids, 10, flags=search.HM_FLAG_FORCE_EXACT)
+    assert exact["n_exact"] == len(tids)
+    for key in ("ids", "scores", "n", "conf", "skip", "postings"):
+        assert (fast[key] == exact[key]).all(), key
+
+
+def test_duplicate_and_unknown_terms(c1):
+    base = c1["tids"][:100]
+    tids = [np.concatenate([t, t[:1], [search.NO_TERM], t[-1:]]) for t in base]
+    got = c1["dev"].search_lists(tids, 10)
+    ids, sc, n, post = c1["orc"].topk(tids, 10)
+    check_batch(got, ids, sc, n, post, what="mult")
+
+
+def test_per_query_tau(c1):
+    tids = c1["tids"][:128]
+    tau = np.linspace(0.0, 0.5, len(tids))
+    got = c1["dev"].search_lists(tids, 10, tau=tau)
+    ids, sc, n, _ = c1["orc"].topk(tids, 10)
+    for i in range(len(tids)):
+        conf = restate.margin(sc[i, :n[i]])
+        assert bool(got["skip"][i]) == (conf >= tau[i])
+
+
+def test_empty_and_k0(c1):
+    got = c1["dev"].search_lists([[], [search.NO_TERM]], 10)
+    assert (got["n"] == 0).all() and (got["conf"] == 0).all() and (got["skip"] == 0).all()
+    got = c1["dev"].search_lists(c1["tids"][:5], 0)
+    assert (got["n"] == 0).all()
+    got = c1["dev"].search_lists(c1["tids"][:5], 10, tau_default=0.0)
+    assert (got["skip"] == 1).all()  # tau = 0 => always skip (test_cascade.cpp:93-115)
+
+
+def test_batch_composition_and_concurrency(c1):
+    tids = c1["tids"][:200]
+    full = c1["dev"].search_lists(tids, 10)
+    single = [c1["dev"].search_lists([t], 10) for t in tids[:20]]
+    for i, s in enumerate(single):
+        for key in ("ids", "scores", "n", "conf"):
+            assert (s[key][0] == full[key][i]).all()
+    outs = [None] * 4
+
+    def run(j):
+        outs[j] = c1["dev"].search_lists(tids, 10)
+
+    th = [threading.Thread(target=run, args=(j,)) for j in range(4)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    for o in outs:
+        for key in ("ids", "scores", "n", "conf", "skip"):
+            assert (o[key] == full[key]).all()
+
+
+def test_sentinel_reset_is_load_bearing(c1):
+    """Pitfall 3 (test_twophase.cpp:66-83): without the
+    per-query reset of the candidate state, stale entries of the previous query
+    contaminate the next one."""
+    heavy = max(range(len(c1["tids"])), key=lambda i: len(c1["tids"][i]))
+    tids = [c1["tids"][heavy] if i % 2 == 0 else c1["tids"][i % len(c1["tids"])] for i in range(2000)]
+    ids, sc, n, _ = c1["orc"].topk(tids, 10)
+    good = c1["dev"].search_lists(tids, 10)
+    check_batch(good, ids, sc, n, what="reset on")
+    bad = c1["dev"].search_lists(tids, 10, flags=search.HM_FLAG_DEBUG_NO_RESET)
+    differs = any(bad["n"][i] != n[i] or (bad["ids"][i, :n[i]] != ids[i, :n[i]]).any()
+                  for i in range(len(tids)))
+    assert differs, "disabling the reset should contaminate results"
+
+
+def test_random_instances_vs_reference(gpu):
+    """test_csr.cpp:162-176 shape: random tiny corpora, reference build_index +
+    reference bm25_topk as the oracle."""
+    rng = np.random.default_rng(1234)
+    for trial in range(150):
+        docs, q = random_instance(rng)
+        ri = ref.RefIndex.from_texts(docs, ref.TOK_MINIMAL)
+        idx = export_to_csr(ri)
+        k = 1 + int(rng.integers(0, 10))
+        want_ids, want_sc, want_post = ri.search(q, k)
+        stats = search.SearchStats()
+        got = idx.bm25_topk(q, k, stats=stats)
+        assert_same([g[0] for g in got], [g[1] for g in got], want_ids, want_sc, f"trial {trial}")
+        assert stats.postings_touched == want_post
+
+
+def test_toy_corpus_known_answers(gpu):
+    ri = ref.RefIndex.from_texts(toy_docs(), ref.TOK_MINIMAL)
+    idx = export_to_csr(ri)
+    assert idx.bm25_topk(["unicorn"], 5) == []
+    allc = idx.bm25_topk(["cat"], 100)
+    assert len(allc) == 4 and all(s > 0 for _, s in allc)
+    assert len(idx.bm25_topk(["cat", "dog"], 5)) == 5
+    for q in (["cat"], ["cat", "dog"], ["fish", "cat", "cat"], ["dog", "z00"]):
+        want_ids, want_sc, _ = ri.search(q, 5)
+        got = idx.bm25_topk(q, 5)
+        assert_same([g[0] for g in got], [g[1] for g in got], want_ids, want_sc, str(q))
+
+
+def test_empty_index(gpu):
+    ri = ref.RefIndex.from_texts([], ref.TOK_MINIMAL)
+    idx = export_to_csr(ri)
+    assert idx.bm25_topk(["cat"], 5) == []

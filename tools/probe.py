@@ -1,0 +1,35 @@
+"""Quick perf probe (development aid): time one config's batch on the GPU."""
+import sys, time, os
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np, torch
+from paper_2605_25092_b200 import search, synth
+
+def main(n=8841823, V=1000000, lo=20, hi=60, nq=10000, mint=3, maxt=6, k=10, reps=3):
+    t = time.time()
+    c = synth.Corpus(n_records=n, vocab_size=V, min_doc_tokens=lo, max_doc_tokens=hi)
+    q = synth.Queries(c, n_queries=nq, min_terms=mint, max_terms=maxt)
+    hx = synth.HostIndex(c)
+    print(f"gen+build {time.time()-t:.1f}s P={len(hx.posting_rows)}", flush=True)
+    t = time.time(); dev = search.DeviceIndex.from_host(hx); print(f"upload {time.time()-t:.1f}s fmt={dev.format()} bytes={dev.device_bytes/1e9:.2f}GB", flush=True)
+    tids = hx.resolve(q.term_ranks)
+    off = q.offsets.astype(np.uint32)
+    df = np.diff(hx.term_offsets.astype(np.int64))
+    post = sum(int(df[np.unique(tids[off[i]:off[i+1]])].sum()) for i in range(nq))
+    dq_off = torch.from_numpy(off.astype(np.int32)).cuda(); dq_tid = torch.from_numpy(tids.astype(np.int32)).cuda()
+    out = dict(ids=torch.zeros(nq, k, dtype=torch.int64, device='cuda'), scores=torch.zeros(nq, k, dtype=torch.float64, device='cuda'),
+               n=torch.zeros(nq, dtype=torch.int32, device='cuda'), conf=torch.zeros(nq, dtype=torch.float64, device='cuda'),
+               skip=torch.zeros(nq, dtype=torch.uint8, device='cuda'), postings=torch.zeros(nq, dtype=torch.int64, device='cuda'))
+    for r in range(reps + 1):
+        torch.cuda.synchronize(); e0 = torch.cuda.Event(enable_timing=True); e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(); dev.search_batch_device(dq_off, dq_tid, out, k); e1.record(); torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1)
+        print(f"rep {r}: {ms:.2f} ms  {nq/ms*1e3:.0f} qps  eff {post*8/ms/1e6:.0f} GB/s (8B/posting)  phys {post*4/ms/1e6:.0f} GB/s", flush=True)
+    t = time.time(); r = dev.search_batch(off, tids, k); print(f"host api {time.time()-t:.3f}s n_exact={r['n_exact']}")
+
+if __name__ == "__main__":
+    cfg = sys.argv[1] if len(sys.argv) > 1 else "c2"
+    nq = int(sys.argv[2]) if len(sys.argv) > 2 else None
+    reps = int(sys.argv[3]) if len(sys.argv) > 3 else 3
+    if cfg == "c1": main(100000, 5000, 5, 30, nq or 1000, reps=reps)
+    elif cfg == "c4": main(8841823, 1000000, 40, 80, nq or 4096, 24, 32, 100, reps=reps)
+    else: main(nq=nq or 10000, reps=reps)
