@@ -86,6 +86,9 @@ typedef struct {
 #define HM_FLAG_DEBUG_NO_RESET 2u /* test-only: skip the per-query sentinel reset
                                     of the candidate state (pitfall-3 witness,
                                     src/twophase.cpp:24-27) */
+#define HM_FLAG_TIMING 4u         /* time each kernel with CUDA events on the
+                                    launching stream (the call then synchronises);
+                                    read back with hm_last_batch_timing */
 
 /* Results, caller-allocated.  Row i of ids/scores has stride k; out_n[i] <= k
  * entries ranked by (score desc, DocId asc), zero scores never emitted
@@ -120,6 +123,10 @@ int hm_search_batch_device(hm_index* index, const hm_query_batch* batch_dev,
  * exact fp64 kernel (candidate overflow or non-positive impacts), kernel
  * launches issued. */
 int hm_last_batch_stats(uint32_t* n_exact_fallback, uint32_t* n_launches);
+
+/* Device time (ms) of the last HM_FLAG_TIMING batch on this thread: planner +
+ * LPT sort, the fused selection kernel, the exact fallback kernel. */
+int hm_last_batch_timing(float* ms_plan, float* ms_search, float* ms_exact);
 
 /* Doc-sharded multi-GPU merge (the step after the all-gather of k candidates
  * per query): shard_ids/shard_scores/shard_n hold G blocks of per-shard exact

@@ -5,7 +5,8 @@
 //   * raw tf per posting (from the reference's posting_weights doubles or a
 //     u32 array) and doc length per row define a (tf, len) pair; the 2^cb - 1
 //     most frequent pairs get codes, the rest use the escape code;
-//   * packed posting = (row << cb) | code  (cb = min(8, 32 - row_bits));
+//   * packed posting: long terms (local row << 18) | code18, short terms
+//     (row << cb) | code_cb, cb = min(8, 32 - row_bits) (see kernels/hm_types.h);
 //   * long terms (df > 32 * n_tiles) get a tile-boundary table;
 //   * everything is uploaded once and stays resident in HBM.
 // Search (per batch): upload query tids, plan kernel, LPT sort, persistent
@@ -31,6 +32,7 @@ namespace {
 
 thread_local std::string g_err;
 thread_local uint32_t g_last_exact = 0, g_last_launches = 0;
+thread_local float g_ms_plan = 0.f, g_ms_search = 0.f, g_ms_exact = 0.f;
 
 struct no_device_error : std::runtime_error {
     using std::runtime_error::runtime_error;
@@ -107,6 +109,9 @@ struct Workspace {
     float* w32 = nullptr;
     uint8_t* out_skip = nullptr;
     void* sort_tmp = nullptr;
+    cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+    uint32_t* stab = nullptr;  // per-CTA short-term tile tables
+    uint64_t stab_words = 0;
     // pinned host staging
     unsigned char* pin = nullptr;
     size_t pin_bytes = 0;
@@ -127,6 +132,9 @@ struct Workspace {
     }
     ~Workspace() {
         free_dev();
+        if (stab) cudaFree(stab);
+        for (auto e : ev)
+            if (e) cudaEventDestroy(e);
         if (pin) cudaFreeHost(pin);
         if (stream) cudaStreamDestroy(stream);
     }
@@ -266,13 +274,15 @@ void build_index(const hm_csr_view* v, hm_index* X) {
         if (x.first != y.first) return x.first > y.first;
         return x.second < y.second;
     });
-    const uint32_t n_codes = static_cast<uint32_t>(std::min<size_t>(pairs.size(), esc));
+    // code table: the kMaxCodes most frequent pairs; short-term postings can
+    // only address the first esc_short of them (their code field is cb bits)
+    const uint32_t n_codes = static_cast<uint32_t>(std::min<size_t>(pairs.size(), hm::kMaxCodes));
+    const uint32_t n_codes_short = std::min(n_codes, esc);
     X->n_codes = n_codes;
     X->code_tf.assign(hm::kMaxCodes, 0);
     X->code_len.assign(hm::kMaxCodes, 0);
-    std::vector<uint16_t> dense_code(static_cast<size_t>(kTfD) * kLenD, static_cast<uint16_t>(esc));
+    std::vector<uint16_t> dense_code(static_cast<size_t>(kTfD) * kLenD, 0xFFFF);
     std::unordered_map<uint64_t, uint32_t> sparse_code;
-    uint64_t escaped = 0;
     for (uint32_t c = 0; c < n_codes; ++c) {
         uint64_t kk = pairs[c].second;
         uint32_t f = static_cast<uint32_t>(kk >> 32), l = static_cast<uint32_t>(kk);
@@ -281,24 +291,7 @@ void build_index(const hm_csr_view* v, hm_index* X) {
         if (f < kTfD && l < kLenD) dense_code[static_cast<size_t>(f) * kLenD + l] = static_cast<uint16_t>(c);
         else sparse_code[kk] = c;
     }
-    for (size_t c = n_codes; c < pairs.size(); ++c) escaped += pairs[c].first;
-    X->n_escaped = escaped;
-    // packed postings
-    std::vector<uint32_t> packed(P);
-    par_for(P, [&](int, uint64_t a, uint64_t b) {
-        for (uint64_t i = a; i < b; ++i) {
-            uint32_t r = v->posting_rows[i], f = tf[i], l = v->doc_lens[r];
-            uint32_t code = esc;
-            if (f < kTfD && l < kLenD) {
-                code = dense_code[static_cast<size_t>(f) * kLenD + l];
-            } else {
-                auto it = sparse_code.find(key(f, l));
-                if (it != sparse_code.end()) code = it->second;
-            }
-            packed[i] = (r << cb) | code;
-        }
-    });
-    // long-term tile tables
+    // long terms (tile table) vs short terms
     const uint32_t n_tiles = std::max<uint32_t>(1, (N + hm::kTile - 1) / hm::kTile);
     std::vector<int32_t> slot(V, -1);
     std::vector<uint32_t> long_terms;
@@ -309,6 +302,42 @@ void build_index(const hm_csr_view* v, hm_index* X) {
             long_terms.push_back(t);
         }
     }
+    // packed postings (+8 words of padding for 16-byte bulk copies)
+    std::vector<uint32_t> packed(P + 8, 0);
+    std::atomic<uint64_t> escaped{0};
+    par_for(V, [&](int, uint64_t a, uint64_t b) {
+        uint64_t esc_local = 0;
+        for (uint64_t t = a; t < b; ++t) {
+            const bool lng = slot[t] >= 0;
+            for (uint64_t i = v->term_offsets[t]; i < v->term_offsets[t + 1]; ++i) {
+                uint32_t r = v->posting_rows[i], f = tf[i], l = v->doc_lens[r];
+                uint32_t code = 0xFFFFFFFFu;
+                if (f < kTfD && l < kLenD) {
+                    uint16_t c16 = dense_code[static_cast<size_t>(f) * kLenD + l];
+                    if (c16 != 0xFFFF) code = c16;
+                } else {
+                    auto it = sparse_code.find(key(f, l));
+                    if (it != sparse_code.end()) code = it->second;
+                }
+                if (lng) {
+                    if (code >= n_codes) {
+                        code = hm::kEscLong;
+                        ++esc_local;
+                    }
+                    packed[i] = ((r & (hm::kTile - 1)) << hm::kCodeBitsLong) | code;
+                } else {
+                    if (code >= n_codes_short) {
+                        code = esc;
+                        ++esc_local;
+                    }
+                    packed[i] = (r << cb) | code;
+                }
+            }
+        }
+        escaped += esc_local;
+    });
+    X->n_escaped = escaped;
+    // long-term tile tables
     std::vector<uint32_t> tab(long_terms.size() * (static_cast<uint64_t>(n_tiles) + 1));
     par_for(long_terms.size(), [&](int, uint64_t a, uint64_t b) {
         for (uint64_t s = a; s < b; ++s) {
@@ -330,7 +359,7 @@ void build_index(const hm_csr_view* v, hm_index* X) {
     auto& A = X->allocs;
     auto& B = X->bytes;
     hm::DevIndex& d = X->dev;
-    d.post = dev_upload(packed.data(), P, A, B);
+    d.post = dev_upload(packed.data(), P + 8, A, B);
     std::vector<uint32_t>().swap(packed);
     d.tf = dev_upload(tf.data(), P, A, B);
     std::vector<uint32_t>().swap(tf);
@@ -348,8 +377,9 @@ void build_index(const hm_csr_view* v, hm_index* X) {
     d.n_docs = N;
     d.n_tiles = n_tiles;
     d.code_bits = cb;
+    d.esc_short = esc;
     d.n_codes = n_codes;
-    d.esc = esc;
+    d.n_codes_short = n_codes_short;
     d.avgdl = v->avgdl;
     int sb = 0, eb = 0, sms = 0;
     ck(hm::search_occupancy(&sb, &eb), "occupancy");
@@ -468,6 +498,17 @@ void run_batch(hm_index* X, Workspace* w, const hm_query_batch& hb, const uint32
     a.order = w->order;
     a.counters = w->counters;
     a.exact_list = w->exact_list;
+    a.stab_stride = X->dev.n_tiles + 2;
+    const uint64_t words = static_cast<uint64_t>(X->grid_search) * hm::kMaxTerms * a.stab_stride;
+    if (w->stab_words < words) {
+        ck(cudaStreamSynchronize(w->stream), "sync");
+        if (w->stab) cudaFree(w->stab);
+        w->stab = nullptr;
+        w->stab_words = 0;
+        dalloc(w->stab, words);
+        w->stab_words = words;
+    }
+    a.stab = w->stab;
     a.out_ids = out.ids;
     a.out_scores = out.scores;
     a.out_n = out.n;
@@ -478,13 +519,27 @@ void run_batch(hm_index* X, Workspace* w, const hm_query_batch& hb, const uint32
     cudaStream_t st = w->stream;
     ck(cudaMemcpyAsync(w->w32, pin_w32, hm::kMaxCodes * sizeof(float), cudaMemcpyHostToDevice, st),
        "upload w32");
+    const bool timing = (hb.flags & HM_FLAG_TIMING) != 0;
+    if (timing && !w->ev[0])
+        for (auto& e : w->ev) ck(cudaEventCreate(&e), "event");
     ck(cudaMemsetAsync(w->counters, 0, 4 * sizeof(uint32_t), st), "memset counters");
+    if (timing) ck(cudaEventRecord(w->ev[0], st), "event");
     ck(hm::launch_plan(X->dev, a, w->order_in, st), "plan kernel");
     ck(hm::launch_lpt_sort(w->sort_tmp, w->sort_bytes, a, w->cost_sorted, w->order_in, st),
        "lpt sort");
+    if (timing) ck(cudaEventRecord(w->ev[1], st), "event");
     ck(hm::launch_search(X->dev, a, X->grid_search, st), "search kernel");
+    if (timing) ck(cudaEventRecord(w->ev[2], st), "event");
     ck(hm::launch_exact(X->dev, a, X->grid_exact, st), "exact kernel");
-    g_last_launches = 5;  // plan, cub sort (upsweep/scan/downsweep passes count as 1), search, exact, memset
+    if (timing) ck(cudaEventRecord(w->ev[3], st), "event");
+    g_last_launches = 3;  // our kernels: plan, fused search, exact (plus CUB's sort + a memset)
+}
+
+void read_timing(Workspace* w) {
+    ck(cudaEventSynchronize(w->ev[3]), "event sync");
+    ck(cudaEventElapsedTime(&g_ms_plan, w->ev[0], w->ev[1]), "elapsed");
+    ck(cudaEventElapsedTime(&g_ms_search, w->ev[1], w->ev[2]), "elapsed");
+    ck(cudaEventElapsedTime(&g_ms_exact, w->ev[2], w->ev[3]), "elapsed");
 }
 
 void validate(const hm_index* X, const hm_query_batch* b) {
@@ -592,6 +647,7 @@ int hm_search_batch(hm_index* X, const hm_query_batch* b, hm_results* out) {
             ck(cudaMemcpyAsync(rpost, w->out_post, nq * 8ull, cudaMemcpyDeviceToHost, st), "D2H");
             ck(cudaMemcpyAsync(rcnt, w->counters, 16, cudaMemcpyDeviceToHost, st), "D2H");
             ck(cudaStreamSynchronize(st), "batch");
+            if (b->flags & HM_FLAG_TIMING) read_timing(w);
             g_last_exact = rcnt[1];
             if (rcnt[3] & hm::kErrTooManyTerms)
                 throw std::invalid_argument("a query has more than 256 distinct terms");
@@ -642,6 +698,7 @@ int hm_search_batch_device(hm_index* X, const hm_query_batch* b, hm_results* out
             // pinned w32 staging is reused by the next call on this workspace:
             // make sure the async upload finished before handing it back
             ck(cudaStreamSynchronize(w->stream), "sync");
+            if (b->flags & HM_FLAG_TIMING) read_timing(w);
             cudaEventDestroy(ev);
         } catch (...) {
             cudaStreamSynchronize(w->stream);
@@ -655,6 +712,13 @@ int hm_search_batch_device(hm_index* X, const hm_query_batch* b, hm_results* out
 int hm_last_batch_stats(uint32_t* n_exact, uint32_t* n_launches) {
     if (n_exact) *n_exact = g_last_exact;
     if (n_launches) *n_launches = g_last_launches;
+    return HM_OK;
+}
+
+int hm_last_batch_timing(float* ms_plan, float* ms_search, float* ms_exact) {
+    if (ms_plan) *ms_plan = g_ms_plan;
+    if (ms_search) *ms_search = g_ms_search;
+    if (ms_exact) *ms_exact = g_ms_exact;
     return HM_OK;
 }
 

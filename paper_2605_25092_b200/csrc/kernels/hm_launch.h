@@ -28,5 +28,7 @@ cudaError_t launch_merge(uint32_t n_shards, uint32_t nq, uint32_t k, const uint6
                          uint8_t* out_skip, cudaStream_t st);
 // resident CTAs per SM of the two persistent kernels
 cudaError_t search_occupancy(int* search_blocks_per_sm, int* exact_blocks_per_sm);
+cudaError_t search_occupancy_fast(int* blocks);
+size_t search_smem_bytes();
 
 }  // namespace hm

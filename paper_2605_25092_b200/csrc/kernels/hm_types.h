@@ -1,24 +1,45 @@
 // Host-safe constants and argument structs shared by the kernels and the
 // C-ABI host code (no device intrinsics here; see hm_device.cuh).
+//
+// HBM layout of an index (built once by hm_index_create, host/hm_index.cpp):
+//   post[P+8]    u32 packed postings, term-major, rows strictly increasing:
+//                 * LONG terms (df > kLongFactor * n_tiles, with a tile table):
+//                   (tile-local row << 18) | code18   -- 14-bit row inside the
+//                   kTile-row tile, code18 < n_codes names a (tf, doc_len)
+//                   pair of the code table, code18 == kEscLong means "read tf[]
+//                   and doc_lens[]";
+//                 * SHORT terms: (global row << cb) | code_cb   (cb = min(8,
+//                   32 - row_bits)); only the n_codes_short most frequent
+//                   pairs are addressable, the all-ones code escapes.
+//                 4 B per posting; +8 words of padding for 16-B bulk copies.
+//   tf[P]        u32 raw term frequency (escapes and exact rescoring only)
+//   term_off[V+1] u64, idf[V] f64 (exact), idf32[V] f32 (selection),
+//   order_key[V] f64 (plan order), long_slot[V] i32 (-1 = short),
+//   tile_tab[n_long][n_tiles+1] u32: offset, relative to the term start, of
+//                 the first posting of every tile (long terms only).
+//   doc_lens[N] u32, doc_ids[N] u64, code_tf/code_len[kMaxCodes] u32.
 #pragma once
 #include <cstdint>
 
 namespace hm {
 
-constexpr int kThreads = 512;                 // threads per search CTA
+constexpr int kThreads = 512;                 // consumer / plain CTA threads
 constexpr int kWarps = kThreads / 32;
 constexpr int kTileShift = 14;                // selection tile: 16384 rows
 constexpr int kTile = 1 << kTileShift;
-constexpr int kExactTileShift = 13;           // exact tile: 8192 rows (fp64)
-constexpr int kExactTile = 1 << kExactTileShift;
 constexpr int kMaxTerms = 256;                // distinct terms per query
 constexpr int kCap = 2048;                    // selection candidate list
+constexpr int kPruneAt = 512;                 // prune the list beyond this
 constexpr int kSurvCap = 512;                 // survivors rescored in fp64
 constexpr int kExactCap = 1024;               // exact-kernel candidate list
-constexpr int kMaxCodes = 256;                // (tf, len) code table entries
+constexpr int kMaxCodes = 4096;               // (tf, len) code table entries
+constexpr int kLocalBits = 14;                // long-term posting: local row bits
+constexpr int kCodeBitsLong = 32 - kLocalBits;
+constexpr uint32_t kEscLong = (1u << kCodeBitsLong) - 1;
 constexpr int kMaxK = 256;
 constexpr uint32_t kNoTerm = 0xFFFFFFFFu;
 constexpr int kLongFactor = 32;               // long term: df > 32 * n_tiles
+static_assert(kLocalBits == kTileShift, "local row field must cover one tile");
 
 struct DevIndex {
     const uint32_t* post;
@@ -34,7 +55,10 @@ struct DevIndex {
     const uint32_t* code_tf;   // [kMaxCodes]
     const uint32_t* code_len;  // [kMaxCodes]
     uint32_t n_terms, n_docs, n_tiles;
-    uint32_t code_bits, n_codes, esc;
+    uint32_t code_bits;        // short-term code field width
+    uint32_t esc_short;        // all-ones short code
+    uint32_t n_codes;          // codes usable by long terms (<= kMaxCodes)
+    uint32_t n_codes_short;    // codes usable by short terms (< esc_short)
     double avgdl;
 };
 
@@ -54,9 +78,11 @@ struct BatchArgs {
     uint32_t* plan_len;        // [nq]
     uint64_t* cost;            // [nq] sum of df over the plan (LPT key)
     uint32_t* order;           // [nq] queries, most expensive first
-    uint32_t* counters;        // [0]=work cursor approx, [1]=exact list size,
+    uint32_t* counters;        // [0]=work cursor fast, [1]=exact list size,
                                // [2]=work cursor exact, [3]=error flags
     uint32_t* exact_list;      // [nq]
+    uint32_t* stab;            // per-CTA short-term tile tables
+    uint32_t stab_stride;      // words per short term (>= n_tiles + 2)
     // results (device)
     uint64_t* out_ids;
     double* out_scores;
@@ -67,5 +93,6 @@ struct BatchArgs {
 };
 
 constexpr uint32_t kErrTooManyTerms = 1u;
+constexpr uint32_t kErrNoConverge = 2u;
 
 }  // namespace hm

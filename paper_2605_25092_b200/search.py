@@ -23,6 +23,7 @@ from . import _lib
 
 HM_FLAG_FORCE_EXACT = 1
 HM_FLAG_DEBUG_NO_RESET = 2
+HM_FLAG_TIMING = 4
 NO_TERM = 0xFFFFFFFF
 MAX_K = 256
 
@@ -52,6 +53,7 @@ class Results(C.Structure):
 
 EXPORTS = ["hm_index_create", "hm_index_destroy", "hm_index_device_bytes", "hm_index_format",
            "hm_search_batch", "hm_search_batch_device", "hm_last_batch_stats",
+           "hm_last_batch_timing",
            "hm_merge_shards_device", "hm_margin", "hm_last_error"]
 
 
@@ -71,6 +73,7 @@ def lib():
     L.hm_search_batch.argtypes = [C.c_void_p, P(QueryBatch), P(Results)]
     L.hm_search_batch_device.argtypes = [C.c_void_p, P(QueryBatch), P(Results), C.c_void_p]
     L.hm_last_batch_stats.argtypes = [P(C.c_uint32), P(C.c_uint32)]
+    L.hm_last_batch_timing.argtypes = [P(C.c_float), P(C.c_float), P(C.c_float)]
     L.hm_merge_shards_device.argtypes = [C.c_uint32, C.c_uint32, C.c_uint32, C.c_void_p,
                                          C.c_void_p, C.c_void_p, C.c_void_p, C.c_double,
                                          C.c_double, P(Results), C.c_void_p]
@@ -211,6 +214,22 @@ class DeviceIndex:
         r = Results(out["ids"].data_ptr(), out["scores"].data_ptr(), out["n"].data_ptr(),
                     out["conf"].data_ptr(), out["skip"].data_ptr(), out["postings"].data_ptr())
         _check(lib().hm_search_batch_device(self._h, C.byref(qb), C.byref(r), st.cuda_stream))
+        if flags & HM_FLAG_TIMING:
+            return last_timing()
+
+
+def last_timing():
+    """(ms_plan, ms_search, ms_exact) of this thread's last HM_FLAG_TIMING batch."""
+    a, b, c = C.c_float(), C.c_float(), C.c_float()
+    lib().hm_last_batch_timing(C.byref(a), C.byref(b), C.byref(c))
+    return a.value, b.value, c.value
+
+
+def last_stats():
+    """(n_exact_fallback, n_kernel_launches) of this thread's last batch."""
+    ne, nl = C.c_uint32(), C.c_uint32()
+    lib().hm_last_batch_stats(C.byref(ne), C.byref(nl))
+    return ne.value, nl.value
 
 
 def merge_shards_device(shard_ids, shard_scores, shard_n, out, k, tau=None, tau_default=0.10,

@@ -1,0 +1,76 @@
+"""CPU: the C-ABI library loads, exports every symbol include/hm_b200.h declares,
+and fails loudly (no CPU fallback) when no GPU is present."""
+import ctypes
+import os
+import re
+
+import numpy as np
+import pytest
+
+from paper_2605_25092_b200 import _lib, search, synth
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def declared(header):
+    text = open(os.path.join(ROOT, "include", header)).read()
+    text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+    return sorted(set(re.findall(r"\b(hm_[a-z0-9_]+)\s*\(", text)))
+
+
+def test_hm_b200_exports_every_declared_symbol():
+    names = declared("hm_b200.h")
+    assert "hm_search_batch" in names and "hm_index_create" in names
+    lib = ctypes.CDLL(os.path.join(_lib.LIB_DIR, "libhm_b200.so"))
+    missing = [n for n in names if not hasattr(lib, n)]
+    assert not missing, missing
+    assert set(search.EXPORTS) <= set(names)
+
+
+def test_hm_synth_exports_every_declared_symbol():
+    names = declared("hm_synth.h")
+    lib = ctypes.CDLL(os.path.join(_lib.LIB_DIR, "libhm_synth.so"))
+    missing = [n for n in names if not hasattr(lib, n)]
+    assert not missing, missing
+
+
+def test_margin_export_matches_reference_rule():
+    assert abs(search.margin([8.74, 2.13, 1.40, 0.91, 0.83]) - 0.756) <= 1e-3
+    assert abs(search.margin([4.21, 3.97, 3.48, 3.11, 2.96]) - 0.057) <= 1e-3
+    assert search.margin([]) == 0.0 and search.margin([5.0]) == 0.0 and search.margin([0.0, 0.0]) == 0.0
+
+
+def _has_gpu():
+    try:
+        import torch
+        return torch.cuda.is_available()
+    except Exception:
+        return False
+
+
+@pytest.mark.skipif(_has_gpu(), reason="checks the no-GPU failure mode")
+def test_no_cpu_fallback_without_gpu():
+    hx = synth.HostIndex(synth.Corpus(n_records=100))
+    with pytest.raises(RuntimeError, match="no CUDA device"):
+        search.DeviceIndex.from_host(hx)
+
+
+def test_sm100a_cubin_present():
+    """The library carries sm_100a SASS (not a PTX-only or other-arch build)."""
+    import subprocess
+    out = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "--list-elf",
+                          os.path.join(_lib.LIB_DIR, "libhm_b200.so")],
+                         capture_output=True, text=True).stdout
+    assert "sm_100a" in out
+
+
+def test_k_star_and_temporal_budget_host_logic():
+    assert search.k_star(0.05, 1.4) == 3 and search.k_star(0.01, 0.5) == 10
+    assert search.k_star(0.999999, 1.0) == 1
+    for bad in [(0.0, 1.0), (1.0, 1.0), (0.05, 0.0)]:
+        with pytest.raises(ValueError):
+            search.k_star(*bad)
+    t = search.TemporalIndex(None, np.array([0, 5, 9, 9, 20], np.uint32))
+    assert t.num_partitions() == 4 and t.budget() == 3 and t.window() == (5, 20)
+    t.params.k_max_partitions = 1
+    assert t.window() == (9, 20)
