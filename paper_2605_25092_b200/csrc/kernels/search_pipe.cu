@@ -26,6 +26,8 @@ constexpr int kPipeThreads = kCons + 32;  // + 1 producer warp
 constexpr int kSlots = 6;
 constexpr int kSlotElems = 4096;          // 16 KB per slot
 constexpr int kSegs = 32;                 // segments per slot
+constexpr int kUnroll = 8;                // postings per consumer thread per step
+constexpr int kEscCap = 512;              // deferred escaped postings per tile
 
 struct SlotMeta {
     uint32_t n_seg, last;
@@ -36,7 +38,7 @@ struct SlotMeta {
 struct __align__(128) PipeSmem {
     uint32_t ring[kSlots][kSlotElems];
     float acc[kTile];
-    float w32[kMaxCodes];
+    float w32[kMaxCodes + 4];  // [kMaxCodes] = 0: impact of escaped / padded postings
     uint32_t cand_row[kCap];
     float cand_a[kCap];
     SlotMeta meta[kSlots];
@@ -51,10 +53,15 @@ struct __align__(128) PipeSmem {
     uint32_t pb[2][kMaxTerms], pe[2][kMaxTerms];
     uint32_t hist[256];
     uint32_t sel[2];
+    uint64_t esc_gidx[kEscCap];
+    uint32_t esc_row[kEscCap];
+    uint16_t esc_term[kEscCap];
     uint64_t post;
-    uint32_t q, n_long, n_short, n_c, ovf, bad, n_surv;
+    uint32_t q, n_long, n_short, n_c, ovf, bad, n_surv, n_esc;
     float L;
 };
+
+static_assert(sizeof(PipeSmem) <= 227 * 1024, "PipeSmem exceeds the 227 KB per-CTA shared memory");
 
 struct SurvView {
     double* E;
@@ -70,6 +77,89 @@ __device__ __forceinline__ float esc_w(const DevIndex& ix, uint64_t gidx, uint32
                     static_cast<double>(__ldg(ix.doc_lens + row)), ix.avgdl, k1, b);
 }
 
+// Escaped posting (its (tf, len) pair has no code): queue it for a batched
+// exact lookup after the tile's segments; when the queue is full, apply now.
+__device__ __forceinline__ void defer_escape(PipeSmem& S, const DevIndex& ix, uint32_t row,
+                                             uint64_t gidx, uint32_t term, float c, uint32_t base,
+                                             double k1, double b) {
+    const uint32_t x = atomicAdd(&S.n_esc, 1u);
+    if (x < kEscCap) {
+        S.esc_row[x] = row;
+        S.esc_gidx[x] = gidx;
+        S.esc_term[x] = static_cast<uint16_t>(term);
+    } else {
+        atomicAdd(&S.acc[row - base], c * esc_w(ix, gidx, row, k1, b));
+    }
+}
+
+// One long-term segment [lo, hi) of a ring slot.  Warp w takes 256
+// consecutive postings (8 per lane, lane-interleaved so consecutive lanes hit
+// nearly consecutive rows: conflict-free accumulator banks); warps past the
+// segment end skip.  Rows of one term are distinct, so plain RMW is race-free
+// (terms are separated by a named barrier).  Escaped codes (and the padding
+// entry kMaxCodes) read a zero impact; escapes are then queued.
+template <bool CLIP>
+__device__ __forceinline__ void accum_long(PipeSmem& S, const DevIndex& ix, const uint32_t* src,
+                                           uint32_t lo, uint32_t hi, uint64_t goff, float c,
+                                           uint32_t term, uint32_t base, uint32_t rlo, uint32_t rn,
+                                           double k1, double b) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const uint32_t n_codes = ix.n_codes;
+    for (uint32_t wb = lo + warp * (kUnroll * 32); wb < hi; wb += kUnroll * kCons) {
+        uint32_t p[kUnroll], loc[kUnroll];
+        float w[kUnroll], av[kUnroll];
+        uint32_t cmax = 0;
+#pragma unroll
+        for (int u = 0; u < kUnroll; ++u) {
+            const uint32_t e = wb + u * 32 + lane;
+            p[u] = e < hi ? src[e] : 0u;
+        }
+#pragma unroll
+        for (int u = 0; u < kUnroll; ++u) {
+            loc[u] = p[u] >> kCodeBitsLong;
+            const uint32_t code = p[u] & kEscLong;
+            cmax = max(cmax, code);
+            w[u] = S.w32[min(code, static_cast<uint32_t>(kMaxCodes))];
+            if (CLIP && loc[u] - rlo >= rn) w[u] = 0.f;
+        }
+#pragma unroll
+        for (int u = 0; u < kUnroll; ++u) av[u] = S.acc[loc[u]];
+#pragma unroll
+        for (int u = 0; u < kUnroll; ++u)
+            if (wb + u * 32 + lane < hi) S.acc[loc[u]] = __fmaf_rn(c, w[u], av[u]);
+        if (__any_sync(0xffffffffu, cmax >= n_codes)) {
+#pragma unroll
+            for (int u = 0; u < kUnroll; ++u) {
+                const uint32_t e = wb + u * 32 + lane;
+                if (e < hi && (p[u] & kEscLong) >= n_codes && (!CLIP || loc[u] - rlo < rn))
+                    defer_escape(S, ix, base + loc[u], goff + e, term, c, base, k1, b);
+            }
+        }
+    }
+}
+
+// Short-term segments: same warp mapping, shared-memory atomics (several
+// short terms may share a slot and need no barrier between them).
+__device__ __forceinline__ void accum_short(PipeSmem& S, const DevIndex& ix, const uint32_t* src,
+                                            uint32_t lo, uint32_t hi, uint64_t goff, float c,
+                                            uint32_t term, uint32_t base, double k1, double b) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const uint32_t cb = ix.code_bits, ncs = ix.n_codes_short, escs = ix.esc_short;
+    for (uint32_t wb = lo + warp * (kUnroll * 32); wb < hi; wb += kUnroll * kCons) {
+#pragma unroll
+        for (int u = 0; u < kUnroll; ++u) {
+            const uint32_t e = wb + u * 32 + lane;
+            if (e < hi) {
+                const uint32_t p = src[e];
+                const uint32_t row = p >> cb;
+                const uint32_t code = p & escs;
+                if (code < ncs) atomicAdd(&S.acc[row - base], c * S.w32[code]);
+                else defer_escape(S, ix, row, goff + e, term, c, base, k1, b);
+            }
+        }
+    }
+}
+
 __global__ void __launch_bounds__(kPipeThreads, 1) search_pipe_kernel(DevIndex ix, BatchArgs a) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
     PipeSmem& S = *reinterpret_cast<PipeSmem*>(smem_raw);
@@ -83,7 +173,7 @@ __global__ void __launch_bounds__(kPipeThreads, 1) search_pipe_kernel(DevIndex i
     uint32_t* stab = a.stab + static_cast<uint64_t>(blockIdx.x) * kMaxTerms * stride;
 
     for (int i = tid; i < kTile; i += kPipeThreads) S.acc[i] = 0.f;
-    for (int i = tid; i < kMaxCodes; i += kPipeThreads) S.w32[i] = a.w32[i];
+    for (int i = tid; i < kMaxCodes + 4; i += kPipeThreads) S.w32[i] = i < kMaxCodes ? a.w32[i] : 0.f;
     if (tid == 0) {
         for (int s = 0; s < kSlots; ++s) {
             mbar_init(&S.full[s], 1);
@@ -92,6 +182,7 @@ __global__ void __launch_bounds__(kPipeThreads, 1) search_pipe_kernel(DevIndex i
         mbar_init_fence();
         S.n_c = 0;
         S.L = 0.f;
+        S.n_esc = 0;
     }
     uint32_t ring_use = 0;  // slot uses so far (identical sequence in both roles)
 
@@ -311,6 +402,7 @@ __global__ void __launch_bounds__(kPipeThreads, 1) search_pipe_kernel(DevIndex i
             const uint32_t R0 = max(base, row_lo);
             const uint32_t R1 = min(base + kTile, row_hi);
             const uint32_t rlo = R0 - base, rn = R1 - R0;
+            const bool clip = rn != kTile;
             // ---- drain this tile's ring slots
             int cur = -1;
             bool in_short = false;
@@ -330,36 +422,14 @@ __global__ void __launch_bounds__(kPipeThreads, 1) search_pipe_kernel(DevIndex i
                             if (cur != -1) csync();
                             cur = static_cast<int>(i);
                         }
-                        const uint32_t g0 = lo >> 2, g1 = (hi + 3) >> 2;
-                        for (uint32_t v = g0 + tid; v < g1; v += kCons) {
-                            const uint4 w4 = *reinterpret_cast<const uint4*>(src + 4 * v);
-                            const uint32_t ps[4] = {w4.x, w4.y, w4.z, w4.w};
-#pragma unroll
-                            for (int u = 0; u < 4; ++u) {
-                                const uint32_t e = 4 * v + u;
-                                const uint32_t p = ps[u];
-                                const uint32_t local = p >> kCodeBitsLong;
-                                if (e >= lo && e < hi && local - rlo < rn) {
-                                    const uint32_t code = p & kEscLong;
-                                    const float w = code < ix.n_codes ? S.w32[code]
-                                                                      : esc_w(ix, goff + e, base + local, k1, bb);
-                                    S.acc[local] = __fmaf_rn(c, w, S.acc[local]);
-                                }
-                            }
-                        }
+                        if (clip) accum_long<true>(S, ix, src, lo, hi, goff, c, i, base, rlo, rn, k1, bb);
+                        else accum_long<false>(S, ix, src, lo, hi, goff, c, i, base, rlo, rn, k1, bb);
                     } else {
                         if (!in_short) {
                             csync();
                             in_short = true;
                         }
-                        for (uint32_t e = lo + tid; e < hi; e += kCons) {
-                            const uint32_t p = src[e];
-                            const uint32_t row = p >> cb;
-                            const uint32_t code = p & ix.esc_short;
-                            const float w = code < ix.n_codes_short ? S.w32[code]
-                                                                    : esc_w(ix, goff + e, row, k1, bb);
-                            atomicAdd(&S.acc[row - base], c * w);
-                        }
+                        accum_short(S, ix, src, lo, hi, goff, c, i, base, k1, bb);
                     }
                 }
                 __syncwarp();
@@ -369,6 +439,16 @@ __global__ void __launch_bounds__(kPipeThreads, 1) search_pipe_kernel(DevIndex i
             }
             if (to_exact) continue;  // drain the remaining tiles' slots only
             csync();
+            if (S.n_esc) {  // deferred escaped postings: exact (tf, len) lookups, batched
+                const uint32_t ne = min(S.n_esc, static_cast<uint32_t>(kEscCap));
+                for (uint32_t x = tid; x < ne; x += kCons) {
+                    const uint32_t row = S.esc_row[x];
+                    const float w = esc_w(ix, S.esc_gidx[x], row, k1, bb);
+                    atomicAdd(&S.acc[row - base], S.t_c32[S.esc_term[x]] * w);
+                }
+                csync();
+                if (tid == 0) S.n_esc = 0;
+            }
             // ---- scan, with overflow recovery by re-accumulating from HBM/L2
             for (int attempt = 0;; ++attempt) {
                 {
@@ -382,10 +462,11 @@ __global__ void __launch_bounds__(kPipeThreads, 1) search_pipe_kernel(DevIndex i
                             x = acc4[v];
                             acc4[v] = make_float4(0.f, 0.f, 0.f, 0.f);
                         }
-                        const bool q0 = x.x > 0.f && x.x >= t_emit, q1 = x.y > 0.f && x.y >= t_emit;
-                        const bool q2 = x.z > 0.f && x.z >= t_emit, q3 = x.w > 0.f && x.w >= t_emit;
-                        const uint32_t cnt = q0 + q1 + q2 + q3;
-                        if (__ballot_sync(0xffffffffu, cnt != 0)) {
+                        const float mx = fmaxf(fmaxf(x.x, x.y), fmaxf(x.z, x.w));
+                        if (__ballot_sync(0xffffffffu, mx > 0.f && mx >= t_emit)) {
+                            const bool q0 = x.x > 0.f && x.x >= t_emit, q1 = x.y > 0.f && x.y >= t_emit;
+                            const bool q2 = x.z > 0.f && x.z >= t_emit, q3 = x.w > 0.f && x.w >= t_emit;
+                            const uint32_t cnt = q0 + q1 + q2 + q3;
                             const uint32_t incl = warp_incl_scan(cnt);
                             const uint32_t tot = __shfl_sync(0xffffffffu, incl, 31);
                             uint32_t bse = 0;

@@ -1,0 +1,126 @@
+"""Doc-sharded multi-GPU search: one process per GPU.
+
+The corpus rows are split into G contiguous ranges; rank g holds the sub-CSR
+of rows [lo_g, hi_g) with rows renumbered from 0 and the GLOBAL statistics
+(idf, avgdl, order keys) -- the same device as the reference's SharedStats
+(proj/include/hybrid/csr_index.hpp:28-35) that makes partition-local scoring
+bit-identical to flat scoring (src/temporal_index.cpp:136-142).  Each rank
+computes an exact local top-k (ids are global DocIds), the k candidates per
+query are exchanged with one all-gather (NCCL over NVLink/NVSwitch; gloo in the
+CPU tests), and every rank merges the G*k candidates on device with
+hm_merge_shards_device (score desc, DocId asc) and recomputes the Margin
+confidence / skip decision on the merged list.  Every doc lives on exactly one
+shard, so the merged list equals the single-GPU and CPU answer.
+"""
+import numpy as np
+
+from . import search
+
+
+def shard_bounds(n_docs, world):
+    """Contiguous, balanced row ranges [lo, hi) for `world` shards."""
+    return [(n_docs * g // world, n_docs * (g + 1) // world) for g in range(world)]
+
+
+def shard_arrays(term_offsets, posting_rows, posting_tf, doc_lens, doc_ids, lo, hi):
+    """Sub-CSR of rows [lo, hi): rows renumbered from 0, term ids unchanged."""
+    rows = np.asarray(posting_rows)
+    mask = (rows >= lo) & (rows < hi)
+    cm = np.zeros(len(rows) + 1, np.int64)
+    np.cumsum(mask, out=cm[1:])
+    off = cm[np.asarray(term_offsets, np.int64)].astype(np.uint64)
+    return dict(term_offsets=off, posting_rows=(rows[mask] - lo).astype(np.uint32),
+                posting_tf=np.asarray(posting_tf)[mask].astype(np.uint32),
+                doc_lens=np.asarray(doc_lens)[lo:hi], doc_ids=np.asarray(doc_ids)[lo:hi])
+
+
+def shard_host_index(hx, rank, world):
+    """Shard `rank` of a synth.HostIndex, keeping the global statistics."""
+    lo, hi = shard_bounds(hx.n_docs, world)[rank]
+    d = shard_arrays(hx.term_offsets, hx.posting_rows, hx.posting_tf, hx.doc_lens, hx.doc_ids,
+                     lo, hi)
+    d.update(idf=hx.idf, order_key=hx.order_key, avgdl=hx.avgdl)
+    return d
+
+
+def gather_and_merge(local, k, world, group=None, tau=None, tau_default=0.10,
+                     epsilon_guard=1e-9):
+    """All-gather per-shard top-k (torch tensors on this rank's device) and merge.
+
+    local: dict(ids[nq,k] int64, scores[nq,k] f64, n[nq] int32) on the device.
+    Returns the merged dict (ids, scores, n, conf, skip) on the device.
+    """
+    import torch
+    import torch.distributed as dist
+    nq = local["n"].shape[0]
+    dev = local["n"].device
+    if world > 1:
+        g_ids = torch.empty((world, nq, k), dtype=torch.int64, device=dev)
+        g_sc = torch.empty((world, nq, k), dtype=torch.float64, device=dev)
+        g_n = torch.empty((world, nq), dtype=torch.int32, device=dev)
+        dist.all_gather_into_tensor(g_ids, local["ids"].contiguous(), group=group)
+        dist.all_gather_into_tensor(g_sc, local["scores"].contiguous(), group=group)
+        dist.all_gather_into_tensor(g_n, local["n"].contiguous(), group=group)
+    else:
+        g_ids, g_sc, g_n = local["ids"][None], local["scores"][None], local["n"][None]
+    out = dict(ids=torch.zeros((nq, k), dtype=torch.int64, device=dev),
+               scores=torch.zeros((nq, k), dtype=torch.float64, device=dev),
+               n=torch.zeros(nq, dtype=torch.int32, device=dev),
+               conf=torch.zeros(nq, dtype=torch.float64, device=dev),
+               skip=torch.zeros(nq, dtype=torch.uint8, device=dev))
+    search.merge_shards_device(g_ids.contiguous(), g_sc.contiguous(), g_n.contiguous(), out, k,
+                               tau=tau, tau_default=tau_default, epsilon_guard=epsilon_guard)
+    return out
+
+
+def merge_host(shard_ids, shard_scores, shard_n, k, tau_default=0.10, eps=1e-9):
+    """Host restatement of the merge (used by the gloo CPU tests of the exchange
+    protocol; the product merge is merge_kernel on the device)."""
+    G, nq = shard_n.shape
+    ids = np.zeros((nq, k), np.uint64)
+    sc = np.zeros((nq, k), np.float64)
+    n = np.zeros(nq, np.uint32)
+    conf = np.zeros(nq)
+    for q in range(nq):
+        cand = [(float(shard_scores[g, q, r]), int(shard_ids[g, q, r]))
+                for g in range(G) for r in range(int(shard_n[g, q]))]
+        cand.sort(key=lambda x: (-x[0], x[1]))
+        cand = [c for c in cand if c[0] > 0][:k]
+        n[q] = len(cand)
+        for r, (s, d) in enumerate(cand):
+            ids[q, r] = d
+            sc[q, r] = s
+        conf[q] = search.margin(sc[q, :n[q]], eps) if n[q] else 0.0
+    return ids, sc, n, conf, (conf >= tau_default).astype(np.uint8)
+
+
+class ShardedIndex:
+    """This rank's shard on its GPU plus the exchange; the public multi-GPU API."""
+
+    def __init__(self, hx, rank, world, device=0):
+        d = shard_host_index(hx, rank, world)
+        self.rank, self.world = rank, world
+        self.dev = search.DeviceIndex(d["term_offsets"], d["posting_rows"], d["idf"],
+                                      d["order_key"], d["doc_lens"], d["doc_ids"], d["avgdl"],
+                                      posting_tf=d["posting_tf"], device=device)
+
+    def search_device(self, q_off, q_tid, k, local_out, **kw):
+        """Device-resident batch: local exact top-k, all-gather, merge."""
+        self.dev.search_batch_device(q_off, q_tid, local_out, k, **kw)
+        return gather_and_merge(local_out, k, self.world, tau_default=kw.get("tau_default", 0.10))
+
+    def search_batch(self, q_off, q_tid, k, **kw):
+        """Host buffers in, host results out (H2D, search, all-gather, merge, D2H)."""
+        import torch
+        dev = torch.device("cuda", self.dev.device)
+        d_off = torch.from_numpy(np.ascontiguousarray(q_off, np.uint32).view(np.int32)).to(dev)
+        d_tid = torch.from_numpy(np.ascontiguousarray(q_tid, np.uint32).view(np.int32)).to(dev)
+        nq = len(q_off) - 1
+        loc = dict(ids=torch.zeros((nq, k), dtype=torch.int64, device=dev),
+                   scores=torch.zeros((nq, k), dtype=torch.float64, device=dev),
+                   n=torch.zeros(nq, dtype=torch.int32, device=dev),
+                   conf=torch.zeros(nq, dtype=torch.float64, device=dev),
+                   skip=torch.zeros(nq, dtype=torch.uint8, device=dev),
+                   postings=torch.zeros(nq, dtype=torch.int64, device=dev))
+        out = self.search_device(d_off, d_tid, k, loc, **kw)
+        return {key: v.cpu().numpy() for key, v in out.items()}

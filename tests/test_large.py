@@ -1,0 +1,55 @@
+"""GPU parity at BASELINE.json's full sizes (configs 2 and 4: 8,841,823 docs).
+
+The CPU oracle is too slow for every query at 8.8M docs, so: a sample of
+queries is compared bit-for-bit against the restatement, every query is
+checked against size-independent properties (ranking order, unique ids,
+postings_touched = sum of df, Margin consistency, skip rule), and a subset is
+re-run on the exact fp64 kernel which must agree exactly.
+"""
+import numpy as np
+import pytest
+
+from _util import check_batch, restate, search, synth_setup
+
+pytestmark = [pytest.mark.gpu, pytest.mark.slow]
+
+
+def properties(got, hx, tids, k, tau=0.10):
+    df = np.diff(hx.term_offsets.astype(np.int64))
+    for i in range(len(tids)):
+        n = int(got["n"][i])
+        assert n <= k
+        s = got["scores"][i, :n]
+        ids = got["ids"][i, :n]
+        assert (s > 0).all()
+        assert all((s[j] > s[j + 1]) or (s[j] == s[j + 1] and ids[j] < ids[j + 1]) for j in range(n - 1))
+        assert len(set(ids.tolist())) == n
+        assert got["postings"][i] == df[np.unique(tids[i][tids[i] != search.NO_TERM])].sum()
+        conf = restate.margin(s)
+        assert got["conf"][i] == conf and bool(got["skip"][i]) == (conf >= tau)
+
+
+@pytest.mark.parametrize("cfg", ["c2", "c4"])
+def test_full_size_configs(gpu, cfg):
+    if cfg == "c2":
+        _, q, hx, tids = synth_setup(8841823, 1000000, 20, 60, 10000)
+        k, sample = 10, range(0, 10000, 400)
+    else:
+        _, q, hx, tids = synth_setup(8841823, 1000000, 40, 80, 4096, 24, 32)
+        k, sample = 100, range(0, 4096, 512)
+    dev = search.DeviceIndex.from_host(hx)
+    got = dev.search_lists(tids, k)
+    properties(got, hx, tids, k)
+    orc = restate.OracleIndex.from_host(hx)
+    sub = list(sample)
+    ids, sc, n, post = orc.topk([tids[i] for i in sub], k)
+    sub_got = {key: got[key][sub] for key in ("ids", "scores", "n", "conf", "skip", "postings")}
+    check_batch(sub_got, ids, sc, n, post, what=cfg)
+    # nDCG@10 of the sample equal (exponential gain, gold qrels)
+    for j, i in enumerate(sub):
+        a = restate.ndcg(got["ids"][i, :got["n"][i]], {int(q.gold[i]): 1}, 10)
+        b = restate.ndcg(ids[j, :n[j]], {int(q.gold[i]): 1}, 10)
+        assert abs(a - b) <= 2e-4
+    ex = dev.search_lists([tids[i] for i in sub[:6]], k, flags=search.HM_FLAG_FORCE_EXACT)
+    for key in ("ids", "scores", "n", "conf", "skip"):
+        assert (ex[key] == sub_got[key][:6]).all(), key
