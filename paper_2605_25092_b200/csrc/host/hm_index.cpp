@@ -276,7 +276,8 @@ void build_index(const hm_csr_view* v, hm_index* X) {
     });
     // code table: the kMaxCodes most frequent pairs; short-term postings can
     // only address the first esc_short of them (their code field is cb bits)
-    const uint32_t n_codes = static_cast<uint32_t>(std::min<size_t>(pairs.size(), hm::kMaxCodes));
+    // (code kCodeMask is reserved: a long escape masked to 12 bits lands on it, and its impact is 0)
+    const uint32_t n_codes = static_cast<uint32_t>(std::min<size_t>(pairs.size(), hm::kCodeMask));
     const uint32_t n_codes_short = std::min(n_codes, esc);
     X->n_codes = n_codes;
     X->code_tf.assign(hm::kMaxCodes, 0);
@@ -337,20 +338,32 @@ void build_index(const hm_csr_view* v, hm_index* X) {
         escaped += esc_local;
     });
     X->n_escaped = escaped;
-    // long-term tile tables
-    std::vector<uint32_t> tab(long_terms.size() * (static_cast<uint64_t>(n_tiles) + 1));
+    std::vector<uint8_t> long_esc(std::max<size_t>(long_terms.size(), 1), 0);
+    par_for(long_terms.size(), [&](int, uint64_t a, uint64_t b) {
+        for (uint64_t s = a; s < b; ++s) {
+            uint32_t t = long_terms[s];
+            for (uint64_t i = v->term_offsets[t]; i < v->term_offsets[t + 1]; ++i)
+                if ((packed[i] & hm::kEscLong) == hm::kEscLong) {
+                    long_esc[s] = 1;
+                    break;
+                }
+        }
+    });
+    // long-term sub-tile tables (1024-row granularity; tile j starts at 16*j)
+    const uint64_t n_sub = static_cast<uint64_t>(n_tiles) * hm::kSubPerTile;
+    std::vector<uint32_t> tab(long_terms.size() * (n_sub + 1));
     par_for(long_terms.size(), [&](int, uint64_t a, uint64_t b) {
         for (uint64_t s = a; s < b; ++s) {
             uint32_t t = long_terms[s];
             uint64_t lo = v->term_offsets[t], hi = v->term_offsets[t + 1];
-            uint32_t* row = tab.data() + s * (n_tiles + 1);
+            uint32_t* row = tab.data() + s * (n_sub + 1);
             uint64_t i = lo;
-            for (uint32_t j = 0; j <= n_tiles; ++j) {
-                uint64_t lim = static_cast<uint64_t>(j) * hm::kTile;
+            for (uint64_t j = 0; j <= n_sub; ++j) {
+                uint64_t lim = j << hm::kSubShift;
                 while (i < hi && v->posting_rows[i] < lim) ++i;
                 row[j] = static_cast<uint32_t>(i - lo);
             }
-            row[n_tiles] = static_cast<uint32_t>(hi - lo);
+            row[n_sub] = static_cast<uint32_t>(hi - lo);
         }
     });
     std::vector<float> idf32(V);
@@ -369,6 +382,7 @@ void build_index(const hm_csr_view* v, hm_index* X) {
     d.order_key = dev_upload(v->term_order_keys, V, A, B);
     d.long_slot = dev_upload(slot.data(), V, A, B);
     d.tile_tab = dev_upload(tab.data(), tab.size(), A, B);
+    d.long_esc = dev_upload(long_esc.data(), long_esc.size(), A, B);
     d.doc_lens = dev_upload(v->doc_lens, N, A, B);
     d.doc_ids = dev_upload(v->doc_ids, N, A, B);
     d.code_tf = dev_upload(X->code_tf.data(), hm::kMaxCodes, A, B);
@@ -499,7 +513,7 @@ void run_batch(hm_index* X, Workspace* w, const hm_query_batch& hb, const uint32
     a.counters = w->counters;
     a.exact_list = w->exact_list;
     a.stab_stride = X->dev.n_tiles + 2;
-    const uint64_t words = static_cast<uint64_t>(X->grid_search) * hm::kMaxTerms * a.stab_stride;
+    const uint64_t words = 2ull * X->grid_search * hm::kMaxTerms * a.stab_stride;  // up to 2 CTAs per SM
     if (w->stab_words < words) {
         ck(cudaStreamSynchronize(w->stream), "sync");
         if (w->stab) cudaFree(w->stab);

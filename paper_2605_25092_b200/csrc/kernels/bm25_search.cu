@@ -179,8 +179,8 @@ __global__ void __launch_bounds__(kExactThreads, 1) exact_kernel(DevIndex ix, Ba
                 if (tid < static_cast<int>(m)) {
                     if (S.t_slot[tid] >= 0) {
                         const uint32_t* tb = tile_row(ix, S.t_slot[tid]);
-                        S.t_cur0[tid] = S.t_start[tid] + __ldg(tb + j);
-                        S.t_seg[tid] = S.t_start[tid] + __ldg(tb + j + 1);
+                        S.t_cur0[tid] = S.t_start[tid] + __ldg(tb + j * kSubPerTile);
+                        S.t_seg[tid] = S.t_start[tid] + __ldg(tb + (j + 1) * kSubPerTile);
                     } else {
                         const uint64_t c = S.t_cur[tid];
                         S.t_cur0[tid] = c;

@@ -61,22 +61,23 @@ __device__ __forceinline__ uint64_t lower_bound_row(const uint32_t* post, uint64
 }
 
 __device__ __forceinline__ const uint32_t* tile_row(const DevIndex& ix, int32_t slot) {
-    return ix.tile_tab + static_cast<uint64_t>(slot) * (ix.n_tiles + 1);
+    return ix.tile_tab + static_cast<uint64_t>(slot) * (static_cast<uint64_t>(ix.n_tiles) * kSubPerTile + 1);
 }
 
 // First posting of term [s0, s1) whose row is >= row (any format).
 __device__ __forceinline__ uint64_t first_at_or_after(const DevIndex& ix, int32_t slot, uint64_t s0,
                                                       uint64_t s1, uint32_t row) {
     if (slot < 0) return lower_bound_row(ix.post, s0, s1, row, ix.code_bits);
-    uint32_t j = row >> kTileShift;
-    if (j >= ix.n_tiles) return s1;
+    uint32_t j = row >> kSubShift;
+    if ((row >> kTileShift) >= ix.n_tiles) return s1;
     const uint32_t* tb = tile_row(ix, slot);
     uint64_t lo = s0 + __ldg(tb + j), hi = s0 + __ldg(tb + j + 1);
     return lower_bound_packed(ix.post, lo, hi, (row & (kTile - 1)) << kCodeBitsLong);
 }
 
-// Locate `row` in a term's postings and decode its (tf, doc_len).
-// Returns false when the document does not contain the term.
+// Locate `row` in a term's postings and decode its (tf, doc_len).  s0 is the
+// TERM START (long terms index their sub-tile table from it), s1 the end of
+// the searched range.  Returns false when the document lacks the term.
 __device__ __forceinline__ bool find_posting(const DevIndex& ix, int32_t slot, uint64_t s0,
                                              uint64_t s1, uint32_t row, const uint32_t* code_tf,
                                              const uint32_t* code_len, double* tf, double* dl) {
@@ -93,7 +94,7 @@ __device__ __forceinline__ bool find_posting(const DevIndex& ix, int32_t slot, u
         code = p & ix.esc_short;
         esc = code >= ix.n_codes_short;
     } else {
-        uint32_t j = row >> kTileShift;
+        uint32_t j = row >> kSubShift;
         const uint32_t* tb = tile_row(ix, slot);
         uint64_t lo = s0 + __ldg(tb + j), hi = s0 + __ldg(tb + j + 1);
         uint32_t local = row & (kTile - 1);

@@ -15,8 +15,9 @@
 //   tf[P]        u32 raw term frequency (escapes and exact rescoring only)
 //   term_off[V+1] u64, idf[V] f64 (exact), idf32[V] f32 (selection),
 //   order_key[V] f64 (plan order), long_slot[V] i32 (-1 = short),
-//   tile_tab[n_long][n_tiles+1] u32: offset, relative to the term start, of
-//                 the first posting of every tile (long terms only).
+//   tile_tab[n_long][16*n_tiles+1] u32: offset, relative to the term start,
+//                 of the first posting of every 1024-row sub-tile (long terms
+//                 only); tile j starts at entry 16*j.
 //   doc_lens[N] u32, doc_ids[N] u64, code_tf/code_len[kMaxCodes] u32.
 #pragma once
 #include <cstdint>
@@ -33,6 +34,9 @@ constexpr int kPruneAt = 512;                 // prune the list beyond this
 constexpr int kSurvCap = 512;                 // survivors rescored in fp64
 constexpr int kExactCap = 1024;               // exact-kernel candidate list
 constexpr int kMaxCodes = 4096;               // (tf, len) code table entries
+constexpr uint32_t kCodeMask = kMaxCodes - 1; // long codes < kCodeMask; w32[kCodeMask] = 0
+constexpr int kSubShift = 10;                 // sub-tile (one consumer warp's rows): 1024
+constexpr int kSubPerTile = 1 << (14 - kSubShift);
 constexpr int kLocalBits = 14;                // long-term posting: local row bits
 constexpr int kCodeBitsLong = 32 - kLocalBits;
 constexpr uint32_t kEscLong = (1u << kCodeBitsLong) - 1;
@@ -49,6 +53,7 @@ struct DevIndex {
     const float* idf32;
     const double* order_key;
     const int32_t* long_slot;
+    const uint8_t* long_esc;   // [n_long] 1 if the long term has escaped postings
     const uint32_t* tile_tab;
     const uint32_t* doc_lens;
     const uint64_t* doc_ids;
@@ -57,7 +62,7 @@ struct DevIndex {
     uint32_t n_terms, n_docs, n_tiles;
     uint32_t code_bits;        // short-term code field width
     uint32_t esc_short;        // all-ones short code
-    uint32_t n_codes;          // codes usable by long terms (<= kMaxCodes)
+    uint32_t n_codes;          // codes usable by long terms (< kMaxCodes)
     uint32_t n_codes_short;    // codes usable by short terms (< esc_short)
     double avgdl;
 };

@@ -1,0 +1,124 @@
+// Test driver for the C++ drop-in (paper_2605_25092_b200/csrc/dropin/hybrid_b200.cpp).
+// Linked with the reference's remaining objects (tokenizer, porter, ... but NOT
+// csr_index.o / temporal_index.o) exactly as a maintainer would link the
+// drop-in, it executes a line protocol on stdin and prints results; the pytest
+// side (tests/test_dropin.py) computes the same calls on the unmodified
+// reference library and compares bit patterns.
+#include <cstdio>
+#include <iostream>
+#include <sstream>
+#include <string>
+#include <vector>
+
+#include "hybrid/csr_index.hpp"
+#include "hybrid/temporal_index.hpp"
+
+using namespace hybrid;
+
+static std::string hexd(double v) {
+    char buf[64];
+    std::snprintf(buf, sizeof buf, "%a", v);
+    return buf;
+}
+
+static void print_list(const RankedList& r, const std::string& extra) {
+    std::cout << "R " << r.entries.size() << extra;
+    for (const auto& [id, s] : r.entries) std::cout << ' ' << id << ':' << hexd(s);
+    std::cout << '\n';
+}
+
+int main() {
+    std::ios::sync_with_stdio(false);
+    std::vector<std::pair<DocId, std::string>> docs;
+    std::vector<MemoryRecord> recs;
+    CsrIndex idx;
+    TemporalIndex tidx;
+    std::string line;
+    while (std::getline(std::cin, line)) {
+        std::istringstream in(line);
+        std::string cmd;
+        in >> cmd;
+        try {
+            if (cmd == "DOCS") {
+                std::size_t n;
+                in >> n;
+                docs.clear();
+                for (std::size_t i = 0; i < n; ++i) {
+                    std::getline(std::cin, line);
+                    auto tab = line.find('\t');
+                    docs.emplace_back(std::stoull(line.substr(0, tab)), line.substr(tab + 1));
+                }
+            } else if (cmd == "INDEX") {
+                int mode;
+                double k1, b;
+                in >> mode >> k1 >> b;
+                idx = build_index(docs, static_cast<TokenizerMode>(mode), 50000, Bm25Params{k1, b});
+                std::cout << "OK " << idx.num_docs() << ' ' << idx.num_postings() << '\n';
+            } else if (cmd == "QUERY") {
+                std::size_t k;
+                double k1, b;
+                int ms;
+                in >> k >> k1 >> b >> ms;
+                std::vector<std::string> q;
+                for (std::string t; in >> t;) q.push_back(t);
+                SearchStats st;
+                st.postings_touched = 7;  // stats accumulate (csr_index.cpp:102)
+                RankedList r = ms ? idx.bm25_topk_maxscore(q, k, Bm25Params{k1, b}, &st)
+                                  : idx.bm25_topk(q, k, Bm25Params{k1, b}, &st);
+                print_list(r, " " + std::to_string(st.postings_touched - 7));
+            } else if (cmd == "TERMSCORE") {
+                std::uint32_t t;
+                std::uint64_t i;
+                in >> t >> i;
+                std::cout << "V " << hexd(idx.bm25_term_score(t, i, Bm25Params{})) << '\n';
+            } else if (cmd == "UB") {
+                std::vector<std::string> q;
+                for (std::string t; in >> t;) q.push_back(t);
+                std::cout << "V " << hexd(idx.query_upper_bound(q)) << '\n';
+            } else if (cmd == "RECORDS") {
+                std::size_t n;
+                in >> n;
+                recs.clear();
+                for (std::size_t i = 0; i < n; ++i) {
+                    std::getline(std::cin, line);
+                    std::istringstream r(line);
+                    MemoryRecord m;
+                    std::string rest;
+                    r >> m.id >> m.ts_ms;
+                    std::getline(r, rest);
+                    m.text = rest.empty() ? rest : rest.substr(1);
+                    recs.push_back(std::move(m));
+                }
+            } else if (cmd == "TEMPORAL") {
+                TemporalParams tp;
+                int mode;
+                in >> tp.window_ms >> tp.epsilon >> tp.lambda_hat >> tp.k_max_partitions >> mode;
+                tidx = build_temporal_index(recs, tp, static_cast<TokenizerMode>(mode));
+                std::cout << "OK " << tidx.num_partitions() << '\n';
+            } else if (cmd == "TQUERY") {
+                std::size_t k;
+                int ub;
+                in >> k >> ub;
+                std::vector<std::string> q;
+                for (std::string t; in >> t;) q.push_back(t);
+                TemporalStats st;
+                RankedList r = tidx.topk(q, k, Bm25Params{}, &st, ub != 0);
+                print_list(r, " " + std::to_string(st.partitions_searched));
+            } else if (cmd == "KSTAR") {
+                double e, l;
+                in >> e >> l;
+                std::cout << "V " << k_star(e, l) << '\n';
+            } else {
+                std::cout << "ERR unknown " << cmd << '\n';
+            }
+        } catch (const std::invalid_argument& e) {
+            std::cout << "THROW invalid_argument " << e.what() << '\n';
+        } catch (const std::out_of_range& e) {
+            std::cout << "THROW out_of_range " << e.what() << '\n';
+        } catch (const std::runtime_error& e) {
+            std::cout << "THROW runtime_error " << e.what() << '\n';
+        }
+        std::cout.flush();
+    }
+    return 0;
+}

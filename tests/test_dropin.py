@@ -1,0 +1,95 @@
+"""The C++ drop-in (csrc/dropin/hybrid_b200.cpp compiled against the
+reference's own headers, linked in place of csr_index.o/temporal_index.o)
+against the unmodified reference library, call for call: the reference's
+test_csr.cpp / test_temporal.cpp shapes through hybrid::CsrIndex and
+hybrid::TemporalIndex.  Driver: tests/cpp/dropin_driver.cpp."""
+import os
+import subprocess
+
+import numpy as np
+import pytest
+
+from _util import random_instance, ref, toy_docs
+
+DRIVER = os.path.join(os.path.dirname(os.path.abspath(__file__)), "cpp", "bin", "dropin_driver")
+pytestmark = [pytest.mark.gpu,
+              pytest.mark.skipif(not os.path.exists(DRIVER), reason="drop-in driver not built")]
+
+
+class Driver:
+    def __init__(self):
+        self.p = subprocess.Popen([DRIVER], stdin=subprocess.PIPE, stdout=subprocess.PIPE, text=True)
+
+    def send(self, lines, expect=1):
+        self.p.stdin.write("".join(l + "\n" for l in lines))
+        self.p.stdin.flush()
+        return [self.p.stdout.readline().strip() for _ in range(expect)]
+
+    def close(self):
+        self.p.stdin.close()
+        self.p.wait(timeout=30)
+
+
+def parse(line):
+    parts = line.split()
+    assert parts[0] == "R", line
+    n, extra = int(parts[1]), int(parts[2])
+    ids = [int(x.split(":")[0]) for x in parts[3:3 + n]]
+    sc = [float.fromhex(x.split(":")[1]) for x in parts[3:3 + n]]
+    return ids, sc, extra
+
+
+def bits(xs):
+    return np.asarray(xs, np.float64).view(np.uint64).tolist()
+
+
+def test_csr_dropin_matches_reference(gpu):
+    d = Driver()
+    rng = np.random.default_rng(77)
+    cases = [(toy_docs(), [(["cat"], 100), (["cat", "dog"], 5), (["unicorn"], 5), (["fish", "cat", "cat"], 3)])]
+    for _ in range(60):
+        docs, q = random_instance(rng)
+        cases.append((docs, [(q, 1 + int(rng.integers(0, 10)))]))
+    for docs, queries in cases:
+        d.send([f"DOCS {len(docs)}"] + [f"{i}\t{t}" for i, t in docs], expect=0)
+        assert d.send(["INDEX 0 1.2 0.75"])[0].startswith("OK")
+        ri = ref.RefIndex.from_texts(docs, ref.TOK_MINIMAL)
+        for q, k in queries:
+            for ms in (0, 1):
+                ids, sc, post = parse(d.send([f"QUERY {k} 1.2 0.75 {ms} " + " ".join(q)])[0])
+                w_ids, w_sc, w_post = ri.search(q, k, maxscore=bool(ms))
+                assert ids == w_ids.tolist() and bits(sc) == bits(w_sc), (docs, q, k)
+                if not ms:
+                    assert post == w_post
+    # error mapping: bm25_term_score range check (test_csr.cpp:125-130)
+    d.send([f"DOCS {len(toy_docs())}"] + [f"{i}\t{t}" for i, t in toy_docs()], expect=0)
+    d.send(["INDEX 0 1.2 0.75"])
+    assert d.send(["TERMSCORE 0 3"])[0].startswith("V ")
+    assert d.send(["TERMSCORE 0 4"])[0].startswith("THROW out_of_range")
+    assert d.send(["KSTAR 0.05 1.4"])[0] == "V 3"
+    assert d.send(["KSTAR 0 1"])[0].startswith("THROW invalid_argument")
+    d.close()
+
+
+def test_temporal_dropin_matches_reference(gpu):
+    day = 24 * 3600 * 1000
+    rng = np.random.default_rng(17)
+    n = 300
+    ts = [int(rng.integers(0, 60 * day)) for _ in range(n)]
+    texts = [" ".join("t%d" % int(rng.integers(0, 40)) for _ in range(3 + int(rng.integers(0, 12))))
+             for _ in range(n)]
+    d = Driver()
+    d.send([f"RECORDS {n}"] + [f"{i} {ts[i]} {texts[i]}" for i in range(n)], expect=0)
+    for eps, kmax in [(0.05, 4), (1e-9, 64)]:
+        assert d.send([f"TEMPORAL {7 * day} {eps} 1.4 {kmax} 0"])[0].startswith("OK")
+        rt = ref.RefTemporal.from_records(list(range(n)), ts, texts, epsilon=eps, k_max=kmax,
+                                          tok_mode=ref.TOK_MINIMAL)
+        for _ in range(40):
+            q = ["t%d" % int(rng.integers(0, 40)) for _ in range(1 + int(rng.integers(0, 4)))]
+            k = 1 + int(rng.integers(0, 10))
+            for ub in (1, 0):
+                ids, sc, searched = parse(d.send([f"TQUERY {k} {ub} " + " ".join(q)])[0])
+                w_ids, w_sc, w_searched, _ = rt.topk(q, k, use_ub_stop=bool(ub))
+                assert ids == w_ids.tolist() and bits(sc) == bits(w_sc)
+                assert searched == w_searched
+    d.close()

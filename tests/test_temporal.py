@@ -97,8 +97,8 @@ def test_c3_window_equals_restricted_oracle_and_full_budget_equals_flat(c3_small
     ids, sc, n, post = orc.topk(tids, 10, row_lo=lo, row_hi=hi)
     check_batch(got, ids, sc, n, post, what="window")
     # epsilon -> 0, kmax large: the whole index (flat equivalence, acceptance.cpp:173-208)
-    full = search.TemporalIndex(c["dev"], c["part"], search.TemporalParams(epsilon=1e-9,
-                                                                         k_max_partitions=1 << 20))
+    full = search.TemporalIndex(c["dev"], c["part"], search.TemporalParams(
+        epsilon=1e-9, lambda_hat=0.01, k_max_partitions=1 << 20))  # k* = 2073 >= K
     assert full.window() == (0, c["hx"].n_docs)
     got = full.topk_batch(off, np.concatenate(tids), 7)
     ids, sc, n, post = orc.topk(tids, 7)
