@@ -195,6 +195,64 @@ __device__ __forceinline__ void range_rmw(float* __restrict__ acc, const float* 
     }
 }
 
+
+// Software-pipelined streaming: a "step" is up to 32*kR postings of one long
+// term's range; the loads of step s+1 are issued before step s is applied, so
+// two steps (and two terms at term boundaries) are in flight per lane.
+__device__ __forceinline__ void step_load(uint32_t* p, const uint32_t* __restrict__ pb, uint32_t o,
+                                          uint32_t n) {
+    const uint32_t lane = threadIdx.x & 31;
+#pragma unroll
+    for (int u = 0; u < kR; ++u) {
+        const uint32_t e = o + u * 32 + lane;
+        p[u] = e < n ? ldg_stream(pb + e) : kCodeMask;  // padding: impact 0
+    }
+}
+
+template <bool CLIP, bool ESC>
+__device__ __forceinline__ void step_apply(float* __restrict__ acc, const float* __restrict__ w32,
+                                           const uint32_t* p, uint32_t o, uint32_t n, float c,
+                                           uint32_t rlo, uint32_t rn, const DevIndex& ix,
+                                           uint64_t gbase, uint32_t base, double k1, double b) {
+    const uint32_t lane = threadIdx.x & 31;
+    if (o + 32 * kR <= n) {  // full step: every element valid
+        float av[kR], w[kR];
+#pragma unroll
+        for (int u = 0; u < kR; ++u) {
+            w[u] = w32[p[u] & kCodeMask];
+            if (CLIP && (p[u] >> kCodeBitsLong) - rlo >= rn) w[u] = 0.f;
+            av[u] = acc[p[u] >> kCodeBitsLong];
+        }
+#pragma unroll
+        for (int u = 0; u < kR; ++u) acc[p[u] >> kCodeBitsLong] = __fmaf_rn(c, w[u], av[u]);
+    } else {  // partial step: rows of one term are distinct, so element order is free
+#pragma unroll
+        for (int u = 0; u < kR; ++u) {
+            if (o + u * 32 >= n) break;  // warp-uniform
+            const uint32_t loc = p[u] >> kCodeBitsLong;
+            float w = w32[p[u] & kCodeMask];
+            if (CLIP && loc - rlo >= rn) w = 0.f;
+            if (o + u * 32 + lane < n) acc[loc] = __fmaf_rn(c, w, acc[loc]);
+        }
+    }
+    if (ESC) {  // escaped postings: exact (tf, len) from HBM, added once
+        bool e = false;
+#pragma unroll
+        for (int u = 0; u < kR; ++u) e |= o + u * 32 + lane < n && (p[u] & kEscLong) == kEscLong;
+        if (__any_sync(0xffffffffu, e)) {
+#pragma unroll
+            for (int u = 0; u < kR; ++u) {
+                const uint32_t el = o + u * 32 + lane;
+                const uint32_t loc = p[u] >> kCodeBitsLong;
+                if (el < n && (p[u] & kEscLong) == kEscLong && (!CLIP || loc - rlo < rn))
+                    acc[loc] += c * impact32(static_cast<double>(__ldg(ix.tf + gbase + el)),
+                                             static_cast<double>(__ldg(ix.doc_lens + base + loc)),
+                                             ix.avgdl, k1, b);
+            }
+        }
+    }
+}
+
 // ---------------------------------------------------------------- kernel
 template <int CAPW>
 __global__ void __launch_bounds__(kCons, CAPW == 192 ? 2 : 1) search_fast_kernel(DevIndex ix, BatchArgs a) {
@@ -370,21 +428,56 @@ __global__ void __launch_bounds__(kCons, CAPW == 192 ? 2 : 1) search_fast_kernel
             const bool clip = rn != kTile;
             if (j < j1) load_sub(j + 1);
             // ---- long terms: my contiguous sub-range of each, straight from HBM/L2
-            for (uint32_t x = 0; x < n_long; ++x) {
-                const uint32_t i = S.order_list[x];
-                const float c = S.t_c32[i];
-                const uint64_t s0 = S.t_start[i];
-                const uint32_t rb = S.wsub[warp][x][0], re = S.wsub[warp][x][1];
-                const uint64_t B = s0 + rb;
-                const uint32_t n = re - rb;
-                const bool esc = S.t_esc[i] != 0;
-                if (n) {
-                    if (!clip && !esc) range_rmw<false, false>(S.acc, S.w32, ix.post + B, n, c, rlo, rn, ix, B, base, k1, bb);
-                    else if (!esc) range_rmw<true, false>(S.acc, S.w32, ix.post + B, n, c, rlo, rn, ix, B, base, k1, bb);
-                    else if (!clip) range_rmw<false, true>(S.acc, S.w32, ix.post + B, n, c, rlo, rn, ix, B, base, k1, bb);
-                    else range_rmw<true, true>(S.acc, S.w32, ix.post + B, n, c, rlo, rn, ix, B, base, k1, bb);
+            if (CAPW == 320) {
+                // one CTA per SM (registers to spare): two steps in flight
+                uint32_t x = 0, o = 0;
+                auto range_n = [&](uint32_t xx) { return S.wsub[warp][xx][1] - S.wsub[warp][xx][0]; };
+                auto range_p = [&](uint32_t xx) {
+                    return ix.post + S.t_start[S.order_list[xx]] + S.wsub[warp][xx][0];
+                };
+                while (x < n_long && range_n(x) == 0) ++x;
+                uint32_t pc[kR];
+                if (x < n_long) step_load(pc, range_p(x), 0, range_n(x));
+                while (x < n_long) {
+                    const uint32_t n = range_n(x);
+                    uint32_t nx = x, no = o + 32 * kR;
+                    if (no >= n) {
+                        no = 0;
+                        ++nx;
+                        while (nx < n_long && range_n(nx) == 0) ++nx;
+                    }
+                    uint32_t pn[kR];
+                    if (nx < n_long) step_load(pn, range_p(nx), no, range_n(nx));
+                    const uint32_t i = S.order_list[x];
+                    const float c = S.t_c32[i];
+                    const uint64_t gb = S.t_start[i] + S.wsub[warp][x][0];
+                    const bool esc = S.t_esc[i] != 0;
+                    if (!clip && !esc) step_apply<false, false>(S.acc, S.w32, pc, o, n, c, rlo, rn, ix, gb, base, k1, bb);
+                    else if (!esc) step_apply<true, false>(S.acc, S.w32, pc, o, n, c, rlo, rn, ix, gb, base, k1, bb);
+                    else if (!clip) step_apply<false, true>(S.acc, S.w32, pc, o, n, c, rlo, rn, ix, gb, base, k1, bb);
+                    else step_apply<true, true>(S.acc, S.w32, pc, o, n, c, rlo, rn, ix, gb, base, k1, bb);
+                    if (nx != x) __syncwarp();  // the next term may touch the same rows
+#pragma unroll
+                    for (int u = 0; u < kR; ++u) pc[u] = pn[u];
+                    x = nx;
+                    o = no;
                 }
-                __syncwarp();  // the next term may touch the same rows from other lanes
+            } else {
+                for (uint32_t x = 0; x < n_long; ++x) {
+                    const uint32_t i = S.order_list[x];
+                    const float c = S.t_c32[i];
+                    const uint32_t rb = S.wsub[warp][x][0], re = S.wsub[warp][x][1];
+                    const uint64_t B = S.t_start[i] + rb;
+                    const uint32_t n = re - rb;
+                    const bool esc = S.t_esc[i] != 0;
+                    if (n) {
+                        if (!clip && !esc) range_rmw<false, false>(S.acc, S.w32, ix.post + B, n, c, rlo, rn, ix, B, base, k1, bb);
+                        else if (!esc) range_rmw<true, false>(S.acc, S.w32, ix.post + B, n, c, rlo, rn, ix, B, base, k1, bb);
+                        else if (!clip) range_rmw<false, true>(S.acc, S.w32, ix.post + B, n, c, rlo, rn, ix, B, base, k1, bb);
+                        else range_rmw<true, true>(S.acc, S.w32, ix.post + B, n, c, rlo, rn, ix, B, base, k1, bb);
+                    }
+                    __syncwarp();  // the next term may touch the same rows from other lanes
+                }
             }
             // ---- short terms: the tile segment is small; every warp filters its rows
             for (uint32_t s = 0; s < n_short; ++s) {
@@ -419,47 +512,60 @@ __global__ void __launch_bounds__(kCons, CAPW == 192 ? 2 : 1) search_fast_kernel
             }
             if (r_lo < r_hi) {
                 const uint32_t v0 = r_lo >> 2, v1 = (r_hi + 3) >> 2;
-                float t_emit = fmaxf(Lw, __uint_as_float(S.Lg)) * f_slack;
-                for (uint32_t vb = v0; vb < v1; vb += 32) {
+                // admission: A > 0 and A >= L * slack  <=>  A >= max(L * slack, min denormal)
+                float te = fmaxf(fmaxf(Lw, __uint_as_float(S.Lg)) * f_slack, 1.4e-45f);
+                // append the qualifying entries of one float4 per lane (slow path)
+                auto admit = [&](float4 x4, uint32_t v) {
                     if (nw > static_cast<uint32_t>(CAPW - 128)) {
                         nw = warp_prune(S, warp, nw, k, Lw, f_slack);
-                        t_emit = fmaxf(Lw, __uint_as_float(S.Lg)) * f_slack;
+                        te = fmaxf(fmaxf(Lw, __uint_as_float(S.Lg)) * f_slack, 1.4e-45f);
                         if (nw > static_cast<uint32_t>(CAPW - 128)) {  // near-tie flood
                             flood = true;
-                            for (uint32_t z = vb + lane; z < v1; z += 32)
-                                acc4[z] = make_float4(0.f, 0.f, 0.f, 0.f);
-                            break;
+                            return;
                         }
                     }
-                    const uint32_t v = vb + lane;
-                    float4 x4 = make_float4(0.f, 0.f, 0.f, 0.f);
-                    if (v < v1) {
-                        x4 = acc4[v];
-                        acc4[v] = make_float4(0.f, 0.f, 0.f, 0.f);
+                    const bool q0 = x4.x >= te, q1 = x4.y >= te, q2 = x4.z >= te, q3 = x4.w >= te;
+                    const uint32_t cnt = q0 + q1 + q2 + q3;
+                    if (!__any_sync(0xffffffffu, cnt != 0)) return;
+                    const uint32_t incl = warp_incl_scan(cnt);
+                    uint32_t slot = nw + incl - cnt;
+                    const uint32_t r = base + 4 * v;
+                    auto put = [&](bool ok, uint32_t row, float val) {
+                        if (ok) {
+                            S.cl_row[warp][slot] = row;
+                            S.cl_val[warp][slot] = val;
+                            ++slot;
+                        }
+                    };
+                    put(q0, r, x4.x);
+                    put(q1, r + 1, x4.y);
+                    put(q2, r + 2, x4.z);
+                    put(q3, r + 3, x4.w);
+                    nw += __shfl_sync(0xffffffffu, incl, 31);
+                    __syncwarp();
+                };
+                const float4 z4 = make_float4(0.f, 0.f, 0.f, 0.f);
+                for (uint32_t vb = v0; vb < v1 && !flood; vb += 64) {
+                    const uint32_t va = vb + lane, vc = vb + 32 + lane;
+                    float4 xa = z4, xc = z4;
+                    if (va < v1) {
+                        xa = acc4[va];
+                        acc4[va] = z4;
                     }
-                    const float mx = fmaxf(fmaxf(x4.x, x4.y), fmaxf(x4.z, x4.w));
-                    if (__ballot_sync(0xffffffffu, mx > 0.f && mx >= t_emit)) {
-                        const bool q0 = x4.x > 0.f && x4.x >= t_emit, q1 = x4.y > 0.f && x4.y >= t_emit;
-                        const bool q2 = x4.z > 0.f && x4.z >= t_emit, q3 = x4.w > 0.f && x4.w >= t_emit;
-                        const uint32_t cnt = q0 + q1 + q2 + q3;
-                        const uint32_t incl = warp_incl_scan(cnt);
-                        uint32_t slot = nw + incl - cnt;
-                        const uint32_t r = base + 4 * v;
-                        auto put = [&](bool ok, uint32_t row, float val) {
-                            if (ok) {
-                                S.cl_row[warp][slot] = row;
-                                S.cl_val[warp][slot] = val;
-                                ++slot;
-                            }
-                        };
-                        put(q0, r, x4.x);
-                        put(q1, r + 1, x4.y);
-                        put(q2, r + 2, x4.z);
-                        put(q3, r + 3, x4.w);
-                        nw += __shfl_sync(0xffffffffu, incl, 31);
-                        __syncwarp();
+                    if (vc < v1) {
+                        xc = acc4[vc];
+                        acc4[vc] = z4;
+                    }
+                    const float mx = fmaxf(fmaxf(fmaxf(xa.x, xa.y), fmaxf(xa.z, xa.w)),
+                                           fmaxf(fmaxf(xc.x, xc.y), fmaxf(xc.z, xc.w)));
+                    if (__any_sync(0xffffffffu, mx >= te)) {
+                        admit(xa, va);
+                        if (!flood) admit(xc, vc);
                     }
                 }
+                if (flood)  // the query goes to the exact kernel: finish zeroing my rows
+                    for (uint32_t z = v0 + lane; z < v1; z += 32) acc4[z] = z4;
+                __syncwarp();
             }
         }
         if (lane == 0) {
