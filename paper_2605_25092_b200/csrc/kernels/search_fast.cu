@@ -24,8 +24,11 @@
 // (score desc, DocId asc) (include/hybrid/types.hpp:21-25), and the Margin
 // confidence + skip decision are written (src/cascade.cpp:15-21, 79-84).
 // See bm25_search.cu for the exactness argument of the fp32 selection.
+#include <cstdlib>
+
 #include "hm_device.cuh"
 #include "hm_launch.h"
+#include "hm_ptx.cuh"
 
 namespace hm {
 
@@ -54,7 +57,7 @@ struct __align__(16) FastSmem {
     float t_c32[kFastTerms];
     int32_t t_slot[kFastTerms];
     uint8_t t_esc[kFastTerms];             // long term has escaped postings
-    uint32_t wsub[kConsWarps][kFastTerms][2];  // warp's sub-range of each long term, this tile
+    uint32_t wsub[2][kConsWarps][kFastTerms][2];  // warp's sub-range of each long term (tile parity)
     uint16_t order_list[kFastTerms];       // long terms, then short terms
     uint32_t pref[kFastTerms + 1];         // short-window prefix sums / gather offsets
     uint32_t hist[256];
@@ -402,38 +405,39 @@ __global__ void __launch_bounds__(kCons, CAPW == 192 ? 2 : 1) search_fast_kernel
         bool flood = false;
         // my sub-range of every long term: lane x holds term x's for the next
         // tile (prefetched during the current one), the current tile's are in smem
-        uint32_t nb = 0, ne = 0;
+        // my sub-range of every long term for a tile: copied global -> smem with
+        // cp.async (no registers held), one tile ahead, double-buffered by parity
         auto load_sub = [&](uint32_t j) {
             if (static_cast<uint32_t>(lane) < n_long) {
                 const uint32_t* tb = tile_row(ix, S.t_slot[S.order_list[lane]]);
                 const uint64_t sub = static_cast<uint64_t>(j) * kSubPerTile + warp;
-                nb = __ldg(tb + sub);
-                ne = __ldg(tb + sub + 1);
+                uint32_t* dst = S.wsub[j & 1][warp][lane];
+                asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_addr(dst)), "l"(tb + sub) : "memory");
+                asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_addr(dst + 1)), "l"(tb + sub + 1) : "memory");
             }
+            asm volatile("cp.async.commit_group;" ::: "memory");
         };
-        auto store_sub = [&] {
-            if (static_cast<uint32_t>(lane) < n_long) {
-                S.wsub[warp][lane][0] = nb;
-                S.wsub[warp][lane][1] = ne;
-            }
+        auto wait_sub = [&] {
+            asm volatile("cp.async.wait_group 0;" ::: "memory");
             __syncwarp();
         };
         load_sub(j0);
-        store_sub();
         for (uint32_t j = j0; j <= j1; ++j) {
             const uint32_t base = j << kTileShift;
             const uint32_t R0 = max(base, row_lo);
             const uint32_t R1 = min(base + kTile, row_hi);
             const uint32_t rlo = R0 - base, rn = R1 - R0;
             const bool clip = rn != kTile;
+            wait_sub();
             if (j < j1) load_sub(j + 1);
+            const uint32_t (*wsub)[2] = S.wsub[j & 1][warp];
             // ---- long terms: my contiguous sub-range of each, straight from HBM/L2
             if (CAPW == 320) {
                 // one CTA per SM (registers to spare): two steps in flight
                 uint32_t x = 0, o = 0;
-                auto range_n = [&](uint32_t xx) { return S.wsub[warp][xx][1] - S.wsub[warp][xx][0]; };
+                auto range_n = [&](uint32_t xx) { return wsub[xx][1] - wsub[xx][0]; };
                 auto range_p = [&](uint32_t xx) {
-                    return ix.post + S.t_start[S.order_list[xx]] + S.wsub[warp][xx][0];
+                    return ix.post + S.t_start[S.order_list[xx]] + wsub[xx][0];
                 };
                 while (x < n_long && range_n(x) == 0) ++x;
                 uint32_t pc[kR];
@@ -450,7 +454,7 @@ __global__ void __launch_bounds__(kCons, CAPW == 192 ? 2 : 1) search_fast_kernel
                     if (nx < n_long) step_load(pn, range_p(nx), no, range_n(nx));
                     const uint32_t i = S.order_list[x];
                     const float c = S.t_c32[i];
-                    const uint64_t gb = S.t_start[i] + S.wsub[warp][x][0];
+                    const uint64_t gb = S.t_start[i] + wsub[x][0];
                     const bool esc = S.t_esc[i] != 0;
                     if (!clip && !esc) step_apply<false, false>(S.acc, S.w32, pc, o, n, c, rlo, rn, ix, gb, base, k1, bb);
                     else if (!esc) step_apply<true, false>(S.acc, S.w32, pc, o, n, c, rlo, rn, ix, gb, base, k1, bb);
@@ -466,7 +470,7 @@ __global__ void __launch_bounds__(kCons, CAPW == 192 ? 2 : 1) search_fast_kernel
                 for (uint32_t x = 0; x < n_long; ++x) {
                     const uint32_t i = S.order_list[x];
                     const float c = S.t_c32[i];
-                    const uint32_t rb = S.wsub[warp][x][0], re = S.wsub[warp][x][1];
+                    const uint32_t rb = wsub[x][0], re = wsub[x][1];
                     const uint64_t B = S.t_start[i] + rb;
                     const uint32_t n = re - rb;
                     const bool esc = S.t_esc[i] != 0;
@@ -499,7 +503,6 @@ __global__ void __launch_bounds__(kCons, CAPW == 192 ? 2 : 1) search_fast_kernel
                 }
                 __syncwarp();
             }
-            if (j < j1) store_sub();
             // ---- scan my rows of the tile: admit candidates, zero accumulators
             const uint32_t r_lo = max(wr0, rlo), r_hi = min(wr0 + (1u << kSubShift), rlo + rn);
             float4* acc4 = reinterpret_cast<float4*>(S.acc);
@@ -698,8 +701,13 @@ static cudaError_t fast_attr() {
 }
 
 // CAPW 192 (k <= 32): two 16-warp CTAs per SM; CAPW 320 (k <= 128): one.
+// HM_FAST_CTAS=1 forces the one-CTA variant (experiments).
 cudaError_t launch_search(const DevIndex& ix, const BatchArgs& a, int sms, cudaStream_t st) {
-    if (a.k <= FastCfg<192>::kMaxKServed) {
+    static const bool force1 = [] {
+        const char* e = getenv("HM_FAST_CTAS");
+        return e && e[0] == '1';
+    }();
+    if (a.k <= FastCfg<192>::kMaxKServed && !force1) {
         const cudaError_t e = fast_attr<192>();
         if (e != cudaSuccess) return e;
         search_fast_kernel<192><<<2 * sms, kCons, sizeof(FastSmem<192>), st>>>(ix, a);
