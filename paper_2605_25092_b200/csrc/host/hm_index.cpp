@@ -17,6 +17,7 @@
 #include <cmath>
 #include <cstring>
 #include <mutex>
+#include <shared_mutex>
 #include <stdexcept>
 #include <string>
 #include <thread>
@@ -158,6 +159,14 @@ struct hm_index {
     uint64_t n_escaped = 0;
     std::vector<uint32_t> code_tf, code_len;
     int grid_search = 0, grid_exact = 0;
+    // baked long-term postings (kernels/bake.cu) for one (k1, b)
+    uint32_t* d_long_terms = nullptr;
+    uint32_t n_long = 0;
+    uint32_t* d_bk = nullptr;
+    uint32_t* d_bake_err = nullptr;
+    std::shared_mutex bake_mu;
+    bool bake_valid = false, bake_ok = false;
+    double bake_k1 = 0.0, bake_b = 0.0;
     std::mutex mu;
     std::vector<Workspace*> pool;
 
@@ -387,6 +396,20 @@ void build_index(const hm_csr_view* v, hm_index* X) {
     d.doc_ids = dev_upload(v->doc_ids, N, A, B);
     d.code_tf = dev_upload(X->code_tf.data(), hm::kMaxCodes, A, B);
     d.code_len = dev_upload(X->code_len.data(), hm::kMaxCodes, A, B);
+    X->n_long = static_cast<uint32_t>(long_terms.size());
+    X->d_long_terms = dev_upload(long_terms.data(), long_terms.size(), A, B);
+    {
+        void* p = nullptr;
+        ck(cudaMalloc(&p, std::max<uint64_t>(P, 1) * 4 + 16), "cudaMalloc(bk)");
+        A.push_back(p);
+        B += std::max<uint64_t>(P, 1) * 4 + 16;
+        X->d_bk = static_cast<uint32_t*>(p);
+        ck(cudaMalloc(&p, 16), "cudaMalloc(bake err)");
+        A.push_back(p);
+        X->d_bake_err = static_cast<uint32_t*>(p);
+    }
+    d.bk = X->d_bk;
+    d.bk_eb = 0;
     d.n_terms = V;
     d.n_docs = N;
     d.n_tiles = n_tiles;
@@ -556,6 +579,46 @@ void read_timing(Workspace* w) {
     ck(cudaEventElapsedTime(&g_ms_exact, w->ev[2], w->ev[3]), "elapsed");
 }
 
+// Hold the baked postings for (k1, b) for the duration of a batch: shared
+// lock while they match, exclusive re-bake (K0, ~1 ms at C2) when they do not.
+// Returns false when these parameters cannot be baked (an impact outside the
+// representable range): the batch then runs on the exact fp64 kernel.
+bool ensure_baked(hm_index* X, double k1, double b, std::shared_lock<std::shared_mutex>& lk) {
+    if (needs_exact(k1, b)) {
+        lk = std::shared_lock<std::shared_mutex>(X->bake_mu);
+        return false;
+    }
+    for (;;) {
+        lk = std::shared_lock<std::shared_mutex>(X->bake_mu);
+        if (X->bake_valid && X->bake_k1 == k1 && X->bake_b == b) return X->bake_ok;
+        lk.unlock();
+        std::unique_lock<std::shared_mutex> ul(X->bake_mu);
+        if (X->bake_valid && X->bake_k1 == k1 && X->bake_b == b) continue;
+        X->bake_valid = false;
+        const uint32_t eb = hm::bake_eb(k1);
+        cudaStream_t st = nullptr;
+        ck(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking), "bake stream");
+        uint32_t err = 0;
+        try {
+            ck(cudaMemsetAsync(X->d_bake_err, 0, 4, st), "bake memset");
+            hm::DevIndex d = X->dev;
+            ck(hm::launch_bake(d, X->d_long_terms, X->n_long, k1, b, eb, X->d_bk, X->d_bake_err, st),
+               "bake kernel");
+            ck(cudaMemcpyAsync(&err, X->d_bake_err, 4, cudaMemcpyDeviceToHost, st), "bake D2H");
+            ck(cudaStreamSynchronize(st), "bake sync");
+        } catch (...) {
+            cudaStreamDestroy(st);
+            throw;
+        }
+        cudaStreamDestroy(st);
+        X->dev.bk_eb = eb;
+        X->bake_k1 = k1;
+        X->bake_b = b;
+        X->bake_ok = err == 0;
+        X->bake_valid = true;
+    }
+}
+
 void validate(const hm_index* X, const hm_query_batch* b) {
     if (!b) throw std::invalid_argument("null batch");
     if (b->k > static_cast<uint32_t>(hm::kMaxK))
@@ -618,6 +681,8 @@ int hm_search_batch(hm_index* X, const hm_query_batch* b, hm_results* out) {
             if (b->q_tid[i] != hm::kNoTerm && b->q_tid[i] >= X->dev.n_terms)
                 throw std::out_of_range("term id out of range");
         ck(cudaSetDevice(X->device), "cudaSetDevice");
+        std::shared_lock<std::shared_mutex> bake_lk;
+        const bool baked = ensure_baked(X, b->k1, b->b, bake_lk);
         Workspace* w = acquire(X);
         try {
             const uint32_t k = std::max(b->k, 1u);
@@ -647,6 +712,7 @@ int hm_search_batch(hm_index* X, const hm_query_batch* b, hm_results* out) {
             if (ntid) ck(cudaMemcpyAsync(w->q_tid, ptid, ntid * 4ull, cudaMemcpyHostToDevice, st), "H2D");
             if (b->tau) ck(cudaMemcpyAsync(w->tau, ptau, nq * 8ull, cudaMemcpyHostToDevice, st), "H2D");
             hm_query_batch hb = *b;
+            if (!baked) hb.flags |= HM_FLAG_FORCE_EXACT;
             hm_results dout{w->out_ids, w->out_scores, w->out_n, w->out_conf, w->out_skip, w->out_post};
             // the k used on device must match the output stride
             run_batch(X, w, hb, w->q_off, w->q_tid, b->tau ? w->tau : nullptr, dout, pw);
@@ -695,6 +761,8 @@ int hm_search_batch_device(hm_index* X, const hm_query_batch* b, hm_results* out
         // the batch's tid count is unknown on the host: plan scratch is sized
         // from q_off[nq] read back once (a 4-byte D2H on the caller's stream)
         cudaStream_t ust = static_cast<cudaStream_t>(stream);
+        std::shared_lock<std::shared_mutex> bake_lk;
+        const bool baked = ensure_baked(X, b->k1, b->b, bake_lk);
         uint32_t ntid = 0;
         ck(cudaMemcpyAsync(&ntid, b->q_off + nq, 4, cudaMemcpyDeviceToHost, ust), "D2H q_off");
         ck(cudaStreamSynchronize(ust), "sync");
@@ -706,7 +774,9 @@ int hm_search_batch_device(hm_index* X, const hm_query_batch* b, hm_results* out
             ck(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming), "event");
             ck(cudaEventRecord(ev, ust), "event record");
             ck(cudaStreamWaitEvent(w->stream, ev, 0), "wait");
-            run_batch(X, w, *b, b->q_off, b->q_tid, b->tau, *out, reinterpret_cast<float*>(w->pin));
+            hm_query_batch hb = *b;
+            if (!baked) hb.flags |= HM_FLAG_FORCE_EXACT;
+            run_batch(X, w, hb, b->q_off, b->q_tid, b->tau, *out, reinterpret_cast<float*>(w->pin));
             ck(cudaEventRecord(ev, w->stream), "event record");
             ck(cudaStreamWaitEvent(ust, ev, 0), "wait");
             // pinned w32 staging is reused by the next call on this workspace:

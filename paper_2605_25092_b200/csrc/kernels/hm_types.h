@@ -19,6 +19,21 @@
 //                 of the first posting of every 1024-row sub-tile (long terms
 //                 only); tile j starts at entry 16*j.
 //   doc_lens[N] u32, doc_ids[N] u64, code_tf/code_len[kMaxCodes] u32.
+//   bk[P]        u32 BAKED long-term postings for one (k1, b), same indexing
+//                 as post[] (short-term slots unused), written by bake_kernel:
+//                   (q19 << 13) | (off11 << 2)
+//                 q19 = (float_bits(w) - bk_eb) >> 7: the idf-free impact
+//                 w = tf*(k1+1)/(tf + k1*(1-b+b*len/avgdl)) truncated to 3
+//                 exponent + 16 mantissa bits (8 binades below k1+1, relative
+//                 error < 2^-16); off11 = swz10(r) & 2047, r = tile-local row:
+//                 the row's accumulator inside the search kernel's 2048-row
+//                 warp unit, XOR-swizzled so that read-modify-writes of dense
+//                 runs of rows (lane strides 1, 2, 4 .. 32) are
+//                 bank-conflict-free; the low 13 bits are its byte offset.
+//                 Decoding: float_bits = (word >> 6) + bk_eb (one LEA.HI; the
+//                 offset's top 7 bits land below the 16 kept mantissa bits,
+//                 so the decoded impact stays within 2^-16 of w) and
+//                 offset = word & 0x1FFC (one LOP3).
 #pragma once
 #include <cstdint>
 
@@ -43,6 +58,9 @@ constexpr uint32_t kEscLong = (1u << kCodeBitsLong) - 1;
 constexpr int kMaxK = 256;
 constexpr uint32_t kNoTerm = 0xFFFFFFFFu;
 constexpr int kLongFactor = 32;               // long term: df > 32 * n_tiles
+constexpr int kBakeMantBits = 16;             // baked impact: 3 exponent + 16 mantissa bits
+constexpr int kBakeBinades = 8;
+constexpr int kShortCodes = 256;              // smem impact table of short-term codes
 static_assert(kLocalBits == kTileShift, "local row field must cover one tile");
 
 struct DevIndex {
@@ -65,7 +83,17 @@ struct DevIndex {
     uint32_t n_codes;          // codes usable by long terms (< kMaxCodes)
     uint32_t n_codes_short;    // codes usable by short terms (< esc_short)
     double avgdl;
+    const uint32_t* bk;        // baked long-term postings (see above)
+    uint32_t bk_eb;            // float bits of the lowest baked binade
 };
+
+// swizzled position of a row (only bits 0-4 change, from bits 5-9); an involution
+#ifdef __CUDACC__
+#define HM_HD __host__ __device__ __forceinline__
+#else
+#define HM_HD inline
+#endif
+HM_HD uint32_t swz10(uint32_t r) { return r ^ ((r >> 5) & 31u); }
 
 struct BatchArgs {
     uint32_t nq, k;

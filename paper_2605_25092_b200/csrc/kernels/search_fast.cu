@@ -1,29 +1,37 @@
-// search_fast_kernel: the fused BM25 hot path on sm_100a.
+// search_fast_kernel: the fused BM25 hot path on sm_100a (v12).
 //
-// One CTA (16 warps) owns one query at a time (persistent, LPT order) and
-// sweeps its row window in kTile = 16384-row tiles.  Warp w OWNS rows
-// [1024 w, 1024 w + 1024) of every tile:
-//   * long terms: the sub-tile table gives, for every 1024-row sub-tile, the
-//     offset of its first posting, so a warp streams exactly its own
-//     contiguous sub-range of each term's postings straight from HBM/L2 with
-//     8 independent coalesced loads per lane in flight
-//     (ld.global.nc.L1::no_allocate);
+// Two 8-warp CTAs per SM, persistent; each CTA owns one query at a time (LPT
+// order) and sweeps its row window in kTile = 16384-row tiles.  Warp w OWNS
+// the 2048-row unit [2048 w, 2048 w + 2048) of every tile:
+//   * long terms stream the BAKED postings bk[] (bake.cu): one u32 carries the
+//     byte offset of the row's fp32 accumulator (XOR-swizzled, conflict-free
+//     for dense runs) and the idf-free impact truncated to 3 exponent + 16
+//     mantissa bits -- no code-table lookup, no escapes.  The sub-tile table
+//     gives the warp's contiguous sub-range of each term; it is read with
+//     16-byte loads (ld.global.nc.v4, up to 8 per lane in flight) plus at most
+//     6 unaligned boundary words;
+//   * the first long term of a unit stores (acc = c*w) instead of
+//     read-modify-write: the unit's accumulators are zero at that point;
 //   * short terms: the tile segment (a few postings) is read by every warp and
-//     filtered by row;
-//   * fp32 scores accumulate in shared memory with plain read-modify-writes --
-//     no other warp touches these rows, so there are no atomics and no CTA
+//     filtered by row; their impacts come from a 256-entry code table;
+//   * no other warp touches a unit's rows, so there are no atomics and no CTA
 //     barrier anywhere in the tile loop;
-//   * after a tile the warp scans its 1024 accumulators: docs that can still
-//     reach the top-k join the warp's candidate list, the accumulators are
-//     zeroed (pitfall-3 sentinel reset, src/twophase.cpp:24-27).  A warp prunes
-//     its list locally and publishes its k-th score to a CTA-wide lower bound
-//     Lg that every warp uses as admission threshold.
+//   * after a tile the warp scans its 2048 accumulators: docs that can still
+//     reach the top-k join the warp's candidate list, accumulators are zeroed
+//     (pitfall-3 sentinel reset, src/twophase.cpp:24-27).  A warp prunes its
+//     list locally and publishes its k-th score to a CTA-wide lower bound Lg
+//     that every warp uses as admission threshold.
 // At the end of the query (one CTA barrier) the lists are merged, the
 // survivors are rescored exactly in fp64 in the reference's operation and
 // accumulation order (src/csr_index.cpp:10-15, 87-101), ranked by
 // (score desc, DocId asc) (include/hybrid/types.hpp:21-25), and the Margin
 // confidence + skip decision are written (src/cascade.cpp:15-21, 79-84).
-// See bm25_search.cu for the exactness argument of the fp32 selection.
+//
+// Exactness (bm25_search.cu has the argument): each fp32 contribution is
+// c32 * w with c32 = fl(mult * idf) and w the baked impact, relative error
+// < 2^-16 (truncation) + 2^-24; accumulation adds m roundings.  With
+// delta = (m + 10) 2^-24 + 2^-16 every A(d) is within delta of E(d), and the
+// admission slack 1 - 2.5 delta keeps the exact top-k among the survivors.
 #include <cstdlib>
 
 #include "hm_device.cuh"
@@ -32,14 +40,18 @@
 
 namespace hm {
 
-constexpr int kCons = kThreads;           // 512 threads
-constexpr int kConsWarps = kCons / 32;    // 16: warp w owns sub-tile w of a tile
+constexpr int kCons = 256;                // threads per CTA
+constexpr int kConsWarps = kCons / 32;    // 8: warp w owns unit w of a tile
+constexpr int kUnitShift = 11;            // 2048 rows per warp unit
+constexpr int kUnitRows = 1 << kUnitShift;
+constexpr int kSubPerUnit = kUnitRows >> kSubShift;  // 2 sub-tiles of the table
 constexpr int kFastTerms = 32;            // plan size served by this kernel
-constexpr int kR = 8;                     // postings per lane in flight
-static_assert(kConsWarps == kSubPerTile, "one warp per 1024-row sub-tile");
+constexpr int kU = 8;                     // 16-byte loads per lane in flight
+constexpr uint32_t kOffMask = (kUnitRows * 4 - 1) & ~3u;  // bk: impact (19 bits) | byte offset (13 bits)
+constexpr int kImpShift = 2 + kUnitShift - (23 - kBakeMantBits);
+static_assert(kConsWarps * kUnitRows == kTile, "one warp per 2048-row unit");
+static_assert(2 + kUnitShift + 3 + kBakeMantBits == 32, "bk = 19-bit impact | 13-bit offset");
 
-// per-warp candidate list capacity -> largest k served (room for one scan
-// round of 128 appends plus near-ties)
 template <int CAPW>
 struct FastCfg {
     static constexpr int kMaxKServed = CAPW == 192 ? 32 : 128;
@@ -47,8 +59,8 @@ struct FastCfg {
 
 template <int CAPW>
 struct __align__(16) FastSmem {
-    float acc[kTile];
-    float w32[kMaxCodes];                  // [kCodeMask] = 0
+    float acc[kTile];                      // first member: bk offsets are byte offsets into it
+    float w32s[kShortCodes];               // impacts of the short-term codes
     uint32_t cl_row[kConsWarps][CAPW];     // per-warp candidate lists
     float cl_val[kConsWarps][CAPW];
     uint64_t t_start[kFastTerms], t_wlo[kFastTerms], t_end[kFastTerms];
@@ -56,9 +68,8 @@ struct __align__(16) FastSmem {
     uint32_t t_mult[kFastTerms];
     float t_c32[kFastTerms];
     int32_t t_slot[kFastTerms];
-    uint8_t t_esc[kFastTerms];             // long term has escaped postings
-    uint32_t wsub[2][kConsWarps][kFastTerms][2];  // warp's sub-range of each long term (tile parity)
-    uint16_t order_list[kFastTerms];       // long terms, then short terms
+    uint32_t wsub[2][kConsWarps][kFastTerms][2];  // unit's sub-range of each long term (tile parity)
+    uint16_t order_list[kFastTerms];       // long terms (df descending), then short terms
     uint32_t pref[kFastTerms + 1];         // short-window prefix sums / gather offsets
     uint32_t hist[256];
     uint32_t sel[2];
@@ -133,124 +144,52 @@ __device__ uint32_t warp_prune(FastSmem<CAPW>& S, int w, uint32_t n, uint32_t k,
     return keep;
 }
 
-// Accumulate one contiguous posting range of a long term (the warp's own rows)
-// into the tile accumulators: 8 independent coalesced loads per lane in
-// flight, then plain RMWs (rows of one term are distinct and no other warp
-// owns them).  CLIP: the tile is cut by the row window; ESC: the term has
-// postings whose (tf, len) pair is outside the code table (code kEscLong,
-// which masks to kCodeMask whose impact is 0; their exact impact is added
-// separately).
-template <bool CLIP, bool ESC>
-__device__ __forceinline__ void range_rmw(float* __restrict__ acc, const float* __restrict__ w32,
-                                          const uint32_t* __restrict__ pb, uint32_t n, float c,
-                                          uint32_t rlo, uint32_t rn, const DevIndex& ix,
-                                          uint64_t gbase, uint32_t base, double k1, double b) {
-    const uint32_t lane = threadIdx.x & 31;
-    uint32_t o = 0;
-    for (; o + 32 * kR <= n; o += 32 * kR) {
-        uint32_t p[kR];
-#pragma unroll
-        for (int u = 0; u < kR; ++u) p[u] = ldg_stream(pb + o + u * 32 + lane);
-        float av[kR], w[kR];
-#pragma unroll
-        for (int u = 0; u < kR; ++u) {
-            w[u] = w32[p[u] & kCodeMask];
-            if (CLIP && (p[u] >> kCodeBitsLong) - rlo >= rn) w[u] = 0.f;
-            av[u] = acc[p[u] >> kCodeBitsLong];
-        }
-#pragma unroll
-        for (int u = 0; u < kR; ++u) acc[p[u] >> kCodeBitsLong] = __fmaf_rn(c, w[u], av[u]);
-        if (ESC) {
-            bool e = false;
-#pragma unroll
-            for (int u = 0; u < kR; ++u) e |= (p[u] & kEscLong) == kEscLong;
-            if (__any_sync(0xffffffffu, e)) {
-#pragma unroll
-                for (int u = 0; u < kR; ++u) {
-                    const uint32_t loc = p[u] >> kCodeBitsLong;
-                    if ((p[u] & kEscLong) == kEscLong && (!CLIP || loc - rlo < rn))
-                        acc[loc] += c * impact32(static_cast<double>(__ldg(ix.tf + gbase + o + u * 32 + lane)),
-                                                 static_cast<double>(__ldg(ix.doc_lens + base + loc)),
-                                                 ix.avgdl, k1, b);
-                }
-            }
-        }
-    }
-    if (o < n) {  // remainder (< 256 postings): all of its loads in flight at once
-        uint32_t p[kR];
-#pragma unroll
-        for (int u = 0; u < kR; ++u) {
-            const uint32_t e = o + u * 32 + lane;
-            p[u] = e < n ? ldg_stream(pb + e) : kCodeMask;
-        }
-#pragma unroll
-        for (int u = 0; u < kR; ++u) {
-            if (o + u * 32 >= n) break;  // warp-uniform
-            const uint32_t e = o + u * 32 + lane;
-            const uint32_t loc = p[u] >> kCodeBitsLong;
-            float w = w32[p[u] & kCodeMask];
-            if (CLIP && loc - rlo >= rn) w = 0.f;
-            if (ESC && e < n && (p[u] & kEscLong) == kEscLong && (!CLIP || loc - rlo < rn))
-                w = impact32(static_cast<double>(__ldg(ix.tf + gbase + e)),
-                             static_cast<double>(__ldg(ix.doc_lens + base + loc)), ix.avgdl, k1, b);
-            if (e < n) acc[loc] = __fmaf_rn(c, w, acc[loc]);
-        }
-    }
+// ---------------------------------------------------------------- long terms
+// One baked posting: impact in the top 19 bits, accumulator byte offset in
+// the low 13.  (p >> 6) + eb puts the impact's exponent and 16 mantissa bits
+// in place; the offset's top 7 bits land below them (relative error < 2^-16,
+// covered by delta).  acc is the first smem member and warp units are
+// 8 KB-aligned, so the address is one OR of the unit base.
+template <bool FIRST>
+__device__ __forceinline__ void apply1(float* __restrict__ acc, uint32_t wbase, uint32_t p, float c,
+                                       uint32_t eb) {
+    float* a = reinterpret_cast<float*>(reinterpret_cast<char*>(acc) + (wbase | (p & kOffMask)));
+    const float w = __uint_as_float((p >> kImpShift) + eb);
+    if (FIRST) *a = c * w;
+    else *a = __fmaf_rn(c, w, *a);
 }
 
-
-// Software-pipelined streaming: a "step" is up to 32*kR postings of one long
-// term's range; the loads of step s+1 are issued before step s is applied, so
-// two steps (and two terms at term boundaries) are in flight per lane.
-__device__ __forceinline__ void step_load(uint32_t* p, const uint32_t* __restrict__ pb, uint32_t o,
-                                          uint32_t n) {
+// Accumulate one long term's contiguous posting range (the warp's own rows):
+// unaligned head/tail words by single loads, the 16-byte-aligned body with up
+// to kU 128-bit loads per lane in flight.  Rows of one term are distinct, so
+// the order of the read-modify-writes inside the range is free.
+template <bool FIRST>
+__device__ __forceinline__ void range_baked(float* __restrict__ acc, uint32_t wbase,
+                                            const uint32_t* __restrict__ pb, uint32_t n, float c, uint32_t eb) {
     const uint32_t lane = threadIdx.x & 31;
-#pragma unroll
-    for (int u = 0; u < kR; ++u) {
-        const uint32_t e = o + u * 32 + lane;
-        p[u] = e < n ? ldg_stream(pb + e) : kCodeMask;  // padding: impact 0
+    uint32_t h = static_cast<uint32_t>((16u - (reinterpret_cast<uintptr_t>(pb) & 15u)) & 15u) >> 2;
+    h = min(h, n);
+    const uint32_t body = n - h, nc = body >> 2, tl = body & 3;
+    if (lane < h + tl) {
+        const uint32_t idx = lane < h ? lane : 4 * nc + lane;
+        apply1<FIRST>(acc, wbase, ldg_stream(pb + idx), c, eb);
     }
-}
-
-template <bool CLIP, bool ESC>
-__device__ __forceinline__ void step_apply(float* __restrict__ acc, const float* __restrict__ w32,
-                                           const uint32_t* p, uint32_t o, uint32_t n, float c,
-                                           uint32_t rlo, uint32_t rn, const DevIndex& ix,
-                                           uint64_t gbase, uint32_t base, double k1, double b) {
-    const uint32_t lane = threadIdx.x & 31;
-    if (o + 32 * kR <= n) {  // full step: every element valid
-        float av[kR], w[kR];
+    const uint4* pc = reinterpret_cast<const uint4*>(pb + h);
+    for (uint32_t c0 = 0; c0 < nc; c0 += 32 * kU) {
+        uint4 v[kU];
 #pragma unroll
-        for (int u = 0; u < kR; ++u) {
-            w[u] = w32[p[u] & kCodeMask];
-            if (CLIP && (p[u] >> kCodeBitsLong) - rlo >= rn) w[u] = 0.f;
-            av[u] = acc[p[u] >> kCodeBitsLong];
+        for (int u = 0; u < kU; ++u) {
+            const uint32_t i = c0 + 32 * u + lane;
+            if (c0 + 32 * u < nc) v[u] = i < nc ? ldg_stream(pc + i) : make_uint4(0, 0, 0, 0);
         }
 #pragma unroll
-        for (int u = 0; u < kR; ++u) acc[p[u] >> kCodeBitsLong] = __fmaf_rn(c, w[u], av[u]);
-    } else {  // partial step: rows of one term are distinct, so element order is free
-#pragma unroll
-        for (int u = 0; u < kR; ++u) {
-            if (o + u * 32 >= n) break;  // warp-uniform
-            const uint32_t loc = p[u] >> kCodeBitsLong;
-            float w = w32[p[u] & kCodeMask];
-            if (CLIP && loc - rlo >= rn) w = 0.f;
-            if (o + u * 32 + lane < n) acc[loc] = __fmaf_rn(c, w, acc[loc]);
-        }
-    }
-    if (ESC) {  // escaped postings: exact (tf, len) from HBM, added once
-        bool e = false;
-#pragma unroll
-        for (int u = 0; u < kR; ++u) e |= o + u * 32 + lane < n && (p[u] & kEscLong) == kEscLong;
-        if (__any_sync(0xffffffffu, e)) {
-#pragma unroll
-            for (int u = 0; u < kR; ++u) {
-                const uint32_t el = o + u * 32 + lane;
-                const uint32_t loc = p[u] >> kCodeBitsLong;
-                if (el < n && (p[u] & kEscLong) == kEscLong && (!CLIP || loc - rlo < rn))
-                    acc[loc] += c * impact32(static_cast<double>(__ldg(ix.tf + gbase + el)),
-                                             static_cast<double>(__ldg(ix.doc_lens + base + loc)),
-                                             ix.avgdl, k1, b);
+        for (int u = 0; u < kU; ++u) {
+            if (c0 + 32 * u >= nc) break;  // warp-uniform
+            if (c0 + 32 * u + lane < nc) {
+                apply1<FIRST>(acc, wbase, v[u].x, c, eb);
+                apply1<FIRST>(acc, wbase, v[u].y, c, eb);
+                apply1<FIRST>(acc, wbase, v[u].z, c, eb);
+                apply1<FIRST>(acc, wbase, v[u].w, c, eb);
             }
         }
     }
@@ -258,10 +197,11 @@ __device__ __forceinline__ void step_apply(float* __restrict__ acc, const float*
 
 // ---------------------------------------------------------------- kernel
 template <int CAPW>
-__global__ void __launch_bounds__(kCons, CAPW == 192 ? 2 : 1) search_fast_kernel(DevIndex ix, BatchArgs a) {
+__global__ void __launch_bounds__(kCons, 2) search_fast_kernel(DevIndex ix, BatchArgs a) {
     using Smem = FastSmem<CAPW>;
     constexpr int kGatherBytes = 8 * kConsWarps * CAPW;
-    static_assert(kSurvBytes <= kGatherBytes && kGatherBytes <= static_cast<int>(sizeof(float)) * kTile,
+    static_assert(kSurvBytes <= static_cast<int>(sizeof(float)) * kTile &&
+                      kGatherBytes <= static_cast<int>(sizeof(float)) * kTile,
                   "epilogue buffers fit in the accumulator array");
     extern __shared__ __align__(16) unsigned char smem_raw[];
     Smem& S = *reinterpret_cast<Smem*>(smem_raw);
@@ -270,12 +210,15 @@ __global__ void __launch_bounds__(kCons, CAPW == 192 ? 2 : 1) search_fast_kernel
     const uint32_t cb = ix.code_bits;
     const uint32_t row_lo = a.row_lo, row_hi = a.row_hi;
     const double k1 = a.k1, bb = a.b;
+    const uint32_t eb = ix.bk_eb;
     const uint32_t stride = a.stab_stride;
     uint32_t* stab = a.stab + static_cast<uint64_t>(blockIdx.x) * kMaxTerms * stride;
     const uint32_t kmax = FastCfg<CAPW>::kMaxKServed;
+    const uint32_t wbase = static_cast<uint32_t>(warp) * (kUnitRows * 4);  // my unit, bytes into acc
+    char* const accw = reinterpret_cast<char*>(S.acc) + wbase;
 
     for (int i = tid; i < kTile; i += kCons) S.acc[i] = 0.f;
-    for (int i = tid; i < kMaxCodes; i += kCons) S.w32[i] = a.w32[i];
+    for (int i = tid; i < kShortCodes; i += kCons) S.w32s[i] = a.w32[i];
     if (tid < kConsWarps) S.n_w[tid] = 0;
     if (tid == 0) S.Lg = 0u;
     float Lw = 0.f;  // this warp's own k-th lower bound
@@ -321,7 +264,6 @@ __global__ void __launch_bounds__(kCons, CAPW == 192 ? 2 : 1) search_fast_kernel
             S.t_mult[tid] = mult;
             S.t_c32[tid] = static_cast<float>(static_cast<double>(mult) * idf);
             S.t_slot[tid] = slot;
-            S.t_esc[tid] = slot >= 0 ? ix.long_esc[slot] : 0;
         }
         __syncthreads();
         if (tid == 0) {
@@ -331,7 +273,15 @@ __global__ void __launch_bounds__(kCons, CAPW == 192 ? 2 : 1) search_fast_kernel
                 post += S.t_end[i] - S.t_wlo[i];
                 const double idf = S.t_idf[i];
                 if (!(idf > 0.0) || !isfinite(idf)) bad = 1;
-                if (S.t_slot[i] >= 0) S.order_list[nl++] = static_cast<uint16_t>(i);
+                if (S.t_slot[i] >= 0) {  // long terms by df descending: the first one stores
+                    const uint64_t df = S.t_end[i] - S.t_wlo[i];
+                    uint32_t p = nl++;
+                    while (p > 0 && S.t_end[S.order_list[p - 1]] - S.t_wlo[S.order_list[p - 1]] < df) {
+                        S.order_list[p] = S.order_list[p - 1];
+                        --p;
+                    }
+                    S.order_list[p] = static_cast<uint16_t>(i);
+                }
             }
             S.pref[0] = 0;
             for (uint32_t i = 0; i < m; ++i)
@@ -398,22 +348,22 @@ __global__ void __launch_bounds__(kCons, CAPW == 192 ? 2 : 1) search_fast_kernel
         __syncthreads();
 
         // =============================================== tile sweep (per warp)
-        const float delta = static_cast<float>(m + 10) * 5.9604645e-08f;  // (m+10) * 2^-24
+        const float delta = static_cast<float>(m + 10) * 5.9604645e-08f + 1.5258789e-05f;  // (m+10) 2^-24 + 2^-16
         const float f_slack = 1.0f - 2.5f * delta;
-        const uint32_t wr0 = static_cast<uint32_t>(warp) << kSubShift;  // my rows in a tile
+        const uint32_t wr0 = static_cast<uint32_t>(warp) << kUnitShift;  // my rows in a tile
         uint32_t nw = S.n_w[warp];
         bool flood = false;
-        // my sub-range of every long term: lane x holds term x's for the next
-        // tile (prefetched during the current one), the current tile's are in smem
-        // my sub-range of every long term for a tile: copied global -> smem with
-        // cp.async (no registers held), one tile ahead, double-buffered by parity
+        // my sub-range of every long term for a tile: copied global -> smem
+        // with cp.async (no registers held), one tile ahead, double-buffered
         auto load_sub = [&](uint32_t j) {
             if (static_cast<uint32_t>(lane) < n_long) {
                 const uint32_t* tb = tile_row(ix, S.t_slot[S.order_list[lane]]);
-                const uint64_t sub = static_cast<uint64_t>(j) * kSubPerTile + warp;
+                const uint64_t sub = static_cast<uint64_t>(j) * kSubPerTile + warp * kSubPerUnit;
                 uint32_t* dst = S.wsub[j & 1][warp][lane];
                 asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_addr(dst)), "l"(tb + sub) : "memory");
-                asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_addr(dst + 1)), "l"(tb + sub + 1) : "memory");
+                asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_addr(dst + 1)),
+                             "l"(tb + sub + kSubPerUnit)
+                             : "memory");
             }
             asm volatile("cp.async.commit_group;" ::: "memory");
         };
@@ -424,64 +374,29 @@ __global__ void __launch_bounds__(kCons, CAPW == 192 ? 2 : 1) search_fast_kernel
         load_sub(j0);
         for (uint32_t j = j0; j <= j1; ++j) {
             const uint32_t base = j << kTileShift;
-            const uint32_t R0 = max(base, row_lo);
-            const uint32_t R1 = min(base + kTile, row_hi);
-            const uint32_t rlo = R0 - base, rn = R1 - R0;
-            const bool clip = rn != kTile;
+            // my unit's rows inside the window: [u0, u1) tile-local
+            const uint32_t u0 = max(base + wr0, row_lo) - base;
+            const uint32_t u1 = min(base + wr0 + kUnitRows, row_hi) - base;
             wait_sub();
             if (j < j1) load_sub(j + 1);
+            if (u0 >= u1) continue;  // unit outside the window: nothing accumulated, acc stays zero
+            const bool clip = (u1 - u0) != static_cast<uint32_t>(kUnitRows);
             const uint32_t (*wsub)[2] = S.wsub[j & 1][warp];
-            // ---- long terms: my contiguous sub-range of each, straight from HBM/L2
-            if (CAPW == 320) {
-                // one CTA per SM (registers to spare): two steps in flight
-                uint32_t x = 0, o = 0;
-                auto range_n = [&](uint32_t xx) { return wsub[xx][1] - wsub[xx][0]; };
-                auto range_p = [&](uint32_t xx) {
-                    return ix.post + S.t_start[S.order_list[xx]] + wsub[xx][0];
-                };
-                while (x < n_long && range_n(x) == 0) ++x;
-                uint32_t pc[kR];
-                if (x < n_long) step_load(pc, range_p(x), 0, range_n(x));
-                while (x < n_long) {
-                    const uint32_t n = range_n(x);
-                    uint32_t nx = x, no = o + 32 * kR;
-                    if (no >= n) {
-                        no = 0;
-                        ++nx;
-                        while (nx < n_long && range_n(nx) == 0) ++nx;
-                    }
-                    uint32_t pn[kR];
-                    if (nx < n_long) step_load(pn, range_p(nx), no, range_n(nx));
-                    const uint32_t i = S.order_list[x];
-                    const float c = S.t_c32[i];
-                    const uint64_t gb = S.t_start[i] + wsub[x][0];
-                    const bool esc = S.t_esc[i] != 0;
-                    if (!clip && !esc) step_apply<false, false>(S.acc, S.w32, pc, o, n, c, rlo, rn, ix, gb, base, k1, bb);
-                    else if (!esc) step_apply<true, false>(S.acc, S.w32, pc, o, n, c, rlo, rn, ix, gb, base, k1, bb);
-                    else if (!clip) step_apply<false, true>(S.acc, S.w32, pc, o, n, c, rlo, rn, ix, gb, base, k1, bb);
-                    else step_apply<true, true>(S.acc, S.w32, pc, o, n, c, rlo, rn, ix, gb, base, k1, bb);
-                    if (nx != x) __syncwarp();  // the next term may touch the same rows
-#pragma unroll
-                    for (int u = 0; u < kR; ++u) pc[u] = pn[u];
-                    x = nx;
-                    o = no;
+            // ---- long terms: my contiguous sub-range of each (df descending)
+            bool first = true;
+            for (uint32_t x = 0; x < n_long; ++x) {
+                const uint32_t i = S.order_list[x];
+                uint64_t B = S.t_start[i] + wsub[x][0], E = S.t_start[i] + wsub[x][1];
+                if (clip && B < E) {  // window cuts the unit: narrow by row
+                    B = lower_bound_packed(ix.post, B, E, u0 << kCodeBitsLong);
+                    E = lower_bound_packed(ix.post, B, E, u1 << kCodeBitsLong);
                 }
-            } else {
-                for (uint32_t x = 0; x < n_long; ++x) {
-                    const uint32_t i = S.order_list[x];
-                    const float c = S.t_c32[i];
-                    const uint32_t rb = wsub[x][0], re = wsub[x][1];
-                    const uint64_t B = S.t_start[i] + rb;
-                    const uint32_t n = re - rb;
-                    const bool esc = S.t_esc[i] != 0;
-                    if (n) {
-                        if (!clip && !esc) range_rmw<false, false>(S.acc, S.w32, ix.post + B, n, c, rlo, rn, ix, B, base, k1, bb);
-                        else if (!esc) range_rmw<true, false>(S.acc, S.w32, ix.post + B, n, c, rlo, rn, ix, B, base, k1, bb);
-                        else if (!clip) range_rmw<false, true>(S.acc, S.w32, ix.post + B, n, c, rlo, rn, ix, B, base, k1, bb);
-                        else range_rmw<true, true>(S.acc, S.w32, ix.post + B, n, c, rlo, rn, ix, B, base, k1, bb);
-                    }
-                    __syncwarp();  // the next term may touch the same rows from other lanes
-                }
+                const uint32_t n = static_cast<uint32_t>(E - B);
+                if (n == 0) continue;
+                if (first) range_baked<true>(S.acc, wbase, ix.bk + B, n, S.t_c32[i], eb);
+                else range_baked<false>(S.acc, wbase, ix.bk + B, n, S.t_c32[i], eb);
+                first = false;
+                __syncwarp();  // the next term may touch the same rows from other lanes
             }
             // ---- short terms: the tile segment is small; every warp filters its rows
             for (uint32_t s = 0; s < n_short; ++s) {
@@ -494,82 +409,74 @@ __global__ void __launch_bounds__(kCons, CAPW == 192 ? 2 : 1) search_fast_kernel
                     if (g < e) {
                         const uint32_t p = __ldg(ix.post + g);
                         const uint32_t local = (p >> cb) - base;
-                        if (local - wr0 < (1u << kSubShift)) {
+                        if (local - wr0 < static_cast<uint32_t>(kUnitRows)) {
                             const uint32_t code = p & ix.esc_short;
-                            const float w = code < ix.n_codes_short ? S.w32[code] : esc_w(ix, g, base + local, k1, bb);
-                            S.acc[local] = __fmaf_rn(c, w, S.acc[local]);
+                            const float w = code < ix.n_codes_short ? S.w32s[code] : esc_w(ix, g, base + local, k1, bb);
+                            float* acc = reinterpret_cast<float*>(accw) + (swz10(local) & (kUnitRows - 1));
+                            *acc = __fmaf_rn(c, w, *acc);
                         }
                     }
                 }
                 __syncwarp();
             }
-            // ---- scan my rows of the tile: admit candidates, zero accumulators
-            const uint32_t r_lo = max(wr0, rlo), r_hi = min(wr0 + (1u << kSubShift), rlo + rn);
-            float4* acc4 = reinterpret_cast<float4*>(S.acc);
+            // ---- scan my unit: admit candidates, zero accumulators.  Rows
+            // outside the window were never accumulated (zero), so the whole
+            // unit is scanned.
+            float4* acc4 = reinterpret_cast<float4*>(accw);
+            constexpr uint32_t kV = kUnitRows / 4;
+            const float4 z4 = make_float4(0.f, 0.f, 0.f, 0.f);
             if (flood) {  // this query goes to the exact kernel: only keep acc clean
-                if (r_lo < r_hi)
-                    for (uint32_t z = (r_lo >> 2) + lane; z < ((r_hi + 3) >> 2); z += 32)
-                        acc4[z] = make_float4(0.f, 0.f, 0.f, 0.f);
+                for (uint32_t z = lane; z < kV; z += 32) acc4[z] = z4;
                 __syncwarp();
                 continue;
             }
-            if (r_lo < r_hi) {
-                const uint32_t v0 = r_lo >> 2, v1 = (r_hi + 3) >> 2;
-                // admission: A > 0 and A >= L * slack  <=>  A >= max(L * slack, min denormal)
-                float te = fmaxf(fmaxf(Lw, __uint_as_float(S.Lg)) * f_slack, 1.4e-45f);
-                // append the qualifying entries of one float4 per lane (slow path)
-                auto admit = [&](float4 x4, uint32_t v) {
-                    if (nw > static_cast<uint32_t>(CAPW - 128)) {
-                        nw = warp_prune(S, warp, nw, k, Lw, f_slack);
-                        te = fmaxf(fmaxf(Lw, __uint_as_float(S.Lg)) * f_slack, 1.4e-45f);
-                        if (nw > static_cast<uint32_t>(CAPW - 128)) {  // near-tie flood
-                            flood = true;
-                            return;
-                        }
-                    }
-                    const bool q0 = x4.x >= te, q1 = x4.y >= te, q2 = x4.z >= te, q3 = x4.w >= te;
-                    const uint32_t cnt = q0 + q1 + q2 + q3;
-                    if (!__any_sync(0xffffffffu, cnt != 0)) return;
-                    const uint32_t incl = warp_incl_scan(cnt);
-                    uint32_t slot = nw + incl - cnt;
-                    const uint32_t r = base + 4 * v;
-                    auto put = [&](bool ok, uint32_t row, float val) {
-                        if (ok) {
-                            S.cl_row[warp][slot] = row;
-                            S.cl_val[warp][slot] = val;
-                            ++slot;
-                        }
-                    };
-                    put(q0, r, x4.x);
-                    put(q1, r + 1, x4.y);
-                    put(q2, r + 2, x4.z);
-                    put(q3, r + 3, x4.w);
-                    nw += __shfl_sync(0xffffffffu, incl, 31);
-                    __syncwarp();
-                };
-                const float4 z4 = make_float4(0.f, 0.f, 0.f, 0.f);
-                for (uint32_t vb = v0; vb < v1 && !flood; vb += 64) {
-                    const uint32_t va = vb + lane, vc = vb + 32 + lane;
-                    float4 xa = z4, xc = z4;
-                    if (va < v1) {
-                        xa = acc4[va];
-                        acc4[va] = z4;
-                    }
-                    if (vc < v1) {
-                        xc = acc4[vc];
-                        acc4[vc] = z4;
-                    }
-                    const float mx = fmaxf(fmaxf(fmaxf(xa.x, xa.y), fmaxf(xa.z, xa.w)),
-                                           fmaxf(fmaxf(xc.x, xc.y), fmaxf(xc.z, xc.w)));
-                    if (__any_sync(0xffffffffu, mx >= te)) {
-                        admit(xa, va);
-                        if (!flood) admit(xc, vc);
+            // admission: A > 0 and A >= L * slack  <=>  A >= max(L * slack, min denormal)
+            float te = fmaxf(fmaxf(Lw, __uint_as_float(S.Lg)) * f_slack, 1.4e-45f);
+            // append the qualifying entries of one float4 per lane (slow path)
+            auto admit = [&](float4 x4, uint32_t v) {
+                if (nw > static_cast<uint32_t>(CAPW - 128)) {
+                    nw = warp_prune(S, warp, nw, k, Lw, f_slack);
+                    te = fmaxf(fmaxf(Lw, __uint_as_float(S.Lg)) * f_slack, 1.4e-45f);
+                    if (nw > static_cast<uint32_t>(CAPW - 128)) {  // near-tie flood
+                        flood = true;
+                        return;
                     }
                 }
-                if (flood)  // the query goes to the exact kernel: finish zeroing my rows
-                    for (uint32_t z = v0 + lane; z < v1; z += 32) acc4[z] = z4;
+                const bool q0 = x4.x >= te, q1 = x4.y >= te, q2 = x4.z >= te, q3 = x4.w >= te;
+                const uint32_t cnt = q0 + q1 + q2 + q3;
+                if (!__any_sync(0xffffffffu, cnt != 0)) return;
+                const uint32_t incl = warp_incl_scan(cnt);
+                uint32_t slot = nw + incl - cnt;
+                const uint32_t P = wr0 + 4 * v;  // tile-local position of x4.x
+                auto put = [&](bool ok, uint32_t pos, float val) {
+                    if (ok) {
+                        S.cl_row[warp][slot] = base + swz10(pos);  // position -> row (involution)
+                        S.cl_val[warp][slot] = val;
+                        ++slot;
+                    }
+                };
+                put(q0, P, x4.x);
+                put(q1, P + 1, x4.y);
+                put(q2, P + 2, x4.z);
+                put(q3, P + 3, x4.w);
+                nw += __shfl_sync(0xffffffffu, incl, 31);
                 __syncwarp();
+            };
+            for (uint32_t vb = 0; vb < kV && !flood; vb += 64) {
+                const uint32_t va = vb + lane, vc = vb + 32 + lane;
+                const float4 xa = acc4[va], xc = acc4[vc];
+                acc4[va] = z4;
+                acc4[vc] = z4;
+                const float mx = fmaxf(fmaxf(fmaxf(xa.x, xa.y), fmaxf(xa.z, xa.w)),
+                                       fmaxf(fmaxf(xc.x, xc.y), fmaxf(xc.z, xc.w)));
+                if (__any_sync(0xffffffffu, mx >= te)) {
+                    admit(xa, va);
+                    if (!flood) admit(xc, vc);
+                }
             }
+            if (flood)  // the query goes to the exact kernel: finish zeroing my rows
+                for (uint32_t z = lane; z < kV; z += 32) acc4[z] = z4;
+            __syncwarp();
         }
         if (lane == 0) {
             S.n_w[warp] = nw;
@@ -614,7 +521,7 @@ __global__ void __launch_bounds__(kCons, CAPW == 192 ? 2 : 1) search_fast_kernel
                 const bool keep = i < nc && gv[i] >= theta;
                 const uint32_t bal = __ballot_sync(0xffffffffu, keep);
                 const uint32_t pos = w + __popc(bal & ((1u << lane) - 1));
-                if (keep && pos < kSurvCap) S.cl_row[0][pos] = gr[i];  // list area is free now
+                if (keep && pos < kSurvCap) (&S.cl_row[0][0])[pos] = gr[i];  // list area is free now
                 w += __popc(bal);
                 __syncwarp();
             }
@@ -631,7 +538,7 @@ __global__ void __launch_bounds__(kCons, CAPW == 192 ? 2 : 1) search_fast_kernel
         }
         SurvView sv{reinterpret_cast<double*>(sp), reinterpret_cast<uint64_t*>(sp + 8 * kSurvCap),
                     reinterpret_cast<uint32_t*>(sp + 16 * kSurvCap)};
-        for (uint32_t i = tid; i < ns; i += kCons) sv.row[i] = S.cl_row[0][i];
+        for (uint32_t i = tid; i < ns; i += kCons) sv.row[i] = (&S.cl_row[0][0])[i];
         csync();
         // warp per survivor, lanes over plan terms; fp64 sum in plan order
         for (uint32_t s = warp; s < ns; s += kConsWarps) {
@@ -700,37 +607,32 @@ static cudaError_t fast_attr() {
     return e;
 }
 
-// CAPW 192 (k <= 32): two 16-warp CTAs per SM; CAPW 320 (k <= 128): one.
-// HM_FAST_CTAS=1 forces the one-CTA variant (experiments).
+// CAPW 192 (k <= 32) or 320 (k <= 128); two 8-warp CTAs per SM either way.
 cudaError_t launch_search(const DevIndex& ix, const BatchArgs& a, int sms, cudaStream_t st) {
-    static const bool force1 = [] {
-        const char* e = getenv("HM_FAST_CTAS");
-        return e && e[0] == '1';
-    }();
-    if (a.k <= FastCfg<192>::kMaxKServed && !force1) {
+    if (a.k <= FastCfg<192>::kMaxKServed) {
         const cudaError_t e = fast_attr<192>();
         if (e != cudaSuccess) return e;
         search_fast_kernel<192><<<2 * sms, kCons, sizeof(FastSmem<192>), st>>>(ix, a);
     } else {
         const cudaError_t e = fast_attr<320>();
         if (e != cudaSuccess) return e;
-        search_fast_kernel<320><<<sms, kCons, sizeof(FastSmem<320>), st>>>(ix, a);
+        search_fast_kernel<320><<<2 * sms, kCons, sizeof(FastSmem<320>), st>>>(ix, a);
     }
     return cudaGetLastError();
 }
 
 cudaError_t search_occupancy_fast(int* blocks) {
+    int b[2] = {0, 0};
     cudaError_t e = fast_attr<192>();
+    if (e == cudaSuccess)
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b[0], search_fast_kernel<192>, kCons,
+                                                          sizeof(FastSmem<192>));
+    if (e == cudaSuccess) e = fast_attr<320>();
+    if (e == cudaSuccess)
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b[1], search_fast_kernel<320>, kCons,
+                                                          sizeof(FastSmem<320>));
     if (e != cudaSuccess) return e;
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks, search_fast_kernel<192>, kCons,
-                                                      sizeof(FastSmem<192>));
-    if (e != cudaSuccess) return e;
-    int b320 = 0;
-    e = fast_attr<320>();
-    if (e != cudaSuccess) return e;
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b320, search_fast_kernel<320>, kCons,
-                                                      sizeof(FastSmem<320>));
-    if (*blocks < 2 || b320 < 1) return cudaErrorInvalidConfiguration;
+    if (b[0] < 2 || b[1] < 2) return cudaErrorInvalidConfiguration;
     *blocks = 1;  // grid is sized in launch_search from the SM count
     return e;
 }

@@ -70,11 +70,13 @@ int main() {
                 std::uint32_t t;
                 std::uint64_t i;
                 in >> t >> i;
-                std::cout << "V " << hexd(idx.bm25_term_score(t, i, Bm25Params{})) << '\n';
+                const double v = idx.bm25_term_score(t, i, Bm25Params{});  // may throw: print nothing first
+                std::cout << "V " << hexd(v) << '\n';
             } else if (cmd == "UB") {
                 std::vector<std::string> q;
                 for (std::string t; in >> t;) q.push_back(t);
-                std::cout << "V " << hexd(idx.query_upper_bound(q)) << '\n';
+                const double v = idx.query_upper_bound(q);
+                std::cout << "V " << hexd(v) << '\n';
             } else if (cmd == "RECORDS") {
                 std::size_t n;
                 in >> n;
@@ -107,7 +109,8 @@ int main() {
             } else if (cmd == "KSTAR") {
                 double e, l;
                 in >> e >> l;
-                std::cout << "V " << k_star(e, l) << '\n';
+                const auto v = k_star(e, l);
+                std::cout << "V " << v << '\n';
             } else {
                 std::cout << "ERR unknown " << cmd << '\n';
             }
