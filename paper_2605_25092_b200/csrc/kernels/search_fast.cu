@@ -145,34 +145,56 @@ __device__ uint32_t warp_prune(FastSmem<CAPW>& S, int w, uint32_t n, uint32_t k,
 }
 
 // ---------------------------------------------------------------- long terms
-// One baked posting: impact in the top 19 bits, accumulator byte offset in
-// the low 13.  (p >> 6) + eb puts the impact's exponent and 16 mantissa bits
-// in place; the offset's top 7 bits land below them (relative error < 2^-16,
+// Baked postings: impact in the top 19 bits, accumulator byte offset in the
+// low 13.  (p >> 6) + eb puts the impact's exponent and 16 mantissa bits in
+// place; the offset's top 7 bits land below them (relative error < 2^-16,
 // covered by delta).  acc is the first smem member and warp units are
-// 8 KB-aligned, so the address is one OR of the unit base.
-template <bool FIRST>
-__device__ __forceinline__ void apply1(float* __restrict__ acc, uint32_t wbase, uint32_t p, float c,
-                                       uint32_t eb) {
-    float* a = reinterpret_cast<float*>(reinterpret_cast<char*>(acc) + (wbase | (p & kOffMask)));
-    const float w = __uint_as_float((p >> kImpShift) + eb);
-    if (FIRST) *a = c * w;
-    else *a = __fmaf_rn(c, w, *a);
+// 8 KB-aligned, so the address is one OR of the unit base.  CLIP (a window
+// cuts the unit; the bake permuted the range, so it cannot be narrowed):
+// postings whose tile-local row is outside [u0, u1) are skipped.
+struct Clip {
+    uint32_t wr0, u0, u1;
+};
+__device__ __forceinline__ uint32_t bk_off(uint32_t wbase, uint32_t p) { return wbase | (p & kOffMask); }
+__device__ __forceinline__ float bk_w(uint32_t p, uint32_t eb) { return __uint_as_float((p >> kImpShift) + eb); }
+__device__ __forceinline__ bool bk_in(const Clip& k, uint32_t p) {
+    return (k.wr0 + swz10((p & kOffMask) >> 2)) - k.u0 < k.u1 - k.u0;
 }
 
-// Accumulate one long term's contiguous posting range (the warp's own rows):
-// unaligned head/tail words by single loads, the 16-byte-aligned body with up
-// to kU 128-bit loads per lane in flight.  Rows of one term are distinct, so
-// the order of the read-modify-writes inside the range is free.
-template <bool FIRST>
+// apply N baked postings (the rows are distinct: all loads, then all stores)
+template <bool FIRST, bool CLIP, int N>
+__device__ __forceinline__ void apply_n(float* __restrict__ acc, uint32_t wbase, const uint32_t* p, float c,
+                                        uint32_t eb, const Clip& k) {
+    char* base = reinterpret_cast<char*>(acc);
+    float a[N];
+    if (!FIRST) {
+#pragma unroll
+        for (int e = 0; e < N; ++e)
+            if (!CLIP || bk_in(k, p[e])) a[e] = *reinterpret_cast<float*>(base + bk_off(wbase, p[e]));
+    }
+#pragma unroll
+    for (int e = 0; e < N; ++e) {
+        if (CLIP && !bk_in(k, p[e])) continue;
+        float* dst = reinterpret_cast<float*>(base + bk_off(wbase, p[e]));
+        if (FIRST) *dst = c * bk_w(p[e], eb);
+        else *dst = __fmaf_rn(c, bk_w(p[e], eb), a[e]);
+    }
+}
+
+// Accumulate one long term's posting range of the warp's unit: unaligned
+// head/tail words in one instruction, the 16-byte-aligned body with up to kU
+// 128-bit loads per lane in flight, applied two chunks (8 postings) at a time.
+template <bool FIRST, bool CLIP>
 __device__ __forceinline__ void range_baked(float* __restrict__ acc, uint32_t wbase,
-                                            const uint32_t* __restrict__ pb, uint32_t n, float c, uint32_t eb) {
+                                            const uint32_t* __restrict__ pb, uint32_t n, float c, uint32_t eb,
+                                            const Clip& k) {
     const uint32_t lane = threadIdx.x & 31;
     uint32_t h = static_cast<uint32_t>((16u - (reinterpret_cast<uintptr_t>(pb) & 15u)) & 15u) >> 2;
     h = min(h, n);
     const uint32_t body = n - h, nc = body >> 2, tl = body & 3;
     if (lane < h + tl) {
-        const uint32_t idx = lane < h ? lane : 4 * nc + lane;
-        apply1<FIRST>(acc, wbase, ldg_stream(pb + idx), c, eb);
+        const uint32_t p = ldg_stream(pb + (lane < h ? lane : 4 * nc + lane));
+        apply_n<FIRST, CLIP, 1>(acc, wbase, &p, c, eb, k);
     }
     const uint4* pc = reinterpret_cast<const uint4*>(pb + h);
     for (uint32_t c0 = 0; c0 < nc; c0 += 32 * kU) {
@@ -180,16 +202,19 @@ __device__ __forceinline__ void range_baked(float* __restrict__ acc, uint32_t wb
 #pragma unroll
         for (int u = 0; u < kU; ++u) {
             const uint32_t i = c0 + 32 * u + lane;
-            if (c0 + 32 * u < nc) v[u] = i < nc ? ldg_stream(pc + i) : make_uint4(0, 0, 0, 0);
+            v[u] = make_uint4(0, 0, 0, 0);
+            if (c0 + 32 * u < nc && i < nc) v[u] = ldg_stream(pc + i);
         }
 #pragma unroll
-        for (int u = 0; u < kU; ++u) {
+        for (int u = 0; u < kU; u += 2) {
             if (c0 + 32 * u >= nc) break;  // warp-uniform
-            if (c0 + 32 * u + lane < nc) {
-                apply1<FIRST>(acc, wbase, v[u].x, c, eb);
-                apply1<FIRST>(acc, wbase, v[u].y, c, eb);
-                apply1<FIRST>(acc, wbase, v[u].z, c, eb);
-                apply1<FIRST>(acc, wbase, v[u].w, c, eb);
+            const bool ok0 = c0 + 32 * u + lane < nc, ok1 = c0 + 32 * (u + 1) + lane < nc;
+            if (ok1) {  // both chunks
+                const uint32_t p[8] = {v[u].x, v[u].y, v[u].z, v[u].w, v[u + 1].x, v[u + 1].y, v[u + 1].z, v[u + 1].w};
+                apply_n<FIRST, CLIP, 8>(acc, wbase, p, c, eb, k);
+            } else if (ok0) {
+                const uint32_t p[4] = {v[u].x, v[u].y, v[u].z, v[u].w};
+                apply_n<FIRST, CLIP, 4>(acc, wbase, p, c, eb, k);
             }
         }
     }
@@ -381,20 +406,23 @@ __global__ void __launch_bounds__(kCons, 2) search_fast_kernel(DevIndex ix, Batc
             if (j < j1) load_sub(j + 1);
             if (u0 >= u1) continue;  // unit outside the window: nothing accumulated, acc stays zero
             const bool clip = (u1 - u0) != static_cast<uint32_t>(kUnitRows);
+            const Clip ck{wr0, u0, u1};
             const uint32_t (*wsub)[2] = S.wsub[j & 1][warp];
             // ---- long terms: my contiguous sub-range of each (df descending)
             bool first = true;
             for (uint32_t x = 0; x < n_long; ++x) {
                 const uint32_t i = S.order_list[x];
-                uint64_t B = S.t_start[i] + wsub[x][0], E = S.t_start[i] + wsub[x][1];
-                if (clip && B < E) {  // window cuts the unit: narrow by row
-                    B = lower_bound_packed(ix.post, B, E, u0 << kCodeBitsLong);
-                    E = lower_bound_packed(ix.post, B, E, u1 << kCodeBitsLong);
-                }
-                const uint32_t n = static_cast<uint32_t>(E - B);
+                const uint64_t B = S.t_start[i] + wsub[x][0];
+                const uint32_t n = wsub[x][1] - wsub[x][0];
                 if (n == 0) continue;
-                if (first) range_baked<true>(S.acc, wbase, ix.bk + B, n, S.t_c32[i], eb);
-                else range_baked<false>(S.acc, wbase, ix.bk + B, n, S.t_c32[i], eb);
+                const float c = S.t_c32[i];
+                if (!clip) {
+                    if (first) range_baked<true, false>(S.acc, wbase, ix.bk + B, n, c, eb, ck);
+                    else range_baked<false, false>(S.acc, wbase, ix.bk + B, n, c, eb, ck);
+                } else {
+                    if (first) range_baked<true, true>(S.acc, wbase, ix.bk + B, n, c, eb, ck);
+                    else range_baked<false, true>(S.acc, wbase, ix.bk + B, n, c, eb, ck);
+                }
                 first = false;
                 __syncwarp();  // the next term may touch the same rows from other lanes
             }
