@@ -46,7 +46,7 @@ constexpr int kUnitShift = 11;            // 2048 rows per warp unit
 constexpr int kUnitRows = 1 << kUnitShift;
 constexpr int kSubPerUnit = kUnitRows >> kSubShift;  // 2 sub-tiles of the table
 constexpr int kFastTerms = 32;            // plan size served by this kernel
-constexpr int kU = 8;                     // 16-byte loads per lane in flight
+constexpr int kU = 4;                     // 16-byte loads per lane per pipeline step
 constexpr uint32_t kOffMask = (kUnitRows * 4 - 1) & ~3u;  // bk: impact (19 bits) | byte offset (13 bits)
 constexpr int kImpShift = 2 + kUnitShift - (23 - kBakeMantBits);
 static_assert(kConsWarps * kUnitRows == kTile, "one warp per 2048-row unit");
@@ -181,41 +181,55 @@ __device__ __forceinline__ void apply_n(float* __restrict__ acc, uint32_t wbase,
     }
 }
 
-// Accumulate one long term's posting range of the warp's unit: unaligned
-// head/tail words in one instruction, the 16-byte-aligned body with up to kU
-// 128-bit loads per lane in flight, applied two chunks (8 postings) at a time.
-template <bool FIRST, bool CLIP>
-__device__ __forceinline__ void range_baked(float* __restrict__ acc, uint32_t wbase,
-                                            const uint32_t* __restrict__ pb, uint32_t n, float c, uint32_t eb,
-                                            const Clip& k) {
+// One pipeline step of a long term's posting range in the warp's unit: the
+// range's unaligned head/tail words (first step only, one per lane) and up to
+// 32*kU 16-byte chunks of its aligned body.
+struct Step {
+    uint64_t B;        // range start (element index into bk / post)
+    uint32_t j, x, o;  // tile, range (long-term slot in order_list), chunk offset; j > j1: none
+    uint32_t n;        // postings in the range
+    float c;           // mult * idf of the term (fp32)
+    bool first;        // first range of the unit in this tile: store instead of read-modify-write
+};
+struct StepGeom {
+    uint32_t h, nc, tl;
+};
+__device__ __forceinline__ StepGeom step_geom(uint64_t B, uint32_t n) {
+    const uint32_t h = min((4u - (static_cast<uint32_t>(B) & 3u)) & 3u, n);
+    return {h, (n - h) >> 2, (n - h) & 3};
+}
+
+__device__ __forceinline__ void step_load(const uint32_t* __restrict__ bk, const Step& s, uint4 (&v)[kU],
+                                          uint32_t& sc) {
     const uint32_t lane = threadIdx.x & 31;
-    uint32_t h = static_cast<uint32_t>((16u - (reinterpret_cast<uintptr_t>(pb) & 15u)) & 15u) >> 2;
-    h = min(h, n);
-    const uint32_t body = n - h, nc = body >> 2, tl = body & 3;
-    if (lane < h + tl) {
-        const uint32_t p = ldg_stream(pb + (lane < h ? lane : 4 * nc + lane));
-        apply_n<FIRST, CLIP, 1>(acc, wbase, &p, c, eb, k);
+    const StepGeom g = step_geom(s.B, s.n);
+    const uint32_t* pb = bk + s.B;
+    if (s.o == 0 && lane < g.h + g.tl) sc = ldg_stream(pb + (lane < g.h ? lane : 4 * g.nc + lane));
+    const uint4* pc = reinterpret_cast<const uint4*>(pb + g.h);
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+        const uint32_t i = s.o + 32 * u + lane;
+        v[u] = make_uint4(0, 0, 0, 0);
+        if (s.o + 32 * u < g.nc && i < g.nc) v[u] = ldg_stream(pc + i);
     }
-    const uint4* pc = reinterpret_cast<const uint4*>(pb + h);
-    for (uint32_t c0 = 0; c0 < nc; c0 += 32 * kU) {
-        uint4 v[kU];
+}
+
+template <bool FIRST, bool CLIP>
+__device__ __forceinline__ void step_apply(float* __restrict__ acc, uint32_t wbase, const Step& s,
+                                           const uint4 (&v)[kU], uint32_t sc, uint32_t eb, const Clip& k) {
+    const uint32_t lane = threadIdx.x & 31;
+    const StepGeom g = step_geom(s.B, s.n);
+    if (s.o == 0 && lane < g.h + g.tl) apply_n<FIRST, CLIP, 1>(acc, wbase, &sc, s.c, eb, k);
 #pragma unroll
-        for (int u = 0; u < kU; ++u) {
-            const uint32_t i = c0 + 32 * u + lane;
-            v[u] = make_uint4(0, 0, 0, 0);
-            if (c0 + 32 * u < nc && i < nc) v[u] = ldg_stream(pc + i);
-        }
-#pragma unroll
-        for (int u = 0; u < kU; u += 2) {
-            if (c0 + 32 * u >= nc) break;  // warp-uniform
-            const bool ok0 = c0 + 32 * u + lane < nc, ok1 = c0 + 32 * (u + 1) + lane < nc;
-            if (ok1) {  // both chunks
-                const uint32_t p[8] = {v[u].x, v[u].y, v[u].z, v[u].w, v[u + 1].x, v[u + 1].y, v[u + 1].z, v[u + 1].w};
-                apply_n<FIRST, CLIP, 8>(acc, wbase, p, c, eb, k);
-            } else if (ok0) {
-                const uint32_t p[4] = {v[u].x, v[u].y, v[u].z, v[u].w};
-                apply_n<FIRST, CLIP, 4>(acc, wbase, p, c, eb, k);
-            }
+    for (int u = 0; u < kU; u += 2) {
+        if (s.o + 32 * u >= g.nc) break;  // warp-uniform
+        const bool ok0 = s.o + 32 * u + lane < g.nc, ok1 = s.o + 32 * (u + 1) + lane < g.nc;
+        if (ok1) {  // both chunks
+            const uint32_t p[8] = {v[u].x, v[u].y, v[u].z, v[u].w, v[u + 1].x, v[u + 1].y, v[u + 1].z, v[u + 1].w};
+            apply_n<FIRST, CLIP, 8>(acc, wbase, p, s.c, eb, k);
+        } else if (ok0) {
+            const uint32_t p[4] = {v[u].x, v[u].y, v[u].z, v[u].w};
+            apply_n<FIRST, CLIP, 4>(acc, wbase, p, s.c, eb, k);
         }
     }
 }
@@ -396,36 +410,85 @@ __global__ void __launch_bounds__(kCons, 2) search_fast_kernel(DevIndex ix, Batc
             asm volatile("cp.async.wait_group 0;" ::: "memory");
             __syncwarp();
         };
+        // Long terms run as a software pipeline of steps over (tile, range,
+        // chunk): the loads of the next step -- possibly the first range of a
+        // later tile -- are in flight while the current step is applied, and
+        // across the short-term pass and the scan of a tile.
+        uint32_t ready = j0;  // last tile whose sub-ranges are resident in wsub
         load_sub(j0);
+        wait_sub();
+        if (j0 < j1) load_sub(j0 + 1);
+        auto live = [&](uint32_t j, uint32_t& u0, uint32_t& u1) {
+            const uint32_t base = j << kTileShift;
+            u0 = max(base + wr0, row_lo) - base;
+            u1 = min(base + wr0 + kUnitRows, row_hi) - base;
+            return u0 < u1;
+        };
+        // first nonempty range at or after (j, x)
+        auto seek = [&](uint32_t j, uint32_t x, bool fst) -> Step {
+            for (;;) {
+                if (j > j1) return Step{0, j, 0, 0, 0, 0.f, false};
+                if (j > ready) {
+                    wait_sub();
+                    ready = j;
+                    if (j < j1) load_sub(j + 1);
+                }
+                uint32_t u0, u1;
+                if (live(j, u0, u1)) {
+                    const uint32_t (*ws)[2] = S.wsub[j & 1][warp];
+                    for (; x < n_long; ++x) {
+                        const uint32_t n = ws[x][1] - ws[x][0];
+                        if (n) {
+                            const uint32_t i = S.order_list[x];
+                            return Step{S.t_start[i] + ws[x][0], j, x, 0, n, S.t_c32[i], fst};
+                        }
+                    }
+                }
+                ++j;
+                x = 0;
+                fst = true;
+            }
+        };
+        auto advance = [&](const Step& s) -> Step {
+            const StepGeom g = step_geom(s.B, s.n);
+            if (s.o + 32 * kU < g.nc) {
+                Step t = s;
+                t.o += 32 * kU;
+                return t;
+            }
+            return seek(s.j, s.x + 1, false);
+        };
+        Step cur = seek(j0, 0, true);
+        uint4 va[kU];
+        uint32_t sa = 0;
+        if (cur.j <= j1) step_load(ix.bk, cur, va, sa);
         for (uint32_t j = j0; j <= j1; ++j) {
             const uint32_t base = j << kTileShift;
-            // my unit's rows inside the window: [u0, u1) tile-local
-            const uint32_t u0 = max(base + wr0, row_lo) - base;
-            const uint32_t u1 = min(base + wr0 + kUnitRows, row_hi) - base;
-            wait_sub();
-            if (j < j1) load_sub(j + 1);
-            if (u0 >= u1) continue;  // unit outside the window: nothing accumulated, acc stays zero
+            uint32_t u0, u1;
+            const bool unit_live = live(j, u0, u1);
             const bool clip = (u1 - u0) != static_cast<uint32_t>(kUnitRows);
             const Clip ck{wr0, u0, u1};
-            const uint32_t (*wsub)[2] = S.wsub[j & 1][warp];
-            // ---- long terms: my contiguous sub-range of each (df descending)
-            bool first = true;
-            for (uint32_t x = 0; x < n_long; ++x) {
-                const uint32_t i = S.order_list[x];
-                const uint64_t B = S.t_start[i] + wsub[x][0];
-                const uint32_t n = wsub[x][1] - wsub[x][0];
-                if (n == 0) continue;
-                const float c = S.t_c32[i];
+            // ---- long terms of this tile (df descending; the first one stores)
+            while (cur.j == j) {
+                const Step nxt = advance(cur);
+                uint4 vb[kU];
+                uint32_t sb = 0;
+                if (nxt.j <= j1) step_load(ix.bk, nxt, vb, sb);
                 if (!clip) {
-                    if (first) range_baked<true, false>(S.acc, wbase, ix.bk + B, n, c, eb, ck);
-                    else range_baked<false, false>(S.acc, wbase, ix.bk + B, n, c, eb, ck);
+                    if (cur.first) step_apply<true, false>(S.acc, wbase, cur, va, sa, eb, ck);
+                    else step_apply<false, false>(S.acc, wbase, cur, va, sa, eb, ck);
                 } else {
-                    if (first) range_baked<true, true>(S.acc, wbase, ix.bk + B, n, c, eb, ck);
-                    else range_baked<false, true>(S.acc, wbase, ix.bk + B, n, c, eb, ck);
+                    if (cur.first) step_apply<true, true>(S.acc, wbase, cur, va, sa, eb, ck);
+                    else step_apply<false, true>(S.acc, wbase, cur, va, sa, eb, ck);
                 }
-                first = false;
-                __syncwarp();  // the next term may touch the same rows from other lanes
+                // the next range (another term) may touch the same rows from other lanes
+                if (nxt.j != cur.j || nxt.x != cur.x) __syncwarp();
+                cur = nxt;
+#pragma unroll
+                for (int u = 0; u < kU; ++u) va[u] = vb[u];
+                sa = sb;
             }
+            if (!unit_live) continue;  // unit outside the window: nothing accumulated, acc stays zero
             // ---- short terms: the tile segment is small; every warp filters its rows
             for (uint32_t s = 0; s < n_short; ++s) {
                 const uint32_t i = S.order_list[n_long + s];
