@@ -398,18 +398,40 @@ void build_index(const hm_csr_view* v, hm_index* X) {
     d.code_len = dev_upload(X->code_len.data(), hm::kMaxCodes, A, B);
     X->n_long = static_cast<uint32_t>(long_terms.size());
     X->d_long_terms = dev_upload(long_terms.data(), long_terms.size(), A, B);
+    // baked-posting index space: every (long term, 2048-row unit) range padded
+    // to a multiple of 4 words and 16-byte aligned (kernels/bake.cu)
     {
+        const uint64_t n_units = static_cast<uint64_t>(n_tiles) * hm::kUnitsPerTile;
+        std::vector<uint64_t> base(std::max<size_t>(long_terms.size(), 1), 0);
+        std::vector<uint32_t> uoff(long_terms.size() * (n_units + 1));
+        uint64_t tot = 0;
+        for (size_t s = 0; s < long_terms.size(); ++s) {
+            const uint32_t* row = tab.data() + s * (n_sub + 1);
+            uint32_t* uo = uoff.data() + s * (n_units + 1);
+            base[s] = tot;
+            uint32_t acc = 0;
+            for (uint64_t u = 0; u < n_units; ++u) {
+                uo[u] = acc;
+                const uint32_t n = row[(u + 1) * hm::kSubPerUnit] - row[u * hm::kSubPerUnit];
+                acc += (n + 3) & ~3u;
+            }
+            uo[n_units] = acc;
+            tot += acc;
+        }
+        d.bk_base = dev_upload(base.data(), base.size(), A, B);
+        d.bk_uoff = dev_upload(uoff.data(), uoff.size(), A, B);
+        d.n_units = static_cast<uint32_t>(n_units);
         void* p = nullptr;
-        ck(cudaMalloc(&p, std::max<uint64_t>(P, 1) * 4 + 16), "cudaMalloc(bk)");
+        ck(cudaMalloc(&p, std::max<uint64_t>(tot, 4) * 4), "cudaMalloc(bk)");
         A.push_back(p);
-        B += std::max<uint64_t>(P, 1) * 4 + 16;
+        B += std::max<uint64_t>(tot, 4) * 4;
         X->d_bk = static_cast<uint32_t*>(p);
         ck(cudaMalloc(&p, 16), "cudaMalloc(bake err)");
         A.push_back(p);
         X->d_bake_err = static_cast<uint32_t*>(p);
     }
     d.bk = X->d_bk;
-    d.bk_eb = 0;
+    d.bk_ks = 0;
     d.n_terms = V;
     d.n_docs = N;
     d.n_tiles = n_tiles;
@@ -595,14 +617,14 @@ bool ensure_baked(hm_index* X, double k1, double b, std::shared_lock<std::shared
         std::unique_lock<std::shared_mutex> ul(X->bake_mu);
         if (X->bake_valid && X->bake_k1 == k1 && X->bake_b == b) continue;
         X->bake_valid = false;
-        const uint32_t eb = hm::bake_eb(k1);
+        const uint32_t ks = hm::bake_ks(k1);
         cudaStream_t st = nullptr;
         ck(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking), "bake stream");
         uint32_t err = 0;
         try {
             ck(cudaMemsetAsync(X->d_bake_err, 0, 4, st), "bake memset");
             hm::DevIndex d = X->dev;
-            ck(hm::launch_bake(d, X->d_long_terms, X->n_long, k1, b, eb, X->d_bk, X->d_bake_err, st),
+            ck(hm::launch_bake(d, X->d_long_terms, X->n_long, k1, b, ks, X->d_bk, X->d_bake_err, st),
                "bake kernel");
             ck(cudaMemcpyAsync(&err, X->d_bake_err, 4, cudaMemcpyDeviceToHost, st), "bake D2H");
             ck(cudaStreamSynchronize(st), "bake sync");
@@ -611,7 +633,7 @@ bool ensure_baked(hm_index* X, double k1, double b, std::shared_lock<std::shared
             throw;
         }
         cudaStreamDestroy(st);
-        X->dev.bk_eb = eb;
+        X->dev.bk_ks = ks;
         X->bake_k1 = k1;
         X->bake_b = b;
         X->bake_ok = err == 0;

@@ -27,10 +27,10 @@ cudaError_t launch_merge(uint32_t n_shards, uint32_t nq, uint32_t k, const uint6
                          double* out_scores, uint32_t* out_n, double* out_conf,
                          uint8_t* out_skip, cudaStream_t st);
 // K0: bake the long-term postings into bk[] for (k1, b); *err |= 1 when an
-// impact falls outside the 8 representable binades (kernels/bake.cu)
-uint32_t bake_eb(double k1);
+// impact falls outside the 7 representable binades (kernels/bake.cu)
+uint32_t bake_ks(double k1);
 cudaError_t launch_bake(const DevIndex& ix, const uint32_t* long_terms, uint32_t n_long, double k1,
-                        double b, uint32_t eb, uint32_t* bk, uint32_t* err, cudaStream_t st);
+                        double b, uint32_t ks, uint32_t* bk, uint32_t* err, cudaStream_t st);
 // resident CTAs per SM of the two persistent kernels
 cudaError_t search_occupancy(int* search_blocks_per_sm, int* exact_blocks_per_sm);
 cudaError_t search_occupancy_fast(int* blocks);

@@ -19,21 +19,26 @@
 //                 of the first posting of every 1024-row sub-tile (long terms
 //                 only); tile j starts at entry 16*j.
 //   doc_lens[N] u32, doc_ids[N] u64, code_tf/code_len[kMaxCodes] u32.
-//   bk[P]        u32 BAKED long-term postings for one (k1, b), same indexing
-//                 as post[] (short-term slots unused), written by bake_kernel:
-//                   (q19 << 13) | (off11 << 2)
-//                 q19 = (float_bits(w) - bk_eb) >> 7: the idf-free impact
-//                 w = tf*(k1+1)/(tf + k1*(1-b+b*len/avgdl)) truncated to 3
-//                 exponent + 16 mantissa bits (8 binades below k1+1, relative
-//                 error < 2^-16); off11 = swz10(r) & 2047, r = tile-local row:
-//                 the row's accumulator inside the search kernel's 2048-row
-//                 warp unit, XOR-swizzled so that read-modify-writes of dense
-//                 runs of rows (lane strides 1, 2, 4 .. 32) are
-//                 bank-conflict-free; the low 13 bits are its byte offset.
-//                 Decoding: float_bits = (word >> 6) + bk_eb (one LEA.HI; the
-//                 offset's top 7 bits land below the 16 kept mantissa bits,
-//                 so the decoded impact stays within 2^-16 of w) and
-//                 offset = word & 0x1FFC (one LOP3).
+//   bk[]         u32 BAKED long-term postings for one (k1, b) (bake_kernel),
+//                 in their own index space: the range of long term `slot` in
+//                 2048-row unit u (= the rows a search-kernel warp owns in one
+//                 tile) is bk[bk_base[slot] + bk_uoff[slot][u] ..
+//                 bk_base[slot] + bk_uoff[slot][u+1]), padded to a multiple
+//                 of 4 words and 16-byte aligned.  Word = (q19 << 13) | off13:
+//                   q19 = float_bits(w * 2^-ks) >> 7 -- the idf-free impact
+//                         w = tf*(k1+1)/(tf + k1*(1-b+b*len/avgdl)) scaled
+//                         into the 7 lowest normal binades (exponent field
+//                         1..7) and truncated to 16 mantissa bits (relative
+//                         error < 2^-16); q19 = 0 is a NULL posting (padding);
+//                   off13 = (swz10(r) & 2047) * 4, r = tile-local row: the
+//                         byte offset of the row's accumulator inside the unit,
+//                         XOR-swizzled so that read-modify-writes of dense runs
+//                         of rows (lane strides 1, 2, 4 .. 32) are
+//                         bank-conflict-free.
+//                 Decoding is one shift: float(word >> 6) is w * 2^-ks with
+//                 the offset's top 7 bits below the kept mantissa bits (error
+//                 < 2^-16), and a NULL decodes to a denormal that the kernel's
+//                 flush-to-zero multiply turns into an exact 0.
 #pragma once
 #include <cstdint>
 
@@ -59,7 +64,11 @@ constexpr int kMaxK = 256;
 constexpr uint32_t kNoTerm = 0xFFFFFFFFu;
 constexpr int kLongFactor = 32;               // long term: df > 32 * n_tiles
 constexpr int kBakeMantBits = 16;             // baked impact: 3 exponent + 16 mantissa bits
-constexpr int kBakeBinades = 8;
+constexpr int kBakeBinades = 7;               // normal exponent fields 1..7
+constexpr int kUnitShift = 11;                // search-kernel warp unit: 2048 rows
+constexpr int kUnitsPerTile = 1 << (kTileShift - kUnitShift);
+constexpr int kSubPerUnit = 1 << (kUnitShift - kSubShift);
+constexpr int kScoreShift = 61;               // fp32 selection scores are score * 2^-61
 constexpr int kShortCodes = 256;              // smem impact table of short-term codes
 static_assert(kLocalBits == kTileShift, "local row field must cover one tile");
 
@@ -84,7 +93,10 @@ struct DevIndex {
     uint32_t n_codes_short;    // codes usable by short terms (< esc_short)
     double avgdl;
     const uint32_t* bk;        // baked long-term postings (see above)
-    uint32_t bk_eb;            // float bits of the lowest baked binade
+    const uint64_t* bk_base;   // [n_long] start of each long term's baked ranges
+    const uint32_t* bk_uoff;   // [n_long][n_units + 1] unit offsets relative to bk_base
+    uint32_t n_units;          // n_tiles * kUnitsPerTile
+    uint32_t bk_ks;            // impact scale exponent: stored value = w * 2^-ks
 };
 
 // swizzled position of a row (only bits 0-4 change, from bits 5-9); an involution

@@ -42,19 +42,18 @@ namespace hm {
 
 constexpr int kCons = 256;                // threads per CTA
 constexpr int kConsWarps = kCons / 32;    // 8: warp w owns unit w of a tile
-constexpr int kUnitShift = 11;            // 2048 rows per warp unit
-constexpr int kUnitRows = 1 << kUnitShift;
-constexpr int kSubPerUnit = kUnitRows >> kSubShift;  // 2 sub-tiles of the table
+constexpr int kUnitRows = 1 << kUnitShift;  // 2048 rows per warp unit (hm_types.h)
 constexpr int kFastTerms = 32;            // plan size served by this kernel
-constexpr int kU = 4;                     // 16-byte loads per lane per pipeline step
 constexpr uint32_t kOffMask = (kUnitRows * 4 - 1) & ~3u;  // bk: impact (19 bits) | byte offset (13 bits)
 constexpr int kImpShift = 2 + kUnitShift - (23 - kBakeMantBits);
+constexpr float kFltMin = 1.17549435e-38f;
 static_assert(kConsWarps * kUnitRows == kTile, "one warp per 2048-row unit");
 static_assert(2 + kUnitShift + 3 + kBakeMantBits == 32, "bk = 19-bit impact | 13-bit offset");
 
 template <int CAPW>
 struct FastCfg {
     static constexpr int kMaxKServed = CAPW == 192 ? 32 : 128;
+    static constexpr int kC = CAPW == 192 ? 3 : 2;  // 16-byte chunks per lane per pipeline step
 };
 
 template <int CAPW>
@@ -68,7 +67,9 @@ struct __align__(16) FastSmem {
     uint32_t t_mult[kFastTerms];
     float t_c32[kFastTerms];
     int32_t t_slot[kFastTerms];
-    uint32_t wsub[2][kConsWarps][kFastTerms][2];  // unit's sub-range of each long term (tile parity)
+    uint4 stg[kConsWarps][2][FastCfg<CAPW>::kC * 32];  // per-warp cp.async staging of baked postings (2 steps)
+    uint64_t t_bkb[kFastTerms];            // long terms: start of the term's baked ranges in bk
+    uint32_t wsub[2][kConsWarps][kFastTerms][2];  // unit's baked range of each long term (tile parity)
     uint16_t order_list[kFastTerms];       // long terms (df descending), then short terms
     uint32_t pref[kFastTerms + 1];         // short-window prefix sums / gather offsets
     uint32_t hist[256];
@@ -145,26 +146,37 @@ __device__ uint32_t warp_prune(FastSmem<CAPW>& S, int w, uint32_t n, uint32_t k,
 }
 
 // ---------------------------------------------------------------- long terms
-// Baked postings: impact in the top 19 bits, accumulator byte offset in the
-// low 13.  (p >> 6) + eb puts the impact's exponent and 16 mantissa bits in
-// place; the offset's top 7 bits land below them (relative error < 2^-16,
-// covered by delta).  acc is the first smem member and warp units are
-// 8 KB-aligned, so the address is one OR of the unit base.  CLIP (a window
-// cuts the unit; the bake permuted the range, so it cannot be narrowed):
-// postings whose tile-local row is outside [u0, u1) are skipped.
+// Baked postings (hm_types.h): impact in the top 19 bits, accumulator byte
+// offset in the low 13.  float(p >> 6) is the impact times 2^-ks (the
+// offset's top 7 bits land below the 16 kept mantissa bits: relative error
+// < 2^-16, covered by delta); a NULL posting decodes to a denormal and the
+// flush-to-zero multiply makes its contribution exactly 0.  acc is the first
+// smem member and warp units are 8 KB-aligned: the address is one OR.  CLIP (a
+// window cuts the unit): postings whose tile-local row is outside [u0, u1)
+// are skipped.
 struct Clip {
     uint32_t wr0, u0, u1;
 };
 __device__ __forceinline__ uint32_t bk_off(uint32_t wbase, uint32_t p) { return wbase | (p & kOffMask); }
-__device__ __forceinline__ float bk_w(uint32_t p, uint32_t eb) { return __uint_as_float((p >> kImpShift) + eb); }
+__device__ __forceinline__ float bk_w(uint32_t p) { return __uint_as_float(p >> kImpShift); }
 __device__ __forceinline__ bool bk_in(const Clip& k, uint32_t p) {
     return (k.wr0 + swz10((p & kOffMask) >> 2)) - k.u0 < k.u1 - k.u0;
+}
+__device__ __forceinline__ float mul_ftz(float a, float b) {
+    float d;
+    asm("mul.rn.ftz.f32 %0, %1, %2;" : "=f"(d) : "f"(a), "f"(b));
+    return d;
+}
+__device__ __forceinline__ float fma_ftz(float a, float b, float c) {
+    float d;
+    asm("fma.rn.ftz.f32 %0, %1, %2, %3;" : "=f"(d) : "f"(a), "f"(b), "f"(c));
+    return d;
 }
 
 // apply N baked postings (the rows are distinct: all loads, then all stores)
 template <bool FIRST, bool CLIP, int N>
 __device__ __forceinline__ void apply_n(float* __restrict__ acc, uint32_t wbase, const uint32_t* p, float c,
-                                        uint32_t eb, const Clip& k) {
+                                        const Clip& k) {
     char* base = reinterpret_cast<char*>(acc);
     float a[N];
     if (!FIRST) {
@@ -176,60 +188,52 @@ __device__ __forceinline__ void apply_n(float* __restrict__ acc, uint32_t wbase,
     for (int e = 0; e < N; ++e) {
         if (CLIP && !bk_in(k, p[e])) continue;
         float* dst = reinterpret_cast<float*>(base + bk_off(wbase, p[e]));
-        if (FIRST) *dst = c * bk_w(p[e], eb);
-        else *dst = __fmaf_rn(c, bk_w(p[e], eb), a[e]);
+        if (FIRST) *dst = mul_ftz(c, bk_w(p[e]));
+        else *dst = fma_ftz(c, bk_w(p[e]), a[e]);
     }
 }
 
-// One pipeline step of a long term's posting range in the warp's unit: the
-// range's unaligned head/tail words (first step only, one per lane) and up to
-// 32*kU 16-byte chunks of its aligned body.
+// One pipeline step of a long term's baked range in the warp's unit: up to
+// 32*kC 16-byte chunks, staged in shared memory by per-lane cp.async (each
+// lane copies and later reads only its own chunks: no warp sync needed).
 struct Step {
-    uint64_t B;        // range start (element index into bk / post)
-    uint32_t j, x, o;  // tile, range (long-term slot in order_list), chunk offset; j > j1: none
-    uint32_t n;        // postings in the range
-    float c;           // mult * idf of the term (fp32)
-    bool first;        // first range of the unit in this tile: store instead of read-modify-write
+    const uint4* base;    // the range's first chunk in bk
+    uint32_t o, nch;      // chunk offset of this step, chunks in the range
+    uint32_t j, x;        // tile, range (long-term slot in order_list); j > j1: none
+    float c;              // mult * idf * 2^(ks - 61) of the term
+    bool first;           // first range of the unit in this tile: store instead of read-modify-write
 };
-struct StepGeom {
-    uint32_t h, nc, tl;
-};
-__device__ __forceinline__ StepGeom step_geom(uint64_t B, uint32_t n) {
-    const uint32_t h = min((4u - (static_cast<uint32_t>(B) & 3u)) & 3u, n);
-    return {h, (n - h) >> 2, (n - h) & 3};
-}
 
-__device__ __forceinline__ void step_load(const uint32_t* __restrict__ bk, const Step& s, uint4 (&v)[kU],
-                                          uint32_t& sc) {
+template <int KC>
+__device__ __forceinline__ void step_issue(const Step& s, uint4* stg) {
     const uint32_t lane = threadIdx.x & 31;
-    const StepGeom g = step_geom(s.B, s.n);
-    const uint32_t* pb = bk + s.B;
-    if (s.o == 0 && lane < g.h + g.tl) sc = ldg_stream(pb + (lane < g.h ? lane : 4 * g.nc + lane));
-    const uint4* pc = reinterpret_cast<const uint4*>(pb + g.h);
 #pragma unroll
-    for (int u = 0; u < kU; ++u) {
-        const uint32_t i = s.o + 32 * u + lane;
-        v[u] = make_uint4(0, 0, 0, 0);
-        if (s.o + 32 * u < g.nc && i < g.nc) v[u] = ldg_stream(pc + i);
+    for (int u = 0; u < KC; ++u) {
+        const uint32_t c = s.o + 32 * u + lane;
+        if (c < s.nch)
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_addr(stg + 32 * u + lane)),
+                         "l"(s.base + c)
+                         : "memory");
     }
 }
 
-template <bool FIRST, bool CLIP>
+template <int KC, bool FIRST, bool CLIP>
 __device__ __forceinline__ void step_apply(float* __restrict__ acc, uint32_t wbase, const Step& s,
-                                           const uint4 (&v)[kU], uint32_t sc, uint32_t eb, const Clip& k) {
+                                           const uint4* stg, const Clip& k) {
     const uint32_t lane = threadIdx.x & 31;
-    const StepGeom g = step_geom(s.B, s.n);
-    if (s.o == 0 && lane < g.h + g.tl) apply_n<FIRST, CLIP, 1>(acc, wbase, &sc, s.c, eb, k);
 #pragma unroll
-    for (int u = 0; u < kU; u += 2) {
-        if (s.o + 32 * u >= g.nc) break;  // warp-uniform
-        const bool ok0 = s.o + 32 * u + lane < g.nc, ok1 = s.o + 32 * (u + 1) + lane < g.nc;
-        if (ok1) {  // both chunks
-            const uint32_t p[8] = {v[u].x, v[u].y, v[u].z, v[u].w, v[u + 1].x, v[u + 1].y, v[u + 1].z, v[u + 1].w};
-            apply_n<FIRST, CLIP, 8>(acc, wbase, p, s.c, eb, k);
+    for (int u = 0; u < KC; u += 2) {
+        if (s.o + 32 * u >= s.nch) break;  // warp-uniform
+        const bool ok0 = s.o + 32 * u + lane < s.nch;
+        const bool ok1 = u + 1 < KC && s.o + 32 * (u + 1) + lane < s.nch;
+        if (ok1) {
+            const uint4 v0 = stg[32 * u + lane], v1 = stg[32 * (u + 1) + lane];
+            const uint32_t p[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
+            apply_n<FIRST, CLIP, 8>(acc, wbase, p, s.c, k);
         } else if (ok0) {
-            const uint32_t p[4] = {v[u].x, v[u].y, v[u].z, v[u].w};
-            apply_n<FIRST, CLIP, 4>(acc, wbase, p, s.c, eb, k);
+            const uint4 v0 = stg[32 * u + lane];
+            const uint32_t p[4] = {v0.x, v0.y, v0.z, v0.w};
+            apply_n<FIRST, CLIP, 4>(acc, wbase, p, s.c, k);
         }
     }
 }
@@ -249,10 +253,10 @@ __global__ void __launch_bounds__(kCons, 2) search_fast_kernel(DevIndex ix, Batc
     const uint32_t cb = ix.code_bits;
     const uint32_t row_lo = a.row_lo, row_hi = a.row_hi;
     const double k1 = a.k1, bb = a.b;
-    const uint32_t eb = ix.bk_eb;
     const uint32_t stride = a.stab_stride;
     uint32_t* stab = a.stab + static_cast<uint64_t>(blockIdx.x) * kMaxTerms * stride;
     const uint32_t kmax = FastCfg<CAPW>::kMaxKServed;
+    constexpr int kC = FastCfg<CAPW>::kC;
     const uint32_t wbase = static_cast<uint32_t>(warp) * (kUnitRows * 4);  // my unit, bytes into acc
     char* const accw = reinterpret_cast<char*>(S.acc) + wbase;
 
@@ -301,8 +305,12 @@ __global__ void __launch_bounds__(kCons, 2) search_fast_kernel(DevIndex ix, Batc
             S.t_end[tid] = w1;
             S.t_idf[tid] = idf;
             S.t_mult[tid] = mult;
-            S.t_c32[tid] = static_cast<float>(static_cast<double>(mult) * idf);
+            // selection scores are score * 2^-61; long terms pair c with the
+            // baked impact * 2^-ks, short terms with the plain impact table
+            const int sh = slot >= 0 ? static_cast<int>(ix.bk_ks) - kScoreShift : -kScoreShift;
+            S.t_c32[tid] = static_cast<float>(ldexp(static_cast<double>(mult) * idf, sh));
             S.t_slot[tid] = slot;
+            S.t_bkb[tid] = slot >= 0 ? ix.bk_base[slot] : 0;
         }
         __syncthreads();
         if (tid == 0) {
@@ -396,12 +404,12 @@ __global__ void __launch_bounds__(kCons, 2) search_fast_kernel(DevIndex ix, Batc
         // with cp.async (no registers held), one tile ahead, double-buffered
         auto load_sub = [&](uint32_t j) {
             if (static_cast<uint32_t>(lane) < n_long) {
-                const uint32_t* tb = tile_row(ix, S.t_slot[S.order_list[lane]]);
-                const uint64_t sub = static_cast<uint64_t>(j) * kSubPerTile + warp * kSubPerUnit;
+                const uint32_t* uo = ix.bk_uoff +
+                                     static_cast<uint64_t>(S.t_slot[S.order_list[lane]]) * (ix.n_units + 1) +
+                                     j * kUnitsPerTile + warp;
                 uint32_t* dst = S.wsub[j & 1][warp][lane];
-                asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_addr(dst)), "l"(tb + sub) : "memory");
-                asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_addr(dst + 1)),
-                             "l"(tb + sub + kSubPerUnit)
+                asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_addr(dst)), "l"(uo) : "memory");
+                asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_addr(dst + 1)), "l"(uo + 1)
                              : "memory");
             }
             asm volatile("cp.async.commit_group;" ::: "memory");
@@ -427,7 +435,7 @@ __global__ void __launch_bounds__(kCons, 2) search_fast_kernel(DevIndex ix, Batc
         // first nonempty range at or after (j, x)
         auto seek = [&](uint32_t j, uint32_t x, bool fst) -> Step {
             for (;;) {
-                if (j > j1) return Step{0, j, 0, 0, 0, 0.f, false};
+                if (j > j1) return Step{nullptr, 0, 0, j, 0, 0.f, false};
                 if (j > ready) {
                     wait_sub();
                     ready = j;
@@ -440,7 +448,8 @@ __global__ void __launch_bounds__(kCons, 2) search_fast_kernel(DevIndex ix, Batc
                         const uint32_t n = ws[x][1] - ws[x][0];
                         if (n) {
                             const uint32_t i = S.order_list[x];
-                            return Step{S.t_start[i] + ws[x][0], j, x, 0, n, S.t_c32[i], fst};
+                            return Step{reinterpret_cast<const uint4*>(ix.bk + S.t_bkb[i] + ws[x][0]), 0, n >> 2, j, x,
+                                        S.t_c32[i], fst};
                         }
                     }
                 }
@@ -450,18 +459,17 @@ __global__ void __launch_bounds__(kCons, 2) search_fast_kernel(DevIndex ix, Batc
             }
         };
         auto advance = [&](const Step& s) -> Step {
-            const StepGeom g = step_geom(s.B, s.n);
-            if (s.o + 32 * kU < g.nc) {
+            if (s.o + 32 * kC < s.nch) {
                 Step t = s;
-                t.o += 32 * kU;
+                t.o += 32 * kC;
                 return t;
             }
             return seek(s.j, s.x + 1, false);
         };
         Step cur = seek(j0, 0, true);
-        uint4 va[kU];
-        uint32_t sa = 0;
-        if (cur.j <= j1) step_load(ix.bk, cur, va, sa);
+        uint32_t stage = 0;
+        if (cur.j <= j1) step_issue<kC>(cur, S.stg[warp][0]);
+        asm volatile("cp.async.commit_group;" ::: "memory");
         for (uint32_t j = j0; j <= j1; ++j) {
             const uint32_t base = j << kTileShift;
             uint32_t u0, u1;
@@ -471,22 +479,21 @@ __global__ void __launch_bounds__(kCons, 2) search_fast_kernel(DevIndex ix, Batc
             // ---- long terms of this tile (df descending; the first one stores)
             while (cur.j == j) {
                 const Step nxt = advance(cur);
-                uint4 vb[kU];
-                uint32_t sb = 0;
-                if (nxt.j <= j1) step_load(ix.bk, nxt, vb, sb);
+                if (nxt.j <= j1) step_issue<kC>(nxt, S.stg[warp][stage ^ 1]);
+                asm volatile("cp.async.commit_group;" ::: "memory");
+                asm volatile("cp.async.wait_group 1;" ::: "memory");  // cur's chunks have landed
+                const uint4* stg = S.stg[warp][stage];
                 if (!clip) {
-                    if (cur.first) step_apply<true, false>(S.acc, wbase, cur, va, sa, eb, ck);
-                    else step_apply<false, false>(S.acc, wbase, cur, va, sa, eb, ck);
+                    if (cur.first) step_apply<kC, true, false>(S.acc, wbase, cur, stg, ck);
+                    else step_apply<kC, false, false>(S.acc, wbase, cur, stg, ck);
                 } else {
-                    if (cur.first) step_apply<true, true>(S.acc, wbase, cur, va, sa, eb, ck);
-                    else step_apply<false, true>(S.acc, wbase, cur, va, sa, eb, ck);
+                    if (cur.first) step_apply<kC, true, true>(S.acc, wbase, cur, stg, ck);
+                    else step_apply<kC, false, true>(S.acc, wbase, cur, stg, ck);
                 }
                 // the next range (another term) may touch the same rows from other lanes
                 if (nxt.j != cur.j || nxt.x != cur.x) __syncwarp();
                 cur = nxt;
-#pragma unroll
-                for (int u = 0; u < kU; ++u) va[u] = vb[u];
-                sa = sb;
+                stage ^= 1;
             }
             if (!unit_live) continue;  // unit outside the window: nothing accumulated, acc stays zero
             // ---- short terms: the tile segment is small; every warp filters its rows
@@ -521,13 +528,14 @@ __global__ void __launch_bounds__(kCons, 2) search_fast_kernel(DevIndex ix, Batc
                 __syncwarp();
                 continue;
             }
-            // admission: A > 0 and A >= L * slack  <=>  A >= max(L * slack, min denormal)
-            float te = fmaxf(fmaxf(Lw, __uint_as_float(S.Lg)) * f_slack, 1.4e-45f);
+            // admission: A > 0 and A >= L * slack  <=>  A >= max(L * slack, FLT_MIN) (scaled
+            // scores of real documents are >= ~1e-29, far above FLT_MIN)
+            float te = fmaxf(fmaxf(Lw, __uint_as_float(S.Lg)) * f_slack, kFltMin);
             // append the qualifying entries of one float4 per lane (slow path)
             auto admit = [&](float4 x4, uint32_t v) {
                 if (nw > static_cast<uint32_t>(CAPW - 128)) {
                     nw = warp_prune(S, warp, nw, k, Lw, f_slack);
-                    te = fmaxf(fmaxf(Lw, __uint_as_float(S.Lg)) * f_slack, 1.4e-45f);
+                    te = fmaxf(fmaxf(Lw, __uint_as_float(S.Lg)) * f_slack, kFltMin);
                     if (nw > static_cast<uint32_t>(CAPW - 128)) {  // near-tie flood
                         flood = true;
                         return;
