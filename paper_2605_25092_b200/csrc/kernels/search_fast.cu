@@ -162,6 +162,11 @@ __device__ __forceinline__ float bk_w(uint32_t p) { return __uint_as_float(p >> 
 __device__ __forceinline__ bool bk_in(const Clip& k, uint32_t p) {
     return (k.wr0 + swz10((p & kOffMask) >> 2)) - k.u0 < k.u1 - k.u0;
 }
+__device__ __forceinline__ float max3f(float a, float b, float c) {  // FMNMX3 (sm_100)
+    float d;
+    asm("max.f32 %0, %1, %2, %3;" : "=f"(d) : "f"(a), "f"(b), "f"(c));
+    return d;
+}
 __device__ __forceinline__ float mul_ftz(float a, float b) {
     float d;
     asm("mul.rn.ftz.f32 %0, %1, %2;" : "=f"(d) : "f"(a), "f"(b));
@@ -561,16 +566,22 @@ __global__ void __launch_bounds__(kCons, 2) search_fast_kernel(DevIndex ix, Batc
                 nw += __shfl_sync(0xffffffffu, incl, 31);
                 __syncwarp();
             };
-            for (uint32_t vb = 0; vb < kV && !flood; vb += 64) {
-                const uint32_t va = vb + lane, vc = vb + 32 + lane;
-                const float4 xa = acc4[va], xc = acc4[vc];
-                acc4[va] = z4;
-                acc4[vc] = z4;
-                const float mx = fmaxf(fmaxf(fmaxf(xa.x, xa.y), fmaxf(xa.z, xa.w)),
-                                       fmaxf(fmaxf(xc.x, xc.y), fmaxf(xc.z, xc.w)));
+#pragma unroll 1
+            for (uint32_t vb = 0; vb < kV && !flood; vb += 128) {  // 4 float4 (16 rows) per lane
+                float4 x[4];
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    x[q] = acc4[vb + 32 * q + lane];
+                    acc4[vb + 32 * q + lane] = z4;
+                }
+                const float m0 = max3f(x[0].x, x[0].y, x[0].z), m1 = max3f(x[0].w, x[1].x, x[1].y);
+                const float m2 = max3f(x[1].z, x[1].w, x[2].x), m3 = max3f(x[2].y, x[2].z, x[2].w);
+                const float m4 = max3f(x[3].x, x[3].y, x[3].z);
+                const float mx = fmaxf(max3f(m0, m1, m2), max3f(m3, m4, x[3].w));
                 if (__any_sync(0xffffffffu, mx >= te)) {
-                    admit(xa, va);
-                    if (!flood) admit(xc, vc);
+#pragma unroll
+                    for (int q = 0; q < 4; ++q)
+                        if (!flood) admit(x[q], vb + 32 * q + lane);
                 }
             }
             if (flood)  // the query goes to the exact kernel: finish zeroing my rows
