@@ -136,6 +136,33 @@ def test_batch_composition_and_concurrency(c1):
             assert (o[key] == full[key]).all()
 
 
+def test_concurrent_batches_with_different_params(c1):
+    """Batches with different Bm25Params from concurrent threads: each (k1, b)
+    needs its own baked postings (bake.cu); the index re-bakes under an
+    exclusive lock while same-parameter batches share it.  Every result must
+    still be the oracle's for its own parameters."""
+    tids = c1["tids"][:150]
+    params = [(1.2, 0.75), (0.9, 0.4), (1.2, 0.75), (2.0, 1.0)]
+    want = {p: c1["orc"].topk(tids, 10, k1=p[0], b=p[1]) for p in set(params)}
+    errs = []
+
+    def run(p):
+        try:
+            for _ in range(3):
+                got = c1["dev"].search_lists(tids, 10, k1=p[0], b=p[1])
+                ids, sc, n, post = want[p]
+                check_batch(got, ids, sc, n, post, what=f"concurrent k1={p[0]} b={p[1]}")
+        except Exception as e:  # surfaced below
+            errs.append(e)
+
+    th = [threading.Thread(target=run, args=(p,)) for p in params]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    assert not errs, errs[0]
+
+
 def test_sentinel_reset_is_load_bearing(c1):
     """Pitfall 3 (test_twophase.cpp:66-83): without the
     per-query reset of the candidate state, stale entries of the previous query
