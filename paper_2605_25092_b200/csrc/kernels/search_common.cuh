@@ -1,0 +1,332 @@
+// Device pieces of the fused search kernel (search_fast.cu): CTA geometry,
+// shared-memory layout, per-warp candidate lists, the baked-posting
+// decode/apply, the cp.async step pipeline and the exact epilogue.
+#pragma once
+#include "hm_device.cuh"
+#include "hm_ptx.cuh"
+
+namespace hm {
+constexpr int kCons = 256;                // threads per CTA
+constexpr int kConsWarps = kCons / 32;    // 8: warp w owns unit w of a tile
+constexpr int kUnitRows = 1 << kUnitShift;  // 2048 rows per warp unit (hm_types.h)
+constexpr int kFastTerms = 32;            // plan size served by this kernel
+constexpr uint32_t kOffMask = (kUnitRows * 4 - 1) & ~3u;  // bk: impact (19 bits) | byte offset (13 bits)
+constexpr int kImpShift = 2 + kUnitShift - (23 - kBakeMantBits);
+constexpr float kFltMin = 1.17549435e-38f;
+static_assert(kConsWarps * kUnitRows == kTile, "one warp per 2048-row unit");
+static_assert(2 + kUnitShift + 3 + kBakeMantBits == 32, "bk = 19-bit impact | 13-bit offset");
+
+template <int CAPW>
+struct FastCfg {
+    static constexpr int kMaxKServed = CAPW == 192 ? 32 : 128;
+    static constexpr int kC = CAPW == 192 ? 3 : 2;  // 16-byte chunks per lane per pipeline step
+};
+
+template <int CAPW>
+struct __align__(16) FastSmem {
+    float acc[kTile];                      // first member: bk offsets are byte offsets into it
+    float w32s[kShortCodes];               // impacts of the short-term codes
+    uint32_t cl_row[kConsWarps][CAPW];     // per-warp candidate lists
+    float cl_val[kConsWarps][CAPW];
+    uint64_t t_start[kFastTerms], t_wlo[kFastTerms], t_end[kFastTerms];
+    double t_idf[kFastTerms];
+    uint32_t t_mult[kFastTerms];
+    float t_c32[kFastTerms];
+    int32_t t_slot[kFastTerms];
+    uint4 stg[kConsWarps][2][FastCfg<CAPW>::kC * 32];  // per-warp cp.async staging of baked postings (2 steps)
+    uint64_t t_bkb[kFastTerms];            // long terms: start of the term's baked ranges in bk
+    uint32_t wsub[2][kConsWarps][kFastTerms][2];  // unit's baked range of each long term (tile parity)
+    uint16_t order_list[kFastTerms];       // long terms (df descending), then short terms
+    uint32_t pref[kFastTerms + 1];         // short-window prefix sums / gather offsets
+    uint32_t hist[256];
+    uint32_t sel[2];
+    uint32_t n_w[kConsWarps];
+    uint64_t post;
+    uint32_t q, n_long, n_short, bad, n_surv, flood, Lg, total;
+};
+
+struct SurvView {
+    double* E;
+    uint64_t* id;
+    uint32_t* row;
+};
+constexpr int kSurvBytes = 20 * kSurvCap;
+
+__device__ __forceinline__ float esc_w(const DevIndex& ix, uint64_t gidx, uint32_t row, double k1,
+                                       double b) {
+    return impact32(static_cast<double>(__ldg(ix.tf + gidx)),
+                    static_cast<double>(__ldg(ix.doc_lens + row)), ix.avgdl, k1, b);
+}
+
+// ---------------------------------------------------------------- per-warp list
+// Raise the warp's k-th bound from its own list (exact k-th largest by a
+// binary search over the float bit pattern, values are >= 0), keep the
+// admissible entries (>= max(Lw, Lg) * slack, stable compaction), publish the
+// bound to the CTA-wide Lg.  Warp-synchronous; returns the new list length.
+template <int CAPW>
+__device__ uint32_t warp_prune(FastSmem<CAPW>& S, int w, uint32_t n, uint32_t k, float& Lw, float slack) {
+    const int lane = threadIdx.x & 31;
+    uint32_t* rows = S.cl_row[w];
+    float* vals = S.cl_val[w];
+    constexpr int R = CAPW / 32;
+    float v[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+        const uint32_t i = lane + 32 * r;
+        v[r] = i < n ? vals[i] : -1.f;
+    }
+    if (n >= k) {
+        uint32_t lo = 0, hi = 0x7F800001u;  // count(>= lo) >= k > count(>= hi)
+        while (hi - lo > 1) {
+            const uint32_t mid = lo + ((hi - lo) >> 1);
+            const float t = __uint_as_float(mid);
+            uint32_t c = 0;
+#pragma unroll
+            for (int r = 0; r < R; ++r) c += v[r] >= t;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+            if (c >= k) lo = mid;
+            else hi = mid;
+        }
+        Lw = fmaxf(Lw, __uint_as_float(lo));
+        if (lane == 0) atomicMax(&S.Lg, __float_as_uint(Lw));
+    }
+    const float thr = fmaxf(Lw, __uint_as_float(S.Lg)) * slack;
+    uint32_t keep = 0;
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+        const uint32_t i = lane + 32 * r;
+        const bool ok = i < n && v[r] >= thr;
+        const uint32_t bal = __ballot_sync(0xffffffffu, ok);
+        const uint32_t row = i < n ? rows[i] : 0u;
+        __syncwarp();
+        if (ok) {
+            const uint32_t pos = keep + __popc(bal & ((1u << lane) - 1));
+            rows[pos] = row;
+            vals[pos] = v[r];
+        }
+        keep += __popc(bal);
+        __syncwarp();
+    }
+    return keep;
+}
+
+// ---------------------------------------------------------------- long terms
+// Baked postings (hm_types.h): impact in the top 19 bits, accumulator byte
+// offset in the low 13.  float(p >> 6) is the impact times 2^-ks (the
+// offset's top 7 bits land below the 16 kept mantissa bits: relative error
+// < 2^-16, covered by delta); a NULL posting decodes to a denormal and the
+// flush-to-zero multiply makes its contribution exactly 0.  acc is the first
+// smem member and warp units are 8 KB-aligned: the address is one OR.  CLIP (a
+// window cuts the unit): postings whose tile-local row is outside [u0, u1)
+// are skipped.
+struct Clip {
+    uint32_t wr0, u0, u1;
+};
+__device__ __forceinline__ uint32_t bk_off(uint32_t wbase, uint32_t p) { return wbase | (p & kOffMask); }
+__device__ __forceinline__ float bk_w(uint32_t p) { return __uint_as_float(p >> kImpShift); }
+__device__ __forceinline__ bool bk_in(const Clip& k, uint32_t p) {
+    return (k.wr0 + swz10((p & kOffMask) >> 2)) - k.u0 < k.u1 - k.u0;
+}
+__device__ __forceinline__ float max3f(float a, float b, float c) {  // FMNMX3 (sm_100)
+    float d;
+    asm("max.f32 %0, %1, %2, %3;" : "=f"(d) : "f"(a), "f"(b), "f"(c));
+    return d;
+}
+__device__ __forceinline__ float mul_ftz(float a, float b) {
+    float d;
+    asm("mul.rn.ftz.f32 %0, %1, %2;" : "=f"(d) : "f"(a), "f"(b));
+    return d;
+}
+__device__ __forceinline__ float fma_ftz(float a, float b, float c) {
+    float d;
+    asm("fma.rn.ftz.f32 %0, %1, %2, %3;" : "=f"(d) : "f"(a), "f"(b), "f"(c));
+    return d;
+}
+
+// apply N baked postings (the rows are distinct: all loads, then all stores)
+template <bool FIRST, bool CLIP, int N>
+__device__ __forceinline__ void apply_n(float* __restrict__ acc, uint32_t wbase, const uint32_t* p, float c,
+                                        const Clip& k) {
+    char* base = reinterpret_cast<char*>(acc);
+    float a[N];
+    if (!FIRST) {
+#pragma unroll
+        for (int e = 0; e < N; ++e)
+            if (!CLIP || bk_in(k, p[e])) a[e] = *reinterpret_cast<float*>(base + bk_off(wbase, p[e]));
+    }
+#pragma unroll
+    for (int e = 0; e < N; ++e) {
+        if (CLIP && !bk_in(k, p[e])) continue;
+        float* dst = reinterpret_cast<float*>(base + bk_off(wbase, p[e]));
+        if (FIRST) *dst = mul_ftz(c, bk_w(p[e]));
+        else *dst = fma_ftz(c, bk_w(p[e]), a[e]);
+    }
+}
+
+// One pipeline step of a long term's baked range in the warp's unit: up to
+// 32*kC 16-byte chunks, staged in shared memory by per-lane cp.async (each
+// lane copies and later reads only its own chunks: no warp sync needed).
+struct Step {
+    const uint4* base;    // the range's first chunk in bk
+    uint32_t o, nch;      // chunk offset of this step, chunks in the range
+    uint32_t j, x;        // tile, range (long-term slot in order_list); j > j1: none
+    float c;              // mult * idf * 2^(ks - 61) of the term
+    bool first;           // first range of the unit in this tile: store instead of read-modify-write
+};
+
+template <int KC>
+__device__ __forceinline__ void step_issue(const Step& s, uint4* stg) {
+    const uint32_t lane = threadIdx.x & 31;
+#pragma unroll
+    for (int u = 0; u < KC; ++u) {
+        const uint32_t c = s.o + 32 * u + lane;
+        if (c < s.nch)
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_addr(stg + 32 * u + lane)),
+                         "l"(s.base + c)
+                         : "memory");
+    }
+}
+
+template <int KC, bool FIRST, bool CLIP>
+__device__ __forceinline__ void step_apply(float* __restrict__ acc, uint32_t wbase, const Step& s,
+                                           const uint4* stg, const Clip& k) {
+    const uint32_t lane = threadIdx.x & 31;
+#pragma unroll
+    for (int u = 0; u < KC; u += 2) {
+        if (s.o + 32 * u >= s.nch) break;  // warp-uniform
+        const bool ok0 = s.o + 32 * u + lane < s.nch;
+        const bool ok1 = u + 1 < KC && s.o + 32 * (u + 1) + lane < s.nch;
+        if (ok1) {
+            const uint4 v0 = stg[32 * u + lane], v1 = stg[32 * (u + 1) + lane];
+            const uint32_t p[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
+            apply_n<FIRST, CLIP, 8>(acc, wbase, p, s.c, k);
+        } else if (ok0) {
+            const uint4 v0 = stg[32 * u + lane];
+            const uint32_t p[4] = {v0.x, v0.y, v0.z, v0.w};
+            apply_n<FIRST, CLIP, 4>(acc, wbase, p, s.c, k);
+        }
+    }
+}
+
+// Epilogue of a query (both kernels): merge the warps' candidate lists, keep
+// the survivors of the k-th fp32 value (slack f_slack), rescore them exactly
+// in fp64 in plan order with the reference's operation order
+// (src/csr_index.cpp:10-15, 87-101), rank by (score desc, DocId asc)
+// (include/hybrid/types.hpp:21-25), write the top-k, postings_touched and the
+// Margin confidence + skip (src/cascade.cpp:15-21, 79-84).  A near-tie flood
+// (> kSurvCap survivors) hands the query to the exact kernel.  Leaves the
+// accumulator area zero.
+template <int CAPW>
+__device__ __forceinline__ void finish_query(const DevIndex& ix, const BatchArgs& a, FastSmem<CAPW>& S, uint32_t q,
+                                             uint32_t m, uint32_t k, uint32_t nw, float f_slack, double k1,
+                                             double bb) {
+    constexpr int kGatherBytes = 8 * kConsWarps * CAPW;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    auto csync = [] { __syncthreads(); };
+    char* sp = reinterpret_cast<char*>(S.acc);
+    float* gv = reinterpret_cast<float*>(sp);
+    uint32_t* gr = reinterpret_cast<uint32_t*>(sp + 4 * kConsWarps * CAPW);
+    if (tid == 0) {
+        uint32_t t = 0;
+        for (int w = 0; w < kConsWarps; ++w) {
+            S.pref[w] = t;  // reused: gather offsets
+            t += S.n_w[w];
+        }
+        S.total = t;
+    }
+    csync();
+    {
+        const uint32_t off = S.pref[warp];
+        for (uint32_t i = lane; i < nw; i += 32) {
+            gv[off + i] = S.cl_val[warp][i];
+            gr[off + i] = S.cl_row[warp][i];
+        }
+    }
+    csync();
+    const uint32_t nc = S.total;
+    float theta = 0.f;
+    if (nc >= k) theta = block_kth_largest<kCons>(gv, nc, k, S.hist, S.sel, csync) * f_slack;
+    if (warp == 0) {
+        uint32_t w = 0;
+        for (uint32_t b0 = 0; b0 < nc; b0 += 32) {
+            const uint32_t i = b0 + lane;
+            const bool keep = i < nc && gv[i] >= theta;
+            const uint32_t bal = __ballot_sync(0xffffffffu, keep);
+            const uint32_t pos = w + __popc(bal & ((1u << lane) - 1));
+            if (keep && pos < kSurvCap) (&S.cl_row[0][0])[pos] = gr[i];  // list area is free now
+            w += __popc(bal);
+            __syncwarp();
+        }
+        if (lane == 0) S.n_surv = w;
+    }
+    csync();
+    const uint32_t ns = S.n_surv;
+    for (int i = tid; i < kGatherBytes / 4; i += kCons) S.acc[i] = 0.f;  // zero for the next query
+    if (tid < kConsWarps) S.n_w[tid] = 0;
+    csync();
+    if (ns > kSurvCap) {  // near-tie flood: the exact kernel takes the query
+        if (tid == 0) a.exact_list[atomicAdd(&a.counters[1], 1u)] = q;
+        return;
+    }
+    SurvView sv{reinterpret_cast<double*>(sp), reinterpret_cast<uint64_t*>(sp + 8 * kSurvCap),
+                reinterpret_cast<uint32_t*>(sp + 16 * kSurvCap)};
+    for (uint32_t i = tid; i < ns; i += kCons) sv.row[i] = (&S.cl_row[0][0])[i];
+    csync();
+    // warp per survivor, lanes over plan terms; fp64 sum in plan order
+    for (uint32_t s = warp; s < ns; s += kConsWarps) {
+        const uint32_t row = sv.row[s];
+        double E = 0.0;
+        for (uint32_t t0 = 0; t0 < m; t0 += 32) {
+            const uint32_t t = t0 + lane;
+            double val = 0.0;
+            bool present = false;
+            if (t < m) {
+                double tf, dl;
+                if (find_posting(ix, S.t_slot[t], S.t_start[t], S.t_end[t], row, ix.code_tf,
+                                 ix.code_len, &tf, &dl)) {
+                    val = bm25_exact(tf, S.t_idf[t], dl, ix.avgdl, k1, bb);
+                    present = true;
+                }
+            }
+            const uint32_t cnt = min(32u, m - t0);
+            for (uint32_t u = 0; u < cnt; ++u) {
+                const double x = __shfl_sync(0xffffffffu, val, u);
+                const bool pr = __shfl_sync(0xffffffffu, present, u);
+                if (pr) {
+                    const uint32_t mu = S.t_mult[t0 + u];
+                    for (uint32_t r = 0; r < mu; ++r) E = __dadd_rn(E, x);  // :94
+                }
+            }
+        }
+        if (lane == 0) {
+            sv.E[s] = E;
+            sv.id[s] = __ldg(ix.doc_ids + row);
+        }
+    }
+    csync();
+    const uint32_t n2 = pow2_ceil(ns);
+    for (uint32_t i = ns + tid; i < n2; i += kCons) {
+        sv.E[i] = -INFINITY;
+        sv.id[i] = ~0ull;
+        sv.row[i] = 0;
+    }
+    csync();
+    block_bitonic<kCons>(sv.E, sv.id, sv.row, n2, csync);
+    if (tid == 0) {
+        uint32_t nout = 0;
+        for (uint32_t i = 0; i < ns && nout < k; ++i) {
+            if (!(sv.E[i] > 0.0)) break;  // zero scores never emitted (:56)
+            a.out_ids[static_cast<uint64_t>(q) * k + nout] = sv.id[i];
+            a.out_scores[static_cast<uint64_t>(q) * k + nout] = sv.E[i];
+            ++nout;
+        }
+        a.out_n[q] = nout;
+        if (a.out_post) a.out_post[q] = S.post;
+        write_decision(a, q, sv.E, nout);
+    }
+    csync();
+    for (int i = tid; i < kSurvBytes / 4; i += kCons) S.acc[i] = 0.f;
+}
+
+}  // namespace hm

@@ -21,7 +21,7 @@ def main(n=8841823, V=1000000, lo=20, hi=60, nq=10000, mint=3, maxt=6, k=10, rep
                skip=torch.zeros(nq, dtype=torch.uint8, device='cuda'), postings=torch.zeros(nq, dtype=torch.int64, device='cuda'))
     for r in range(reps + 1):
         torch.cuda.synchronize(); e0 = torch.cuda.Event(enable_timing=True); e1 = torch.cuda.Event(enable_timing=True)
-        e0.record(); dev.search_batch_device(dq_off, dq_tid, out, k); e1.record(); torch.cuda.synchronize()
+        e0.record(); dev.search_batch_device(dq_off, dq_tid, out, k, flags=int(os.environ.get('HM_PROBE_FLAGS', '0'))); e1.record(); torch.cuda.synchronize()
         ms = e0.elapsed_time(e1)
         print(f"rep {r}: {ms:.2f} ms  {nq/ms*1e3:.0f} qps  eff {post*8/ms/1e6:.0f} GB/s (8B/posting)  phys {post*4/ms/1e6:.0f} GB/s", flush=True)
     t = time.time(); r = dev.search_batch(off, tids, k); print(f"host api {time.time()-t:.3f}s n_exact={r['n_exact']}")
