@@ -19,7 +19,8 @@ static_assert(2 + kUnitShift + 3 + kBakeMantBits == 32, "bk = 19-bit impact | 13
 template <int CAPW>
 struct FastCfg {
     static constexpr int kMaxKServed = CAPW == 192 ? 32 : 128;
-    static constexpr int kC = CAPW == 192 ? 3 : 2;  // 16-byte chunks per lane per pipeline step
+    static constexpr int kC = CAPW == 192 ? 3 : 2;   // 16-byte chunks per lane per pipeline step
+    static constexpr int kStages = 2;  // staged steps (1 applied + kStages - 1 in flight)
 };
 
 template <int CAPW>
@@ -33,7 +34,7 @@ struct __align__(16) FastSmem {
     uint32_t t_mult[kFastTerms];
     float t_c32[kFastTerms];
     int32_t t_slot[kFastTerms];
-    uint4 stg[kConsWarps][2][FastCfg<CAPW>::kC * 32];  // per-warp cp.async staging of baked postings (2 steps)
+    uint4 stg[kConsWarps][FastCfg<CAPW>::kStages][FastCfg<CAPW>::kC * 32];  // per-warp cp.async staging of baked postings
     uint64_t t_bkb[kFastTerms];            // long terms: start of the term's baked ranges in bk
     uint32_t wsub[2][kConsWarps][kFastTerms][2];  // unit's baked range of each long term (tile parity)
     uint16_t order_list[kFastTerms];       // long terms (df descending), then short terms

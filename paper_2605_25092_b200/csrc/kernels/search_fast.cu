@@ -204,32 +204,35 @@ __global__ void __launch_bounds__(kCons, 2) search_fast_kernel(DevIndex ix, Batc
         const uint32_t wr0 = static_cast<uint32_t>(warp) << kUnitShift;  // my rows in a tile
         uint32_t nw = S.n_w[warp];
         bool flood = false;
-        // my sub-range of every long term for a tile: copied global -> smem
-        // with cp.async (no registers held), one tile ahead, double-buffered
-        auto load_sub = [&](uint32_t j) {
+        // my baked range of every long term for a tile: lane x prefetches term
+        // x's two unit offsets for the NEXT tile into registers (plain loads,
+        // latency covered by a tile's work) and installs them in smem when the
+        // pipeline enters that tile
+        uint32_t pre0 = 0, pre1 = 0;
+        auto prefetch = [&](uint32_t j) {
             if (static_cast<uint32_t>(lane) < n_long) {
                 const uint32_t* uo = ix.bk_uoff +
                                      static_cast<uint64_t>(S.t_slot[S.order_list[lane]]) * (ix.n_units + 1) +
                                      j * kUnitsPerTile + warp;
-                uint32_t* dst = S.wsub[j & 1][warp][lane];
-                asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_addr(dst)), "l"(uo) : "memory");
-                asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_addr(dst + 1)), "l"(uo + 1)
-                             : "memory");
+                pre0 = __ldg(uo);
+                pre1 = __ldg(uo + 1);
             }
-            asm volatile("cp.async.commit_group;" ::: "memory");
         };
-        auto wait_sub = [&] {
-            asm volatile("cp.async.wait_group 0;" ::: "memory");
+        auto install = [&](uint32_t j) {
+            if (static_cast<uint32_t>(lane) < n_long) {
+                S.wsub[j & 1][warp][lane][0] = pre0;
+                S.wsub[j & 1][warp][lane][1] = pre1;
+            }
             __syncwarp();
+            if (j < j1) prefetch(j + 1);
         };
         // Long terms run as a software pipeline of steps over (tile, range,
-        // chunk): the loads of the next step -- possibly the first range of a
-        // later tile -- are in flight while the current step is applied, and
-        // across the short-term pass and the scan of a tile.
+        // chunk), three stages deep: the loads of the next two steps --
+        // possibly ranges of later tiles -- are in flight while the current
+        // step is applied, and across the short-term pass and the scan.
         uint32_t ready = j0;  // last tile whose sub-ranges are resident in wsub
-        load_sub(j0);
-        wait_sub();
-        if (j0 < j1) load_sub(j0 + 1);
+        prefetch(j0);
+        install(j0);
         auto live = [&](uint32_t j, uint32_t& u0, uint32_t& u1) {
             const uint32_t base = j << kTileShift;
             u0 = max(base + wr0, row_lo) - base;
@@ -241,9 +244,8 @@ __global__ void __launch_bounds__(kCons, 2) search_fast_kernel(DevIndex ix, Batc
             for (;;) {
                 if (j > j1) return Step{nullptr, 0, 0, j, 0, 0.f, false};
                 if (j > ready) {
-                    wait_sub();
                     ready = j;
-                    if (j < j1) load_sub(j + 1);
+                    install(j);
                 }
                 uint32_t u0, u1;
                 if (live(j, u0, u1)) {
@@ -271,9 +273,16 @@ __global__ void __launch_bounds__(kCons, 2) search_fast_kernel(DevIndex ix, Batc
             return seek(s.j, s.x + 1, false);
         };
         Step cur = seek(j0, 0, true);
-        uint32_t stage = 0;
+        constexpr int kSt = FastCfg<CAPW>::kStages;
+        uint32_t stage = 0;  // cur's stage; nx1 (3 stages) is in stage + 1
         if (cur.j <= j1) step_issue<kC>(cur, S.stg[warp][0]);
         asm volatile("cp.async.commit_group;" ::: "memory");
+        Step nx1 = cur;
+        if (kSt == 3) {
+            nx1 = cur.j <= j1 ? advance(cur) : cur;
+            if (nx1.j <= j1) step_issue<kC>(nx1, S.stg[warp][1]);
+            asm volatile("cp.async.commit_group;" ::: "memory");
+        }
         for (uint32_t j = j0; j <= j1; ++j) {
             const uint32_t base = j << kTileShift;
             uint32_t u0, u1;
@@ -282,10 +291,20 @@ __global__ void __launch_bounds__(kCons, 2) search_fast_kernel(DevIndex ix, Batc
             const Clip ck{wr0, u0, u1};
             // ---- long terms of this tile (df descending; the first one stores)
             while (cur.j == j) {
-                const Step nxt = advance(cur);
-                if (nxt.j <= j1) step_issue<kC>(nxt, S.stg[warp][stage ^ 1]);
-                asm volatile("cp.async.commit_group;" ::: "memory");
-                asm volatile("cp.async.wait_group 1;" ::: "memory");  // cur's chunks have landed
+                Step nxt;  // the step after cur
+                if (kSt == 3) {
+                    const Step nx2 = nx1.j <= j1 ? advance(nx1) : nx1;
+                    if (nx2.j <= j1) step_issue<kC>(nx2, S.stg[warp][stage >= 1 ? stage - 1 : 2]);
+                    asm volatile("cp.async.commit_group;" ::: "memory");
+                    asm volatile("cp.async.wait_group 2;" ::: "memory");  // cur's chunks have landed
+                    nxt = nx1;
+                    nx1 = nx2;
+                } else {
+                    nxt = advance(cur);
+                    if (nxt.j <= j1) step_issue<kC>(nxt, S.stg[warp][stage ^ 1]);
+                    asm volatile("cp.async.commit_group;" ::: "memory");
+                    asm volatile("cp.async.wait_group 1;" ::: "memory");  // cur's chunks have landed
+                }
                 const uint4* stg = S.stg[warp][stage];
                 if (!clip) {
                     if (cur.first) step_apply<kC, true, false>(S.acc, wbase, cur, stg, ck);
@@ -294,12 +313,12 @@ __global__ void __launch_bounds__(kCons, 2) search_fast_kernel(DevIndex ix, Batc
                     if (cur.first) step_apply<kC, true, true>(S.acc, wbase, cur, stg, ck);
                     else step_apply<kC, false, true>(S.acc, wbase, cur, stg, ck);
                 }
-                // the next range (another term) may touch the same rows from other lanes
+                // the next range (another term) may touch the same rows from other
+                // lanes (a lane only ever reads the stage slots it filled itself)
                 if (nxt.j != cur.j || nxt.x != cur.x) __syncwarp();
                 cur = nxt;
-                stage ^= 1;
+                stage = stage + 1 == static_cast<uint32_t>(kSt) ? 0 : stage + 1;
             }
-            if (!unit_live) continue;  // unit outside the window: nothing accumulated, acc stays zero
             // ---- short terms: the tile segment is small; every warp filters its rows
             for (uint32_t s = 0; s < n_short; ++s) {
                 const uint32_t i = S.order_list[n_long + s];
