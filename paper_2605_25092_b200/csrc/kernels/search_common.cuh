@@ -36,7 +36,8 @@ struct __align__(16) FastSmem {
     int32_t t_slot[kFastTerms];
     uint4 stg[kConsWarps][FastCfg<CAPW>::kStages][FastCfg<CAPW>::kC * 32];  // per-warp cp.async staging of baked postings
     uint64_t t_bkb[kFastTerms];            // long terms: start of the term's baked ranges in bk
-    uint32_t wsub[2][kConsWarps][kFastTerms][2];  // unit's baked range of each long term (tile parity)
+    uint4 rdesc[kConsWarps][kFastTerms];  // per warp: the unit's nonempty long-term ranges in this tile
+                                          // {bk address lo, hi, chunks, c bits}, df descending
     uint16_t order_list[kFastTerms];       // long terms (df descending), then short terms
     uint32_t pref[kFastTerms + 1];         // short-window prefix sums / gather offsets
     uint32_t hist[256];

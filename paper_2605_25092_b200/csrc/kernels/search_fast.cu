@@ -218,11 +218,34 @@ __global__ void __launch_bounds__(kCons, 2) search_fast_kernel(DevIndex ix, Batc
                 pre1 = __ldg(uo + 1);
             }
         };
+        // lane x: term x's baked base address and fp32 weight
+        const uint32_t* my_bk = nullptr;
+        float my_c = 0.f;
+        if (static_cast<uint32_t>(lane) < n_long) {
+            const uint32_t i = S.order_list[lane];
+            my_bk = ix.bk + S.t_bkb[i];
+            my_c = S.t_c32[i];
+        }
+        uint32_t nrd = 0;  // ranges in rdesc for the installed tile
+        auto live = [&](uint32_t j, uint32_t& u0, uint32_t& u1) {
+            const uint32_t base = j << kTileShift;
+            u0 = max(base + wr0, row_lo) - base;
+            u1 = min(base + wr0 + kUnitRows, row_hi) - base;
+            return u0 < u1;
+        };
+        // tile j's nonempty ranges of my unit as a compact descriptor list (the
+        // previous tile's list is no longer read once the pipeline enters j)
         auto install = [&](uint32_t j) {
-            if (static_cast<uint32_t>(lane) < n_long) {
-                S.wsub[j & 1][warp][lane][0] = pre0;
-                S.wsub[j & 1][warp][lane][1] = pre1;
+            uint32_t u0, u1;
+            const bool ok = static_cast<uint32_t>(lane) < n_long && pre1 > pre0 && live(j, u0, u1);
+            const uint32_t bal = __ballot_sync(0xffffffffu, ok);
+            if (ok) {
+                const uint64_t addr = reinterpret_cast<uint64_t>(my_bk + pre0);
+                S.rdesc[warp][__popc(bal & ((1u << lane) - 1u))] =
+                    make_uint4(static_cast<uint32_t>(addr), static_cast<uint32_t>(addr >> 32), (pre1 - pre0) >> 2,
+                               __float_as_uint(my_c));
             }
+            nrd = __popc(bal);
             __syncwarp();
             if (j < j1) prefetch(j + 1);
         };
@@ -230,15 +253,9 @@ __global__ void __launch_bounds__(kCons, 2) search_fast_kernel(DevIndex ix, Batc
         // chunk), three stages deep: the loads of the next two steps --
         // possibly ranges of later tiles -- are in flight while the current
         // step is applied, and across the short-term pass and the scan.
-        uint32_t ready = j0;  // last tile whose sub-ranges are resident in wsub
+        uint32_t ready = j0;  // the tile whose ranges are in rdesc
         prefetch(j0);
         install(j0);
-        auto live = [&](uint32_t j, uint32_t& u0, uint32_t& u1) {
-            const uint32_t base = j << kTileShift;
-            u0 = max(base + wr0, row_lo) - base;
-            u1 = min(base + wr0 + kUnitRows, row_hi) - base;
-            return u0 < u1;
-        };
         // first nonempty range at or after (j, x)
         auto seek = [&](uint32_t j, uint32_t x, bool fst) -> Step {
             for (;;) {
@@ -247,21 +264,13 @@ __global__ void __launch_bounds__(kCons, 2) search_fast_kernel(DevIndex ix, Batc
                     ready = j;
                     install(j);
                 }
-                uint32_t u0, u1;
-                if (live(j, u0, u1)) {
-                    const uint32_t (*ws)[2] = S.wsub[j & 1][warp];
-                    for (; x < n_long; ++x) {
-                        const uint32_t n = ws[x][1] - ws[x][0];
-                        if (n) {
-                            const uint32_t i = S.order_list[x];
-                            return Step{reinterpret_cast<const uint4*>(ix.bk + S.t_bkb[i] + ws[x][0]), 0, n >> 2, j, x,
-                                        S.t_c32[i], fst};
-                        }
-                    }
+                if (x < nrd) {
+                    const uint4 d = S.rdesc[warp][x];
+                    return Step{reinterpret_cast<const uint4*>((static_cast<uint64_t>(d.y) << 32) | d.x), 0, d.z, j, x,
+                                __uint_as_float(d.w), x == 0};
                 }
                 ++j;
                 x = 0;
-                fst = true;
             }
         };
         auto advance = [&](const Step& s) -> Step {
