@@ -86,6 +86,11 @@ typedef struct {
 #define HM_FLAG_DEBUG_NO_RESET 2u /* test-only: skip the per-query sentinel reset
                                     of the candidate state (pitfall-3 witness,
                                     src/twophase.cpp:24-27) */
+#define HM_FLAG_EXHAUSTIVE 16u    /* skip the seeded MaxScore pre-pass: every query on the
+                                    exhaustive tile-sweep kernel (same results; the roofline
+                                    measurement of bench.py) */
+#define HM_FLAG_SEED_ALL 32u      /* test-only: the seeded pre-pass tries every query that
+                                    has a short term, whatever its cost estimate or window */
 #define HM_FLAG_TIMING 4u         /* time each kernel with CUDA events on the
                                     launching stream (the call then synchronises);
                                     read back with hm_last_batch_timing */
@@ -127,6 +132,11 @@ int hm_last_batch_stats(uint32_t* n_exact_fallback, uint32_t* n_launches);
 /* Device time (ms) of the last HM_FLAG_TIMING batch on this thread: planner +
  * LPT sort, the fused selection kernel, the exact fallback kernel. */
 int hm_last_batch_timing(float* ms_plan, float* ms_search, float* ms_exact);
+
+/* The seeded MaxScore pre-pass of the last batch on this thread: its device
+ * time (HM_FLAG_TIMING batches) and how many queries it handed to the
+ * exhaustive kernel (0 with HM_FLAG_EXHAUSTIVE). */
+int hm_last_batch_seed(float* ms_seed, uint32_t* n_handed_over);
 
 /* Doc-sharded multi-GPU merge (the step after the all-gather of k candidates
  * per query): shard_ids/shard_scores/shard_n hold G blocks of per-shard exact

@@ -32,8 +32,8 @@
 namespace {
 
 thread_local std::string g_err;
-thread_local uint32_t g_last_exact = 0, g_last_launches = 0;
-thread_local float g_ms_plan = 0.f, g_ms_search = 0.f, g_ms_exact = 0.f;
+thread_local uint32_t g_last_exact = 0, g_last_launches = 0, g_last_handed = 0;
+thread_local float g_ms_plan = 0.f, g_ms_search = 0.f, g_ms_exact = 0.f, g_ms_seed = 0.f;
 
 struct no_device_error : std::runtime_error {
     using std::runtime_error::runtime_error;
@@ -104,13 +104,13 @@ struct Workspace {
     // device
     uint32_t *q_off = nullptr, *q_tid = nullptr, *plan_tid = nullptr, *plan_mult = nullptr,
              *plan_len = nullptr, *order_in = nullptr, *order = nullptr, *counters = nullptr,
-             *exact_list = nullptr, *out_n = nullptr;
+             *exact_list = nullptr, *out_n = nullptr, *fb_list = nullptr;
     uint64_t *cost = nullptr, *cost_sorted = nullptr, *out_ids = nullptr, *out_post = nullptr;
     double *tau = nullptr, *out_scores = nullptr, *out_conf = nullptr;
     float* w32 = nullptr;
     uint8_t* out_skip = nullptr;
     void* sort_tmp = nullptr;
-    cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+    cudaEvent_t ev[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
     uint32_t* stab = nullptr;  // per-CTA short-term tile tables
     uint64_t stab_words = 0;
     // pinned host staging
@@ -119,12 +119,12 @@ struct Workspace {
 
     void free_dev() {
         void* ps[] = {q_off, q_tid, plan_tid, plan_mult, plan_len, order_in, order, counters,
-                      exact_list, out_n, cost, cost_sorted, out_ids, out_post, tau, out_scores,
+                      exact_list, fb_list, out_n, cost, cost_sorted, out_ids, out_post, tau, out_scores,
                       out_conf, w32, out_skip, sort_tmp};
         for (void* p : ps)
             if (p) cudaFree(p);
         q_off = q_tid = plan_tid = plan_mult = plan_len = order_in = order = counters = exact_list =
-            out_n = nullptr;
+            out_n = fb_list = nullptr;
         cost = cost_sorted = out_ids = out_post = nullptr;
         tau = out_scores = out_conf = nullptr;
         w32 = nullptr;
@@ -375,6 +375,21 @@ void build_index(const hm_csr_view* v, hm_index* X) {
             row[n_sub] = static_cast<uint32_t>(hi - lo);
         }
     });
+    // dense probe arrays (seeded kernel): the most frequent long terms get a
+    // per-row u16 (tf, len) code so a probe is one load
+    std::vector<int32_t> dense_of(std::max<size_t>(long_terms.size(), 1), -1);
+    std::vector<uint32_t> dense_slots;
+    if (N >= 65536) {
+        std::vector<uint32_t> cand;
+        auto dfs = [&](uint32_t s) { return v->term_offsets[long_terms[s] + 1] - v->term_offsets[long_terms[s]]; };
+        for (size_t s = 0; s < long_terms.size(); ++s)
+            if (dfs(static_cast<uint32_t>(s)) >= N / hm::kDenseMinDiv) cand.push_back(static_cast<uint32_t>(s));
+        std::sort(cand.begin(), cand.end(),
+                  [&](uint32_t a, uint32_t b) { return dfs(a) > dfs(b) || (dfs(a) == dfs(b) && a < b); });
+        if (cand.size() > static_cast<size_t>(hm::kMaxDense)) cand.resize(hm::kMaxDense);
+        dense_slots = cand;
+        for (size_t dd = 0; dd < cand.size(); ++dd) dense_of[cand[dd]] = static_cast<int32_t>(dd);
+    }
     std::vector<float> idf32(V);
     for (uint32_t t = 0; t < V; ++t) idf32[t] = static_cast<float>(v->term_idfs[t]);
     // upload
@@ -382,7 +397,6 @@ void build_index(const hm_csr_view* v, hm_index* X) {
     auto& B = X->bytes;
     hm::DevIndex& d = X->dev;
     d.post = dev_upload(packed.data(), P + 8, A, B);
-    std::vector<uint32_t>().swap(packed);
     d.tf = dev_upload(tf.data(), P, A, B);
     std::vector<uint32_t>().swap(tf);
     d.term_off = dev_upload(v->term_offsets, static_cast<uint64_t>(V) + 1, A, B);
@@ -396,6 +410,31 @@ void build_index(const hm_csr_view* v, hm_index* X) {
     d.doc_ids = dev_upload(v->doc_ids, N, A, B);
     d.code_tf = dev_upload(X->code_tf.data(), hm::kMaxCodes, A, B);
     d.code_len = dev_upload(X->code_len.data(), hm::kMaxCodes, A, B);
+    {
+        d.dense_of_slot = dev_upload(dense_of.data(), dense_of.size(), A, B);
+        const uint64_t nd = dense_slots.size();
+        void* p = nullptr;
+        ck(cudaMalloc(&p, std::max<uint64_t>(nd * N, 1) * 2), "cudaMalloc(dense)");
+        A.push_back(p);
+        B += std::max<uint64_t>(nd * N, 1) * 2;
+        d.dense = static_cast<const uint16_t*>(p);
+        std::vector<uint16_t> col(N);
+        for (uint64_t dd = 0; dd < nd; ++dd) {
+            const uint32_t s = dense_slots[dd], t = long_terms[s];
+            std::fill(col.begin(), col.end(), hm::kDenseAbsent);
+            for (uint64_t i = v->term_offsets[t]; i < v->term_offsets[t + 1]; ++i) {
+                const uint32_t code = packed[i] & hm::kEscLong;
+                col[v->posting_rows[i]] = code < n_codes ? static_cast<uint16_t>(code) : hm::kDenseEscape;
+            }
+            ck(cudaMemcpy(static_cast<uint16_t*>(p) + dd * N, col.data(), N * 2ull, cudaMemcpyHostToDevice),
+               "cudaMemcpy(dense)");
+        }
+        ck(cudaMalloc(&p, std::max<uint64_t>(V, 1) * 4), "cudaMalloc(tmax)");
+        A.push_back(p);
+        B += std::max<uint64_t>(V, 1) * 4;
+        d.tmax = static_cast<const float*>(p);
+    }
+    std::vector<uint32_t>().swap(packed);
     X->n_long = static_cast<uint32_t>(long_terms.size());
     X->d_long_terms = dev_upload(long_terms.data(), long_terms.size(), A, B);
     // baked-posting index space: every (long term, 2048-row unit) range padded
@@ -481,8 +520,9 @@ void ensure(Workspace* w, uint32_t nq, uint32_t ntid, uint32_t k, bool need_io) 
         dalloc(w->plan_len, NQ);
         dalloc(w->order_in, NQ);
         dalloc(w->order, NQ);
-        dalloc(w->counters, 4);
+        dalloc(w->counters, 8);
         dalloc(w->exact_list, NQ);
+        dalloc(w->fb_list, NQ);
         dalloc(w->cost, NQ);
         dalloc(w->cost_sorted, NQ);
         dalloc(w->tau, NQ);
@@ -581,23 +621,35 @@ void run_batch(hm_index* X, Workspace* w, const hm_query_batch& hb, const uint32
     const bool timing = (hb.flags & HM_FLAG_TIMING) != 0;
     if (timing && !w->ev[0])
         for (auto& e : w->ev) ck(cudaEventCreate(&e), "event");
-    ck(cudaMemsetAsync(w->counters, 0, 4 * sizeof(uint32_t), st), "memset counters");
+    ck(cudaMemsetAsync(w->counters, 0, 8 * sizeof(uint32_t), st), "memset counters");
     if (timing) ck(cudaEventRecord(w->ev[0], st), "event");
     ck(hm::launch_plan(X->dev, a, w->order_in, st), "plan kernel");
     ck(hm::launch_lpt_sort(w->sort_tmp, w->sort_bytes, a, w->cost_sorted, w->order_in, st),
        "lpt sort");
     if (timing) ck(cudaEventRecord(w->ev[1], st), "event");
+    // seeded MaxScore first (exact; serves the queries with a rare term), the
+    // exhaustive kernel for the rest; HM_FLAG_EXHAUSTIVE skips the seeded pass
+    // (a narrow row window -- a recency window of the temporal index -- keeps
+    // every query cheap on the exhaustive kernel: no seeded pass)
+    const bool seeded = !(a.flags & (HM_FLAG_EXHAUSTIVE | HM_FLAG_FORCE_EXACT)) &&
+                        ((a.flags & HM_FLAG_SEED_ALL) || 4ull * (a.row_hi - a.row_lo) >= X->dev.n_docs);
+    if (seeded) {
+        a.fb_list = w->fb_list;
+        ck(hm::launch_search_seed(X->dev, a, X->grid_search, st), "seeded search kernel");
+    }
+    if (timing) ck(cudaEventRecord(w->ev[4], st), "event");
     ck(hm::launch_search(X->dev, a, X->grid_search, st), "search kernel");
     if (timing) ck(cudaEventRecord(w->ev[2], st), "event");
     ck(hm::launch_exact(X->dev, a, X->grid_exact, st), "exact kernel");
     if (timing) ck(cudaEventRecord(w->ev[3], st), "event");
-    g_last_launches = 3;  // our kernels: plan, fused search, exact (plus CUB's sort + a memset)
+    g_last_launches = seeded ? 4 : 3;  // ours: plan, seeded, exhaustive, exact (plus CUB's sort + a memset)
 }
 
 void read_timing(Workspace* w) {
     ck(cudaEventSynchronize(w->ev[3]), "event sync");
     ck(cudaEventElapsedTime(&g_ms_plan, w->ev[0], w->ev[1]), "elapsed");
-    ck(cudaEventElapsedTime(&g_ms_search, w->ev[1], w->ev[2]), "elapsed");
+    ck(cudaEventElapsedTime(&g_ms_seed, w->ev[1], w->ev[4]), "elapsed");
+    ck(cudaEventElapsedTime(&g_ms_search, w->ev[4], w->ev[2]), "elapsed");
     ck(cudaEventElapsedTime(&g_ms_exact, w->ev[2], w->ev[3]), "elapsed");
 }
 
@@ -623,6 +675,8 @@ bool ensure_baked(hm_index* X, double k1, double b, std::shared_lock<std::shared
         uint32_t err = 0;
         try {
             ck(cudaMemsetAsync(X->d_bake_err, 0, 4, st), "bake memset");
+            ck(cudaMemsetAsync(const_cast<float*>(X->dev.tmax), 0, std::max<uint64_t>(X->dev.n_terms, 1) * 4, st),
+               "tmax memset");
             hm::DevIndex d = X->dev;
             ck(hm::launch_bake(d, X->d_long_terms, X->n_long, k1, b, ks, X->d_bk, X->d_bake_err, st),
                "bake kernel");
@@ -725,7 +779,7 @@ int hm_search_batch(hm_index* X, const hm_query_batch* b, hm_results* out) {
             double* rconf = reinterpret_cast<double*>(take(nq * 8ull));
             uint8_t* rskip = take(nq);
             uint64_t* rpost = reinterpret_cast<uint64_t*>(take(nq * 8ull));
-            uint32_t* rcnt = reinterpret_cast<uint32_t*>(take(16));
+            uint32_t* rcnt = reinterpret_cast<uint32_t*>(take(32));
             std::memcpy(poff, b->q_off, (nq + 1ull) * 4);
             if (ntid) std::memcpy(ptid, b->q_tid, ntid * 4ull);
             if (b->tau) std::memcpy(ptau, b->tau, nq * 8ull);
@@ -747,10 +801,11 @@ int hm_search_batch(hm_index* X, const hm_query_batch* b, hm_results* out) {
             ck(cudaMemcpyAsync(rconf, w->out_conf, nq * 8ull, cudaMemcpyDeviceToHost, st), "D2H");
             ck(cudaMemcpyAsync(rskip, w->out_skip, nq, cudaMemcpyDeviceToHost, st), "D2H");
             ck(cudaMemcpyAsync(rpost, w->out_post, nq * 8ull, cudaMemcpyDeviceToHost, st), "D2H");
-            ck(cudaMemcpyAsync(rcnt, w->counters, 16, cudaMemcpyDeviceToHost, st), "D2H");
+            ck(cudaMemcpyAsync(rcnt, w->counters, 32, cudaMemcpyDeviceToHost, st), "D2H");
             ck(cudaStreamSynchronize(st), "batch");
             if (b->flags & HM_FLAG_TIMING) read_timing(w);
             g_last_exact = rcnt[1];
+            g_last_handed = rcnt[4];
             if (rcnt[3] & hm::kErrTooManyTerms)
                 throw std::invalid_argument("a query has more than 256 distinct terms");
             if (rcnt[3] & 2u) throw std::runtime_error("exact kernel failed to converge");
@@ -801,6 +856,13 @@ int hm_search_batch_device(hm_index* X, const hm_query_batch* b, hm_results* out
             run_batch(X, w, hb, b->q_off, b->q_tid, b->tau, *out, reinterpret_cast<float*>(w->pin));
             ck(cudaEventRecord(ev, w->stream), "event record");
             ck(cudaStreamWaitEvent(ust, ev, 0), "wait");
+            if (b->flags & HM_FLAG_TIMING) {  // plus the batch counters (32 B D2H)
+                uint32_t* rc = reinterpret_cast<uint32_t*>(w->pin) + hm::kMaxCodes;
+                ck(cudaMemcpyAsync(rc, w->counters, 32, cudaMemcpyDeviceToHost, w->stream), "D2H counters");
+                ck(cudaStreamSynchronize(w->stream), "sync");
+                g_last_exact = rc[1];
+                g_last_handed = rc[4];
+            }
             // pinned w32 staging is reused by the next call on this workspace:
             // make sure the async upload finished before handing it back
             ck(cudaStreamSynchronize(w->stream), "sync");
@@ -818,6 +880,12 @@ int hm_search_batch_device(hm_index* X, const hm_query_batch* b, hm_results* out
 int hm_last_batch_stats(uint32_t* n_exact, uint32_t* n_launches) {
     if (n_exact) *n_exact = g_last_exact;
     if (n_launches) *n_launches = g_last_launches;
+    return HM_OK;
+}
+
+int hm_last_batch_seed(float* ms_seed, uint32_t* n_handed_over) {
+    if (ms_seed) *ms_seed = g_ms_seed;
+    if (n_handed_over) *n_handed_over = g_last_handed;
     return HM_OK;
 }
 

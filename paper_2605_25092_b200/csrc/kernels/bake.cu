@@ -97,6 +97,7 @@ __global__ void __launch_bounds__(32 * kBakeWarps) bake_kernel(DevIndex ix, cons
     __syncwarp();
     const uint32_t lo = (ks + 1) << 23, hi = (ks + 1 + kBakeBinades) << 23;  // exponent fields 1..7 after scaling
     uint32_t bad = 0;
+    float wmax = 0.f;
     for (uint32_t i = lane; i < n; i += 32) {
         const uint32_t p = ix.post[B + i];
         const uint32_t local = p >> kCodeBitsLong;  // row inside the 16K tile
@@ -111,7 +112,9 @@ __global__ void __launch_bounds__(32 * kBakeWarps) bake_kernel(DevIndex ix, cons
             tf = ix.tf[B + i];
             dl = ix.doc_lens[(j << kTileShift) + local];
         }
-        const uint32_t bits = __float_as_uint(impact32(tf, dl, ix.avgdl, k1, b));
+        const float w = impact32(tf, dl, ix.avgdl, k1, b);
+        wmax = fmaxf(wmax, w);
+        const uint32_t bits = __float_as_uint(w);
         uint32_t q = 0;
         if (bits >= lo && bits < hi) q = (bits - (ks << 23)) >> (23 - kBakeMantBits);
         else bad = 1;
@@ -134,7 +137,31 @@ __global__ void __launch_bounds__(32 * kBakeWarps) bake_kernel(DevIndex ix, cons
             ++pos;
         }
     }
+    // the term's max impact (non-negative floats order like their bit patterns)
+    for (int o = 16; o > 0; o >>= 1) wmax = fmaxf(wmax, __shfl_xor_sync(0xffffffffu, wmax, o));
+    if (lane == 0) atomicMax(reinterpret_cast<unsigned int*>(const_cast<float*>(ix.tmax) + t), __float_as_uint(wmax));
     if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(err, 1u);
+}
+
+// Max impact of every SHORT term (long terms get theirs in bake_kernel).
+__global__ void tmax_short_kernel(DevIndex ix, double k1, double b, float* __restrict__ tmax) {
+    const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= ix.n_terms || ix.long_slot[t] >= 0) return;
+    const uint32_t cb = ix.code_bits;
+    float m = 0.f;
+    for (uint64_t i = ix.term_off[t]; i < ix.term_off[t + 1]; ++i) {
+        const uint32_t p = ix.post[i], code = p & ix.esc_short;
+        double tf, dl;
+        if (code < ix.n_codes_short) {
+            tf = ix.code_tf[code];
+            dl = ix.code_len[code];
+        } else {
+            tf = ix.tf[i];
+            dl = ix.doc_lens[p >> cb];
+        }
+        m = fmaxf(m, impact32(tf, dl, ix.avgdl, k1, b));
+    }
+    tmax[t] = m;
 }
 
 // impact scale: float(k1 + 1), the largest possible impact (tf -> inf, or
@@ -150,9 +177,14 @@ uint32_t bake_ks(double k1) {
 cudaError_t launch_bake(const DevIndex& ix, const uint32_t* long_terms, uint32_t n_long, double k1,
                         double b, uint32_t ks, uint32_t* bk, uint32_t* err, cudaStream_t st) {
     const uint64_t warps = static_cast<uint64_t>(n_long) * ix.n_units;
-    if (warps == 0) return cudaSuccess;
-    const uint64_t blocks = (warps + kBakeWarps - 1) / kBakeWarps;
-    bake_kernel<<<static_cast<unsigned>(blocks), 32 * kBakeWarps, 0, st>>>(ix, long_terms, n_long, k1, b, ks, bk, err);
+    if (warps) {
+        const uint64_t blocks = (warps + kBakeWarps - 1) / kBakeWarps;
+        bake_kernel<<<static_cast<unsigned>(blocks), 32 * kBakeWarps, 0, st>>>(ix, long_terms, n_long, k1, b, ks, bk, err);
+        const cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess) return e;
+    }
+    if (ix.n_terms)
+        tmax_short_kernel<<<(ix.n_terms + 255) / 256, 256, 0, st>>>(ix, k1, b, const_cast<float*>(ix.tmax));
     return cudaGetLastError();
 }
 

@@ -18,6 +18,9 @@ cudaError_t launch_lpt_sort(void* temp, size_t bytes, const BatchArgs& a,
                             cudaStream_t st);
 // persistent fused kernel: TAAT scoring + selection + exact rescoring + margin
 cudaError_t launch_search(const DevIndex& ix, const BatchArgs& a, int grid, cudaStream_t st);
+// seeded MaxScore pre-pass (kernels/search_seed.cu); hands the queries it
+// does not serve to the exhaustive kernel through a.fb_list
+cudaError_t launch_search_seed(const DevIndex& ix, const BatchArgs& a, int grid, cudaStream_t st);
 // persistent exact fp64 kernel for the queries in a.exact_list
 cudaError_t launch_exact(const DevIndex& ix, const BatchArgs& a, int grid, cudaStream_t st);
 // merge of per-shard exact top-k lists (after the all-gather)

@@ -97,7 +97,17 @@ struct DevIndex {
     const uint32_t* bk_uoff;   // [n_long][n_units + 1] unit offsets relative to bk_base
     uint32_t n_units;          // n_tiles * kUnitsPerTile
     uint32_t bk_ks;            // impact scale exponent: stored value = w * 2^-ks
+    const float* tmax;         // [n_terms] max idf-free impact of the term (baked; bounds of the seeded kernel)
+    // dense probe arrays of the most frequent long terms (seeded kernel):
+    // dense[d * n_docs + row] = the posting's (tf, len) code, kDenseAbsent if
+    // the term lacks the row, kDenseEscape if the pair has no code
+    const uint16_t* dense;
+    const int32_t* dense_of_slot;  // [n_long] d or -1
 };
+constexpr uint16_t kDenseAbsent = 0xFFFF;
+constexpr uint16_t kDenseEscape = 0xFFFE;
+constexpr int kMaxDense = 128;             // dense arrays: long terms with df >= n_docs / 32, largest first
+constexpr int kDenseMinDiv = 32;
 
 // swizzled position of a row (only bits 0-4 change, from bits 5-9); an involution
 #ifdef __CUDACC__
@@ -123,9 +133,13 @@ struct BatchArgs {
     uint32_t* plan_len;        // [nq]
     uint64_t* cost;            // [nq] sum of df over the plan (LPT key)
     uint32_t* order;           // [nq] queries, most expensive first
-    uint32_t* counters;        // [0]=work cursor fast, [1]=exact list size,
-                               // [2]=work cursor exact, [3]=error flags
+    uint32_t* counters;        // [0]=work cursor (seeded or exhaustive), [1]=exact list size,
+                               // [2]=work cursor exact, [3]=error flags,
+                               // [4]=fallback list size, [5]=fallback cursor
     uint32_t* exact_list;      // [nq]
+    uint32_t* fb_list;         // [nq] queries the seeded kernel hands to the exhaustive
+                               // kernel (counters[4] entries, cursor counters[5]); null:
+                               // the exhaustive kernel takes every query from `order`
     uint32_t* stab;            // per-CTA short-term tile tables
     uint32_t stab_stride;      // words per short term (>= n_tiles + 2)
     // results (device)

@@ -45,6 +45,12 @@ struct __align__(16) FastSmem {
     uint32_t n_w[kConsWarps];
     uint64_t post;
     uint32_t q, n_long, n_short, bad, n_surv, flood, Lg, total;
+    // seeded MaxScore kernel (search_seed.cu) only
+    float t_cu[kFastTerms];                // mult * idf * 2^-61 (selection-score domain)
+    float t_ms[kFastTerms];                // t_cu * max impact of the term (rounded up)
+    int32_t t_dense[kFastTerms];           // dense probe array of the term, -1 if none
+    uint8_t msorder[kFastTerms];           // plan indices by t_ms ascending
+    uint8_t t_spos[kFastTerms];            // short terms: index among the short terms (stab row)
 };
 
 struct SurvView {

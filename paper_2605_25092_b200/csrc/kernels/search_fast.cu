@@ -73,8 +73,13 @@ __global__ void __launch_bounds__(kCons, 2) search_fast_kernel(DevIndex ix, Batc
     for (;;) {
         __syncthreads();
         if (tid == 0) {
-            const uint32_t w = atomicAdd(&a.counters[0], 1u);
-            S.q = w < a.nq ? a.order[w] : kNoTerm;
+            if (a.fb_list) {  // after the seeded kernel: only the queries it handed over
+                const uint32_t w = atomicAdd(&a.counters[5], 1u);
+                S.q = w < a.counters[4] ? a.fb_list[w] : kNoTerm;
+            } else {
+                const uint32_t w = atomicAdd(&a.counters[0], 1u);
+                S.q = w < a.nq ? a.order[w] : kNoTerm;
+            }
         }
         __syncthreads();
         const uint32_t q = S.q;

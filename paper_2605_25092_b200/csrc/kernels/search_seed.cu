@@ -1,0 +1,372 @@
+// search_seed_kernel: seeded MaxScore -- the sparse, document-at-a-time
+// counterpart of the reference's lossless pruning (CsrIndex::
+// bm25_topk_maxscore, src/csr_index.cpp:106-207; output identical to the
+// exhaustive bm25_topk, acceptance.cpp:144-171), run BEFORE the exhaustive
+// tile sweep.  For every query that has a short plan term (df <= 32 * n_tiles):
+//
+//   1. seeds: every posting of t*, the short term with the largest bound
+//      ms_t = mult * idf * (max impact of the term), is scored completely by
+//      probing each plan term (dense per-row code arrays for the most frequent
+//      terms: one load; binary search in the term's 1,024-row sub-tile range or
+//      short-term tile segment otherwise).  The k-th best seed score theta0 is
+//      the k-th best score of real documents: a valid lower bound L.
+//   2. split: the non-essential terms NE are the longest prefix of the
+//      bound-ascending order with sum(ms) * (1 + 3 delta) < te = L (1 - 2.5
+//      delta).  A document without t* and without any essential term scores
+//      at most that sum: it cannot be admitted.
+//   3. candidates: every posting of the remaining essential terms E' (unless
+//      their postings exceed kEMax -- then the query falls back to the
+//      exhaustive kernel) is scored completely the same way; rows already seen
+//      (they contain t* or an earlier E' term) are skipped by probing those.
+//   4. admission into the per-warp candidate lists with the exhaustive
+//      kernel's rule (A >= L (1 - 2.5 delta)), then the common exact epilogue
+//      (finish_query: survivors rescored in fp64 in the reference's order).
+//
+// Every document the exhaustive kernel would admit is scored here, and all
+// fp32 scores carry the same delta bound, so the survivors -- and the
+// bit-identical fp64 results -- are the same.  Queries without a short term,
+// with too many essential postings, or with more candidates than the lists can
+// hold are appended to the fallback list that the exhaustive kernel serves.
+#include "hm_device.cuh"
+#include "hm_launch.h"
+#include "hm_ptx.cuh"
+#include "search_common.cuh"
+
+namespace hm {
+
+constexpr uint32_t kEMax = 65536;  // essential (non-seed) postings served here
+constexpr uint32_t kSeedMaxTerms = 16;  // longer plans go straight to the exhaustive kernel
+constexpr uint64_t kSeedMinPostings = 65536;  // cheaper queries too (e.g. a recency window)
+
+template <int CAPW>
+struct SeedCtx {
+    const DevIndex& ix;
+    const BatchArgs& a;
+    FastSmem<CAPW>& S;
+    const uint32_t* stab;
+    uint32_t stride, j0, cb;
+    double k1, b;
+};
+
+// Contribution of plan term i (selection-score domain: score * 2^-61) to a row.
+template <int CAPW>
+__device__ __noinline__ float seed_probe(const SeedCtx<CAPW>& c, uint32_t i, uint32_t row) {
+    const DevIndex& ix = c.ix;
+    const int32_t slot = c.S.t_slot[i];
+    float w;
+    if (slot >= 0) {
+        const int32_t d = c.S.t_dense[i];
+        if (d >= 0) {
+            const uint16_t code = __ldg(ix.dense + static_cast<uint64_t>(d) * ix.n_docs + row);
+            if (code == kDenseAbsent) return 0.f;
+            if (code != kDenseEscape) return c.S.t_cu[i] * __ldg(c.a.w32 + code);
+        }
+        const uint32_t* tb = tile_row(ix, slot);
+        const uint32_t sub = row >> kSubShift;
+        const uint64_t s0 = c.S.t_start[i];
+        const uint64_t lo = s0 + __ldg(tb + sub), hi = s0 + __ldg(tb + sub + 1);
+        const uint32_t local = row & (kTile - 1);
+        const uint64_t pos = lower_bound_packed(ix.post, lo, hi, local << kCodeBitsLong);
+        if (pos >= hi) return 0.f;
+        const uint32_t p = __ldg(ix.post + pos);
+        if ((p >> kCodeBitsLong) != local) return 0.f;
+        const uint32_t code = p & kEscLong;
+        w = code < ix.n_codes ? __ldg(c.a.w32 + code)
+                              : impact32(static_cast<double>(__ldg(ix.tf + pos)),
+                                         static_cast<double>(__ldg(ix.doc_lens + row)), ix.avgdl, c.k1, c.b);
+    } else {
+        const uint32_t* tab = c.stab + static_cast<uint64_t>(c.S.t_spos[i]) * c.stride;
+        const uint32_t jj = (row >> kTileShift) - c.j0;
+        const uint64_t s0 = c.S.t_start[i];
+        const uint64_t lo = s0 + tab[jj], hi = s0 + tab[jj + 1];
+        const uint64_t pos = lower_bound_row(ix.post, lo, hi, row, c.cb);
+        if (pos >= hi) return 0.f;
+        const uint32_t p = __ldg(ix.post + pos);
+        if ((p >> c.cb) != row) return 0.f;
+        const uint32_t code = p & ix.esc_short;
+        w = code < ix.n_codes_short ? __ldg(c.a.w32 + code)
+                                    : impact32(static_cast<double>(__ldg(ix.tf + pos)),
+                                               static_cast<double>(__ldg(ix.doc_lens + row)), ix.avgdl, c.k1, c.b);
+    }
+    return c.S.t_cu[i] * w;
+}
+
+template <int CAPW>
+__global__ void __launch_bounds__(kCons, 2) search_seed_kernel(DevIndex ix, BatchArgs a) {
+    using Smem = FastSmem<CAPW>;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    Smem& S = *reinterpret_cast<Smem*>(smem_raw);
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const uint32_t cb = ix.code_bits;
+    const uint32_t row_lo = a.row_lo, row_hi = a.row_hi;
+    const double k1 = a.k1, bb = a.b;
+    const uint32_t stride = a.stab_stride;
+    uint32_t* stab = a.stab + static_cast<uint64_t>(blockIdx.x) * kMaxTerms * stride;
+    float* sA = reinterpret_cast<float*>(stab + static_cast<uint64_t>(kFastTerms) * stride);  // seed scores
+    const uint32_t kmax = FastCfg<CAPW>::kMaxKServed;
+
+    for (int i = tid; i < kTile; i += kCons) S.acc[i] = 0.f;
+    if (tid < kConsWarps) S.n_w[tid] = 0;
+    if (tid == 0) S.Lg = 0u;
+
+    for (;;) {
+        __syncthreads();
+        if (tid == 0) {
+            const uint32_t w = atomicAdd(&a.counters[0], 1u);
+            S.q = w < a.nq ? a.order[w] : kNoTerm;
+        }
+        __syncthreads();
+        const uint32_t q = S.q;
+        if (q == kNoTerm) break;
+        const uint32_t poff = a.q_off[q];
+        const uint32_t m = a.plan_len[q];
+        const uint32_t k = a.k;
+        // anything unusual goes to the exhaustive kernel, which routes it on
+        if (m == 0 || m > kFastTerms || k == 0 || k > kmax || (a.flags & 1u) || row_hi <= row_lo) {
+            if (tid == 0) a.fb_list[atomicAdd(&a.counters[4], 1u)] = q;
+            continue;
+        }
+        // ---------------- prologue: plan, window bounds, bounds
+        if (tid < static_cast<int>(m)) {
+            const uint32_t t = a.plan_tid[poff + tid];
+            const uint32_t mult = a.plan_mult[poff + tid];
+            const double idf = ix.idf[t];
+            const int32_t slot = ix.long_slot[t];
+            const uint64_t s0 = ix.term_off[t], s1 = ix.term_off[t + 1];
+            const uint64_t w0 = row_lo > 0 ? first_at_or_after(ix, slot, s0, s1, row_lo) : s0;
+            const uint64_t w1 = row_hi < ix.n_docs ? first_at_or_after(ix, slot, s0, s1, row_hi) : s1;
+            S.t_start[tid] = s0;
+            S.t_wlo[tid] = w0;
+            S.t_end[tid] = w1;
+            S.t_idf[tid] = idf;
+            S.t_mult[tid] = mult;
+            S.t_slot[tid] = slot;
+            const float cu = static_cast<float>(ldexp(static_cast<double>(mult) * idf, -kScoreShift));
+            S.t_cu[tid] = cu;
+            S.t_ms[tid] = cu * ix.tmax[t] * 1.0000010f;  // rounded up: an upper bound
+            S.t_dense[tid] = slot >= 0 ? ix.dense_of_slot[slot] : -1;
+        }
+        __syncthreads();
+        if (tid == 0) {
+            uint64_t post = 0;
+            uint32_t ns = 0, bad = 0, seed = kNoTerm;
+            S.pref[0] = 0;
+            for (uint32_t i = 0; i < m; ++i) {
+                post += S.t_end[i] - S.t_wlo[i];
+                const double idf = S.t_idf[i];
+                if (!(idf > 0.0) || !isfinite(idf)) bad = 1;
+                if (S.t_slot[i] < 0) {
+                    S.order_list[ns] = static_cast<uint16_t>(i);
+                    S.t_spos[i] = static_cast<uint8_t>(ns);
+                    S.pref[ns + 1] = S.pref[ns] + static_cast<uint32_t>(S.t_end[i] - S.t_wlo[i]);
+                    ++ns;
+                    if (seed == kNoTerm || S.t_ms[i] > S.t_ms[seed]) seed = i;
+                }
+            }
+            // plan indices by bound ascending (ties by index)
+            for (uint32_t i = 0; i < m; ++i) {
+                uint32_t p = i;
+                while (p > 0 && S.t_ms[S.msorder[p - 1]] > S.t_ms[i]) {
+                    S.msorder[p] = S.msorder[p - 1];
+                    --p;
+                }
+                S.msorder[p] = static_cast<uint8_t>(i);
+            }
+            S.post = post;
+            S.n_short = ns;
+            S.n_long = seed;  // reused: the seed term
+            // serve the query here only when probing the seeds is cheaper than
+            // streaming its postings (a dependent-load probe ~ 32 streamed
+            // postings) and the plan is short enough for the bounds to bite
+            bool worth = seed != kNoTerm && (m <= kSeedMaxTerms || (a.flags & 32u));
+            if (worth && !(a.flags & 32u)) {  // HM_FLAG_SEED_ALL (tests) skips the cost rule
+                const uint64_t n_seed = S.t_end[seed] - S.t_wlo[seed];
+                worth = post >= kSeedMinPostings && n_seed * m * 32 < post;
+            }
+            S.bad = bad || !worth;
+            S.flood = 0;
+            S.Lg = 0u;
+        }
+        if (tid < kConsWarps) S.n_w[tid] = 0;
+        __syncthreads();
+        if (S.bad) {  // no short term (or a non-positive idf): the exhaustive kernel
+            if (tid == 0) a.fb_list[atomicAdd(&a.counters[4], 1u)] = q;
+            continue;
+        }
+        const uint32_t n_short = S.n_short, ts = S.n_long;
+        const uint32_t j0 = row_lo >> kTileShift, j1 = (row_hi - 1) >> kTileShift;
+        const uint32_t nt = j1 - j0 + 1;
+        // ---------------- short-term tile tables (probes of short terms)
+        {
+            const uint32_t total = S.pref[n_short];
+            for (uint32_t f = tid; f < total; f += kCons) {
+                uint32_t lo = 0, hi = n_short;  // s: pref[s] <= f < pref[s+1]
+                while (hi - lo > 1) {
+                    const uint32_t mid = (lo + hi) >> 1;
+                    if (S.pref[mid] <= f) lo = mid;
+                    else hi = mid;
+                }
+                const uint32_t s = lo, i = S.order_list[s];
+                const uint64_t w0 = S.t_wlo[i], w1 = S.t_end[i], s0 = S.t_start[i];
+                const uint64_t g = w0 + (f - S.pref[s]);
+                const int jt = static_cast<int>((__ldg(ix.post + g) >> cb) >> kTileShift) - static_cast<int>(j0);
+                const int jp = g == w0 ? -1
+                                       : static_cast<int>((__ldg(ix.post + g - 1) >> cb) >> kTileShift) -
+                                             static_cast<int>(j0);
+                uint32_t* tab = stab + static_cast<uint64_t>(s) * stride;
+                for (int jj = jp + 1; jj <= jt; ++jj) tab[jj] = static_cast<uint32_t>(g - s0);
+                if (g + 1 == w1)
+                    for (int jj = jt + 1; jj <= static_cast<int>(nt); ++jj) tab[jj] = static_cast<uint32_t>(w1 - s0);
+            }
+            for (uint32_t x = tid; x < n_short * (nt + 1); x += kCons) {
+                const uint32_t s = x / (nt + 1), jj = x % (nt + 1), i = S.order_list[s];
+                if (S.t_wlo[i] == S.t_end[i])
+                    stab[static_cast<uint64_t>(s) * stride + jj] = static_cast<uint32_t>(S.t_wlo[i] - S.t_start[i]);
+            }
+        }
+        __syncthreads();
+        const float delta = static_cast<float>(m + 10) * 5.9604645e-08f + 1.5258789e-05f;  // (m+10) 2^-24 + 2^-16
+        const float f_slack = 1.0f - 2.5f * delta;
+        const float f_ub = 1.0f + 3.0f * delta;
+        const SeedCtx<CAPW> sc{ix, a, S, stab, stride, j0, cb, k1, bb};
+        auto full_score = [&](uint32_t row) {
+            float A = 0.f;
+            for (uint32_t i = 0; i < m; ++i) A += seed_probe(sc, i, row);
+            return A;
+        };
+
+        // ---------------- 1. seeds: every posting of t* in the window
+        const uint64_t sw0 = S.t_wlo[ts];
+        const uint32_t n_seed = static_cast<uint32_t>(S.t_end[ts] - sw0);
+        for (uint32_t e = tid; e < n_seed; e += kCons) sA[e] = full_score(__ldg(ix.post + sw0 + e) >> cb);
+        __syncthreads();
+        float L = 0.f;
+        if (n_seed >= k) L = block_kth_largest<kCons>(sA, n_seed, k, S.hist, S.sel, [] { __syncthreads(); });
+        const float te = fmaxf(L * f_slack, kFltMin);  // admission threshold (as the exhaustive kernel's)
+        if (tid == 0) S.Lg = __float_as_uint(L);
+        // ---------------- 2. non-essential terms: longest bound-ascending prefix
+        // whose bound sum cannot reach te; the rest (but t*) must be enumerated
+        if (warp == 0) {
+            float v = static_cast<uint32_t>(lane) < m ? S.t_ms[S.msorder[lane]] : 0.f;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const float nb = __shfl_up_sync(0xffffffffu, v, o);
+                if (lane >= o) v += nb;
+            }
+            const bool isne = static_cast<uint32_t>(lane) < m && v * f_ub < te;
+            const uint32_t ne = __reduce_or_sync(0xffffffffu, isne ? 1u << S.msorder[lane] : 0u);
+            uint64_t ne_post = 0;
+            if (lane == 0) {
+                for (uint32_t i = 0; i < m; ++i)
+                    if (i != ts && !((ne >> i) & 1u)) ne_post += S.t_end[i] - S.t_wlo[i];
+                S.sel[0] = ne;  // reused: essential mask complement
+                S.flood = ne_post > kEMax ? 2u : 0u;
+            }
+        }
+        __syncthreads();
+        if (S.flood == 2u) {  // too many essential postings: the exhaustive kernel
+            if (tid == 0) a.fb_list[atomicAdd(&a.counters[4], 1u)] = q;
+            continue;
+        }
+        const uint32_t ne = S.sel[0];
+        // ---------------- 3./4. admission of seeds, then of essential candidates
+        uint32_t nw = 0;
+        float Lw = 0.f;
+        bool flood = false;
+        auto admit = [&](bool ok_in, uint32_t row, float A) {  // warp-synchronous
+            if (nw > static_cast<uint32_t>(CAPW - 32)) {
+                nw = warp_prune(S, warp, nw, k, Lw, f_slack);
+                if (nw > static_cast<uint32_t>(CAPW - 32)) flood = true;
+            }
+            const float t = fmaxf(fmaxf(fmaxf(Lw, __uint_as_float(S.Lg)) * f_slack, te), kFltMin);
+            const bool ok = ok_in && !flood && A >= t;
+            const uint32_t bal = __ballot_sync(0xffffffffu, ok);
+            if (ok) {
+                const uint32_t pos = nw + __popc(bal & ((1u << lane) - 1u));
+                S.cl_row[warp][pos] = row;
+                S.cl_val[warp][pos] = A;
+            }
+            nw += __popc(bal);
+            __syncwarp();
+        };
+        for (uint32_t e0 = warp * 32; e0 < n_seed && !flood; e0 += kConsWarps * 32) {
+            const uint32_t e = e0 + lane;
+            const bool v = e < n_seed;
+            admit(v, v ? __ldg(ix.post + sw0 + e) >> cb : 0u, v ? sA[e] : 0.f);
+        }
+        // essential candidates: warp w enumerates the term's postings of tile w,
+        // w + 8, ... (long terms: rows from the tile offsets, no per-posting search)
+        auto candidate = [&](bool v, uint32_t row, uint32_t i) {
+            float A = 0.f;
+            if (v) {
+                // one probe per plan term; a row already seen (it holds t* or an
+                // earlier essential term) is not admitted twice
+                for (uint32_t i2 = 0; i2 < m; ++i2) {
+                    const float x = seed_probe(sc, i2, row);
+                    if (x != 0.f && (i2 == ts || (i2 < i && !((ne >> i2) & 1u)))) v = false;
+                    A += x;
+                }
+            }
+            admit(v, row, A);
+        };
+        for (uint32_t i = 0; i < m && !flood; ++i) {
+            if (i == ts || ((ne >> i) & 1u)) continue;
+            const uint64_t w0 = S.t_wlo[i], w1 = S.t_end[i];
+            if (S.t_slot[i] < 0) {
+                const uint32_t n = static_cast<uint32_t>(w1 - w0);
+                for (uint32_t e0 = warp * 32; e0 < n && !flood; e0 += kConsWarps * 32) {
+                    const uint32_t e = e0 + lane;
+                    candidate(e < n, e < n ? __ldg(ix.post + w0 + e) >> cb : 0u, i);
+                }
+            } else {
+                const uint32_t* tb = tile_row(ix, S.t_slot[i]);
+                const uint64_t s0 = S.t_start[i];
+                for (uint32_t j = j0 + warp; j <= j1 && !flood; j += kConsWarps) {
+                    const uint64_t b0 = max(s0 + __ldg(tb + static_cast<uint64_t>(j) * kSubPerTile), w0);
+                    const uint64_t b1 = min(s0 + __ldg(tb + static_cast<uint64_t>(j + 1) * kSubPerTile), w1);
+                    for (uint64_t g0 = b0; g0 < b1 && !flood; g0 += 32) {
+                        const uint64_t g = g0 + lane;
+                        candidate(g < b1, g < b1 ? (j << kTileShift) + (__ldg(ix.post + g) >> kCodeBitsLong) : 0u, i);
+                    }
+                }
+            }
+        }
+        if (lane == 0) {
+            S.n_w[warp] = nw;
+            if (flood) S.flood = 1;
+        }
+        __syncthreads();
+        if (S.flood) {  // the lists cannot hold the near-ties: the exhaustive kernel
+            if (tid == 0) a.fb_list[atomicAdd(&a.counters[4], 1u)] = q;
+            __syncthreads();
+            if (tid < kConsWarps) S.n_w[tid] = 0;
+            continue;
+        }
+        finish_query<CAPW>(ix, a, S, q, m, k, nw, f_slack, k1, bb);
+    }
+}
+
+template <int CAPW>
+static cudaError_t seed_attr() {
+    static bool done = false;
+    if (done) return cudaSuccess;
+    const cudaError_t e = cudaFuncSetAttribute(search_seed_kernel<CAPW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                               static_cast<int>(sizeof(FastSmem<CAPW>)));
+    if (e == cudaSuccess) done = true;
+    return e;
+}
+
+cudaError_t launch_search_seed(const DevIndex& ix, const BatchArgs& a, int sms, cudaStream_t st) {
+    if (a.k <= FastCfg<192>::kMaxKServed) {
+        const cudaError_t e = seed_attr<192>();
+        if (e != cudaSuccess) return e;
+        search_seed_kernel<192><<<2 * sms, kCons, sizeof(FastSmem<192>), st>>>(ix, a);
+    } else {
+        const cudaError_t e = seed_attr<320>();
+        if (e != cudaSuccess) return e;
+        search_seed_kernel<320><<<2 * sms, kCons, sizeof(FastSmem<320>), st>>>(ix, a);
+    }
+    return cudaGetLastError();
+}
+
+}  // namespace hm

@@ -24,6 +24,8 @@ from . import _lib
 HM_FLAG_FORCE_EXACT = 1
 HM_FLAG_DEBUG_NO_RESET = 2
 HM_FLAG_TIMING = 4
+HM_FLAG_EXHAUSTIVE = 16
+HM_FLAG_SEED_ALL = 32
 NO_TERM = 0xFFFFFFFF
 MAX_K = 256
 
@@ -53,7 +55,7 @@ class Results(C.Structure):
 
 EXPORTS = ["hm_index_create", "hm_index_destroy", "hm_index_device_bytes", "hm_index_format",
            "hm_search_batch", "hm_search_batch_device", "hm_last_batch_stats",
-           "hm_last_batch_timing",
+           "hm_last_batch_timing", "hm_last_batch_seed",
            "hm_merge_shards_device", "hm_margin", "hm_last_error"]
 
 
@@ -74,6 +76,7 @@ def lib():
     L.hm_search_batch_device.argtypes = [C.c_void_p, P(QueryBatch), P(Results), C.c_void_p]
     L.hm_last_batch_stats.argtypes = [P(C.c_uint32), P(C.c_uint32)]
     L.hm_last_batch_timing.argtypes = [P(C.c_float), P(C.c_float), P(C.c_float)]
+    L.hm_last_batch_seed.argtypes = [P(C.c_float), P(C.c_uint32)]
     L.hm_merge_shards_device.argtypes = [C.c_uint32, C.c_uint32, C.c_uint32, C.c_void_p,
                                          C.c_void_p, C.c_void_p, C.c_void_p, C.c_double,
                                          C.c_double, P(Results), C.c_void_p]
@@ -225,6 +228,14 @@ def last_timing():
     return a.value, b.value, c.value
 
 
+def last_seed():
+    """(ms_seed, n_handed_over): the seeded MaxScore pass of this thread's last
+    batch (its time on HM_FLAG_TIMING batches; queries left to the exhaustive kernel)."""
+    a, n = C.c_float(), C.c_uint32()
+    lib().hm_last_batch_seed(C.byref(a), C.byref(n))
+    return a.value, n.value
+
+
 def last_stats():
     """(n_exact_fallback, n_kernel_launches) of this thread's last batch."""
     ne, nl = C.c_uint32(), C.c_uint32()
@@ -299,10 +310,10 @@ class CsrIndex:
     def resolve(self, query_terms):
         return [self.vocab.get(t, NO_TERM) for t in query_terms]
 
-    def bm25_topk(self, query_terms, k, p=None, stats=None):
+    def bm25_topk(self, query_terms, k, p=None, stats=None, flags=0):
         """-> list[(doc_id, score)] ranked (score desc, id asc) (csr_index.cpp:77-104)."""
         p = p or Bm25Params()
-        r = self.dev().search_lists([self.resolve(query_terms)], k, k1=p.k1, b=p.b)
+        r = self.dev().search_lists([self.resolve(query_terms)], k, k1=p.k1, b=p.b, flags=flags)
         if stats is not None:
             stats.postings_touched += int(r["postings"][0])
         n = int(r["n"][0])

@@ -163,6 +163,30 @@ def test_concurrent_batches_with_different_params(c1):
     assert not errs, errs[0]
 
 
+@pytest.mark.parametrize("k", [1, 10, 100])
+def test_c1_seeded_everything_identical(c1, k):
+    """HM_FLAG_SEED_ALL: the seeded MaxScore pre-pass (search_seed.cu) serves
+    every query that has a short term -- seeds, essential candidates and the
+    hand-over to the exhaustive kernel must not change a single bit."""
+    got = c1["dev"].search_lists(c1["tids"], k, flags=search.HM_FLAG_SEED_ALL)
+    ids, sc, n, post = c1["orc"].topk(c1["tids"], k)
+    check_batch(got, ids, sc, n, post, what=f"C1 seeded k={k}")
+
+
+@pytest.mark.parametrize("k1,b", [(0.9, 0.4), (2.0, 1.0)])
+def test_c1_seeded_other_params(c1, k1, b):
+    tids = c1["tids"][:300]
+    got = c1["dev"].search_lists(tids, 10, k1=k1, b=b, flags=search.HM_FLAG_SEED_ALL)
+    ids, sc, n, post = c1["orc"].topk(tids, 10, k1=k1, b=b)
+    check_batch(got, ids, sc, n, post, what=f"seeded k1={k1} b={b}")
+
+
+def test_c1_exhaustive_only_identical(c1):
+    got = c1["dev"].search_lists(c1["tids"], 10, flags=search.HM_FLAG_EXHAUSTIVE)
+    ids, sc, n, post = c1["orc"].topk(c1["tids"], 10)
+    check_batch(got, ids, sc, n, post, what="C1 exhaustive only")
+
+
 def test_sentinel_reset_is_load_bearing(c1):
     """Pitfall 3 (test_twophase.cpp:66-83): without the
     per-query reset of the candidate state, stale entries of the previous query
@@ -172,7 +196,7 @@ def test_sentinel_reset_is_load_bearing(c1):
     ids, sc, n, _ = c1["orc"].topk(tids, 10)
     good = c1["dev"].search_lists(tids, 10)
     check_batch(good, ids, sc, n, what="reset on")
-    bad = c1["dev"].search_lists(tids, 10, flags=search.HM_FLAG_DEBUG_NO_RESET)
+    bad = c1["dev"].search_lists(tids, 10, flags=search.HM_FLAG_DEBUG_NO_RESET | search.HM_FLAG_EXHAUSTIVE)
     differs = any(bad["n"][i] != n[i] or (bad["ids"][i, :n[i]] != ids[i, :n[i]]).any()
                   for i in range(len(tids)))
     assert differs, "disabling the reset should contaminate results"
@@ -192,6 +216,8 @@ def test_random_instances_vs_reference(gpu):
         got = idx.bm25_topk(q, k, stats=stats)
         assert_same([g[0] for g in got], [g[1] for g in got], want_ids, want_sc, f"trial {trial}")
         assert stats.postings_touched == want_post
+        got = idx.bm25_topk(q, k, flags=search.HM_FLAG_SEED_ALL)
+        assert_same([g[0] for g in got], [g[1] for g in got], want_ids, want_sc, f"trial {trial} seeded")
 
 
 def test_toy_corpus_known_answers(gpu):

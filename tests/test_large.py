@@ -53,3 +53,8 @@ def test_full_size_configs(gpu, cfg):
     ex = dev.search_lists([tids[i] for i in sub[:6]], k, flags=search.HM_FLAG_FORCE_EXACT)
     for key in ("ids", "scores", "n", "conf", "skip"):
         assert (ex[key] == sub_got[key][:6]).all(), key
+    # the default path (seeded pre-pass + exhaustive hand-over) and the
+    # exhaustive kernel alone agree bit for bit on the whole batch
+    exh = dev.search_lists(tids, k, flags=search.HM_FLAG_EXHAUSTIVE)
+    for key in ("ids", "scores", "n", "conf", "skip", "postings"):
+        assert (exh[key] == got[key]).all(), key

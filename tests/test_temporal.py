@@ -119,3 +119,5 @@ def test_window_edges_not_tile_aligned(c3_small):
         check_batch(got, ids, sc, n, post, what=f"[{lo},{hi})")
         ex = c["dev"].search_lists(tids, 10, row_lo=lo, row_hi=hi, flags=search.HM_FLAG_FORCE_EXACT)
         check_batch(ex, ids, sc, n, post, what=f"exact [{lo},{hi})")
+        sd = c["dev"].search_lists(tids, 10, row_lo=lo, row_hi=hi, flags=search.HM_FLAG_SEED_ALL)
+        check_batch(sd, ids, sc, n, post, what=f"seeded [{lo},{hi})")

@@ -35,6 +35,10 @@ def main(n=8841823, V=1000000, lo=20, hi=60, nq=10000, mint=3, maxt=6, k=10, rep
         e0.record(); dev.search_batch_device(dq_off, dq_tid, out, k, flags=int(os.environ.get('HM_PROBE_FLAGS', '0')), row_lo=row_lo, row_hi=row_hi); e1.record(); torch.cuda.synchronize()
         ms = e0.elapsed_time(e1)
         wpost = int(out["postings"].sum().item())  # postings inside the window
+        if r == reps:
+            fl = int(os.environ.get('HM_PROBE_FLAGS', '0')) | search.HM_FLAG_TIMING
+            dev.search_batch_device(dq_off, dq_tid, out, k, flags=fl, row_lo=row_lo, row_hi=row_hi)
+            print("timing (plan, exhaustive, exact) ms:", search.last_timing(), " seeded (ms, handed over):", search.last_seed())
         print(f"rep {r}: {ms:.2f} ms  {nq/ms*1e3:.0f} qps  eff {wpost*8/ms/1e6:.0f} GB/s (8B/posting)  phys {wpost*4/ms/1e6:.0f} GB/s", flush=True)
     t = time.time(); r = dev.search_batch(off, tids, k, row_lo=row_lo, row_hi=row_hi); print(f"host api {time.time()-t:.3f}s n_exact={r['n_exact']}")
 
