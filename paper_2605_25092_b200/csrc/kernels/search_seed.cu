@@ -91,6 +91,81 @@ __device__ __noinline__ float seed_probe(const SeedCtx<CAPW>& c, uint32_t i, uin
     return c.S.t_cu[i] * w;
 }
 
+// Two independent lower-bound searches advanced in lockstep (their loads
+// overlap): first index of [lo, hi) whose key(post[.]) >= key.
+template <typename KeyOf>
+__device__ __forceinline__ void lower_bound_pair(const uint32_t* post, uint64_t& lo0, uint64_t hi0, uint32_t key0,
+                                                 uint64_t& lo1, uint64_t hi1, uint32_t key1, KeyOf kf) {
+    while (lo0 < hi0 || lo1 < hi1) {
+        const bool a0 = lo0 < hi0, a1 = lo1 < hi1;
+        const uint64_t m0 = lo0 + ((hi0 - lo0) >> 1), m1 = lo1 + ((hi1 - lo1) >> 1);
+        const uint32_t p0 = a0 ? __ldg(post + m0) : 0u, p1 = a1 ? __ldg(post + m1) : 0u;
+        if (a0) {
+            if (kf(p0) < key0) lo0 = m0 + 1;
+            else hi0 = m0;
+        }
+        if (a1) {
+            if (kf(p1) < key1) lo1 = m1 + 1;
+            else hi1 = m1;
+        }
+    }
+}
+
+// seed_probe for two rows at once (row1 ignored unless v1): the dense loads,
+// range loads and searches of both rows are in flight together
+template <int CAPW>
+__device__ __noinline__ float2 seed_probe2(const SeedCtx<CAPW>& c, uint32_t i, uint32_t row0, uint32_t row1, bool v1) {
+    const DevIndex& ix = c.ix;
+    const int32_t slot = c.S.t_slot[i];
+    const float cu = c.S.t_cu[i];
+    if (!v1) row1 = row0;
+    if (slot >= 0) {
+        const int32_t d = c.S.t_dense[i];
+        if (d >= 0) {
+            const uint16_t* col = ix.dense + static_cast<uint64_t>(d) * ix.n_docs;
+            const uint16_t c0 = __ldg(col + row0), c1 = __ldg(col + row1);
+            if (c0 != kDenseEscape && c1 != kDenseEscape)
+                return make_float2(c0 == kDenseAbsent ? 0.f : cu * __ldg(c.a.w32 + c0),
+                                   c1 == kDenseAbsent ? 0.f : cu * __ldg(c.a.w32 + c1));
+            return make_float2(seed_probe(c, i, row0), seed_probe(c, i, row1));  // escapes: rare
+        }
+        const uint32_t* tb = tile_row(ix, slot);
+        const uint64_t s0 = c.S.t_start[i];
+        uint64_t lo0 = s0 + __ldg(tb + (row0 >> kSubShift)), hi0 = s0 + __ldg(tb + (row0 >> kSubShift) + 1);
+        uint64_t lo1 = s0 + __ldg(tb + (row1 >> kSubShift)), hi1 = s0 + __ldg(tb + (row1 >> kSubShift) + 1);
+        const uint32_t l0 = row0 & (kTile - 1), l1 = row1 & (kTile - 1);
+        const uint64_t e0 = hi0, e1 = hi1;
+        lower_bound_pair(ix.post, lo0, hi0, l0, lo1, hi1, l1, [](uint32_t p) { return p >> kCodeBitsLong; });
+        auto w_of = [&](uint64_t pos, uint64_t end, uint32_t local, uint32_t row) {
+            if (pos >= end) return 0.f;
+            const uint32_t p = __ldg(ix.post + pos);
+            if ((p >> kCodeBitsLong) != local) return 0.f;
+            const uint32_t code = p & kEscLong;
+            return code < ix.n_codes ? __ldg(c.a.w32 + code)
+                                     : impact32(static_cast<double>(__ldg(ix.tf + pos)),
+                                                static_cast<double>(__ldg(ix.doc_lens + row)), ix.avgdl, c.k1, c.b);
+        };
+        return make_float2(cu * w_of(lo0, e0, l0, row0), cu * w_of(lo1, e1, l1, row1));
+    }
+    const uint32_t* tab = c.stab + static_cast<uint64_t>(c.S.t_spos[i]) * c.stride;
+    const uint64_t s0 = c.S.t_start[i];
+    const uint32_t j0 = (row0 >> kTileShift) - c.j0, j1 = (row1 >> kTileShift) - c.j0;
+    uint64_t lo0 = s0 + tab[j0], hi0 = s0 + tab[j0 + 1], lo1 = s0 + tab[j1], hi1 = s0 + tab[j1 + 1];
+    const uint64_t e0 = hi0, e1 = hi1;
+    const uint32_t cb = c.cb;
+    lower_bound_pair(ix.post, lo0, hi0, row0, lo1, hi1, row1, [cb](uint32_t p) { return p >> cb; });
+    auto w_of = [&](uint64_t pos, uint64_t end, uint32_t row) {
+        if (pos >= end) return 0.f;
+        const uint32_t p = __ldg(ix.post + pos);
+        if ((p >> cb) != row) return 0.f;
+        const uint32_t code = p & ix.esc_short;
+        return code < ix.n_codes_short ? __ldg(c.a.w32 + code)
+                                       : impact32(static_cast<double>(__ldg(ix.tf + pos)),
+                                                  static_cast<double>(__ldg(ix.doc_lens + row)), ix.avgdl, c.k1, c.b);
+    };
+    return make_float2(cu * w_of(lo0, e0, row0), cu * w_of(lo1, e1, row1));
+}
+
 template <int CAPW>
 __global__ void __launch_bounds__(kCons, 2) search_seed_kernel(DevIndex ix, BatchArgs a) {
     using Smem = FastSmem<CAPW>;
@@ -238,7 +313,19 @@ __global__ void __launch_bounds__(kCons, 2) search_seed_kernel(DevIndex ix, Batc
         // ---------------- 1. seeds: every posting of t* in the window
         const uint64_t sw0 = S.t_wlo[ts];
         const uint32_t n_seed = static_cast<uint32_t>(S.t_end[ts] - sw0);
-        for (uint32_t e = tid; e < n_seed; e += kCons) sA[e] = full_score(__ldg(ix.post + sw0 + e) >> cb);
+        for (uint32_t e = tid; e < n_seed; e += 2 * kCons) {  // two seeds per thread, probed together
+            const uint32_t e1 = e + kCons;
+            const bool v1 = e1 < n_seed;
+            const uint32_t r0 = __ldg(ix.post + sw0 + e) >> cb, r1 = v1 ? __ldg(ix.post + sw0 + e1) >> cb : r0;
+            float A0 = 0.f, A1 = 0.f;
+            for (uint32_t i = 0; i < m; ++i) {
+                const float2 x = seed_probe2(sc, i, r0, r1, v1);
+                A0 += x.x;
+                A1 += x.y;
+            }
+            sA[e] = A0;
+            if (v1) sA[e1] = A1;
+        }
         __syncthreads();
         float L = 0.f;
         if (n_seed >= k) L = block_kth_largest<kCons>(sA, n_seed, k, S.hist, S.sel, [] { __syncthreads(); });
@@ -296,27 +383,33 @@ __global__ void __launch_bounds__(kCons, 2) search_seed_kernel(DevIndex ix, Batc
         }
         // essential candidates: warp w enumerates the term's postings of tile w,
         // w + 8, ... (long terms: rows from the tile offsets, no per-posting search)
-        auto candidate = [&](bool v, uint32_t row, uint32_t i) {
-            float A = 0.f;
-            if (v) {
-                // one probe per plan term; a row already seen (it holds t* or an
-                // earlier essential term) is not admitted twice
+        // two candidates per lane, probed together; a row already seen (it holds
+        // t* or an earlier essential term) is not admitted twice
+        auto candidates = [&](bool v0, uint32_t r0, bool v1, uint32_t r1, uint32_t i) {
+            float A0 = 0.f, A1 = 0.f;
+            if (v0 || v1) {
+                if (!v0) r0 = r1;
                 for (uint32_t i2 = 0; i2 < m; ++i2) {
-                    const float x = seed_probe(sc, i2, row);
-                    if (x != 0.f && (i2 == ts || (i2 < i && !((ne >> i2) & 1u)))) v = false;
-                    A += x;
+                    const float2 x = seed_probe2(sc, i2, r0, r1, v1);
+                    const bool seen = i2 == ts || (i2 < i && !((ne >> i2) & 1u));
+                    if (seen && x.x != 0.f) v0 = false;
+                    if (seen && x.y != 0.f) v1 = false;
+                    A0 += x.x;
+                    A1 += x.y;
                 }
             }
-            admit(v, row, A);
+            admit(v0, r0, A0);
+            admit(v1, r1, A1);
         };
         for (uint32_t i = 0; i < m && !flood; ++i) {
             if (i == ts || ((ne >> i) & 1u)) continue;
             const uint64_t w0 = S.t_wlo[i], w1 = S.t_end[i];
             if (S.t_slot[i] < 0) {
                 const uint32_t n = static_cast<uint32_t>(w1 - w0);
-                for (uint32_t e0 = warp * 32; e0 < n && !flood; e0 += kConsWarps * 32) {
-                    const uint32_t e = e0 + lane;
-                    candidate(e < n, e < n ? __ldg(ix.post + w0 + e) >> cb : 0u, i);
+                for (uint32_t e0 = warp * 64; e0 < n && !flood; e0 += kConsWarps * 64) {
+                    const uint32_t ea = e0 + lane, eb = e0 + 32 + lane;
+                    candidates(ea < n, ea < n ? __ldg(ix.post + w0 + ea) >> cb : 0u, eb < n,
+                               eb < n ? __ldg(ix.post + w0 + eb) >> cb : 0u, i);
                 }
             } else {
                 const uint32_t* tb = tile_row(ix, S.t_slot[i]);
@@ -324,9 +417,11 @@ __global__ void __launch_bounds__(kCons, 2) search_seed_kernel(DevIndex ix, Batc
                 for (uint32_t j = j0 + warp; j <= j1 && !flood; j += kConsWarps) {
                     const uint64_t b0 = max(s0 + __ldg(tb + static_cast<uint64_t>(j) * kSubPerTile), w0);
                     const uint64_t b1 = min(s0 + __ldg(tb + static_cast<uint64_t>(j + 1) * kSubPerTile), w1);
-                    for (uint64_t g0 = b0; g0 < b1 && !flood; g0 += 32) {
-                        const uint64_t g = g0 + lane;
-                        candidate(g < b1, g < b1 ? (j << kTileShift) + (__ldg(ix.post + g) >> kCodeBitsLong) : 0u, i);
+                    const uint32_t base = j << kTileShift;
+                    for (uint64_t g0 = b0; g0 < b1 && !flood; g0 += 64) {
+                        const uint64_t ga = g0 + lane, gb = g0 + 32 + lane;
+                        candidates(ga < b1, ga < b1 ? base + (__ldg(ix.post + ga) >> kCodeBitsLong) : 0u, gb < b1,
+                                   gb < b1 ? base + (__ldg(ix.post + gb) >> kCodeBitsLong) : 0u, i);
                     }
                 }
             }
