@@ -69,7 +69,7 @@ constexpr int kUnitShift = 11;                // search-kernel warp unit: 2048 r
 constexpr int kUnitsPerTile = 1 << (kTileShift - kUnitShift);
 constexpr int kSubPerUnit = 1 << (kUnitShift - kSubShift);
 constexpr int kScoreShift = 61;               // fp32 selection scores are score * 2^-61
-constexpr int kShortCodes = 256;              // smem impact table of short-term codes
+constexpr int kShortCodes = 1024;             // smem impact table of the first codes (short terms use < 256)
 static_assert(kLocalBits == kTileShift, "local row field must cover one tile");
 
 struct DevIndex {

@@ -14,10 +14,10 @@
 //      bound-ascending order with sum(ms) * (1 + 3 delta) < te = L (1 - 2.5
 //      delta).  A document without t* and without any essential term scores
 //      at most that sum: it cannot be admitted.
-//   3. candidates: every posting of the remaining essential terms E' (unless
-//      their postings exceed kEMax -- then the query falls back to the
-//      exhaustive kernel) is scored completely the same way; rows already seen
-//      (they contain t* or an earlier E' term) are skipped by probing those.
+//   3. candidates: every posting of the remaining essential terms E' is scored
+//      completely the same way, unless they are more than kEMax postings --
+//      then the query falls back to the exhaustive kernel; rows already seen
+//      (they contain t* or an earlier E' term) are recognised from the probes.
 //   4. admission into the per-warp candidate lists with the exhaustive
 //      kernel's rule (A >= L (1 - 2.5 delta)), then the common exact epilogue
 //      (finish_query: survivors rescored in fp64 in the reference's order).
@@ -34,7 +34,8 @@
 
 namespace hm {
 
-constexpr uint32_t kEMax = 65536;  // essential (non-seed) postings served here
+constexpr uint64_t kProbeCost = 32;  // seeds: a probe (short dependent-load chain) ~ 32 streamed postings
+constexpr uint64_t kEMax = 65536;    // essential (non-seed) postings served here (best measured on C2)
 constexpr uint32_t kSeedMaxTerms = 16;  // longer plans go straight to the exhaustive kernel
 constexpr uint64_t kSeedMinPostings = 65536;  // cheaper queries too (e.g. a recency window)
 
@@ -48,6 +49,12 @@ struct SeedCtx {
     double k1, b;
 };
 
+// impact of a (tf, len) code: the first kShortCodes from shared memory
+template <int CAPW>
+__device__ __forceinline__ float code_w(const SeedCtx<CAPW>& c, uint32_t code) {
+    return code < static_cast<uint32_t>(kShortCodes) ? c.S.w32s[code] : __ldg(c.a.w32 + code);
+}
+
 // Contribution of plan term i (selection-score domain: score * 2^-61) to a row.
 template <int CAPW>
 __device__ __noinline__ float seed_probe(const SeedCtx<CAPW>& c, uint32_t i, uint32_t row) {
@@ -59,7 +66,7 @@ __device__ __noinline__ float seed_probe(const SeedCtx<CAPW>& c, uint32_t i, uin
         if (d >= 0) {
             const uint16_t code = __ldg(ix.dense + static_cast<uint64_t>(d) * ix.n_docs + row);
             if (code == kDenseAbsent) return 0.f;
-            if (code != kDenseEscape) return c.S.t_cu[i] * __ldg(c.a.w32 + code);
+            if (code != kDenseEscape) return c.S.t_cu[i] * code_w(c, code);
         }
         const uint32_t* tb = tile_row(ix, slot);
         const uint32_t sub = row >> kSubShift;
@@ -71,7 +78,7 @@ __device__ __noinline__ float seed_probe(const SeedCtx<CAPW>& c, uint32_t i, uin
         const uint32_t p = __ldg(ix.post + pos);
         if ((p >> kCodeBitsLong) != local) return 0.f;
         const uint32_t code = p & kEscLong;
-        w = code < ix.n_codes ? __ldg(c.a.w32 + code)
+        w = code < ix.n_codes ? code_w(c, code)
                               : impact32(static_cast<double>(__ldg(ix.tf + pos)),
                                          static_cast<double>(__ldg(ix.doc_lens + row)), ix.avgdl, c.k1, c.b);
     } else {
@@ -84,86 +91,138 @@ __device__ __noinline__ float seed_probe(const SeedCtx<CAPW>& c, uint32_t i, uin
         const uint32_t p = __ldg(ix.post + pos);
         if ((p >> c.cb) != row) return 0.f;
         const uint32_t code = p & ix.esc_short;
-        w = code < ix.n_codes_short ? __ldg(c.a.w32 + code)
+        w = code < ix.n_codes_short ? c.S.w32s[code]
                                     : impact32(static_cast<double>(__ldg(ix.tf + pos)),
                                                static_cast<double>(__ldg(ix.doc_lens + row)), ix.avgdl, c.k1, c.b);
     }
     return c.S.t_cu[i] * w;
 }
 
-// Two independent lower-bound searches advanced in lockstep (their loads
-// overlap): first index of [lo, hi) whose key(post[.]) >= key.
-template <typename KeyOf>
-__device__ __forceinline__ void lower_bound_pair(const uint32_t* post, uint64_t& lo0, uint64_t hi0, uint32_t key0,
-                                                 uint64_t& lo1, uint64_t hi1, uint32_t key1, KeyOf kf) {
-    while (lo0 < hi0 || lo1 < hi1) {
-        const bool a0 = lo0 < hi0, a1 = lo1 < hi1;
-        const uint64_t m0 = lo0 + ((hi0 - lo0) >> 1), m1 = lo1 + ((hi1 - lo1) >> 1);
-        const uint32_t p0 = a0 ? __ldg(post + m0) : 0u, p1 = a1 ? __ldg(post + m1) : 0u;
-        if (a0) {
-            if (kf(p0) < key0) lo0 = m0 + 1;
-            else hi0 = m0;
-        }
-        if (a1) {
-            if (kf(p1) < key1) lo1 = m1 + 1;
-            else hi1 = m1;
-        }
-    }
-}
-
-// seed_probe for two rows at once (row1 ignored unless v1): the dense loads,
-// range loads and searches of both rows are in flight together
-template <int CAPW>
-__device__ __noinline__ float2 seed_probe2(const SeedCtx<CAPW>& c, uint32_t i, uint32_t row0, uint32_t row1, bool v1) {
+// seed_probe for N rows at once (rows whose bit is clear in vmask are not
+// needed): all N dense loads / range loads / search steps are in flight
+// together.  Escaped dense codes (rare) fall back to the scalar probe.
+template <int N>
+struct RowsN {
+    uint32_t r[N];
+};
+template <int N>
+struct ValsN {
+    float v[N];
+};
+template <int CAPW, int N>
+__device__ __noinline__ ValsN<N> seed_probeN(const SeedCtx<CAPW>& c, uint32_t i, RowsN<N> rw, uint32_t vmask) {
     const DevIndex& ix = c.ix;
     const int32_t slot = c.S.t_slot[i];
     const float cu = c.S.t_cu[i];
-    if (!v1) row1 = row0;
+    ValsN<N> out;
+#pragma unroll
+    for (int u = 0; u < N; ++u)
+        if (!((vmask >> u) & 1u)) rw.r[u] = rw.r[0];
     if (slot >= 0) {
         const int32_t d = c.S.t_dense[i];
         if (d >= 0) {
             const uint16_t* col = ix.dense + static_cast<uint64_t>(d) * ix.n_docs;
-            const uint16_t c0 = __ldg(col + row0), c1 = __ldg(col + row1);
-            if (c0 != kDenseEscape && c1 != kDenseEscape)
-                return make_float2(c0 == kDenseAbsent ? 0.f : cu * __ldg(c.a.w32 + c0),
-                                   c1 == kDenseAbsent ? 0.f : cu * __ldg(c.a.w32 + c1));
-            return make_float2(seed_probe(c, i, row0), seed_probe(c, i, row1));  // escapes: rare
+            uint16_t code[N];
+#pragma unroll
+            for (int u = 0; u < N; ++u) code[u] = __ldg(col + rw.r[u]);
+#pragma unroll
+            for (int u = 0; u < N; ++u)
+                out.v[u] = code[u] == kDenseAbsent ? 0.f
+                           : code[u] == kDenseEscape ? seed_probe(c, i, rw.r[u])
+                                                     : cu * code_w(c, code[u]);
+            return out;
         }
         const uint32_t* tb = tile_row(ix, slot);
         const uint64_t s0 = c.S.t_start[i];
-        uint64_t lo0 = s0 + __ldg(tb + (row0 >> kSubShift)), hi0 = s0 + __ldg(tb + (row0 >> kSubShift) + 1);
-        uint64_t lo1 = s0 + __ldg(tb + (row1 >> kSubShift)), hi1 = s0 + __ldg(tb + (row1 >> kSubShift) + 1);
-        const uint32_t l0 = row0 & (kTile - 1), l1 = row1 & (kTile - 1);
-        const uint64_t e0 = hi0, e1 = hi1;
-        lower_bound_pair(ix.post, lo0, hi0, l0, lo1, hi1, l1, [](uint32_t p) { return p >> kCodeBitsLong; });
-        auto w_of = [&](uint64_t pos, uint64_t end, uint32_t local, uint32_t row) {
-            if (pos >= end) return 0.f;
-            const uint32_t p = __ldg(ix.post + pos);
-            if ((p >> kCodeBitsLong) != local) return 0.f;
-            const uint32_t code = p & kEscLong;
-            return code < ix.n_codes ? __ldg(c.a.w32 + code)
-                                     : impact32(static_cast<double>(__ldg(ix.tf + pos)),
-                                                static_cast<double>(__ldg(ix.doc_lens + row)), ix.avgdl, c.k1, c.b);
-        };
-        return make_float2(cu * w_of(lo0, e0, l0, row0), cu * w_of(lo1, e1, l1, row1));
+        uint64_t lo[N], hi[N], end[N];
+#pragma unroll
+        for (int u = 0; u < N; ++u) {
+            lo[u] = s0 + __ldg(tb + (rw.r[u] >> kSubShift));
+            hi[u] = s0 + __ldg(tb + (rw.r[u] >> kSubShift) + 1);
+            end[u] = hi[u];
+        }
+        for (;;) {
+            bool any = false;
+            uint32_t p[N];
+#pragma unroll
+            for (int u = 0; u < N; ++u) {
+                const uint64_t mid = lo[u] + ((hi[u] - lo[u]) >> 1);
+                p[u] = lo[u] < hi[u] ? __ldg(ix.post + mid) : 0u;
+            }
+#pragma unroll
+            for (int u = 0; u < N; ++u) {
+                if (lo[u] < hi[u]) {
+                    const uint64_t mid = lo[u] + ((hi[u] - lo[u]) >> 1);
+                    if ((p[u] >> kCodeBitsLong) < (rw.r[u] & (kTile - 1))) lo[u] = mid + 1;
+                    else hi[u] = mid;
+                }
+                any |= lo[u] < hi[u];
+            }
+            if (!any) break;
+        }
+#pragma unroll
+        for (int u = 0; u < N; ++u) {
+            float w = 0.f;
+            if (lo[u] < end[u]) {
+                const uint32_t pp = __ldg(ix.post + lo[u]);
+                if ((pp >> kCodeBitsLong) == (rw.r[u] & (kTile - 1))) {
+                    const uint32_t code = pp & kEscLong;
+                    w = code < ix.n_codes ? code_w(c, code)
+                                          : impact32(static_cast<double>(__ldg(ix.tf + lo[u])),
+                                                     static_cast<double>(__ldg(ix.doc_lens + rw.r[u])), ix.avgdl,
+                                                     c.k1, c.b);
+                }
+            }
+            out.v[u] = cu * w;
+        }
+        return out;
     }
     const uint32_t* tab = c.stab + static_cast<uint64_t>(c.S.t_spos[i]) * c.stride;
     const uint64_t s0 = c.S.t_start[i];
-    const uint32_t j0 = (row0 >> kTileShift) - c.j0, j1 = (row1 >> kTileShift) - c.j0;
-    uint64_t lo0 = s0 + tab[j0], hi0 = s0 + tab[j0 + 1], lo1 = s0 + tab[j1], hi1 = s0 + tab[j1 + 1];
-    const uint64_t e0 = hi0, e1 = hi1;
     const uint32_t cb = c.cb;
-    lower_bound_pair(ix.post, lo0, hi0, row0, lo1, hi1, row1, [cb](uint32_t p) { return p >> cb; });
-    auto w_of = [&](uint64_t pos, uint64_t end, uint32_t row) {
-        if (pos >= end) return 0.f;
-        const uint32_t p = __ldg(ix.post + pos);
-        if ((p >> cb) != row) return 0.f;
-        const uint32_t code = p & ix.esc_short;
-        return code < ix.n_codes_short ? __ldg(c.a.w32 + code)
-                                       : impact32(static_cast<double>(__ldg(ix.tf + pos)),
-                                                  static_cast<double>(__ldg(ix.doc_lens + row)), ix.avgdl, c.k1, c.b);
-    };
-    return make_float2(cu * w_of(lo0, e0, row0), cu * w_of(lo1, e1, row1));
+    uint64_t lo[N], hi[N], end[N];
+#pragma unroll
+    for (int u = 0; u < N; ++u) {
+        const uint32_t jj = (rw.r[u] >> kTileShift) - c.j0;
+        lo[u] = s0 + tab[jj];
+        hi[u] = s0 + tab[jj + 1];
+        end[u] = hi[u];
+    }
+    for (;;) {
+        bool any = false;
+        uint32_t p[N];
+#pragma unroll
+        for (int u = 0; u < N; ++u) {
+            const uint64_t mid = lo[u] + ((hi[u] - lo[u]) >> 1);
+            p[u] = lo[u] < hi[u] ? __ldg(ix.post + mid) : 0u;
+        }
+#pragma unroll
+        for (int u = 0; u < N; ++u) {
+            if (lo[u] < hi[u]) {
+                const uint64_t mid = lo[u] + ((hi[u] - lo[u]) >> 1);
+                if ((p[u] >> cb) < rw.r[u]) lo[u] = mid + 1;
+                else hi[u] = mid;
+            }
+            any |= lo[u] < hi[u];
+        }
+        if (!any) break;
+    }
+#pragma unroll
+    for (int u = 0; u < N; ++u) {
+        float w = 0.f;
+        if (lo[u] < end[u]) {
+            const uint32_t pp = __ldg(ix.post + lo[u]);
+            if ((pp >> cb) == rw.r[u]) {
+                const uint32_t code = pp & ix.esc_short;
+                w = code < ix.n_codes_short ? c.S.w32s[code]
+                                            : impact32(static_cast<double>(__ldg(ix.tf + lo[u])),
+                                                       static_cast<double>(__ldg(ix.doc_lens + rw.r[u])), ix.avgdl,
+                                                       c.k1, c.b);
+            }
+        }
+        out.v[u] = cu * w;
+    }
+    return out;
 }
 
 template <int CAPW>
@@ -181,6 +240,7 @@ __global__ void __launch_bounds__(kCons, 2) search_seed_kernel(DevIndex ix, Batc
     const uint32_t kmax = FastCfg<CAPW>::kMaxKServed;
 
     for (int i = tid; i < kTile; i += kCons) S.acc[i] = 0.f;
+    for (int i = tid; i < kShortCodes; i += kCons) S.w32s[i] = a.w32[i];
     if (tid < kConsWarps) S.n_w[tid] = 0;
     if (tid == 0) S.Lg = 0u;
 
@@ -256,7 +316,7 @@ __global__ void __launch_bounds__(kCons, 2) search_seed_kernel(DevIndex ix, Batc
             bool worth = seed != kNoTerm && (m <= kSeedMaxTerms || (a.flags & 32u));
             if (worth && !(a.flags & 32u)) {  // HM_FLAG_SEED_ALL (tests) skips the cost rule
                 const uint64_t n_seed = S.t_end[seed] - S.t_wlo[seed];
-                worth = post >= kSeedMinPostings && n_seed * m * 32 < post;
+                worth = post >= kSeedMinPostings && n_seed * m * kProbeCost < post;
             }
             S.bad = bad || !worth;
             S.flood = 0;
@@ -313,18 +373,25 @@ __global__ void __launch_bounds__(kCons, 2) search_seed_kernel(DevIndex ix, Batc
         // ---------------- 1. seeds: every posting of t* in the window
         const uint64_t sw0 = S.t_wlo[ts];
         const uint32_t n_seed = static_cast<uint32_t>(S.t_end[ts] - sw0);
-        for (uint32_t e = tid; e < n_seed; e += 2 * kCons) {  // two seeds per thread, probed together
-            const uint32_t e1 = e + kCons;
-            const bool v1 = e1 < n_seed;
-            const uint32_t r0 = __ldg(ix.post + sw0 + e) >> cb, r1 = v1 ? __ldg(ix.post + sw0 + e1) >> cb : r0;
-            float A0 = 0.f, A1 = 0.f;
-            for (uint32_t i = 0; i < m; ++i) {
-                const float2 x = seed_probe2(sc, i, r0, r1, v1);
-                A0 += x.x;
-                A1 += x.y;
+        constexpr int kP = 4;  // seeds per thread, probed together
+        for (uint32_t e = tid; e < n_seed; e += kP * kCons) {
+            RowsN<kP> rw;
+            uint32_t vm = 0;
+#pragma unroll
+            for (int u = 0; u < kP; ++u) {
+                const uint32_t eu = e + u * kCons;
+                rw.r[u] = eu < n_seed ? __ldg(ix.post + sw0 + eu) >> cb : 0u;
+                vm |= (eu < n_seed ? 1u : 0u) << u;
             }
-            sA[e] = A0;
-            if (v1) sA[e1] = A1;
+            float A[kP] = {};
+            for (uint32_t i = 0; i < m; ++i) {
+                const ValsN<kP> x = seed_probeN<CAPW, kP>(sc, i, rw, vm);
+#pragma unroll
+                for (int u = 0; u < kP; ++u) A[u] += x.v[u];
+            }
+#pragma unroll
+            for (int u = 0; u < kP; ++u)
+                if ((vm >> u) & 1u) sA[e + u * kCons] = A[u];
         }
         __syncthreads();
         float L = 0.f;
@@ -347,7 +414,7 @@ __global__ void __launch_bounds__(kCons, 2) search_seed_kernel(DevIndex ix, Batc
                 for (uint32_t i = 0; i < m; ++i)
                     if (i != ts && !((ne >> i) & 1u)) ne_post += S.t_end[i] - S.t_wlo[i];
                 S.sel[0] = ne;  // reused: essential mask complement
-                S.flood = ne_post > kEMax ? 2u : 0u;
+                S.flood = ne_post > kEMax && !(a.flags & 32u) ? 2u : 0u;
             }
         }
         __syncthreads();
@@ -383,33 +450,39 @@ __global__ void __launch_bounds__(kCons, 2) search_seed_kernel(DevIndex ix, Batc
         }
         // essential candidates: warp w enumerates the term's postings of tile w,
         // w + 8, ... (long terms: rows from the tile offsets, no per-posting search)
-        // two candidates per lane, probed together; a row already seen (it holds
+        // kP candidates per lane, probed together; a row already seen (it holds
         // t* or an earlier essential term) is not admitted twice
-        auto candidates = [&](bool v0, uint32_t r0, bool v1, uint32_t r1, uint32_t i) {
-            float A0 = 0.f, A1 = 0.f;
-            if (v0 || v1) {
-                if (!v0) r0 = r1;
+        auto candidates = [&](const RowsN<kP>& rw, uint32_t vm, uint32_t i) {
+            float A[kP] = {};
+            if (vm) {
                 for (uint32_t i2 = 0; i2 < m; ++i2) {
-                    const float2 x = seed_probe2(sc, i2, r0, r1, v1);
+                    const ValsN<kP> x = seed_probeN<CAPW, kP>(sc, i2, rw, vm);
                     const bool seen = i2 == ts || (i2 < i && !((ne >> i2) & 1u));
-                    if (seen && x.x != 0.f) v0 = false;
-                    if (seen && x.y != 0.f) v1 = false;
-                    A0 += x.x;
-                    A1 += x.y;
+#pragma unroll
+                    for (int u = 0; u < kP; ++u) {
+                        if (seen && x.v[u] != 0.f) vm &= ~(1u << u);
+                        A[u] += x.v[u];
+                    }
                 }
             }
-            admit(v0, r0, A0);
-            admit(v1, r1, A1);
+#pragma unroll
+            for (int u = 0; u < kP; ++u) admit((vm >> u) & 1u, rw.r[u], A[u]);
         };
         for (uint32_t i = 0; i < m && !flood; ++i) {
             if (i == ts || ((ne >> i) & 1u)) continue;
             const uint64_t w0 = S.t_wlo[i], w1 = S.t_end[i];
             if (S.t_slot[i] < 0) {
                 const uint32_t n = static_cast<uint32_t>(w1 - w0);
-                for (uint32_t e0 = warp * 64; e0 < n && !flood; e0 += kConsWarps * 64) {
-                    const uint32_t ea = e0 + lane, eb = e0 + 32 + lane;
-                    candidates(ea < n, ea < n ? __ldg(ix.post + w0 + ea) >> cb : 0u, eb < n,
-                               eb < n ? __ldg(ix.post + w0 + eb) >> cb : 0u, i);
+                for (uint32_t e0 = warp * 32 * kP; e0 < n && !flood; e0 += kConsWarps * 32 * kP) {
+                    RowsN<kP> rw;
+                    uint32_t vm = 0;
+#pragma unroll
+                    for (int u = 0; u < kP; ++u) {
+                        const uint32_t eu = e0 + 32 * u + lane;
+                        rw.r[u] = eu < n ? __ldg(ix.post + w0 + eu) >> cb : 0u;
+                        vm |= (eu < n ? 1u : 0u) << u;
+                    }
+                    candidates(rw, vm, i);
                 }
             } else {
                 const uint32_t* tb = tile_row(ix, S.t_slot[i]);
@@ -418,10 +491,16 @@ __global__ void __launch_bounds__(kCons, 2) search_seed_kernel(DevIndex ix, Batc
                     const uint64_t b0 = max(s0 + __ldg(tb + static_cast<uint64_t>(j) * kSubPerTile), w0);
                     const uint64_t b1 = min(s0 + __ldg(tb + static_cast<uint64_t>(j + 1) * kSubPerTile), w1);
                     const uint32_t base = j << kTileShift;
-                    for (uint64_t g0 = b0; g0 < b1 && !flood; g0 += 64) {
-                        const uint64_t ga = g0 + lane, gb = g0 + 32 + lane;
-                        candidates(ga < b1, ga < b1 ? base + (__ldg(ix.post + ga) >> kCodeBitsLong) : 0u, gb < b1,
-                                   gb < b1 ? base + (__ldg(ix.post + gb) >> kCodeBitsLong) : 0u, i);
+                    for (uint64_t g0 = b0; g0 < b1 && !flood; g0 += 32 * kP) {
+                        RowsN<kP> rw;
+                        uint32_t vm = 0;
+#pragma unroll
+                        for (int u = 0; u < kP; ++u) {
+                            const uint64_t gu = g0 + 32 * u + lane;
+                            rw.r[u] = gu < b1 ? base + (__ldg(ix.post + gu) >> kCodeBitsLong) : 0u;
+                            vm |= (gu < b1 ? 1u : 0u) << u;
+                        }
+                        candidates(rw, vm, i);
                     }
                 }
             }
