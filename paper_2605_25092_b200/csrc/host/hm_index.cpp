@@ -113,6 +113,7 @@ struct Workspace {
     cudaEvent_t ev[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
     uint32_t* stab = nullptr;  // per-CTA short-term tile tables
     uint64_t stab_words = 0;
+    uint32_t* seed_scratch = nullptr;  // per-CTA seeded-pass scratch
     // pinned host staging
     unsigned char* pin = nullptr;
     size_t pin_bytes = 0;
@@ -134,6 +135,7 @@ struct Workspace {
     ~Workspace() {
         free_dev();
         if (stab) cudaFree(stab);
+        if (seed_scratch) cudaFree(seed_scratch);
         for (auto e : ev)
             if (e) cudaEventDestroy(e);
         if (pin) cudaFreeHost(pin);
@@ -608,6 +610,8 @@ void run_batch(hm_index* X, Workspace* w, const hm_query_batch& hb, const uint32
         w->stab_words = words;
     }
     a.stab = w->stab;
+    if (!w->seed_scratch) dalloc(w->seed_scratch, 2ull * X->grid_search * hm::kSeedScratch);  // up to 2 CTAs per SM
+    a.seed_scratch = w->seed_scratch;
     a.out_ids = out.ids;
     a.out_scores = out.scores;
     a.out_n = out.n;

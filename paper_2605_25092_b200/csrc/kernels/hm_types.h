@@ -106,6 +106,7 @@ struct DevIndex {
 };
 constexpr uint16_t kDenseAbsent = 0xFFFF;
 constexpr uint16_t kDenseEscape = 0xFFFE;
+constexpr uint32_t kSeedScratch = 2 * 57344;  // words per CTA (search_seed.cu: kSeedMaxDf scores + rows)
 constexpr int kMaxDense = 128;             // dense arrays: long terms with df >= n_docs / 32, largest first
 constexpr int kDenseMinDiv = 32;
 
@@ -141,6 +142,7 @@ struct BatchArgs {
                                // kernel (counters[4] entries, cursor counters[5]); null:
                                // the exhaustive kernel takes every query from `order`
     uint32_t* stab;            // per-CTA short-term tile tables
+    uint32_t* seed_scratch;    // per-CTA seeded-pass scratch: kSeedScratch words (scores, rows)
     uint32_t stab_stride;      // words per short term (>= n_tiles + 2)
     // results (device)
     uint64_t* out_ids;

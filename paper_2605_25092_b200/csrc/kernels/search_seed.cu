@@ -37,6 +37,7 @@ namespace hm {
 constexpr uint64_t kProbeCost = 32;  // seeds: a probe (short dependent-load chain) ~ 32 streamed postings
 constexpr uint64_t kEMax = 65536;    // essential (non-seed) postings served here (best measured on C2)
 constexpr uint32_t kSeedMaxTerms = 16;  // longer plans go straight to the exhaustive kernel
+constexpr uint64_t kSeedMaxDf = kSeedScratch / 2;  // seed term: the strongest bound among terms with fewer postings
 constexpr uint64_t kSeedMinPostings = 65536;  // cheaper queries too (e.g. a recency window)
 
 template <int CAPW>
@@ -236,7 +237,7 @@ __global__ void __launch_bounds__(kCons, 2) search_seed_kernel(DevIndex ix, Batc
     const double k1 = a.k1, bb = a.b;
     const uint32_t stride = a.stab_stride;
     uint32_t* stab = a.stab + static_cast<uint64_t>(blockIdx.x) * kMaxTerms * stride;
-    float* sA = reinterpret_cast<float*>(stab + static_cast<uint64_t>(kFastTerms) * stride);  // seed scores
+    float* sA = reinterpret_cast<float*>(a.seed_scratch + static_cast<uint64_t>(blockIdx.x) * kSeedScratch);  // seed scores
     const uint32_t kmax = FastCfg<CAPW>::kMaxKServed;
 
     for (int i = tid; i < kTile; i += kCons) S.acc[i] = 0.f;
@@ -295,8 +296,9 @@ __global__ void __launch_bounds__(kCons, 2) search_seed_kernel(DevIndex ix, Batc
                     S.t_spos[i] = static_cast<uint8_t>(ns);
                     S.pref[ns + 1] = S.pref[ns] + static_cast<uint32_t>(S.t_end[i] - S.t_wlo[i]);
                     ++ns;
-                    if (seed == kNoTerm || S.t_ms[i] > S.t_ms[seed]) seed = i;
                 }
+                if (S.t_end[i] - S.t_wlo[i] <= kSeedMaxDf && (seed == kNoTerm || S.t_ms[i] > S.t_ms[seed]))
+                    seed = i;
             }
             // plan indices by bound ascending (ties by index)
             for (uint32_t i = 0; i < m; ++i) {
@@ -370,19 +372,13 @@ __global__ void __launch_bounds__(kCons, 2) search_seed_kernel(DevIndex ix, Batc
             return A;
         };
 
-        // ---------------- 1. seeds: every posting of t* in the window
+        // ---------------- 1. seeds: every posting of t* in the window; its row
+        // and complete score land at the posting's index in the scratch
         const uint64_t sw0 = S.t_wlo[ts];
         const uint32_t n_seed = static_cast<uint32_t>(S.t_end[ts] - sw0);
-        constexpr int kP = 4;  // seeds per thread, probed together
-        for (uint32_t e = tid; e < n_seed; e += kP * kCons) {
-            RowsN<kP> rw;
-            uint32_t vm = 0;
-#pragma unroll
-            for (int u = 0; u < kP; ++u) {
-                const uint32_t eu = e + u * kCons;
-                rw.r[u] = eu < n_seed ? __ldg(ix.post + sw0 + eu) >> cb : 0u;
-                vm |= (eu < n_seed ? 1u : 0u) << u;
-            }
+        uint32_t* sR = reinterpret_cast<uint32_t*>(sA) + kSeedMaxDf;  // seed rows
+        constexpr int kP = 4;  // rows per lane, probed together
+        auto score_rows = [&](const RowsN<kP>& rw, uint32_t vm, uint64_t g0, uint32_t step) {
             float A[kP] = {};
             for (uint32_t i = 0; i < m; ++i) {
                 const ValsN<kP> x = seed_probeN<CAPW, kP>(sc, i, rw, vm);
@@ -391,7 +387,42 @@ __global__ void __launch_bounds__(kCons, 2) search_seed_kernel(DevIndex ix, Batc
             }
 #pragma unroll
             for (int u = 0; u < kP; ++u)
-                if ((vm >> u) & 1u) sA[e + u * kCons] = A[u];
+                if ((vm >> u) & 1u) {
+                    const uint32_t e = static_cast<uint32_t>(g0 + u * step - sw0);
+                    sA[e] = A[u];
+                    sR[e] = rw.r[u];
+                }
+        };
+        if (S.t_slot[ts] < 0) {
+            for (uint32_t e = tid; e < n_seed; e += kP * kCons) {
+                RowsN<kP> rw;
+                uint32_t vm = 0;
+#pragma unroll
+                for (int u = 0; u < kP; ++u) {
+                    const uint32_t eu = e + u * kCons;
+                    rw.r[u] = eu < n_seed ? __ldg(ix.post + sw0 + eu) >> cb : 0u;
+                    vm |= (eu < n_seed ? 1u : 0u) << u;
+                }
+                score_rows(rw, vm, sw0 + e, kCons);
+            }
+        } else {  // a long seed term: its postings tile by tile (rows from the tile offsets)
+            const uint32_t* tb = tile_row(ix, S.t_slot[ts]);
+            const uint64_t s0 = S.t_start[ts], sw1 = S.t_end[ts];
+            for (uint32_t j = j0 + warp; j <= j1; j += kConsWarps) {
+                const uint64_t b0 = max(s0 + __ldg(tb + static_cast<uint64_t>(j) * kSubPerTile), sw0);
+                const uint64_t b1 = min(s0 + __ldg(tb + static_cast<uint64_t>(j + 1) * kSubPerTile), sw1);
+                for (uint64_t g0 = b0; g0 < b1; g0 += 32 * kP) {
+                    RowsN<kP> rw;
+                    uint32_t vm = 0;
+#pragma unroll
+                    for (int u = 0; u < kP; ++u) {
+                        const uint64_t gu = g0 + 32 * u + lane;
+                        rw.r[u] = gu < b1 ? (j << kTileShift) + (__ldg(ix.post + gu) >> kCodeBitsLong) : 0u;
+                        vm |= (gu < b1 ? 1u : 0u) << u;
+                    }
+                    score_rows(rw, vm, g0 + lane, 32);
+                }
+            }
         }
         __syncthreads();
         float L = 0.f;
@@ -446,7 +477,7 @@ __global__ void __launch_bounds__(kCons, 2) search_seed_kernel(DevIndex ix, Batc
         for (uint32_t e0 = warp * 32; e0 < n_seed && !flood; e0 += kConsWarps * 32) {
             const uint32_t e = e0 + lane;
             const bool v = e < n_seed;
-            admit(v, v ? __ldg(ix.post + sw0 + e) >> cb : 0u, v ? sA[e] : 0.f);
+            admit(v, v ? sR[e] : 0u, v ? sA[e] : 0.f);
         }
         // essential candidates: warp w enumerates the term's postings of tile w,
         // w + 8, ... (long terms: rows from the tile offsets, no per-posting search)
