@@ -51,6 +51,7 @@ struct __align__(16) FastSmem {
     int32_t t_dense[kFastTerms];           // dense probe array of the term, -1 if none
     uint8_t msorder[kFastTerms];           // plan indices by t_ms ascending
     uint8_t t_spos[kFastTerms];            // short terms: index among the short terms (stab row)
+    float ubne_q;                          // sum of the non-essential terms' bounds
 };
 
 struct SurvView {

@@ -440,6 +440,9 @@ __global__ void __launch_bounds__(kCons, 2) search_seed_kernel(DevIndex ix, Batc
             }
             const bool isne = static_cast<uint32_t>(lane) < m && v * f_ub < te;
             const uint32_t ne = __reduce_or_sync(0xffffffffu, isne ? 1u << S.msorder[lane] : 0u);
+            const uint32_t bal = __ballot_sync(0xffffffffu, isne);
+            const float ub = bal ? __shfl_sync(0xffffffffu, v, 31 - __clz(bal)) : 0.f;
+            if (lane == 0) S.ubne_q = ub;
             uint64_t ne_post = 0;
             if (lane == 0) {
                 for (uint32_t i = 0; i < m; ++i)
@@ -483,18 +486,37 @@ __global__ void __launch_bounds__(kCons, 2) search_seed_kernel(DevIndex ix, Batc
         // w + 8, ... (long terms: rows from the tile offsets, no per-posting search)
         // kP candidates per lane, probed together; a row already seen (it holds
         // t* or an earlier essential term) is not admitted twice
+        // Essential terms first (t* and E'); only rows whose essential partial
+        // score plus the non-essential bound can still reach te get the
+        // non-essential probes: (A_E + U_NE) (1 + 3 delta) < te bounds the
+        // full score below te, exactly as for rows without essential terms.
+        const float ubne = S.ubne_q;
         auto candidates = [&](const RowsN<kP>& rw, uint32_t vm, uint32_t i) {
             float A[kP] = {};
             if (vm) {
                 for (uint32_t i2 = 0; i2 < m; ++i2) {
+                    if ((ne >> i2) & 1u) continue;
                     const ValsN<kP> x = seed_probeN<CAPW, kP>(sc, i2, rw, vm);
-                    const bool seen = i2 == ts || (i2 < i && !((ne >> i2) & 1u));
+                    const bool seen = i2 == ts || i2 < i;
 #pragma unroll
                     for (int u = 0; u < kP; ++u) {
                         if (seen && x.v[u] != 0.f) vm &= ~(1u << u);
                         A[u] += x.v[u];
                     }
                 }
+                uint32_t need = 0;
+                const float tn = fmaxf(fmaxf(Lw, __uint_as_float(S.Lg)) * f_slack, te);
+#pragma unroll
+                for (int u = 0; u < kP; ++u)
+                    if (((vm >> u) & 1u) && (A[u] + ubne) * f_ub >= tn) need |= 1u << u;
+                vm = need;
+                if (ne && vm)
+                    for (uint32_t i2 = 0; i2 < m; ++i2) {
+                        if (!((ne >> i2) & 1u)) continue;
+                        const ValsN<kP> x = seed_probeN<CAPW, kP>(sc, i2, rw, vm);
+#pragma unroll
+                        for (int u = 0; u < kP; ++u) A[u] += x.v[u];
+                    }
             }
 #pragma unroll
             for (int u = 0; u < kP; ++u) admit((vm >> u) & 1u, rw.r[u], A[u]);
