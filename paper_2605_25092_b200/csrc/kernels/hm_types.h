@@ -136,11 +136,11 @@ struct BatchArgs {
     uint32_t* order;           // [nq] queries, most expensive first
     uint32_t* counters;        // [0]=work cursor (seeded or exhaustive), [1]=exact list size,
                                // [2]=work cursor exact, [3]=error flags,
-                               // [4]=fallback list size, [5]=fallback cursor
+                               // [4]=queries handed over, [5]=exhaustive cursor after the seeded pass
     uint32_t* exact_list;      // [nq]
-    uint32_t* fb_list;         // [nq] queries the seeded kernel hands to the exhaustive
-                               // kernel (counters[4] entries, cursor counters[5]); null:
-                               // the exhaustive kernel takes every query from `order`
+    uint32_t* fb_list;         // [nq] 1 = the seeded kernel handed the query to the
+                               // exhaustive kernel (which walks `order` with cursor
+                               // counters[5] and skips the others); null: every query
     uint32_t* stab;            // per-CTA short-term tile tables
     uint32_t* seed_scratch;    // per-CTA seeded-pass scratch: kSeedScratch words (scores, rows)
     uint32_t stab_stride;      // words per short term (>= n_tiles + 2)

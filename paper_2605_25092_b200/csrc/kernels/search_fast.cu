@@ -73,13 +73,16 @@ __global__ void __launch_bounds__(kCons, 2) search_fast_kernel(DevIndex ix, Batc
     for (;;) {
         __syncthreads();
         if (tid == 0) {
-            if (a.fb_list) {  // after the seeded kernel: only the queries it handed over
-                const uint32_t w = atomicAdd(&a.counters[5], 1u);
-                S.q = w < a.counters[4] ? a.fb_list[w] : kNoTerm;
-            } else {
-                const uint32_t w = atomicAdd(&a.counters[0], 1u);
-                S.q = w < a.nq ? a.order[w] : kNoTerm;
+            // after the seeded kernel: only the queries it handed over, still in
+            // LPT order (the ones it served are skipped)
+            uint32_t q = kNoTerm;
+            for (;;) {
+                const uint32_t w = atomicAdd(&a.counters[a.fb_list ? 5 : 0], 1u);
+                if (w >= a.nq) break;
+                q = a.order[w];
+                if (!a.fb_list || a.fb_list[q]) break;
             }
+            S.q = q;
         }
         __syncthreads();
         const uint32_t q = S.q;

@@ -226,6 +226,12 @@ __device__ __noinline__ ValsN<N> seed_probeN(const SeedCtx<CAPW>& c, uint32_t i,
     return out;
 }
 
+// leave query q to the exhaustive kernel (which walks the LPT order itself)
+__device__ __forceinline__ void hand_over(const BatchArgs& a, uint32_t q) {
+    a.fb_list[q] = 1u;
+    atomicAdd(&a.counters[4], 1u);
+}
+
 template <int CAPW>
 __global__ void __launch_bounds__(kCons, 2) search_seed_kernel(DevIndex ix, BatchArgs a) {
     using Smem = FastSmem<CAPW>;
@@ -259,7 +265,7 @@ __global__ void __launch_bounds__(kCons, 2) search_seed_kernel(DevIndex ix, Batc
         const uint32_t k = a.k;
         // anything unusual goes to the exhaustive kernel, which routes it on
         if (m == 0 || m > kFastTerms || k == 0 || k > kmax || (a.flags & 1u) || row_hi <= row_lo) {
-            if (tid == 0) a.fb_list[atomicAdd(&a.counters[4], 1u)] = q;
+            if (tid == 0) hand_over(a, q);
             continue;
         }
         // ---------------- prologue: plan, window bounds, bounds
@@ -327,7 +333,7 @@ __global__ void __launch_bounds__(kCons, 2) search_seed_kernel(DevIndex ix, Batc
         if (tid < kConsWarps) S.n_w[tid] = 0;
         __syncthreads();
         if (S.bad) {  // no short term (or a non-positive idf): the exhaustive kernel
-            if (tid == 0) a.fb_list[atomicAdd(&a.counters[4], 1u)] = q;
+            if (tid == 0) hand_over(a, q);
             continue;
         }
         const uint32_t n_short = S.n_short, ts = S.n_long;
@@ -453,7 +459,7 @@ __global__ void __launch_bounds__(kCons, 2) search_seed_kernel(DevIndex ix, Batc
         }
         __syncthreads();
         if (S.flood == 2u) {  // too many essential postings: the exhaustive kernel
-            if (tid == 0) a.fb_list[atomicAdd(&a.counters[4], 1u)] = q;
+            if (tid == 0) hand_over(a, q);
             continue;
         }
         const uint32_t ne = S.sel[0];
@@ -564,7 +570,7 @@ __global__ void __launch_bounds__(kCons, 2) search_seed_kernel(DevIndex ix, Batc
         }
         __syncthreads();
         if (S.flood) {  // the lists cannot hold the near-ties: the exhaustive kernel
-            if (tid == 0) a.fb_list[atomicAdd(&a.counters[4], 1u)] = q;
+            if (tid == 0) hand_over(a, q);
             __syncthreads();
             if (tid < kConsWarps) S.n_w[tid] = 0;
             continue;
