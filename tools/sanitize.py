@@ -1,0 +1,43 @@
+"""Small batches through every kernel path, for compute-sanitizer
+(memcheck / racecheck / initcheck / synccheck):
+
+    compute-sanitizer --tool memcheck python tools/sanitize.py
+
+Runs C1-shaped searches (default path, HM_FLAG_SEED_ALL, HM_FLAG_EXHAUSTIVE,
+HM_FLAG_FORCE_EXACT, a row window, k=100, other Bm25Params) and checks them
+against the C restatement of the reference (oracle/)."""
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np
+
+from oracle import restate
+from paper_2605_25092_b200 import search, synth
+
+
+def main():
+    c = synth.Corpus(n_records=20000, vocab_size=2000)
+    q = synth.Queries(c, n_queries=96)
+    hx = synth.HostIndex(c)
+    dev = search.DeviceIndex.from_host(hx)
+    orc = restate.OracleIndex.from_host(hx)
+    tids = [hx.resolve(q.term_ranks[q.offsets[i]:q.offsets[i + 1]]) for i in range(len(q))]
+    cases = [dict(), dict(flags=search.HM_FLAG_SEED_ALL), dict(flags=search.HM_FLAG_EXHAUSTIVE),
+             dict(flags=search.HM_FLAG_FORCE_EXACT), dict(row_lo=3000, row_hi=17000),
+             dict(row_lo=3000, row_hi=17000, flags=search.HM_FLAG_SEED_ALL), dict(k=100),
+             dict(k1=0.9, b=0.4, flags=search.HM_FLAG_SEED_ALL)]
+    for kw in cases:
+        k = kw.pop("k", 10)
+        got = dev.search_lists(tids, k, **kw)
+        okw = {x: kw[x] for x in ("k1", "b", "row_lo", "row_hi") if x in kw}
+        ids, sc, n, _ = orc.topk(tids, k, **okw)
+        assert (got["n"] == n).all(), kw
+        for i in range(len(tids)):
+            assert (got["ids"][i, :n[i]] == ids[i, :n[i]]).all(), (kw, i)
+            assert (got["scores"][i, :n[i]].view(np.uint64) == sc[i, :n[i]].view(np.uint64)).all(), (kw, i)
+    print("sanitize cases ok:", len(cases))
+
+
+if __name__ == "__main__":
+    main()
