@@ -149,6 +149,24 @@ int hm_merge_shards_device(uint32_t n_shards, uint32_t n_queries, uint32_t k,
                            const uint32_t* shard_n, const double* tau, double tau_default,
                            double epsilon_guard, hm_results* out_dev, void* stream);
 
+/* The reference's on-disk index, HIDX v1 (proj/src/io.cpp:91-157, 223-232):
+ * parsed straight into host arrays, validated with the reference's messages
+ * ("not an index file (bad magic)", "unsupported index version N",
+ * "unsupported idf convention: X", "index file truncated reading <field>").
+ * hm_hidx_view fills an hm_csr_view for hm_index_create (a BM25-mode index:
+ * mode 0; a Bridge-mode file is rejected there with the reference's
+ * "BM25 scoring requires a BM25-mode index"); hm_hidx_term returns the
+ * length of term `tid` and points *s at its bytes (not NUL-terminated).
+ * Replaces: hybrid::load_index (src/io.cpp:229-232) on the search path. */
+typedef struct hm_hidx hm_hidx;
+int hm_hidx_load(const char* path, hm_hidx** out);
+const char* hm_hidx_last_error(void);
+int hm_hidx_view(const hm_hidx* h, hm_csr_view* view, uint32_t* mode, double* build_k1,
+                 double* build_b);
+uint32_t hm_hidx_term(const hm_hidx* h, uint32_t tid, const char** s);
+const double* hm_hidx_maxscores(const hm_hidx* h);
+void hm_hidx_free(hm_hidx* h);
+
 /* Margin confidence over a ranked score list (src/cascade.cpp:10-21). */
 double hm_margin(const double* scores, uint32_t n, double epsilon_guard);
 

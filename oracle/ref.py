@@ -49,6 +49,8 @@ def lib():
     L.ref_index_from_arrays.argtypes = [u32, P(C.c_char_p), P(u64), P(u32), P(dbl), P(dbl),
                                         P(dbl), P(dbl), u32, P(u32), P(u64), dbl, dbl, dbl, P(vp)]
     L.ref_index_free.argtypes = [vp]
+    L.ref_save_index.argtypes = [vp, C.c_char_p]
+    L.ref_load_index.argtypes = [C.c_char_p, P(vp)]
     L.ref_index_sizes.argtypes = [vp, P(u64)]
     L.ref_index_export.argtypes = [vp, C.c_char_p, P(u64), P(u32), P(dbl), P(dbl), P(dbl),
                                    P(dbl), P(u32), P(u64), P(dbl)]
@@ -179,6 +181,17 @@ class RefIndex:
     def __del__(self):
         if getattr(self, "h", None):
             lib().ref_index_free(self.h)
+
+    def save(self, path):
+        """hybrid::save_index (io.cpp:223-227): a HIDX v1 file."""
+        _chk(lib().ref_save_index(self.h, str(path).encode()))
+
+    @classmethod
+    def load(cls, path):
+        """hybrid::load_index (io.cpp:229-232)."""
+        h = C.c_void_p()
+        _chk(lib().ref_load_index(str(path).encode(), C.byref(h)))
+        return cls(h)
 
     def export(self):
         L = lib()

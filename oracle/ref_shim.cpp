@@ -9,6 +9,7 @@
 //   * the reference searches     CsrIndex::bm25_topk        (csr_index.cpp:77-104)
 //                                CsrIndex::bm25_topk_maxscore (csr_index.cpp:106-207)
 //                                TemporalIndex::topk        (temporal_index.cpp:72-123)
+//   * the reference HIDX container  save_index / load_index   (io.cpp:91-157, 223-232)
 //   * confidence / k_star / ndcg_at_k / TwoPhaseSelector known-answer hooks
 //   * a CPU batch driver shaped like hybridmem's cmd_search parallel_for
 //     (tools/hybridmem.cpp:58-71, 305-313) for the CPU baseline timing.
@@ -26,6 +27,7 @@
 #include "hybrid/cascade.hpp"
 #include "hybrid/csr_index.hpp"
 #include "hybrid/eval.hpp"
+#include "hybrid/io.hpp"
 #include "hybrid/temporal_index.hpp"
 #include "hybrid/twophase.hpp"
 #include "hybrid/workload.hpp"
@@ -230,6 +232,18 @@ int ref_index_from_arrays(std::uint32_t n_terms, const char* const* terms,
 }
 
 void ref_index_free(void* h) { delete static_cast<Index*>(h); }
+
+// HIDX v1 files written / read by the reference's own io.cpp
+int ref_save_index(void* h, const char* path) {
+    return guard([&] { save_index(static_cast<Index*>(h)->idx, path); });
+}
+int ref_load_index(const char* path, void** out) {
+    return guard([&] {
+        auto ix = std::make_unique<Index>();
+        ix->idx = load_index(path);
+        *out = ix.release();
+    });
+}
 
 // sizes[0]=n_terms sizes[1]=n_postings sizes[2]=n_docs sizes[3]=term_bytes
 void ref_index_sizes(void* h, std::uint64_t* sizes) {

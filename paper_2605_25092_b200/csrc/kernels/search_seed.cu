@@ -110,15 +110,17 @@ template <int N>
 struct ValsN {
     float v[N];
 };
-template <int CAPW, int N>
+template <int CAPW, int N>  // vmask != 0
 __device__ __noinline__ ValsN<N> seed_probeN(const SeedCtx<CAPW>& c, uint32_t i, RowsN<N> rw, uint32_t vmask) {
     const DevIndex& ix = c.ix;
     const int32_t slot = c.S.t_slot[i];
     const float cu = c.S.t_cu[i];
     ValsN<N> out;
+    // rows not needed take a needed row's value (every probe stays in the window)
+    const uint32_t fill = rw.r[__ffs(vmask) - 1];
 #pragma unroll
     for (int u = 0; u < N; ++u)
-        if (!((vmask >> u) & 1u)) rw.r[u] = rw.r[0];
+        if (!((vmask >> u) & 1u)) rw.r[u] = fill;
     if (slot >= 0) {
         const int32_t d = c.S.t_dense[i];
         if (d >= 0) {
@@ -385,6 +387,7 @@ __global__ void __launch_bounds__(kCons, 2) search_seed_kernel(DevIndex ix, Batc
         uint32_t* sR = reinterpret_cast<uint32_t*>(sA) + kSeedMaxDf;  // seed rows
         constexpr int kP = 4;  // rows per lane, probed together
         auto score_rows = [&](const RowsN<kP>& rw, uint32_t vm, uint64_t g0, uint32_t step) {
+            if (!vm) return;  // seed_probeN needs at least one real row
             float A[kP] = {};
             for (uint32_t i = 0; i < m; ++i) {
                 const ValsN<kP> x = seed_probeN<CAPW, kP>(sc, i, rw, vm);
@@ -500,7 +503,7 @@ __global__ void __launch_bounds__(kCons, 2) search_seed_kernel(DevIndex ix, Batc
         auto candidates = [&](const RowsN<kP>& rw, uint32_t vm, uint32_t i) {
             float A[kP] = {};
             if (vm) {
-                for (uint32_t i2 = 0; i2 < m; ++i2) {
+                for (uint32_t i2 = 0; i2 < m && vm; ++i2) {  // (every row may turn out seen)
                     if ((ne >> i2) & 1u) continue;
                     const ValsN<kP> x = seed_probeN<CAPW, kP>(sc, i2, rw, vm);
                     const bool seen = i2 == ts || i2 < i;

@@ -56,6 +56,8 @@ class Results(C.Structure):
 EXPORTS = ["hm_index_create", "hm_index_destroy", "hm_index_device_bytes", "hm_index_format",
            "hm_search_batch", "hm_search_batch_device", "hm_last_batch_stats",
            "hm_last_batch_timing", "hm_last_batch_seed",
+           "hm_hidx_load", "hm_hidx_last_error", "hm_hidx_view", "hm_hidx_term", "hm_hidx_maxscores",
+           "hm_hidx_free",
            "hm_merge_shards_device", "hm_margin", "hm_last_error"]
 
 
@@ -77,6 +79,14 @@ def lib():
     L.hm_last_batch_stats.argtypes = [P(C.c_uint32), P(C.c_uint32)]
     L.hm_last_batch_timing.argtypes = [P(C.c_float), P(C.c_float), P(C.c_float)]
     L.hm_last_batch_seed.argtypes = [P(C.c_float), P(C.c_uint32)]
+    L.hm_hidx_load.argtypes = [C.c_char_p, P(C.c_void_p)]
+    L.hm_hidx_last_error.restype = C.c_char_p
+    L.hm_hidx_view.argtypes = [C.c_void_p, P(CsrView), P(C.c_uint32), P(C.c_double), P(C.c_double)]
+    L.hm_hidx_term.argtypes = [C.c_void_p, C.c_uint32, P(C.c_char_p)]
+    L.hm_hidx_term.restype = C.c_uint32
+    L.hm_hidx_maxscores.argtypes = [C.c_void_p]
+    L.hm_hidx_maxscores.restype = P(C.c_double)
+    L.hm_hidx_free.argtypes = [C.c_void_p]
     L.hm_merge_shards_device.argtypes = [C.c_uint32, C.c_uint32, C.c_uint32, C.c_void_p,
                                          C.c_void_p, C.c_void_p, C.c_void_p, C.c_double,
                                          C.c_double, P(Results), C.c_void_p]
@@ -142,6 +152,17 @@ class DeviceIndex:
         self.n_docs = len(k["doc_ids"])
         self.df = np.diff(k["term_offsets"].astype(np.int64))
         self._keep = None  # borrowed only for the duration of create
+
+    @classmethod
+    def _adopt(cls, h, device, n_terms, n_docs, df):
+        self = cls.__new__(cls)
+        self._h, self.device, self.n_terms, self.n_docs, self.df, self._keep = h, device, n_terms, n_docs, df, None
+        return self
+
+    @classmethod
+    def from_hidx(cls, path, device=0):
+        """From a HIDX v1 file written by the reference's save_index."""
+        return Hidx(path).device_index(device)
 
     @classmethod
     def from_host(cls, hx, device=0):
@@ -287,6 +308,16 @@ class CsrIndex:
         self._dev = None
 
     @classmethod
+    def load(cls, path, device=0):
+        """hybrid::load_index (io.cpp:229-232) of a HIDX v1 file, native reader."""
+        hd = Hidx(path)
+        a = hd.arrays()
+        if hd.mode != 0:
+            raise RuntimeError("BM25 scoring requires a BM25-mode index")
+        return cls(hd.terms(), a["term_offsets"], a["posting_rows"], a["posting_weights"], a["idf"],
+                   a["order_key"], a["doc_lens"], a["doc_ids"], a["avgdl"], hd.build_params, device)
+
+    @classmethod
     def from_host(cls, hx, device=0):
         idx = cls(hx.term_strings(), hx.term_offsets, hx.posting_rows,
                   hx.posting_tf.astype(np.float64), hx.idf, hx.order_key, hx.doc_lens,
@@ -330,6 +361,65 @@ class CsrIndex:
         return self.dev().search_lists([self.resolve(q) for q in queries], k, k1=p.k1, b=p.b,
                                        tau=tau, tau_default=tau_default, row_lo=row_lo,
                                        row_hi=row_hi, flags=flags)
+
+
+class Hidx:
+    """A HIDX v1 file (the reference's save_index output, io.cpp:91-157) parsed
+    by the framework's native reader; `arrays()` views its host arrays."""
+
+    def __init__(self, path):
+        L = lib()
+        h = C.c_void_p()
+        if L.hm_hidx_load(str(path).encode(), C.byref(h)) != 0:
+            raise RuntimeError(L.hm_hidx_last_error().decode())
+        self._h = h
+        self.view = CsrView()
+        mode, k1, b = C.c_uint32(), C.c_double(), C.c_double()
+        L.hm_hidx_view(h, C.byref(self.view), C.byref(mode), C.byref(k1), C.byref(b))
+        self.mode, self.build_params = mode.value, Bm25Params(k1.value, b.value)
+
+    def terms(self):
+        L, out, p = lib(), [], C.c_char_p()
+        for t in range(self.view.n_terms):
+            n = L.hm_hidx_term(self._h, t, C.byref(p))
+            out.append(C.string_at(p, n).decode())
+        return out
+
+    def arrays(self):
+        v, nt, nd = self.view, self.view.n_terms, self.view.n_docs
+        cts = {np.uint64: C.c_uint64, np.uint32: C.c_uint32, np.float64: C.c_double}
+
+        def arr(ptr, n, dt):
+            if not n:
+                return np.zeros(0, dt)
+            p = C.cast(ptr, C.POINTER(cts[dt]))
+            return np.ctypeslib.as_array(p, (n,)).astype(dt, copy=True)
+        P = int(arr(v.term_offsets, nt + 1, np.uint64)[-1]) if nt else 0
+        return dict(term_offsets=arr(v.term_offsets, nt + 1, np.uint64),
+                    posting_rows=arr(v.posting_rows, P, np.uint32),
+                    posting_weights=arr(v.posting_weights, P, np.float64),
+                    idf=arr(v.term_idfs, nt, np.float64),
+                    maxscore=arr(lib().hm_hidx_maxscores(self._h), nt, np.float64),
+                    order_key=arr(v.term_order_keys, nt, np.float64),
+                    doc_lens=arr(v.doc_lens, nd, np.uint32), doc_ids=arr(v.doc_ids, nd, np.uint64),
+                    avgdl=v.avgdl)
+
+    def device_index(self, device=0):
+        """Upload straight from the parsed file (no Python copies)."""
+        if self.mode != 0:
+            raise RuntimeError("BM25 scoring requires a BM25-mode index")
+        h = C.c_void_p()
+        _check(lib().hm_index_create(C.byref(self.view), device, C.byref(h)))
+        return DeviceIndex._adopt(h, device, self.view.n_terms, self.view.n_docs,
+                                  np.diff(self.arrays()["term_offsets"].astype(np.int64)))
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib().hm_hidx_free(self._h)
+            self._h = None
+
+    def __del__(self):
+        self.close()
 
 
 def k_star(epsilon, lam):

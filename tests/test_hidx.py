@@ -1,0 +1,99 @@
+"""The reference's on-disk index (HIDX v1, proj/src/io.cpp:91-157, 223-232)
+through the framework's native reader (hm_hidx_*).
+
+Files are written by the UNMODIFIED reference (oracle/_ref: hybrid::save_index);
+the reader must reproduce hybrid::load_index -- every array bit for bit, the
+same rejections with the same messages (test_config_io.cpp:116-152 pins the
+reference's truncation behaviour) -- and an index uploaded straight from the
+file must search exactly like the reference on it.
+"""
+import struct
+
+import numpy as np
+import pytest
+
+from _util import random_instance, ref, search, toy_docs
+
+KEYS = ("term_offsets", "posting_rows", "posting_weights", "idf", "maxscore", "order_key",
+        "doc_lens", "doc_ids")
+
+
+def _ref_error(path):
+    try:
+        ref.RefIndex.load(path)
+    except RuntimeError as e:
+        return str(e)
+    return None
+
+
+def _our_error(path):
+    try:
+        search.Hidx(path)
+    except RuntimeError as e:
+        return str(e)
+    return None
+
+
+def test_hidx_arrays_identical_to_reference_load(tmp_path):
+    rng = np.random.default_rng(7)
+    for trial in range(20):
+        docs, _ = random_instance(rng)
+        ri = ref.RefIndex.from_texts(docs, ref.TOK_MINIMAL, k1=1.2 + 0.1 * (trial % 3), b=0.75)
+        p = tmp_path / f"r{trial}.hidx"
+        ri.save(p)
+        want = ref.RefIndex.load(p).export()
+        h = search.Hidx(p)
+        got = h.arrays()
+        assert h.terms() == want["terms"]
+        for k in KEYS:
+            assert got[k].dtype == want[k].dtype and (got[k].view(np.uint8) == want[k].view(np.uint8)).all(), k
+        assert struct.pack("<d", got["avgdl"]) == struct.pack("<d", want["avgdl"])
+        assert h.mode == 0 and abs(h.build_params.k1 - (1.2 + 0.1 * (trial % 3))) < 1e-12
+
+
+def test_hidx_rejections_match_reference(tmp_path):
+    ri = ref.RefIndex.from_texts(toy_docs(), ref.TOK_MINIMAL)
+    good = tmp_path / "toy.hidx"
+    ri.save(good)
+    data = good.read_bytes()
+    cases = {
+        "magic": b"HIDY" + data[4:],
+        "version": data[:4] + struct.pack("<I", 2) + data[8:],
+        "conv": data[:26] + b"X" + data[27:],  # a byte of the idf-convention string
+        "empty": b"",
+    }
+    for cut in (3, 9, 30, 60, len(data) // 2, len(data) - 8, len(data) - 1):
+        cases[f"cut{cut}"] = data[:cut]
+    for name, blob in cases.items():
+        p = tmp_path / f"bad_{name}.hidx"
+        p.write_bytes(blob)
+        want = _ref_error(p)
+        assert want is not None, name
+        assert _our_error(p) == want, (name, _our_error(p), want)
+    missing = str(tmp_path / "nope.hidx")
+    assert _our_error(missing) == _ref_error(missing) == "cannot open " + missing
+
+
+def test_hidx_abi_exports():
+    L = search.lib()
+    for sym in ("hm_hidx_load", "hm_hidx_view", "hm_hidx_term", "hm_hidx_maxscores", "hm_hidx_free",
+                "hm_hidx_last_error"):
+        assert hasattr(L, sym), sym
+
+
+@pytest.mark.gpu
+def test_hidx_device_index_searches_like_reference(gpu, tmp_path):
+    corpus = ref.RefCorpus(30000, vocab_size=3000)
+    ri = ref.RefIndex.from_corpus(corpus)
+    queries = ref.RefQueries(corpus, n_queries=300)
+    p = tmp_path / "c.hidx"
+    ri.save(p)
+    dev = search.DeviceIndex.from_hidx(p)
+    idx = search.CsrIndex.load(p)
+    for q in queries.terms[:300]:
+        want_ids, want_sc, want_post = ri.search(q, 10)
+        r = dev.search_lists([idx.resolve(q)], 10)
+        n = int(r["n"][0])
+        assert r["ids"][0, :n].tolist() == list(want_ids)
+        assert (r["scores"][0, :n].view(np.uint64) == np.asarray(want_sc).view(np.uint64)).all()
+        assert int(r["postings"][0]) == want_post

@@ -36,7 +36,20 @@ def main():
         for i in range(len(tids)):
             assert (got["ids"][i, :n[i]] == ids[i, :n[i]]).all(), (kw, i)
             assert (got["scores"][i, :n[i]].view(np.uint64) == sc[i, :n[i]].view(np.uint64)).all(), (kw, i)
-    print("sanitize cases ok:", len(cases))
+    # a larger index: long seed terms enumerated tile by tile, windows cutting tiles
+    c2 = synth.Corpus(n_records=200000, vocab_size=5000)
+    q2 = synth.Queries(c2, n_queries=64)
+    hx2 = synth.HostIndex(c2)
+    dev2 = search.DeviceIndex.from_host(hx2)
+    orc2 = restate.OracleIndex.from_host(hx2)
+    t2 = [hx2.resolve(q2.term_ranks[q2.offsets[i]:q2.offsets[i + 1]]) for i in range(len(q2))]
+    for lo, hi in ((0, 0), (12345, 190001), (70000, 70000 + 40000)):
+        got = dev2.search_lists(t2, 10, row_lo=lo, row_hi=hi, flags=search.HM_FLAG_SEED_ALL)
+        ids, sc, n, _ = orc2.topk(t2, 10, row_lo=lo, row_hi=hi or hx2.n_docs)
+        assert (got["n"] == n).all()
+        for i in range(len(t2)):
+            assert (got["ids"][i, :n[i]] == ids[i, :n[i]]).all(), (lo, hi, i)
+    print("sanitize cases ok:", len(cases) + 3)
 
 
 if __name__ == "__main__":
