@@ -167,6 +167,24 @@ uint32_t hm_hidx_term(const hm_hidx* h, uint32_t tid, const char** s);
 const double* hm_hidx_maxscores(const hm_hidx* h);
 void hm_hidx_free(hm_hidx* h);
 
+/* The reference's temporal container, HTIX v1 (proj/src/io.cpp:234-318),
+ * assembled as ONE flat index whose rows are laid out partition by partition
+ * (oldest first) over the shared statistics -- the layout hm_search_batch
+ * scores the newest min(k*, k_max, K) partitions of with a row window
+ * (TemporalIndex::topk, src/temporal_index.cpp:72-123).  hm_htix_flat is an
+ * hm_hidx (view / terms / free it through hm_htix_free only); part_row has
+ * n_partitions + 1 entries.  Errors as the reference reader ("not a temporal
+ * index file (bad magic)", "unsupported temporal index version N", partition
+ * bodies as HIDX).  Replaces: hybrid::load_temporal_index. */
+typedef struct hm_htix hm_htix;
+int hm_htix_load(const char* path, hm_htix** out);
+const hm_hidx* hm_htix_flat(const hm_htix* t);
+int hm_htix_partitions(const hm_htix* t, uint32_t* n_partitions, const uint32_t** part_row,
+                       const int64_t** window_start, const int64_t** window_end);
+int hm_htix_params(const hm_htix* t, int64_t* window_ms, double* epsilon, double* lambda_hat,
+                   uint32_t* k_max, uint64_t* total_docs);
+void hm_htix_free(hm_htix* t);
+
 /* Margin confidence over a ranked score list (src/cascade.cpp:10-21). */
 double hm_margin(const double* scores, uint32_t n, double epsilon_guard);
 

@@ -50,6 +50,8 @@ def lib():
                                         P(dbl), P(dbl), u32, P(u32), P(u64), dbl, dbl, dbl, P(vp)]
     L.ref_index_free.argtypes = [vp]
     L.ref_save_index.argtypes = [vp, C.c_char_p]
+    L.ref_save_temporal.argtypes = [vp, C.c_char_p]
+    L.ref_load_temporal.argtypes = [C.c_char_p, P(vp)]
     L.ref_load_index.argtypes = [C.c_char_p, P(vp)]
     L.ref_index_sizes.argtypes = [vp, P(u64)]
     L.ref_index_export.argtypes = [vp, C.c_char_p, P(u64), P(u32), P(dbl), P(dbl), P(dbl),
@@ -271,6 +273,17 @@ class RefTemporal:
     def __del__(self):
         if getattr(self, "h", None):
             lib().ref_temporal_free(self.h)
+
+    def save(self, path):
+        """hybrid::save_temporal_index (io.cpp:234-268): a HTIX v1 file."""
+        _chk(lib().ref_save_temporal(self.h, str(path).encode()))
+
+    @classmethod
+    def load(cls, path):
+        """hybrid::load_temporal_index (io.cpp:270-318)."""
+        h = C.c_void_p()
+        _chk(lib().ref_load_temporal(str(path).encode(), C.byref(h)))
+        return cls(h)
 
     def partitions(self):
         K = lib().ref_temporal_num_partitions(self.h)

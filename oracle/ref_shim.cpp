@@ -386,6 +386,18 @@ int ref_build_temporal_corpus(void* corpus, std::int64_t window_ms,
     });
 }
 void ref_temporal_free(void* h) { delete static_cast<Temporal*>(h); }
+
+// HTIX v1 files written / read by the reference's own io.cpp (:234-318)
+int ref_save_temporal(void* h, const char* path) {
+    return guard([&] { save_temporal_index(static_cast<Temporal*>(h)->t, path); });
+}
+int ref_load_temporal(const char* path, void** out) {
+    return guard([&] {
+        auto t = std::make_unique<Temporal>();
+        t->t = load_temporal_index(path);
+        *out = t.release();
+    });
+}
 std::uint32_t ref_temporal_num_partitions(void* h) {
     return static_cast<Temporal*>(h)->t.num_partitions();
 }

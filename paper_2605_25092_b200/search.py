@@ -57,7 +57,8 @@ EXPORTS = ["hm_index_create", "hm_index_destroy", "hm_index_device_bytes", "hm_i
            "hm_search_batch", "hm_search_batch_device", "hm_last_batch_stats",
            "hm_last_batch_timing", "hm_last_batch_seed",
            "hm_hidx_load", "hm_hidx_last_error", "hm_hidx_view", "hm_hidx_term", "hm_hidx_maxscores",
-           "hm_hidx_free",
+           "hm_hidx_free", "hm_htix_load", "hm_htix_flat", "hm_htix_partitions", "hm_htix_params",
+           "hm_htix_free",
            "hm_merge_shards_device", "hm_margin", "hm_last_error"]
 
 
@@ -87,6 +88,13 @@ def lib():
     L.hm_hidx_maxscores.argtypes = [C.c_void_p]
     L.hm_hidx_maxscores.restype = P(C.c_double)
     L.hm_hidx_free.argtypes = [C.c_void_p]
+    L.hm_htix_load.argtypes = [C.c_char_p, P(C.c_void_p)]
+    L.hm_htix_flat.argtypes = [C.c_void_p]
+    L.hm_htix_flat.restype = C.c_void_p
+    L.hm_htix_partitions.argtypes = [C.c_void_p, P(C.c_uint32), P(C.c_void_p), P(C.c_void_p), P(C.c_void_p)]
+    L.hm_htix_params.argtypes = [C.c_void_p, P(C.c_int64), P(C.c_double), P(C.c_double), P(C.c_uint32),
+                                 P(C.c_uint64)]
+    L.hm_htix_free.argtypes = [C.c_void_p]
     L.hm_merge_shards_device.argtypes = [C.c_uint32, C.c_uint32, C.c_uint32, C.c_void_p,
                                          C.c_void_p, C.c_void_p, C.c_void_p, C.c_double,
                                          C.c_double, P(Results), C.c_void_p]
@@ -367,12 +375,15 @@ class Hidx:
     """A HIDX v1 file (the reference's save_index output, io.cpp:91-157) parsed
     by the framework's native reader; `arrays()` views its host arrays."""
 
-    def __init__(self, path):
+    def __init__(self, path=None, handle=None, owner=None):
         L = lib()
-        h = C.c_void_p()
-        if L.hm_hidx_load(str(path).encode(), C.byref(h)) != 0:
-            raise RuntimeError(L.hm_hidx_last_error().decode())
-        self._h = h
+        if handle is None:
+            h = C.c_void_p()
+            if L.hm_hidx_load(str(path).encode(), C.byref(h)) != 0:
+                raise RuntimeError(L.hm_hidx_last_error().decode())
+        else:  # a view into another container (an HTIX's flat index)
+            h = C.c_void_p(handle)
+        self._h, self._owner = h, owner
         self.view = CsrView()
         mode, k1, b = C.c_uint32(), C.c_double(), C.c_double()
         L.hm_hidx_view(h, C.byref(self.view), C.byref(mode), C.byref(k1), C.byref(b))
@@ -415,7 +426,49 @@ class Hidx:
 
     def close(self):
         if getattr(self, "_h", None):
-            lib().hm_hidx_free(self._h)
+            if getattr(self, "_owner", None) is None:
+                lib().hm_hidx_free(self._h)
+            self._h = None
+
+    def __del__(self):
+        self.close()
+
+
+class Htix:
+    """A HTIX v1 file (save_temporal_index, io.cpp:234-268) read by the native
+    reader as one partition-ordered flat index over the shared statistics."""
+
+    def __init__(self, path):
+        L = lib()
+        h = C.c_void_p()
+        if L.hm_htix_load(str(path).encode(), C.byref(h)) != 0:
+            raise RuntimeError(L.hm_hidx_last_error().decode())
+        self._h = h
+        self.flat = Hidx(handle=L.hm_htix_flat(h), owner=self)
+        K = C.c_uint32()
+        pr, ws, we = C.c_void_p(), C.c_void_p(), C.c_void_p()
+        L.hm_htix_partitions(h, C.byref(K), C.byref(pr), C.byref(ws), C.byref(we))
+        n = K.value
+        self.part_row = np.ctypeslib.as_array(C.cast(pr, C.POINTER(C.c_uint32)), (n + 1,)).copy()
+        self.window_start = np.ctypeslib.as_array(C.cast(ws, C.POINTER(C.c_int64)), (n,)).copy() if n else np.zeros(0, np.int64)
+        self.window_end = np.ctypeslib.as_array(C.cast(we, C.POINTER(C.c_int64)), (n,)).copy() if n else np.zeros(0, np.int64)
+        w, e, lam, km, td = C.c_int64(), C.c_double(), C.c_double(), C.c_uint32(), C.c_uint64()
+        L.hm_htix_params(h, C.byref(w), C.byref(e), C.byref(lam), C.byref(km), C.byref(td))
+        self.params = TemporalParams(w.value, e.value, lam.value, km.value)
+        self.total_docs = td.value
+
+    def temporal_index(self, device=0):
+        """(TemporalIndex on the device, the CsrIndex mirror for term lookup)."""
+        a = self.flat.arrays()
+        idx = CsrIndex(self.flat.terms(), a["term_offsets"], a["posting_rows"], a["posting_weights"],
+                       a["idf"], a["order_key"], a["doc_lens"], a["doc_ids"], a["avgdl"],
+                       self.flat.build_params, device)
+        return TemporalIndex(self.flat.device_index(device), self.part_row, self.params), idx
+
+    def close(self):
+        if getattr(self, "_h", None):
+            self.flat._h = None
+            lib().hm_htix_free(self._h)
             self._h = None
 
     def __del__(self):

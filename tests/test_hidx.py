@@ -97,3 +97,90 @@ def test_hidx_device_index_searches_like_reference(gpu, tmp_path):
         assert r["ids"][0, :n].tolist() == list(want_ids)
         assert (r["scores"][0, :n].view(np.uint64) == np.asarray(want_sc).view(np.uint64)).all()
         assert int(r["postings"][0]) == want_post
+
+
+# ---------------------------------------------------------------- HTIX v1
+DAY = 24 * 3600 * 1000
+
+
+def _records(seed, n=400, vocab=60, span_days=45):
+    rng = np.random.default_rng(seed)
+    ids = np.arange(1, n + 1, dtype=np.uint64) * 7
+    ts = rng.integers(0, span_days * DAY, n).astype(np.int64)
+    texts = [" ".join("w%d" % rng.integers(0, vocab) for _ in range(rng.integers(2, 14))) for _ in range(n)]
+    return ids, ts, texts
+
+
+def test_htix_assembles_the_partition_ordered_flat_index(tmp_path):
+    """The flat index assembled from HTIX equals the reference's own flat
+    build over the records in partition order (same shared statistics,
+    temporal_index.cpp:136-142), array for array."""
+    for seed in range(4):
+        ids, ts, texts = _records(seed)
+        rt = ref.RefTemporal.from_records(ids, ts, texts)
+        p = tmp_path / f"t{seed}.htix"
+        rt.save(p)
+        h = search.Htix(p)
+        ws, we, nd = rt.partitions()
+        assert (h.window_start == ws).all() and (h.window_end == we).all()
+        assert (np.diff(h.part_row.astype(np.int64)) == nd).all() and h.total_docs == len(ids)
+        # records in partition order: window index, stable by insertion
+        t0 = int(ts.min())
+        order = np.argsort((ts - t0) // (7 * DAY), kind="stable")
+        flat = ref.RefIndex.from_texts([(int(ids[r]), texts[r]) for r in order], ref.TOK_MINIMAL).export()
+        got = h.flat.arrays()
+        assert h.flat.terms() == flat["terms"]
+        for k in ("term_offsets", "posting_rows", "posting_weights", "idf", "order_key", "doc_lens", "doc_ids"):
+            assert (got[k].view(np.uint8) == flat[k].view(np.uint8)).all(), (seed, k)
+
+
+def test_htix_rejections_match_reference(tmp_path):
+    ids, ts, texts = _records(9)
+    rt = ref.RefTemporal.from_records(ids, ts, texts)
+    good = tmp_path / "t.htix"
+    rt.save(good)
+    data = good.read_bytes()
+
+    def ref_err(path):
+        try:
+            ref.RefTemporal.load(path)
+        except RuntimeError as e:
+            return str(e)
+        return None
+
+    def our_err(path):
+        try:
+            search.Htix(path)
+        except RuntimeError as e:
+            return str(e)
+        return None
+
+    cases = {"magic": b"HTIY" + data[4:], "version": data[:4] + struct.pack("<I", 3) + data[8:]}
+    for cut in (2, 10, 50, len(data) // 3, len(data) - 20, len(data) - 1):
+        cases[f"cut{cut}"] = data[:cut]
+    for name, blob in cases.items():
+        p = tmp_path / f"bad_{name}.htix"
+        p.write_bytes(blob)
+        want = ref_err(p)
+        assert want is not None and our_err(p) == want, (name, our_err(p), want)
+
+
+@pytest.mark.gpu
+def test_htix_temporal_search_like_reference(gpu, tmp_path):
+    """TemporalIndex::topk (temporal_index.cpp:72-123) on a HTIX file, through
+    the framework's temporal path (newest partitions as a row window)."""
+    ids, ts, texts = _records(11, n=3000, vocab=200, span_days=60)
+    rt = ref.RefTemporal.from_records(ids, ts, texts)
+    p = tmp_path / "t.htix"
+    rt.save(p)
+    tix, idx = search.Htix(p).temporal_index()
+    rng = np.random.default_rng(5)
+    queries = [["w%d" % rng.integers(0, 220) for _ in range(rng.integers(1, 5))] for _ in range(200)]
+    tids = [idx.resolve(q) for q in queries]
+    off = np.concatenate([[0], np.cumsum([len(t) for t in tids])]).astype(np.uint32)
+    got = tix.topk_batch(off, np.array([x for t in tids for x in t], np.uint32), 10)
+    for i, q in enumerate(queries):
+        want_ids, want_sc = rt.topk(q, 10)[:2]
+        n = int(got["n"][i])
+        assert got["ids"][i, :n].tolist() == list(want_ids), q
+        assert (got["scores"][i, :n].view(np.uint64) == np.asarray(want_sc).view(np.uint64)).all(), q
