@@ -258,9 +258,10 @@ __global__ void __launch_bounds__(kCons, 2) search_fast_kernel(DevIndex ix, Batc
             if (j < j1) prefetch(j + 1);
         };
         // Long terms run as a software pipeline of steps over (tile, range,
-        // chunk), three stages deep: the loads of the next two steps --
-        // possibly ranges of later tiles -- are in flight while the current
-        // step is applied, and across the short-term pass and the scan.
+        // chunk), FastCfg::kStages deep (2 measured best on C2; 3 supported):
+        // the loads of the next step(s) -- possibly ranges of later tiles --
+        // are in flight while the current step is applied, and across the
+        // short-term pass and the scan.
         uint32_t ready = j0;  // the tile whose ranges are in rdesc
         prefetch(j0);
         install(j0);
