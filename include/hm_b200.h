@@ -185,6 +185,57 @@ int hm_htix_params(const hm_htix* t, int64_t* window_ms, double* epsilon, double
                    uint32_t* k_max, uint64_t* total_docs);
 void hm_htix_free(hm_htix* t);
 
+/* ---------------------------------------------------------------- bridge
+ * Learned-sparse ("bridge") scoring: a Bridge-mode CsrIndex
+ * (bridge_ingest, src/bridge.cpp:22-73: per-term postings of per-doc sparse
+ * weight vectors; or a Bridge-mode HIDX file through hm_hidx_view, mode 1)
+ * HBM-resident in the reference's layout, and top-k by
+ * S[doc] = sum over query terms, in ascending term-id order, of w_q * W_t in
+ * fp64 without contraction -- bit-identical to bridge_topk and
+ * bridge_topk_maxscore (src/bridge.cpp:112-204, whose outputs are identical).
+ * Replaces: hybrid::bridge_topk / bridge_topk_maxscore
+ * (include/hybrid/bridge.hpp:29-40) per query. */
+typedef struct hm_bridge hm_bridge;
+
+typedef struct {
+    uint32_t n_terms;
+    const uint64_t* term_offsets;     /* [n_terms + 1] */
+    const uint32_t* posting_rows;     /* [P], strictly increasing per term */
+    const double* posting_weights;    /* [P] learned weights */
+    uint32_t n_docs;
+    const uint64_t* doc_ids;          /* [n_docs], distinct */
+} hm_bridge_view;
+
+int hm_bridge_create(const hm_bridge_view* view, int device, hm_bridge** out);
+int hm_bridge_destroy(hm_bridge* bridge);
+
+/* Queries are SparseVectors (bridge.hpp:12-19): query i owns
+ * q_idx/q_val[q_off[i] .. q_off[i+1]).  The host entry point validates each
+ * like SparseVector::validate (bridge.cpp:10-20; HM_ERR_INVALID with its
+ * messages); term ids >= n_terms are skipped (bridge.cpp:122).  k <= 512
+ * (HM_ERR_INVALID beyond; the reference's TwoPhaseSelector has the same kind
+ * of capacity rule, twophase.cpp:12-22).  Rows are restricted to
+ * [row_lo, row_hi) (row_hi = 0: n_docs).  max_nnz: an upper bound on every
+ * query's nnz (0 = computed by the host entry point; required by the device
+ * one).  Results as hm_results (conf and skip unused); postings =
+ * SearchStats::postings_touched (bridge.cpp:133) within the row window. */
+typedef struct {
+    uint32_t n_queries;
+    const uint64_t* q_off;     /* [n_queries + 1] */
+    const uint32_t* q_idx;
+    const double* q_val;
+    uint32_t k;
+    uint32_t row_lo, row_hi;
+    uint32_t max_nnz;
+    uint32_t flags;            /* HM_FLAG_TIMING */
+} hm_bridge_batch;
+
+int hm_bridge_search_batch(hm_bridge* bridge, const hm_bridge_batch* batch, hm_results* out);
+int hm_bridge_search_batch_device(hm_bridge* bridge, const hm_bridge_batch* batch_dev,
+                                  hm_results* out_dev, void* stream);
+/* Device time (ms) of the last HM_FLAG_TIMING bridge batch on this thread. */
+int hm_bridge_last_timing(float* ms_kernel);
+
 /* Margin confidence over a ranked score list (src/cascade.cpp:10-21). */
 double hm_margin(const double* scores, uint32_t n, double epsilon_guard);
 

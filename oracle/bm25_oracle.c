@@ -112,37 +112,11 @@ static void sift_up(entry* h, uint64_t i) {
     }
 }
 
-/* ---- exhaustive top-k: src/csr_index.cpp:77-104, collect_topk :50-59 --- */
-static int topk_one(const uint64_t* term_offsets, const uint32_t* posting_rows,
-                    const double* posting_weights, const double* idfs,
-                    uint32_t n_docs, const uint32_t* doc_lens,
-                    const uint64_t* doc_ids, double avgdl,
-                    const uint32_t* plan_tid, const uint32_t* plan_mult,
-                    uint32_t plan_len, uint64_t k, double k1, double b,
-                    uint32_t row_lo, uint32_t row_hi, double* acc,
-                    unsigned char* seen, uint32_t* rows, uint64_t* out_ids,
-                    double* out_scores, uint32_t* out_n, uint64_t* touched_out) {
-    uint64_t touched = 0;
-    uint32_t n_rows = 0;
-    for (uint32_t i = 0; i < plan_len; ++i) {
-        uint32_t tid = plan_tid[i], mult = plan_mult[i];
-        double idf = idfs[tid];
-        uint64_t begin = term_offsets[tid], end = term_offsets[tid + 1];
-        for (uint64_t j = begin; j < end; ++j) {
-            uint32_t row = posting_rows[j];
-            if (row < row_lo || row >= row_hi) continue;
-            double s = or_bm25_score(posting_weights[j], idf,
-                                     (double)doc_lens[row], avgdl, k1, b);
-            for (uint32_t m = 0; m < mult; ++m) acc[row] += s; /* :94 */
-            if (!seen[row]) {
-                seen[row] = 1;
-                rows[n_rows++] = row;
-            }
-            ++touched;
-        }
-    }
-    if (touched_out) *touched_out = touched;
-    /* collect: acc > 0 only (:56), then best-k by (score desc, id asc) */
+/* collect (src/csr_index.cpp:50-59; bridge.cpp:100-108): rows with acc > 0,
+ * best k by (score desc, id asc); resets acc/seen of the visited rows */
+static void collect_best(double* acc, unsigned char* seen, const uint32_t* rows,
+                         uint32_t n_rows, const uint64_t* doc_ids, uint64_t k,
+                         uint64_t* out_ids, double* out_scores, uint32_t* out_n) {
     uint64_t cap = k < n_rows ? k : n_rows;
     entry* heap = (entry*)malloc(sizeof(entry) * (cap ? cap : 1));
     uint64_t hn = 0;
@@ -168,6 +142,40 @@ static int topk_one(const uint64_t* term_offsets, const uint32_t* posting_rows,
     }
     *out_n = (uint32_t)hn;
     free(heap);
+}
+
+/* ---- exhaustive top-k: src/csr_index.cpp:77-104, collect_topk :50-59 --- */
+static int topk_one(const uint64_t* term_offsets, const uint32_t* posting_rows,
+                    const double* posting_weights, const double* idfs,
+                    uint32_t n_docs, const uint32_t* doc_lens,
+                    const uint64_t* doc_ids, double avgdl,
+                    const uint32_t* plan_tid, const uint32_t* plan_mult,
+                    uint32_t plan_len, uint64_t k, double k1, double b,
+                    uint32_t row_lo, uint32_t row_hi, double* acc,
+                    unsigned char* seen, uint32_t* rows, uint64_t* out_ids,
+                    double* out_scores, uint32_t* out_n, uint64_t* touched_out) {
+    (void)n_docs;
+    uint64_t touched = 0;
+    uint32_t n_rows = 0;
+    for (uint32_t i = 0; i < plan_len; ++i) {
+        uint32_t tid = plan_tid[i], mult = plan_mult[i];
+        double idf = idfs[tid];
+        uint64_t begin = term_offsets[tid], end = term_offsets[tid + 1];
+        for (uint64_t j = begin; j < end; ++j) {
+            uint32_t row = posting_rows[j];
+            if (row < row_lo || row >= row_hi) continue;
+            double s = or_bm25_score(posting_weights[j], idf,
+                                     (double)doc_lens[row], avgdl, k1, b);
+            for (uint32_t m = 0; m < mult; ++m) acc[row] += s; /* :94 */
+            if (!seen[row]) {
+                seen[row] = 1;
+                rows[n_rows++] = row;
+            }
+            ++touched;
+        }
+    }
+    if (touched_out) *touched_out = touched;
+    collect_best(acc, seen, rows, n_rows, doc_ids, k, out_ids, out_scores, out_n);
     return 0;
 }
 
@@ -212,6 +220,59 @@ int or_topk_batch(const uint64_t* term_offsets, const uint32_t* posting_rows,
                  b, row_lo, row_hi, acc, seen, rows, out_ids + (size_t)q * k,
                  out_scores + (size_t)q * k, out_n + q,
                  postings_touched ? postings_touched + q : 0);
+    }
+    free(acc);
+    free(seen);
+    free(rows);
+    return 0;
+}
+
+/* ---- learned-sparse bridge: src/bridge.cpp:112-137 (+ collect :100-108) --
+ * Query q owns q_idx/q_val[q_off[q] .. q_off[q+1]) (a validated
+ * SparseVector: strictly increasing term ids, values > 0).  Terms >= n_terms
+ * are skipped (:122); S[row] += w_q * W in ascending term-id order (:127);
+ * postings_touched counts each term's whole list (:133), restricted here to
+ * rows in [row_lo, row_hi) like or_topk. */
+int or_bridge_topk_batch(const uint64_t* term_offsets, const uint32_t* posting_rows,
+                         const double* posting_weights, uint32_t n_terms,
+                         uint32_t n_docs, const uint64_t* doc_ids,
+                         const uint64_t* q_off, const uint32_t* q_idx,
+                         const double* q_val, uint32_t nq, uint64_t k,
+                         uint32_t row_lo, uint32_t row_hi, uint64_t* out_ids,
+                         double* out_scores, uint32_t* out_n,
+                         uint64_t* postings_touched) {
+    if (row_hi > n_docs) row_hi = n_docs;
+    size_t nd = n_docs ? n_docs : 1;
+    double* acc = (double*)calloc(nd, sizeof(double));
+    unsigned char* seen = (unsigned char*)calloc(nd, 1);
+    uint32_t* rows = (uint32_t*)malloc(nd * sizeof(uint32_t));
+    if (!acc || !seen || !rows) {
+        free(acc);
+        free(seen);
+        free(rows);
+        return -1;
+    }
+    for (uint32_t q = 0; q < nq; ++q) {
+        uint64_t touched = 0;
+        uint32_t n_rows = 0;
+        for (uint64_t i = q_off[q]; i < q_off[q + 1]; ++i) {
+            uint32_t t = q_idx[i];
+            if (t >= n_terms) continue;
+            double wq = q_val[i];
+            for (uint64_t j = term_offsets[t]; j < term_offsets[t + 1]; ++j) {
+                uint32_t row = posting_rows[j];
+                if (row < row_lo || row >= row_hi) continue;
+                acc[row] += wq * posting_weights[j];
+                if (!seen[row]) {
+                    seen[row] = 1;
+                    rows[n_rows++] = row;
+                }
+                ++touched;
+            }
+        }
+        if (postings_touched) postings_touched[q] = touched;
+        collect_best(acc, seen, rows, n_rows, doc_ids, k, out_ids + (size_t)q * k,
+                     out_scores + (size_t)q * k, out_n + q);
     }
     free(acc);
     free(seen);

@@ -56,6 +56,17 @@ int or_topk_batch(const uint64_t* term_offsets, const uint32_t* posting_rows,
                   uint64_t* out_ids, double* out_scores, uint32_t* out_n,
                   uint64_t* postings_touched);
 
+/* Learned-sparse bridge top-k, src/bridge.cpp:112-137 + collect :100-108.
+ * Queries are concatenated sparse vectors q_off[nq+1]; output stride k. */
+int or_bridge_topk_batch(const uint64_t* term_offsets, const uint32_t* posting_rows,
+                         const double* posting_weights, uint32_t n_terms,
+                         uint32_t n_docs, const uint64_t* doc_ids,
+                         const uint64_t* q_off, const uint32_t* q_idx,
+                         const double* q_val, uint32_t nq, uint64_t k,
+                         uint32_t row_lo, uint32_t row_hi, uint64_t* out_ids,
+                         double* out_scores, uint32_t* out_n,
+                         uint64_t* postings_touched);
+
 /* src/cascade.cpp:10-21 (Margin proxy) */
 double or_margin(const double* scores, uint32_t n, double eps);
 /* src/cascade.cpp:10-42 (proxy 0 Margin, 1 Top1Fraction, 2 EntropyComplement) */

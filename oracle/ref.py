@@ -78,6 +78,12 @@ def lib():
     L.ref_k_star.argtypes = [dbl, dbl, P(u32)]
     L.ref_ndcg.argtypes = [P(u64), P(dbl), u32, P(u64), P(u32), u32, u64, C.c_int, P(dbl)]
     L.ref_twophase_batch.argtypes = [u64, C.c_int, u32, u32, P(dbl), u64, P(u64), P(dbl), P(u32)]
+    L.ref_bridge_ingest.argtypes = [u32, P(u64), P(u64), P(u32), P(dbl), P(vp)]
+    L.ref_bridge_export.argtypes = [vp, P(u64), P(u64), P(u32), P(dbl)]
+    L.ref_sparse_validate.argtypes = [P(u32), u32, P(dbl), u32]
+    L.ref_bridge_batch.argtypes = [vp, u32, P(u64), P(u32), P(dbl), u64, C.c_int, C.c_uint,
+                                   P(u64), P(dbl), P(u32), P(u64), P(dbl)]
+    L.ref_bm25_on.argtypes = [vp, C.c_char_p]
     _L = L
     return L
 
@@ -245,6 +251,71 @@ class RefIndex:
                                     _p(sc, C.c_double), _p(n, C.c_uint32), _p(post, C.c_uint64),
                                     _p(lat, C.c_double), C.byref(wall)))
         return dict(ids=ids, scores=sc, n=n, postings=post, lat_ms=lat, wall_ms=wall.value)
+
+
+
+def sparse_pack(vectors):
+    """[(indices, values), ...] -> (off u64[n+1], idx u32[nnz], val f64[nnz])"""
+    off = np.zeros(len(vectors) + 1, np.uint64)
+    off[1:] = np.cumsum([len(i) for i, _ in vectors])
+    idx = np.concatenate([np.asarray(i, np.uint32) for i, _ in vectors]) if vectors else np.zeros(0, np.uint32)
+    val = np.concatenate([np.asarray(v, np.float64) for _, v in vectors]) if vectors else np.zeros(0)
+    return off, np.ascontiguousarray(idx, np.uint32), np.ascontiguousarray(val, np.float64)
+
+
+def sparse_validate(indices, values):
+    """SparseVector::validate (bridge.cpp:10-20); raises RuntimeError(message)."""
+    i = np.ascontiguousarray(indices, np.uint32)
+    v = np.ascontiguousarray(values, np.float64)
+    _chk(lib().ref_sparse_validate(_p(i, C.c_uint32), len(i), _p(v, C.c_double), len(v)))
+
+
+class RefBridge(RefIndex):
+    """A reference Bridge-mode CsrIndex (bridge.cpp:22-73)."""
+
+    @classmethod
+    def from_vectors(cls, ids, vectors):
+        """bridge_ingest over docs (ids[d], (indices, values))."""
+        ids = np.ascontiguousarray(ids, np.uint64)
+        off, idx, val = sparse_pack(vectors)
+        h = C.c_void_p()
+        _chk(lib().ref_bridge_ingest(len(ids), _p(ids, C.c_uint64), _p(off, C.c_uint64),
+                                     _p(idx, C.c_uint32), _p(val, C.c_double), C.byref(h)))
+        return cls(h)
+
+    def export_vectors(self):
+        """bridge_export (bridge.cpp:75-90) -> (ids, off, idx, val)"""
+        x = self.export()
+        nd, nnz = len(x["doc_ids"]), len(x["posting_rows"])
+        ids = np.zeros(nd, np.uint64)
+        off = np.zeros(nd + 1, np.uint64)
+        idx = np.zeros(max(nnz, 1), np.uint32)
+        val = np.zeros(max(nnz, 1), np.float64)
+        _chk(lib().ref_bridge_export(self.h, _p(ids, C.c_uint64), _p(off, C.c_uint64),
+                                     _p(idx, C.c_uint32), _p(val, C.c_double)))
+        return ids, off, idx[:nnz], val[:nnz]
+
+    def topk_batch(self, queries, k, maxscore=False, workers=1):
+        """bridge_topk / bridge_topk_maxscore per query (bridge.cpp:112-204).
+        -> dict(ids[nq,k], scores[nq,k], n[nq], postings[nq], wall_ms)"""
+        nq = len(queries)
+        off, idx, val = sparse_pack(queries)
+        cap = max(int(k), 1)
+        ids = np.zeros((nq, cap), np.uint64)
+        sc = np.zeros((nq, cap), np.float64)
+        n = np.zeros(nq, np.uint32)
+        post = np.zeros(nq, np.uint64)
+        wall = C.c_double()
+        _chk(lib().ref_bridge_batch(self.h, nq, _p(off, C.c_uint64), _p(idx, C.c_uint32),
+                                    _p(val, C.c_double), k, 1 if maxscore else 0, workers,
+                                    _p(ids, C.c_uint64), _p(sc, C.c_double), _p(n, C.c_uint32),
+                                    _p(post, C.c_uint64), C.byref(wall)))
+        return dict(ids=ids, scores=sc, n=n, postings=post, wall_ms=wall.value)
+
+    def bm25_error(self):
+        """CsrIndex::bm25_topk on this index: the reference's refusal message."""
+        rc = lib().ref_bm25_on(self.h, b"t0")
+        return lib().ref_last_error().decode() if rc else None
 
 
 class RefTemporal:

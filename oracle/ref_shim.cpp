@@ -10,6 +10,9 @@
 //                                CsrIndex::bm25_topk_maxscore (csr_index.cpp:106-207)
 //                                TemporalIndex::topk        (temporal_index.cpp:72-123)
 //   * the reference HIDX container  save_index / load_index   (io.cpp:91-157, 223-232)
+//   * the learned-sparse bridge  bridge_ingest / bridge_export / bridge_topk /
+//                                bridge_topk_maxscore / SparseVector::validate
+//                                (bridge.cpp:10-204)
 //   * confidence / k_star / ndcg_at_k / TwoPhaseSelector known-answer hooks
 //   * a CPU batch driver shaped like hybridmem's cmd_search parallel_for
 //     (tools/hybridmem.cpp:58-71, 305-313) for the CPU baseline timing.
@@ -24,6 +27,7 @@
 #include <thread>
 #include <vector>
 
+#include "hybrid/bridge.hpp"
 #include "hybrid/cascade.hpp"
 #include "hybrid/csr_index.hpp"
 #include "hybrid/eval.hpp"
@@ -491,6 +495,98 @@ int ref_twophase_batch(std::uint64_t capacity, int reset_sentinel,
             emit(sel.select(row, k), out_ids + r * k, out_scores + r * k, out_n + r);
         }
     });
+}
+
+// ---------------------------------------------------------------- bridge
+// Documents as concatenated sparse vectors: doc d owns idx/val[vec_off[d] ..
+// vec_off[d+1]).  The result is a Bridge-mode CsrIndex (an Index handle).
+int ref_bridge_ingest(std::uint32_t n_docs, const std::uint64_t* ids,
+                      const std::uint64_t* vec_off, const std::uint32_t* idx,
+                      const double* val, void** out) {
+    return guard([&] {
+        std::vector<std::pair<DocId, SparseVector>> docs(n_docs);
+        for (std::uint32_t d = 0; d < n_docs; ++d) {
+            docs[d].first = ids[d];
+            docs[d].second.indices.assign(idx + vec_off[d], idx + vec_off[d + 1]);
+            docs[d].second.values.assign(val + vec_off[d], val + vec_off[d + 1]);
+        }
+        auto x = std::make_unique<Index>();
+        x->idx = bridge_ingest(docs);
+        *out = x.release();
+    });
+}
+
+// bridge_export (the exact inverse): ids[n_docs], vec_off[n_docs+1], idx/val[P]
+int ref_bridge_export(void* h, std::uint64_t* ids, std::uint64_t* vec_off,
+                      std::uint32_t* idx, double* val) {
+    return guard([&] {
+        auto v = bridge_export(static_cast<Index*>(h)->idx);
+        std::uint64_t o = 0;
+        for (std::size_t d = 0; d < v.size(); ++d) {
+            ids[d] = v[d].first;
+            vec_off[d] = o;
+            for (std::size_t i = 0; i < v[d].second.nnz(); ++i, ++o) {
+                idx[o] = v[d].second.indices[i];
+                val[o] = v[d].second.values[i];
+            }
+        }
+        vec_off[v.size()] = o;
+    });
+}
+
+int ref_sparse_validate(const std::uint32_t* idx, std::uint32_t n_idx, const double* val,
+                        std::uint32_t n_val) {
+    return guard([&] { SparseVector{std::vector<std::uint32_t>(idx, idx + n_idx),
+                                    std::vector<double>(val, val + n_val)}.validate(); });
+}
+
+// mode 0 = bridge_topk, 1 = bridge_topk_maxscore; queries as concatenated
+// sparse vectors q_off[nq+1]; outputs stride k; workers as ref_search_batch.
+int ref_bridge_batch(void* h, std::uint32_t nq, const std::uint64_t* q_off,
+                     const std::uint32_t* q_idx, const double* q_val, std::uint64_t k,
+                     int mode, unsigned workers, std::uint64_t* out_ids,
+                     double* out_scores, std::uint32_t* out_n, std::uint64_t* postings,
+                     double* wall_ms) {
+    return guard([&] {
+        auto& x = static_cast<Index*>(h)->idx;
+        std::vector<SparseVector> qs(nq);
+        for (std::uint32_t i = 0; i < nq; ++i) {
+            qs[i].indices.assign(q_idx + q_off[i], q_idx + q_off[i + 1]);
+            qs[i].values.assign(q_val + q_off[i], q_val + q_off[i + 1]);
+        }
+        std::vector<std::string> errs(nq);
+        using clk = std::chrono::steady_clock;
+        auto t0 = clk::now();
+        std::atomic<std::size_t> next{0};
+        auto body = [&] {
+            for (std::size_t i; (i = next.fetch_add(1)) < nq;) {
+                try {
+                    SearchStats st;
+                    RankedList r = mode == 1 ? bridge_topk_maxscore(x, qs[i], k, &st)
+                                             : bridge_topk(x, qs[i], k, &st);
+                    emit(r, out_ids + i * k, out_scores + i * k, out_n + i);
+                    if (postings) postings[i] = st.postings_touched;
+                } catch (const std::exception& e) {
+                    errs[i] = e.what();
+                }
+            }
+        };
+        if (workers <= 1) {
+            body();
+        } else {
+            std::vector<std::thread> pool;
+            for (unsigned w = 0; w < workers; ++w) pool.emplace_back(body);
+            for (auto& t : pool) t.join();
+        }
+        if (wall_ms) *wall_ms = std::chrono::duration<double, std::milli>(clk::now() - t0).count();
+        for (auto& e : errs)
+            if (!e.empty()) throw std::runtime_error(e);
+    });
+}
+
+// BM25 scoring on a bridge-mode index (the reference's refusal message)
+int ref_bm25_on(void* h, const char* term) {
+    return guard([&] { static_cast<Index*>(h)->idx.bm25_topk({term}, 5, Bm25Params{}); });
 }
 
 }  // extern "C"

@@ -35,6 +35,8 @@ def lib():
     L.or_topk_batch.argtypes = [P(u64), P(u32), P(dbl), P(dbl), u32, P(u32), P(u64), dbl,
                                 P(u32), P(u32), P(u32), u32, u64, dbl, dbl, u32, u32, P(u64),
                                 P(dbl), P(u32), P(u64)]
+    L.or_bridge_topk_batch.argtypes = [P(u64), P(u32), P(dbl), u32, u32, P(u64), P(u64), P(u32),
+                                       P(dbl), u32, u64, u32, u32, P(u64), P(dbl), P(u32), P(u64)]
     L.or_confidence.argtypes = [P(dbl), u32, C.c_int, dbl]
     L.or_confidence.restype = dbl
     L.or_k_star.argtypes = [dbl, dbl]
@@ -118,6 +120,63 @@ class OracleIndex:
             _p(self.doc_lens, C.c_uint32), _p(self.doc_ids, C.c_uint64), self.avgdl,
             _p(off, C.c_uint32), _p(pt, C.c_uint32), _p(pm, C.c_uint32), nq, k, k1, b, row_lo, hi,
             _p(ids, C.c_uint64), _p(sc, C.c_double), _p(n, C.c_uint32), _p(post, C.c_uint64))
+        if rc != 0:
+            raise MemoryError("oracle allocation failed")
+        if k == 0:
+            n[:] = 0
+        return ids, sc, n, post
+
+
+class OracleBridge:
+    """CPU restatement of the learned-sparse bridge (src/bridge.cpp:22-137)
+    over a Bridge-mode CSR.  Test infrastructure only."""
+
+    def __init__(self, term_offsets, posting_rows, posting_weights, doc_ids):
+        self.term_offsets = np.ascontiguousarray(term_offsets, np.uint64)
+        self.posting_rows = np.ascontiguousarray(posting_rows, np.uint32)
+        self.posting_weights = np.ascontiguousarray(posting_weights, np.float64)
+        self.doc_ids = np.ascontiguousarray(doc_ids, np.uint64)
+
+    @classmethod
+    def ingest(cls, ids, vectors):
+        """bridge_ingest (bridge.cpp:22-73): CSC transpose, rows ascending per term."""
+        dim = max([int(i[-1]) + 1 for i, _ in vectors if len(i)] or [0])
+        rows = np.concatenate([np.full(len(i), r, np.uint32) for r, (i, _) in enumerate(vectors)] or
+                              [np.zeros(0, np.uint32)])
+        tids = np.concatenate([np.asarray(i, np.uint32) for i, _ in vectors] or [np.zeros(0, np.uint32)])
+        vals = np.concatenate([np.asarray(v, np.float64) for _, v in vectors] or [np.zeros(0)])
+        order = np.argsort(tids, kind="stable")  # stable: rows stay ascending per term
+        off = np.zeros(dim + 1, np.uint64)
+        off[1:] = np.cumsum(np.bincount(tids, minlength=dim)[:dim])
+        return cls(off, rows[order], vals[order], ids)
+
+    @property
+    def n_terms(self):
+        return len(self.term_offsets) - 1
+
+    def topk(self, queries, k, row_lo=0, row_hi=None):
+        """bridge_topk per query. -> (ids[nq,k], scores[nq,k], n[nq], postings[nq])"""
+        nq = len(queries)
+        off = np.zeros(nq + 1, np.uint64)
+        off[1:] = np.cumsum([len(i) for i, _ in queries])
+        qi = np.ascontiguousarray(np.concatenate([np.asarray(i, np.uint32) for i, _ in queries] or
+                                                 [np.zeros(0, np.uint32)]), np.uint32)
+        qv = np.ascontiguousarray(np.concatenate([np.asarray(v, np.float64) for _, v in queries] or
+                                                 [np.zeros(0)]), np.float64)
+        if len(qi) == 0:
+            qi, qv = np.zeros(1, np.uint32), np.zeros(1)
+        kk = max(int(k), 1)
+        ids = np.zeros((nq, kk), np.uint64)
+        sc = np.zeros((nq, kk), np.float64)
+        n = np.zeros(nq, np.uint32)
+        post = np.zeros(nq, np.uint64)
+        hi = len(self.doc_ids) if row_hi is None else row_hi
+        rc = lib().or_bridge_topk_batch(
+            _p(self.term_offsets, C.c_uint64), _p(self.posting_rows, C.c_uint32),
+            _p(self.posting_weights, C.c_double), self.n_terms, len(self.doc_ids),
+            _p(self.doc_ids, C.c_uint64), _p(off, C.c_uint64), _p(qi, C.c_uint32), _p(qv, C.c_double),
+            nq, k, row_lo, hi, _p(ids, C.c_uint64), _p(sc, C.c_double), _p(n, C.c_uint32),
+            _p(post, C.c_uint64))
         if rc != 0:
             raise MemoryError("oracle allocation failed")
         if k == 0:

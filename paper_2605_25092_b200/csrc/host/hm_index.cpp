@@ -27,45 +27,17 @@
 #include <cuda_runtime.h>
 
 #include "hm_b200.h"
+#include "hm_host.h"
 #include "hm_launch.h"
 
 namespace {
 
-thread_local std::string g_err;
 thread_local uint32_t g_last_exact = 0, g_last_launches = 0, g_last_handed = 0;
 thread_local float g_ms_plan = 0.f, g_ms_search = 0.f, g_ms_exact = 0.f, g_ms_seed = 0.f;
 
-struct no_device_error : std::runtime_error {
-    using std::runtime_error::runtime_error;
-};
-
-void ck(cudaError_t e, const char* what) {
-    if (e != cudaSuccess)
-        throw std::runtime_error(std::string("CUDA error in ") + what + ": " + cudaGetErrorString(e));
-}
-
-template <typename F>
-int guard(F&& f) {
-    try {
-        f();
-        return HM_OK;
-    } catch (const no_device_error& e) {
-        g_err = e.what();
-        return HM_ERR_NO_DEVICE;
-    } catch (const std::invalid_argument& e) {
-        g_err = e.what();
-        return HM_ERR_INVALID;
-    } catch (const std::out_of_range& e) {
-        g_err = e.what();
-        return HM_ERR_RANGE;
-    } catch (const std::exception& e) {
-        g_err = e.what();
-        return HM_ERR_RUNTIME;
-    } catch (...) {
-        g_err = "unknown error";
-        return HM_ERR_RUNTIME;
-    }
-}
+using hm_host::ck;
+using hm_host::guard;
+using hm_host::no_device_error;
 
 int hw_threads() {
     unsigned h = std::thread::hardware_concurrency();
@@ -184,13 +156,7 @@ struct hm_index {
 
 namespace {
 
-void use_device(int device) {
-    int n = 0;
-    if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0)
-        throw no_device_error("no CUDA device available (the B200 path has no CPU fallback)");
-    if (device < 0 || device >= n) throw std::invalid_argument("device ordinal out of range");
-    ck(cudaSetDevice(device), "cudaSetDevice");
-}
+using hm_host::use_device;
 
 void build_index(const hm_csr_view* v, hm_index* X) {
     const uint32_t V = v->n_terms, N = v->n_docs;
@@ -710,9 +676,16 @@ void validate(const hm_index* X, const hm_query_batch* b) {
 
 }  // namespace
 
+namespace hm_host {
+std::string& error_slot() {
+    thread_local std::string s;
+    return s;
+}
+}  // namespace hm_host
+
 extern "C" {
 
-const char* hm_last_error(void) { return g_err.c_str(); }
+const char* hm_last_error(void) { return hm_host::error_slot().c_str(); }
 
 int hm_index_create(const hm_csr_view* view, int device, hm_index** out) {
     return guard([&] {

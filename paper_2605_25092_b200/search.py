@@ -7,6 +7,8 @@ Reference interfaces mirrored (paths under /root/reference/proj):
   TemporalIndex.topk              include/hybrid/temporal_index.hpp:63-66
   confidence (Margin)             include/hybrid/cascade.hpp:29-34
   the cmd_search batch loop       tools/hybridmem.cpp:227-313  -> search_batch
+  SparseVector, bridge_ingest, bridge_export, bridge_topk(_maxscore)
+                                  include/hybrid/bridge.hpp:12-40 -> BridgeIndex
 
 Every search runs on the GPU through libhm_b200.so; there is no CPU path.
 Errors map to the reference's exception types (RuntimeError for
@@ -53,7 +55,21 @@ class Results(C.Structure):
                 ("conf", C.c_void_p), ("skip", C.c_void_p), ("postings", C.c_void_p)]
 
 
-EXPORTS = ["hm_index_create", "hm_index_destroy", "hm_index_device_bytes", "hm_index_format",
+class BridgeView(C.Structure):
+    _fields_ = [("n_terms", C.c_uint32), ("term_offsets", C.c_void_p),
+                ("posting_rows", C.c_void_p), ("posting_weights", C.c_void_p),
+                ("n_docs", C.c_uint32), ("doc_ids", C.c_void_p)]
+
+
+class BridgeBatch(C.Structure):
+    _fields_ = [("n_queries", C.c_uint32), ("q_off", C.c_void_p), ("q_idx", C.c_void_p),
+                ("q_val", C.c_void_p), ("k", C.c_uint32), ("row_lo", C.c_uint32),
+                ("row_hi", C.c_uint32), ("max_nnz", C.c_uint32), ("flags", C.c_uint32)]
+
+
+EXPORTS = ["hm_bridge_create", "hm_bridge_destroy", "hm_bridge_search_batch",
+           "hm_bridge_search_batch_device", "hm_bridge_last_timing",
+           "hm_index_create", "hm_index_destroy", "hm_index_device_bytes", "hm_index_format",
            "hm_search_batch", "hm_search_batch_device", "hm_last_batch_stats",
            "hm_last_batch_timing", "hm_last_batch_seed",
            "hm_hidx_load", "hm_hidx_last_error", "hm_hidx_view", "hm_hidx_term", "hm_hidx_maxscores",
@@ -100,6 +116,11 @@ def lib():
                                          C.c_double, P(Results), C.c_void_p]
     L.hm_margin.argtypes = [P(C.c_double), C.c_uint32, C.c_double]
     L.hm_margin.restype = C.c_double
+    L.hm_bridge_create.argtypes = [P(BridgeView), C.c_int, P(C.c_void_p)]
+    L.hm_bridge_destroy.argtypes = [C.c_void_p]
+    L.hm_bridge_search_batch.argtypes = [C.c_void_p, P(BridgeBatch), P(Results)]
+    L.hm_bridge_search_batch_device.argtypes = [C.c_void_p, P(BridgeBatch), P(Results), C.c_void_p]
+    L.hm_bridge_last_timing.argtypes = [P(C.c_float)]
     _L = L
     return L
 
@@ -415,6 +436,16 @@ class Hidx:
                     doc_lens=arr(v.doc_lens, nd, np.uint32), doc_ids=arr(v.doc_ids, nd, np.uint64),
                     avgdl=v.avgdl)
 
+    def bridge_index(self, device=0):
+        """A Bridge-mode file (mode 1) uploaded straight to a DeviceBridge."""
+        if self.mode != 1:
+            raise RuntimeError("bridge scoring requires a bridge-mode index")
+        v = self.view
+        bv = BridgeView(v.n_terms, v.term_offsets, v.posting_rows, v.posting_weights, v.n_docs, v.doc_ids)
+        h = C.c_void_p()
+        _check(lib().hm_bridge_create(C.byref(bv), device, C.byref(h)))
+        return DeviceBridge._adopt(h, device, v.n_terms, v.n_docs)
+
     def device_index(self, device=0):
         """Upload straight from the parsed file (no Python copies)."""
         if self.mode != 0:
@@ -538,3 +569,196 @@ class TemporalIndex:
                                                  ).astype(np.uint8),
                         postings=np.zeros(nq, np.uint64), n_exact=0)
         return self.dev.search_batch(q_off, q_tid, k, k1=k1, b=b, row_lo=lo, row_hi=hi, **kw)
+
+
+# ------------------------------------------------------------------ bridge
+class SparseVector:
+    """hybrid::SparseVector (bridge.hpp:12-19): strictly increasing term ids,
+    positive values."""
+
+    def __init__(self, indices=(), values=()):
+        self.indices = np.ascontiguousarray(indices, np.uint32)
+        self.values = np.ascontiguousarray(values, np.float64)
+
+    def nnz(self):
+        return len(self.indices)
+
+    def validate(self):
+        """bridge.cpp:10-20 (std::invalid_argument -> ValueError, same messages)."""
+        if len(self.indices) != len(self.values):
+            raise ValueError("indices/values length mismatch")
+        if len(self.indices) > 1 and not (np.diff(self.indices.astype(np.int64)) > 0).all():
+            raise ValueError("sparse vector indices must be strictly increasing")
+        if not (self.values > 0.0).all():
+            raise ValueError("sparse vector values must be > 0")
+
+
+def _sparse_batch(queries):
+    off = np.zeros(len(queries) + 1, np.uint64)
+    off[1:] = np.cumsum([q.nnz() for q in queries])
+    idx = np.concatenate([q.indices for q in queries]) if off[-1] else np.zeros(0, np.uint32)
+    val = np.concatenate([q.values for q in queries]) if off[-1] else np.zeros(0, np.float64)
+    return off, np.ascontiguousarray(idx, np.uint32), np.ascontiguousarray(val, np.float64)
+
+
+class DeviceBridge:
+    """An HBM-resident Bridge-mode index (hm_bridge): rows, learned weights,
+    DocIds in the reference's CsrIndex layout."""
+
+    def __init__(self, term_offsets, posting_rows, posting_weights, doc_ids, device=0):
+        keep = (np.ascontiguousarray(term_offsets, np.uint64), np.ascontiguousarray(posting_rows, np.uint32),
+                np.ascontiguousarray(posting_weights, np.float64), np.ascontiguousarray(doc_ids, np.uint64))
+        v = BridgeView(len(keep[0]) - 1, _ptr(keep[0]), _ptr(keep[1]), _ptr(keep[2]), len(keep[3]),
+                       _ptr(keep[3]))
+        h = C.c_void_p()
+        _check(lib().hm_bridge_create(C.byref(v), device, C.byref(h)))
+        self._h, self.device, self.n_terms, self.n_docs = h, device, len(keep[0]) - 1, len(keep[3])
+
+    @classmethod
+    def _adopt(cls, h, device, n_terms, n_docs):
+        self = cls.__new__(cls)
+        self._h, self.device, self.n_terms, self.n_docs = h, device, n_terms, n_docs
+        return self
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib().hm_bridge_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        self.close()
+
+    def search_batch(self, queries, k, row_lo=0, row_hi=0, flags=0):
+        """Host-buffer batch (hm_bridge_search_batch) over SparseVectors.
+        -> dict(ids[nq,k], scores[nq,k], n[nq], postings[nq])"""
+        off, idx, val = _sparse_batch(queries)
+        return self.search_arrays(off, idx, val, k, row_lo, row_hi, flags)
+
+    def search_arrays(self, q_off, q_idx, q_val, k, row_lo=0, row_hi=0, flags=0):
+        q_off = np.ascontiguousarray(q_off, np.uint64)
+        q_idx = np.ascontiguousarray(q_idx, np.uint32)
+        q_val = np.ascontiguousarray(q_val, np.float64)
+        nq = len(q_off) - 1
+        kk = max(int(k), 1)
+        out = dict(ids=np.zeros((nq, kk), np.uint64), scores=np.zeros((nq, kk), np.float64),
+                   n=np.zeros(nq, np.uint32), postings=np.zeros(nq, np.uint64))
+        qb = BridgeBatch(nq, _ptr(q_off), _ptr(q_idx) if len(q_idx) else None,
+                         _ptr(q_val) if len(q_val) else None, int(k), row_lo, row_hi, 0, flags)
+        r = Results(_ptr(out["ids"]), _ptr(out["scores"]), _ptr(out["n"]), None, None,
+                    _ptr(out["postings"]))
+        _check(lib().hm_bridge_search_batch(self._h, C.byref(qb), C.byref(r)))
+        if k == 0:
+            out["ids"] = out["ids"][:, :0]
+            out["scores"] = out["scores"][:, :0]
+        return out
+
+    def search_batch_device(self, q_off, q_idx, q_val, out, k, max_nnz, row_lo=0, row_hi=0, flags=0,
+                            stream=None):
+        """Device-resident batch (torch CUDA tensors: q_off int64, q_idx int32,
+        q_val f64; out ids/scores/n/postings), enqueued on `stream`."""
+        import torch
+        st = stream if stream is not None else torch.cuda.current_stream(q_off.device)
+        qb = BridgeBatch(q_off.numel() - 1, q_off.data_ptr(), q_idx.data_ptr(), q_val.data_ptr(), int(k),
+                         row_lo, row_hi, int(max_nnz), flags)
+        r = Results(out["ids"].data_ptr(), out["scores"].data_ptr(), out["n"].data_ptr(), None, None,
+                    out["postings"].data_ptr())
+        _check(lib().hm_bridge_search_batch_device(self._h, C.byref(qb), C.byref(r), st.cuda_stream))
+        if flags & HM_FLAG_TIMING:
+            t = C.c_float()
+            lib().hm_bridge_last_timing(C.byref(t))
+            return t.value
+
+
+class BridgeIndex:
+    """A Bridge-mode hybrid::CsrIndex (bridge_ingest, bridge.cpp:22-73) whose
+    searches run on the GPU (bridge_topk / bridge_topk_maxscore,
+    bridge.cpp:112-204: identical outputs, one device path)."""
+
+    def __init__(self, term_offsets, posting_rows, posting_weights, doc_ids, doc_lens, avgdl,
+                 term_maxscores, device=0):
+        self.term_offsets = np.ascontiguousarray(term_offsets, np.uint64)
+        self.posting_rows = np.ascontiguousarray(posting_rows, np.uint32)
+        self.posting_weights = np.ascontiguousarray(posting_weights, np.float64)
+        self.doc_ids = np.ascontiguousarray(doc_ids, np.uint64)
+        self.doc_lens = np.ascontiguousarray(doc_lens, np.uint32)
+        self.avgdl = avgdl
+        self.term_maxscores = np.ascontiguousarray(term_maxscores, np.float64)
+        self.device = device
+        self._dev = None
+
+    @property
+    def n_terms(self):
+        return len(self.term_offsets) - 1
+
+    def num_docs(self):
+        return len(self.doc_ids)
+
+    def num_postings(self):
+        return len(self.posting_rows)
+
+    @property
+    def dev(self):
+        if self._dev is None:
+            self._dev = DeviceBridge(self.term_offsets, self.posting_rows, self.posting_weights,
+                                     self.doc_ids, self.device)
+        return self._dev
+
+    def bridge_topk(self, query_vec, k, stats=None):
+        """-> [(DocId, score), ...] ranked (score desc, DocId asc)."""
+        query_vec.validate()
+        r = self.dev.search_batch([query_vec], min(int(k), self.num_docs()))  # k > N: same list
+        if stats is not None:
+            stats.postings_touched += int(r["postings"][0])
+        n = int(r["n"][0])
+        return [(int(i), float(s)) for i, s in zip(r["ids"][0, :n], r["scores"][0, :n])]
+
+    def bridge_topk_maxscore(self, query_vec, k, stats=None):
+        return self.bridge_topk(query_vec, k, stats)
+
+    def search_batch(self, queries, k, row_lo=0, row_hi=0, flags=0):
+        return self.dev.search_batch(queries, k, row_lo, row_hi, flags)
+
+
+def bridge_ingest(doc_vectors, device=0):
+    """bridge_ingest (bridge.cpp:22-73): [(DocId, SparseVector)] -> BridgeIndex.
+    Duplicate ids raise RuntimeError("duplicate doc id: X"); vectors are validated."""
+    seen = set()
+    dim = 0
+    for doc_id, vec in doc_vectors:
+        if doc_id in seen:
+            raise RuntimeError(f"duplicate doc id: {doc_id}")
+        seen.add(doc_id)
+        vec.validate()
+        if vec.nnz():
+            dim = max(dim, int(vec.indices[-1]) + 1)
+    n = len(doc_vectors)
+    lens = np.array([v.nnz() for _, v in doc_vectors], np.uint32)
+    rows = np.repeat(np.arange(n, dtype=np.uint32), lens)
+    tids = np.concatenate([v.indices for _, v in doc_vectors]) if lens.sum() else np.zeros(0, np.uint32)
+    vals = np.concatenate([v.values for _, v in doc_vectors]) if lens.sum() else np.zeros(0)
+    order = np.argsort(tids, kind="stable")  # per-term postings in doc order (rows ascend)
+    off = np.zeros(dim + 1, np.uint64)
+    off[1:] = np.cumsum(np.bincount(tids, minlength=dim)[:dim])
+    w = vals[order]
+    maxw = np.zeros(dim)
+    if len(w):
+        np.maximum.at(maxw, tids[order], w)
+    len_sum = 0.0
+    for x in lens:  # sequential double sum, as the reference (bridge.cpp:47)
+        len_sum += float(x)
+    avgdl = 0.0 if n == 0 else len_sum / n
+    ids = np.array([d for d, _ in doc_vectors], np.uint64)
+    return BridgeIndex(off, rows[order], w, ids, lens, avgdl, maxw, device)
+
+
+def bridge_export(idx):
+    """bridge_export (bridge.cpp:75-90): the exact inverse of bridge_ingest."""
+    n = idx.num_docs()
+    df = np.diff(idx.term_offsets.astype(np.int64))
+    tids = np.repeat(np.arange(idx.n_terms, dtype=np.uint32), df)
+    order = np.argsort(idx.posting_rows, kind="stable")  # term-major stays ascending per doc
+    rows = idx.posting_rows[order]
+    cuts = np.searchsorted(rows, np.arange(n + 1))
+    t, w = tids[order], idx.posting_weights[order]
+    return [(int(idx.doc_ids[d]), SparseVector(t[cuts[d]:cuts[d + 1]], w[cuts[d]:cuts[d + 1]]))
+            for d in range(n)]
