@@ -5,11 +5,13 @@
 // side (tests/test_dropin.py) computes the same calls on the unmodified
 // reference library and compares bit patterns.
 #include <cstdio>
+#include <cstdlib>
 #include <iostream>
 #include <sstream>
 #include <string>
 #include <vector>
 
+#include "hybrid/bridge.hpp"
 #include "hybrid/csr_index.hpp"
 #include "hybrid/temporal_index.hpp"
 
@@ -19,6 +21,21 @@ static std::string hexd(double v) {
     char buf[64];
     std::snprintf(buf, sizeof buf, "%a", v);
     return buf;
+}
+
+// "nnz i:v i:v ..." with hex-float values (exact)
+static SparseVector read_vec(std::istream& in) {
+    SparseVector v;
+    std::size_t n = 0;
+    in >> n;
+    for (std::size_t i = 0; i < n; ++i) {
+        std::string tok;
+        in >> tok;
+        const auto c = tok.find(':');
+        v.indices.push_back(static_cast<std::uint32_t>(std::stoul(tok.substr(0, c))));
+        v.values.push_back(std::strtod(tok.c_str() + c + 1, nullptr));
+    }
+    return v;
 }
 
 static void print_list(const RankedList& r, const std::string& extra) {
@@ -31,8 +48,9 @@ int main() {
     std::ios::sync_with_stdio(false);
     std::vector<std::pair<DocId, std::string>> docs;
     std::vector<MemoryRecord> recs;
-    CsrIndex idx;
+    CsrIndex idx, bidx;
     TemporalIndex tidx;
+    std::vector<std::pair<DocId, SparseVector>> bdocs;
     std::string line;
     while (std::getline(std::cin, line)) {
         std::istringstream in(line);
@@ -106,6 +124,47 @@ int main() {
                 TemporalStats st;
                 RankedList r = tidx.topk(q, k, Bm25Params{}, &st, ub != 0);
                 print_list(r, " " + std::to_string(st.partitions_searched));
+            } else if (cmd == "BDOCS") {  // n lines of "id nnz i:v ..."
+                std::size_t n;
+                in >> n;
+                bdocs.clear();
+                for (std::size_t i = 0; i < n; ++i) {
+                    std::getline(std::cin, line);
+                    std::istringstream r(line);
+                    DocId id;
+                    r >> id;
+                    bdocs.emplace_back(id, read_vec(r));
+                }
+            } else if (cmd == "BINGEST") {
+                bidx = bridge_ingest(bdocs);
+                std::cout << "OK " << bidx.num_docs() << ' ' << bidx.num_postings() << ' ' << hexd(bidx.avgdl)
+                          << '\n';
+            } else if (cmd == "BQUERY") {  // k ms nnz i:v ...
+                std::size_t k;
+                int ms;
+                in >> k >> ms;
+                const SparseVector q = read_vec(in);
+                SearchStats st;
+                st.postings_touched = 5;
+                RankedList r = ms ? bridge_topk_maxscore(bidx, q, k, &st) : bridge_topk(bidx, q, k, &st);
+                print_list(r, " " + std::to_string(st.postings_touched - 5));
+            } else if (cmd == "BEXPORT") {  // one line: per doc "id:nnz" then the checksum of values
+                auto v = bridge_export(bidx);
+                std::cout << "E " << v.size();
+                for (const auto& [id, sv] : v) {
+                    std::cout << ' ' << id << ':' << sv.nnz();
+                    for (std::size_t i = 0; i < sv.nnz(); ++i) std::cout << ',' << sv.indices[i] << '=' << hexd(sv.values[i]);
+                }
+                std::cout << '\n';
+            } else if (cmd == "BVALIDATE") {
+                read_vec(in).validate();
+                std::cout << "OK\n";
+            } else if (cmd == "BM25ONBRIDGE") {
+                bidx.bm25_topk({"0"}, 5, Bm25Params{});
+                std::cout << "OK\n";
+            } else if (cmd == "BONBM25") {
+                bridge_topk(idx, SparseVector{{0}, {1.0}}, 5);
+                std::cout << "OK\n";
             } else if (cmd == "KSTAR") {
                 double e, l;
                 in >> e >> l;

@@ -93,3 +93,62 @@ def test_temporal_dropin_matches_reference(gpu):
                 assert ids == w_ids.tolist() and bits(sc) == bits(w_sc)
                 assert searched == w_searched
     d.close()
+
+
+def _vec_str(idx, val):
+    return f"{len(idx)} " + " ".join(f"{int(i)}:{float(v).hex()}" for i, v in zip(idx, val))
+
+
+def test_bridge_dropin_matches_reference(gpu):
+    """hybrid::bridge_ingest / bridge_export / bridge_topk(_maxscore) /
+    SparseVector::validate through the drop-in (csrc/dropin/bridge_b200.cpp)
+    against the reference's bridge.cpp, call for call."""
+    rng = np.random.default_rng(5)
+    d = Driver()
+    for ndocs, vocab, dens in ((10, 200, 0.05), (1000, 200, 0.05), (4000, 1000, 0.005)):
+        docs = []
+        for _ in range(ndocs):
+            idx = np.nonzero(rng.random(vocab) < dens)[0]
+            docs.append((idx, 0.05 + rng.random(len(idx)) * 3.0))
+        ids = rng.permutation(5 * ndocs)[:ndocs]
+        d.send([f"BDOCS {ndocs}"] + [f"{int(i)} " + _vec_str(*v) for i, v in zip(ids, docs)], expect=0)
+        ok = d.send(["BINGEST"])[0].split()
+        rb = ref.RefBridge.from_vectors(ids.astype(np.uint64), docs)
+        x = rb.export()
+        assert ok[0] == "OK" and int(ok[1]) == ndocs and int(ok[2]) == len(x["posting_rows"])
+        assert float.fromhex(ok[3]) == x["avgdl"]
+        # export round trip, exact
+        e = d.send(["BEXPORT"])[0].split()
+        w_ids, w_off, w_idx, w_val = rb.export_vectors()
+        assert int(e[1]) == ndocs
+        for r, tok in enumerate(e[2:]):
+            head, *rest = tok.split(",")
+            assert head == f"{int(w_ids[r])}:{int(w_off[r + 1] - w_off[r])}"
+            for j, kv in enumerate(rest):
+                t, v = kv.split("=")
+                assert int(t) == int(w_idx[w_off[r] + j]) and float.fromhex(v) == w_val[w_off[r] + j]
+        for _ in range(30):
+            qi = np.nonzero(rng.random(vocab + 5) < 0.03)[0]
+            qv = 0.1 + rng.random(len(qi))
+            k = int(rng.choice([1, 5, 10, 100]))
+            want = rb.topk_batch([(qi, qv)], k)
+            for ms in (0, 1):
+                got_ids, got_sc, post = parse(d.send([f"BQUERY {k} {ms} " + _vec_str(qi, qv)])[0])
+                n = int(want["n"][0])
+                assert got_ids == want["ids"][0, :n].tolist() and bits(got_sc) == bits(want["scores"][0, :n])
+                assert post == int(want["postings"][0])
+    # validation messages and mode checks (test_bridge.cpp:141-167)
+    for idx, val in (([3, 1], [1.0, 1.0]), ([1, 1], [1.0, 1.0]), ([1, 2], [1.0, 0.0]), ([1, 2], [0.5, 1.0])):
+        try:
+            ref.sparse_validate(idx, val)
+            want = "OK"
+        except RuntimeError as ex:
+            want = "THROW invalid_argument " + str(ex)
+        assert d.send(["BVALIDATE " + _vec_str(idx, val)])[0] == want
+    assert d.send(["BM25ONBRIDGE"])[0] == "THROW runtime_error BM25 scoring requires a BM25-mode index"
+    d.send([f"DOCS {len(toy_docs())}"] + [f"{i}\t{t}" for i, t in toy_docs()], expect=0)
+    d.send(["INDEX 0 1.2 0.75"])
+    assert d.send(["BONBM25"])[0] == "THROW runtime_error bridge scoring requires a bridge-mode index"
+    d.send(["BDOCS 2", "3 1 1:0x1p+0", "3 1 2:0x1p+0"], expect=0)
+    assert d.send(["BINGEST"])[0] == "THROW runtime_error duplicate doc id: 3"
+    d.close()
