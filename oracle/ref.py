@@ -84,6 +84,7 @@ def lib():
     L.ref_bridge_batch.argtypes = [vp, u32, P(u64), P(u32), P(dbl), u64, C.c_int, C.c_uint,
                                    P(u64), P(dbl), P(u32), P(u64), P(dbl)]
     L.ref_bm25_on.argtypes = [vp, C.c_char_p]
+    L.ref_bridge_from_arrays.argtypes = [u32, P(u64), P(u32), P(dbl), u32, P(u64), P(u32), dbl, P(vp)]
     _L = L
     return L
 
@@ -281,6 +282,18 @@ class RefBridge(RefIndex):
         h = C.c_void_p()
         _chk(lib().ref_bridge_ingest(len(ids), _p(ids, C.c_uint64), _p(off, C.c_uint64),
                                      _p(idx, C.c_uint32), _p(val, C.c_double), C.byref(h)))
+        return cls(h)
+
+    @classmethod
+    def from_csr(cls, term_offsets, posting_rows, posting_weights, doc_ids, doc_lens, avgdl):
+        """Adopt bridge_ingest-shaped CSR arrays (timing workloads)."""
+        a = [np.ascontiguousarray(term_offsets, np.uint64), np.ascontiguousarray(posting_rows, np.uint32),
+             np.ascontiguousarray(posting_weights, np.float64), np.ascontiguousarray(doc_ids, np.uint64),
+             np.ascontiguousarray(doc_lens, np.uint32)]
+        h = C.c_void_p()
+        _chk(lib().ref_bridge_from_arrays(len(a[0]) - 1, _p(a[0], C.c_uint64), _p(a[1], C.c_uint32),
+                                          _p(a[2], C.c_double), len(a[3]), _p(a[3], C.c_uint64),
+                                          _p(a[4], C.c_uint32), avgdl, C.byref(h)))
         return cls(h)
 
     def export_vectors(self):

@@ -17,6 +17,7 @@
 //   * a CPU batch driver shaped like hybridmem's cmd_search parallel_for
 //     (tools/hybridmem.cpp:58-71, 305-313) for the CPU baseline timing.
 // Nothing here re-implements reference logic; it only marshals arrays.
+#include <algorithm>
 #include <atomic>
 #include <chrono>
 #include <cstdint>
@@ -581,6 +582,38 @@ int ref_bridge_batch(void* h, std::uint32_t nq, const std::uint64_t* q_off,
         if (wall_ms) *wall_ms = std::chrono::duration<double, std::milli>(clk::now() - t0).count();
         for (auto& e : errs)
             if (!e.empty()) throw std::runtime_error(e);
+    });
+}
+
+// A Bridge-mode CsrIndex adopted from CSR arrays (the layout bridge_ingest
+// produces, bridge.cpp:38-72), for large timing workloads where building
+// per-doc vectors first would dominate.  Marshalling only: fields are filled
+// as bridge_ingest fills them.
+int ref_bridge_from_arrays(std::uint32_t n_terms, const std::uint64_t* term_offsets,
+                           const std::uint32_t* rows, const double* weights,
+                           std::uint32_t n_docs, const std::uint64_t* doc_ids,
+                           const std::uint32_t* doc_lens, double avgdl, void** out) {
+    return guard([&] {
+        auto x = std::make_unique<Index>();
+        CsrIndex& idx = x->idx;
+        idx.mode = IndexMode::Bridge;
+        const std::uint64_t P = term_offsets[n_terms];
+        idx.term_offsets.assign(term_offsets, term_offsets + n_terms + 1);
+        idx.posting_rows.assign(rows, rows + P);
+        idx.posting_weights.assign(weights, weights + P);
+        idx.doc_ids.assign(doc_ids, doc_ids + n_docs);
+        idx.doc_lens.assign(doc_lens, doc_lens + n_docs);
+        idx.avgdl = avgdl;
+        for (std::uint32_t t = 0; t < n_terms; ++t) {
+            idx.terms.push_back(std::to_string(t));
+            idx.vocab.emplace(idx.terms.back(), t);
+            double maxw = 0.0;
+            for (std::uint64_t i = term_offsets[t]; i < term_offsets[t + 1]; ++i) maxw = std::max(maxw, weights[i]);
+            idx.term_idfs.push_back(0.0);
+            idx.term_maxscores.push_back(maxw);
+        }
+        idx.term_order_keys = idx.term_maxscores;
+        *out = x.release();
     });
 }
 

@@ -172,7 +172,7 @@ hm::BridgeArgs make_args(const hm_bridge* X, const hm_bridge_batch* b, BridgeWs*
 }
 
 uint64_t scratch_words(const hm_bridge* X, uint32_t k, uint32_t m_max) {
-    return static_cast<uint64_t>(hm::bridge_grid(k, X->sms)) * (3 + 8) * std::max(m_max, 1u);
+    return static_cast<uint64_t>(hm::bridge_grid(k, X->sms)) * (3 + 2 * 8) * std::max(m_max, 1u);
 }
 
 void run(hm_bridge* X, const hm::BridgeArgs& a, BridgeWs* w, cudaStream_t st, bool timing) {

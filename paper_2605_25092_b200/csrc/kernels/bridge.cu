@@ -94,11 +94,13 @@ __global__ void __launch_bounds__(kBrThreads) bridge_kernel(BridgeDev ix, Bridge
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const uint32_t k = a.k;
     const uint32_t mstride = a.m_max;
-    // per-CTA scratch: t_beg, t_end, t_wq [m_max] then cursors [8][m_max]
-    uint64_t* const t_beg = a.scratch + static_cast<uint64_t>(blockIdx.x) * (3 + kBrWarps) * mstride;
+    // per-CTA scratch: t_beg, t_end, t_wq [m_max], cursors [8][m_max], peeks [8][m_max]
+    // (cursors/peeks of terms beyond the first 128 of a query; the rest live in registers)
+    uint64_t* const t_beg = a.scratch + static_cast<uint64_t>(blockIdx.x) * (3 + 2 * kBrWarps) * mstride;
     uint64_t* const t_end = t_beg + mstride;
     double* const t_wq = reinterpret_cast<double*>(t_end + mstride);
     uint64_t* const cur_g = t_end + 2 * mstride + static_cast<uint64_t>(warp) * mstride;
+    uint64_t* const pk_g = cur_g + static_cast<uint64_t>(kBrWarps) * mstride;
     double* const acc = S.acc[warp];
 
     for (uint32_t i = lane; i < kBrUnit; i += 32) acc[i] = 0.0;
@@ -156,16 +158,25 @@ __global__ void __launch_bounds__(kBrThreads) bridge_kernel(BridgeDev ix, Bridge
             }
             return lo;
         };
+        // lane j of group g: term 32g + j's cursor (first posting at or after the
+        // current unit), the end of its postings in my span, and the row at the
+        // cursor ("peek", kNone when exhausted) -- carried across units, so a
+        // unit costs no load for the terms without postings in it
         uint64_t creg[kRegGroups], ereg[kRegGroups];
+        uint32_t preg[kRegGroups];
         unsigned long long post = 0;  // postings of my span (SearchStats, bridge.cpp:133)
 #pragma unroll
-        for (int g = 0; g < kRegGroups; ++g) creg[g] = ereg[g] = 0;
+        for (int g = 0; g < kRegGroups; ++g) {
+            creg[g] = ereg[g] = 0;
+            preg[g] = kNone;
+        }
         for (uint32_t g = 0; g * 32 < m; ++g) {
             const uint32_t j = g * 32 + lane;
             if (j < m) {
                 const uint64_t b = t_beg[j], e = t_end[j];
                 const uint64_t c = lo_w == 0 ? b : lower_bound(b, e, lo_w);
                 const uint64_t d = hi_w >= ix.n_docs ? e : lower_bound(c, e, hi_w);
+                const uint32_t pk = c < d ? __ldg(ix.rows + c) : kNone;
                 post += d - c;
                 if (g < kRegGroups) {
 #pragma unroll
@@ -173,9 +184,11 @@ __global__ void __launch_bounds__(kBrThreads) bridge_kernel(BridgeDev ix, Bridge
                         if (u == static_cast<int>(g)) {
                             creg[u] = c;
                             ereg[u] = d;
+                            preg[u] = pk;
                         }
                 } else {
                     cur_g[j] = c;
+                    pk_g[j] = pk;
                 }
             }
         }
@@ -192,45 +205,95 @@ __global__ void __launch_bounds__(kBrThreads) bridge_kernel(BridgeDev ix, Bridge
         // [ub, uhi), in ascending order
         uint32_t nw = S.nw[warp];
         double Lw = 0.0;
-        auto walk_group = [&](uint32_t g, uint64_t& c, uint64_t e, uint32_t ub, uint32_t uhi) {
-            const uint32_t j = g * 32 + lane;
-            const uint32_t peek = (j < m && c < e) ? __ldg(ix.rows + c) : kNone;
-            uint32_t act = __ballot_sync(0xffffffffu, peek < uhi);
+        // Terms are applied in ascending order, but their loads are not
+        // serialised: the first 32 postings of up to kBatch active terms are
+        // loaded together, and a term with more postings in the unit continues
+        // 4 chunks (128 postings) at a time.  The row that ends a term's run
+        // is its next peek.
+        auto walk_group = [&](uint32_t g, uint64_t& c, uint32_t& pk, uint64_t e, uint32_t ub, uint32_t uhi) {
+            constexpr int kBatch = 4;
+            uint32_t act = __ballot_sync(0xffffffffu, pk < uhi);
             while (act) {
-                const int i = __ffs(act) - 1;
-                act &= act - 1;
-                uint64_t c0 = __shfl_sync(0xffffffffu, c, i);
-                const uint64_t e0 = __shfl_sync(0xffffffffu, e, i);
-                const double wq = t_wq[g * 32 + i];
-                for (;;) {
-                    const uint64_t p = c0 + lane;
-                    uint32_t r = kNone;
-                    double w = 0.0;
-                    if (p < e0) {
-                        r = __ldg(ix.rows + p);
-                        w = __ldg(ix.w + p);
+                int ti[kBatch];
+                uint64_t cb[kBatch], eb[kBatch];
+                uint32_t rr[kBatch];
+                double ww[kBatch];
+#pragma unroll
+                for (int u = 0; u < kBatch; ++u) {
+                    ti[u] = -1;
+                    if (act) {
+                        ti[u] = __ffs(act) - 1;
+                        act &= act - 1;
                     }
-                    const bool v = r < uhi;
-                    if (v) acc[r - ub] = __dadd_rn(acc[r - ub], __dmul_rn(wq, w));
-                    const uint32_t n = __popc(__ballot_sync(0xffffffffu, v));
-                    c0 += n;
-                    if (n < 32) break;
+                    const int src = ti[u] < 0 ? 0 : ti[u];
+                    cb[u] = __shfl_sync(0xffffffffu, c, src);
+                    eb[u] = __shfl_sync(0xffffffffu, e, src);
+                    rr[u] = kNone;
+                    ww[u] = 0.0;
+                    const uint64_t p = cb[u] + lane;
+                    if (ti[u] >= 0 && p < eb[u]) {
+                        rr[u] = __ldg(ix.rows + p);
+                        ww[u] = __ldg(ix.w + p);
+                    }
                 }
-                __syncwarp();
-                if (lane == i) c = c0;
+#pragma unroll
+                for (int u = 0; u < kBatch; ++u) {
+                    if (ti[u] < 0) break;  // warp-uniform
+                    const double wq = t_wq[g * 32 + ti[u]];
+                    uint64_t c0 = cb[u];
+                    uint32_t npk;
+                    // first chunk (already loaded)
+                    bool v = rr[u] < uhi;
+                    if (v) acc[rr[u] - ub] = __dadd_rn(acc[rr[u] - ub], __dmul_rn(wq, ww[u]));
+                    uint32_t n = __popc(__ballot_sync(0xffffffffu, v));
+                    c0 += n;
+                    npk = __shfl_sync(0xffffffffu, rr[u], n & 31);
+                    while (n == 32) {  // a dense run: 4 chunks in flight
+                        uint32_t r4[4];
+                        double w4[4];
+#pragma unroll
+                        for (int h = 0; h < 4; ++h) {
+                            const uint64_t p = c0 + 32 * h + lane;
+                            r4[h] = kNone;
+                            w4[h] = 0.0;
+                            if (p < eb[u]) {
+                                r4[h] = __ldg(ix.rows + p);
+                                w4[h] = __ldg(ix.w + p);
+                            }
+                        }
+#pragma unroll
+                        for (int h = 0; h < 4; ++h) {
+                            if (n != 32) break;  // warp-uniform
+                            v = r4[h] < uhi;
+                            if (v) acc[r4[h] - ub] = __dadd_rn(acc[r4[h] - ub], __dmul_rn(wq, w4[h]));
+                            n = __popc(__ballot_sync(0xffffffffu, v));
+                            c0 += n;
+                            npk = __shfl_sync(0xffffffffu, r4[h], n & 31);
+                        }
+                    }
+                    __syncwarp();
+                    if (lane == ti[u]) {
+                        c = c0;
+                        pk = npk;
+                    }
+                }
             }
         };
         for (uint32_t ub = lo_w; ub < hi_w; ub += kBrUnit) {
             const uint32_t uhi = min(ub + kBrUnit, hi_w);
 #pragma unroll
             for (int g = 0; g < kRegGroups; ++g)
-                if (static_cast<uint32_t>(g) * 32 < m) walk_group(g, creg[g], ereg[g], ub, uhi);
+                if (static_cast<uint32_t>(g) * 32 < m) walk_group(g, creg[g], preg[g], ereg[g], ub, uhi);
             for (uint32_t g = kRegGroups; g * 32 < m; ++g) {
                 const uint32_t j = g * 32 + lane;
                 uint64_t c = j < m ? cur_g[j] : 0;
+                uint32_t pk = j < m ? static_cast<uint32_t>(pk_g[j]) : kNone;
                 const uint64_t e = j < m ? t_end[j] : 0;
-                walk_group(g, c, e, ub, uhi);
-                if (j < m) cur_g[j] = c;
+                walk_group(g, c, pk, e, ub, uhi);
+                if (j < m) {
+                    cur_g[j] = c;
+                    pk_g[j] = pk;
+                }
             }
             // ---- scan the unit: zero it, admit S > 0 and S >= bound
             const uint32_t nrow = uhi - ub;

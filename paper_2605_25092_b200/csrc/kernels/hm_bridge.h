@@ -25,7 +25,7 @@ struct BridgeArgs {
     uint32_t k;
     uint32_t row_lo, row_hi;
     uint32_t m_max;            // >= every query's nnz (scratch stride)
-    uint64_t* scratch;         // [grid][(3 + 8) * m_max]
+    uint64_t* scratch;         // [grid][(3 + 2 * 8) * m_max]
     uint32_t* counters;        // [0] query cursor
     uint64_t* out_ids;         // [nq * k]
     double* out_scores;        // [nq * k]
