@@ -40,6 +40,12 @@ constexpr int kBrThreads = kBrWarps * 32;
 constexpr uint32_t kBrUnit = 1024;  // rows per warp unit (8 KB of fp64)
 constexpr uint32_t kNone = 0xFFFFFFFFu;
 constexpr int kRegGroups = 4;       // cursors of the first 128 terms live in registers
+#ifndef HM_BR_BATCH
+#define HM_BR_BATCH 6  // terms whose first chunk is loaded together
+#endif
+#ifndef HM_BR_RUN
+#define HM_BR_RUN 8    // chunks in flight in a dense run
+#endif
 
 __device__ __forceinline__ bool better(double sa, uint64_t ia, double sb, uint64_t ib) {
     return sa > sb || (sa == sb && ia < ib);
@@ -211,7 +217,8 @@ __global__ void __launch_bounds__(kBrThreads) bridge_kernel(BridgeDev ix, Bridge
         // 4 chunks (128 postings) at a time.  The row that ends a term's run
         // is its next peek.
         auto walk_group = [&](uint32_t g, uint64_t& c, uint32_t& pk, uint64_t e, uint32_t ub, uint32_t uhi) {
-            constexpr int kBatch = 4;
+            constexpr int kBatch = HM_BR_BATCH;
+            constexpr int kRun = HM_BR_RUN;
             uint32_t act = __ballot_sync(0xffffffffu, pk < uhi);
             while (act) {
                 int ti[kBatch];
@@ -248,11 +255,11 @@ __global__ void __launch_bounds__(kBrThreads) bridge_kernel(BridgeDev ix, Bridge
                     uint32_t n = __popc(__ballot_sync(0xffffffffu, v));
                     c0 += n;
                     npk = __shfl_sync(0xffffffffu, rr[u], n & 31);
-                    while (n == 32) {  // a dense run: 4 chunks in flight
-                        uint32_t r4[4];
-                        double w4[4];
+                    while (n == 32) {  // a dense run: kRun chunks in flight
+                        uint32_t r4[kRun];
+                        double w4[kRun];
 #pragma unroll
-                        for (int h = 0; h < 4; ++h) {
+                        for (int h = 0; h < kRun; ++h) {
                             const uint64_t p = c0 + 32 * h + lane;
                             r4[h] = kNone;
                             w4[h] = 0.0;
@@ -262,7 +269,7 @@ __global__ void __launch_bounds__(kBrThreads) bridge_kernel(BridgeDev ix, Bridge
                             }
                         }
 #pragma unroll
-                        for (int h = 0; h < 4; ++h) {
+                        for (int h = 0; h < kRun; ++h) {
                             if (n != 32) break;  // warp-uniform
                             v = r4[h] < uhi;
                             if (v) acc[r4[h] - ub] = __dadd_rn(acc[r4[h] - ub], __dmul_rn(wq, w4[h]));
