@@ -236,6 +236,42 @@ int hm_bridge_search_batch_device(hm_bridge* bridge, const hm_bridge_batch* batc
 /* Device time (ms) of the last HM_FLAG_TIMING bridge batch on this thread. */
 int hm_bridge_last_timing(float* ms_kernel);
 
+/* ---------------------------------------------------------------- dense
+ * The cascade's escalate channel: brute-force inner-product
+ * top-k over a hybrid::EmbeddingMatrix (include/hybrid/dense.hpp:13-22: unit
+ * vectors, row-major fp32, one DocId per row) held in HBM.  Scores are
+ * sum_j double(r_j) * q_j in fp64, j ascending, every row ranked by
+ * (score desc, DocId asc) -- bit-identical to hybrid::dense_topk
+ * (src/dense.cpp:86-101).  k <= 256 (HM_ERR_INVALID beyond); a query whose
+ * dim differs from the matrix's fails with the reference's
+ * "query dimension mismatch" (HM_ERR_INVALID).  Results as hm_results
+ * (conf, skip, postings unused).  Replaces: hybrid::dense_topk per query. */
+typedef struct hm_dense hm_dense;
+
+typedef struct {
+    uint32_t dim;
+    uint32_t count;
+    const float* data;         /* [count * dim] row-major */
+    const uint64_t* doc_ids;   /* [count] */
+} hm_dense_view;
+
+int hm_dense_create(const hm_dense_view* view, int device, hm_dense** out);
+int hm_dense_destroy(hm_dense* dense);
+
+typedef struct {
+    uint32_t n_queries;
+    uint32_t dim;
+    const float* queries;      /* [n_queries * dim] */
+    uint32_t k;
+    uint32_t flags;            /* HM_FLAG_TIMING */
+} hm_dense_batch;
+
+int hm_dense_search_batch(hm_dense* dense, const hm_dense_batch* batch, hm_results* out);
+int hm_dense_search_batch_device(hm_dense* dense, const hm_dense_batch* batch_dev,
+                                 hm_results* out_dev, void* stream);
+/* Device time (ms) of the last HM_FLAG_TIMING dense batch on this thread. */
+int hm_dense_last_timing(float* ms_kernels);
+
 /* Margin confidence over a ranked score list (src/cascade.cpp:10-21). */
 double hm_margin(const double* scores, uint32_t n, double epsilon_guard);
 

@@ -280,6 +280,43 @@ int or_bridge_topk_batch(const uint64_t* term_offsets, const uint32_t* posting_r
     return 0;
 }
 
+/* ---- dense channel: src/dense.cpp:86-101 --------------------------------
+ * dot = sum_j double(r_j) * q_j, j ascending; EVERY row ranked by
+ * (score desc, id asc) (sort_and_truncate over all rows: no score filter). */
+int or_dense_topk_batch(const float* data, const uint64_t* ids, uint64_t count,
+                        uint32_t dim, const float* queries, uint32_t nq,
+                        uint64_t k, uint64_t* out_ids, double* out_scores,
+                        uint32_t* out_n) {
+    uint64_t cap = k < count ? k : count;
+    entry* heap = (entry*)malloc(sizeof(entry) * (cap ? cap : 1));
+    if (!heap) return -1;
+    for (uint32_t q = 0; q < nq; ++q) {
+        const float* qv = queries + (size_t)q * dim;
+        uint64_t hn = 0;
+        for (uint64_t i = 0; i < count && cap; ++i) {
+            const float* r = data + i * dim;
+            double dot = 0.0;
+            for (uint32_t j = 0; j < dim; ++j) dot += (double)r[j] * (double)qv[j];
+            entry e = {ids[i], dot};
+            if (hn < cap) {
+                heap[hn] = e;
+                sift_up(heap, hn++);
+            } else if (better(&e, &heap[0])) {
+                heap[0] = e;
+                sift_down(heap, hn, 0);
+            }
+        }
+        qsort(heap, hn, sizeof(entry), entry_cmp);
+        for (uint64_t i = 0; i < hn; ++i) {
+            out_ids[(size_t)q * k + i] = heap[i].id;
+            out_scores[(size_t)q * k + i] = heap[i].score;
+        }
+        out_n[q] = (uint32_t)hn;
+    }
+    free(heap);
+    return 0;
+}
+
 /* ---- cascade trigger: src/cascade.cpp:10-42, :79-84 --------------------- */
 double or_confidence(const double* s, uint32_t n, int proxy, double eps) {
     if (n == 0 || s[0] <= 0.0) return 0.0;

@@ -67,6 +67,13 @@ int or_bridge_topk_batch(const uint64_t* term_offsets, const uint32_t* posting_r
                          double* out_scores, uint32_t* out_n,
                          uint64_t* postings_touched);
 
+/* Dense channel: exact inner-product top-k, src/dense.cpp:86-101.
+ * queries [nq x dim]; output stride k. */
+int or_dense_topk_batch(const float* data, const uint64_t* ids, uint64_t count,
+                        uint32_t dim, const float* queries, uint32_t nq,
+                        uint64_t k, uint64_t* out_ids, double* out_scores,
+                        uint32_t* out_n);
+
 /* src/cascade.cpp:10-21 (Margin proxy) */
 double or_margin(const double* scores, uint32_t n, double eps);
 /* src/cascade.cpp:10-42 (proxy 0 Margin, 1 Top1Fraction, 2 EntropyComplement) */

@@ -84,6 +84,12 @@ def lib():
     L.ref_bridge_batch.argtypes = [vp, u32, P(u64), P(u32), P(dbl), u64, C.c_int, C.c_uint,
                                    P(u64), P(dbl), P(u32), P(u64), P(dbl)]
     L.ref_bm25_on.argtypes = [vp, C.c_char_p]
+    L.ref_hash_embed.argtypes = [C.c_char_p, u32, u64, P(C.c_float)]
+    L.ref_dense_batch.argtypes = [u32, u64, P(C.c_float), P(u64), u32, u32, P(C.c_float), u64, C.c_uint,
+                                  P(u64), P(dbl), P(u32), P(dbl)]
+    L.ref_save_embeddings.argtypes = [u32, u64, P(C.c_float), P(u64), C.c_char_p]
+    L.ref_agent_rrf.argtypes = [P(u64), P(dbl), u32, P(u64), P(dbl), u32, P(u64), P(i64), P(dbl), u32,
+                                i64, C.c_char_p, dbl, dbl, i64, dbl, u64, P(u64), P(dbl), P(u32)]
     L.ref_bridge_from_arrays.argtypes = [u32, P(u64), P(u32), P(dbl), u32, P(u64), P(u32), dbl, P(vp)]
     _L = L
     return L
@@ -329,6 +335,62 @@ class RefBridge(RefIndex):
         """CsrIndex::bm25_topk on this index: the reference's refusal message."""
         rc = lib().ref_bm25_on(self.h, b"t0")
         return lib().ref_last_error().decode() if rc else None
+
+
+def hash_embed(text, dim, seed):
+    """hybrid::hash_embed (dense.cpp:54-84)."""
+    out = np.zeros(dim, np.float32)
+    _chk(lib().ref_hash_embed(text.encode(), dim, seed, _p(out, C.c_float)))
+    return out
+
+
+def dense_topk_batch(data, ids, queries, k, workers=1):
+    """hybrid::dense_topk per query (dense.cpp:86-101) over the matrix
+    (data [count x dim] fp32, ids).  -> dict(ids, scores, n, wall_ms)"""
+    data = np.ascontiguousarray(data, np.float32)
+    ids = np.ascontiguousarray(ids, np.uint64)
+    queries = np.ascontiguousarray(queries, np.float32)
+    nq, qdim = queries.shape
+    cap = max(int(k), 1)
+    o_ids = np.zeros((nq, cap), np.uint64)
+    o_sc = np.zeros((nq, cap), np.float64)
+    o_n = np.zeros(nq, np.uint32)
+    wall = C.c_double()
+    _chk(lib().ref_dense_batch(data.shape[1] if data.ndim == 2 else qdim, len(ids), _p(data, C.c_float),
+                               _p(ids, C.c_uint64), nq, qdim, _p(queries, C.c_float), k, workers,
+                               _p(o_ids, C.c_uint64), _p(o_sc, C.c_double), _p(o_n, C.c_uint32), C.byref(wall)))
+    return dict(ids=o_ids, scores=o_sc, n=o_n, wall_ms=wall.value)
+
+
+def save_embeddings(data, ids, path):
+    """hybrid::save_embeddings (dense.cpp:103-118): a HEMB v1 file."""
+    data = np.ascontiguousarray(data, np.float32)
+    ids = np.ascontiguousarray(ids, np.uint64)
+    _chk(lib().ref_save_embeddings(data.shape[1], len(ids), _p(data, C.c_float), _p(ids, C.c_uint64),
+                                   str(path).encode()))
+
+
+def agent_rrf(sparse, dense, records, query_ts, qtype=None, k_rrf=60.0, alpha=0.005,
+              tau_ms=30 * 24 * 3600 * 1000, beta=0.0):
+    """hybrid::agent_rrf (fusion.cpp:22-50).  sparse/dense: [(id, score)];
+    records: {id: (ts_ms, weight)}.  -> [(id, score)] ranked."""
+    s_ids = np.array([d for d, _ in sparse] or [0], np.uint64)
+    s_sc = np.array([x for _, x in sparse] or [0.0])
+    d_ids = np.array([d for d, _ in dense] or [0], np.uint64)
+    d_sc = np.array([x for _, x in dense] or [0.0])
+    r_ids = np.array(list(records) or [0], np.uint64)
+    r_ts = np.array([records[r][0] for r in records] or [0], np.int64)
+    r_w = np.array([records[r][1] for r in records] or [0.0])
+    cap = len(sparse) + len(dense) + 1
+    o_ids = np.zeros(cap, np.uint64)
+    o_sc = np.zeros(cap)
+    n = C.c_uint32()
+    _chk(lib().ref_agent_rrf(_p(s_ids, C.c_uint64), _p(s_sc, C.c_double), len(sparse), _p(d_ids, C.c_uint64),
+                             _p(d_sc, C.c_double), len(dense), _p(r_ids, C.c_uint64), _p(r_ts, C.c_int64),
+                             _p(r_w, C.c_double), len(records), query_ts,
+                             None if qtype is None else qtype.encode(), k_rrf, alpha, tau_ms, beta, cap,
+                             _p(o_ids, C.c_uint64), _p(o_sc, C.c_double), C.byref(n)))
+    return [(int(o_ids[i]), float(o_sc[i])) for i in range(n.value)]
 
 
 class RefTemporal:

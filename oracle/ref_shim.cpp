@@ -13,6 +13,8 @@
 //   * the learned-sparse bridge  bridge_ingest / bridge_export / bridge_topk /
 //                                bridge_topk_maxscore / SparseVector::validate
 //                                (bridge.cpp:10-204)
+//   * the dense channel          hash_embed / dense_topk / save+load_embeddings
+//                                (dense.cpp:44-192) and agent_rrf (fusion.cpp:22-50)
 //   * confidence / k_star / ndcg_at_k / TwoPhaseSelector known-answer hooks
 //   * a CPU batch driver shaped like hybridmem's cmd_search parallel_for
 //     (tools/hybridmem.cpp:58-71, 305-313) for the CPU baseline timing.
@@ -24,13 +26,17 @@
 #include <cstring>
 #include <exception>
 #include <memory>
+#include <optional>
 #include <string>
 #include <thread>
+#include <unordered_map>
 #include <vector>
 
 #include "hybrid/bridge.hpp"
 #include "hybrid/cascade.hpp"
 #include "hybrid/csr_index.hpp"
+#include "hybrid/dense.hpp"
+#include "hybrid/fusion.hpp"
 #include "hybrid/eval.hpp"
 #include "hybrid/io.hpp"
 #include "hybrid/temporal_index.hpp"
@@ -614,6 +620,101 @@ int ref_bridge_from_arrays(std::uint32_t n_terms, const std::uint64_t* term_offs
         }
         idx.term_order_keys = idx.term_maxscores;
         *out = x.release();
+    });
+}
+
+// ---------------------------------------------------------------- dense
+int ref_hash_embed(const char* text, std::uint32_t dim, std::uint64_t seed, float* out) {
+    return guard([&] {
+        auto v = hash_embed(text, dim, seed);
+        std::memcpy(out, v.data(), v.size() * sizeof(float));
+    });
+}
+
+// dense_topk per query over a matrix adopted from arrays (EmbeddingMatrix is
+// a plain struct, dense.hpp:13-22); queries [nq x qdim]; outputs stride k.
+int ref_dense_batch(std::uint32_t dim, std::uint64_t count, const float* data,
+                    const std::uint64_t* ids, std::uint32_t nq, std::uint32_t qdim,
+                    const float* queries, std::uint64_t k, unsigned workers,
+                    std::uint64_t* out_ids, double* out_scores, std::uint32_t* out_n,
+                    double* wall_ms) {
+    return guard([&] {
+        EmbeddingMatrix m;
+        m.dim = dim;
+        m.doc_ids.assign(ids, ids + count);
+        m.data.assign(data, data + count * dim);
+        std::vector<std::string> errs(nq);
+        using clk = std::chrono::steady_clock;
+        auto t0 = clk::now();
+        std::atomic<std::size_t> next{0};
+        auto body = [&] {
+            for (std::size_t i; (i = next.fetch_add(1)) < nq;) {
+                try {
+                    std::vector<float> q(queries + i * qdim, queries + (i + 1) * qdim);
+                    emit(dense_topk(m, q, k), out_ids + i * k, out_scores + i * k, out_n + i);
+                } catch (const std::exception& e) {
+                    errs[i] = e.what();
+                }
+            }
+        };
+        if (workers <= 1) {
+            body();
+        } else {
+            std::vector<std::thread> pool;
+            for (unsigned w = 0; w < workers; ++w) pool.emplace_back(body);
+            for (auto& t : pool) t.join();
+        }
+        if (wall_ms) *wall_ms = std::chrono::duration<double, std::milli>(clk::now() - t0).count();
+        for (auto& e : errs)
+            if (!e.empty()) throw std::runtime_error(e);
+    });
+}
+
+int ref_save_embeddings(std::uint32_t dim, std::uint64_t count, const float* data,
+                        const std::uint64_t* ids, const char* path) {
+    return guard([&] {
+        EmbeddingMatrix m;
+        m.dim = dim;
+        m.doc_ids.assign(ids, ids + count);
+        m.data.assign(data, data + count * dim);
+        save_embeddings(m, path);
+    });
+}
+
+// agent_rrf (fusion.cpp:22-50) over two ranked lists; records given as
+// parallel arrays (id, ts_ms, weight); qtype NULL = nullopt
+int ref_agent_rrf(const std::uint64_t* s_ids, const double* s_sc, std::uint32_t ns,
+                  const std::uint64_t* d_ids, const double* d_sc, std::uint32_t nd,
+                  const std::uint64_t* rec_ids, const std::int64_t* rec_ts, const double* rec_w,
+                  std::uint32_t n_rec, std::int64_t query_ts, const char* qtype, double k_rrf,
+                  double alpha, std::int64_t tau_ms, double beta, std::uint64_t cap,
+                  std::uint64_t* out_ids, double* out_scores, std::uint32_t* out_n) {
+    return guard([&] {
+        RankedList a, b;
+        for (std::uint32_t i = 0; i < ns; ++i) a.entries.emplace_back(s_ids[i], s_sc[i]);
+        for (std::uint32_t i = 0; i < nd; ++i) b.entries.emplace_back(d_ids[i], d_sc[i]);
+        std::vector<MemoryRecord> recs(n_rec);
+        std::unordered_map<DocId, const MemoryRecord*> by_id;
+        for (std::uint32_t i = 0; i < n_rec; ++i) {
+            recs[i].id = rec_ids[i];
+            recs[i].ts_ms = rec_ts[i];
+            recs[i].weight = rec_w[i];
+        }
+        for (auto& r : recs) by_id[r.id] = &r;
+        RecordLookup lookup = [&](DocId d) -> const MemoryRecord* {
+            auto it = by_id.find(d);
+            return it == by_id.end() ? nullptr : it->second;
+        };
+        FusionParams p;
+        p.k_rrf = k_rrf;
+        p.alpha = alpha;
+        p.tau_ms = tau_ms;
+        p.beta = beta;
+        std::optional<std::string> qt;
+        if (qtype) qt = std::string(qtype);
+        RankedList r = agent_rrf(a, b, lookup, query_ts, qt, p);
+        if (r.entries.size() > cap) r.entries.resize(cap);
+        emit(r, out_ids, out_scores, out_n);
     });
 }
 

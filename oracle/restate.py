@@ -37,6 +37,8 @@ def lib():
                                 P(dbl), P(u32), P(u64)]
     L.or_bridge_topk_batch.argtypes = [P(u64), P(u32), P(dbl), u32, u32, P(u64), P(u64), P(u32),
                                        P(dbl), u32, u64, u32, u32, P(u64), P(dbl), P(u32), P(u64)]
+    L.or_dense_topk_batch.argtypes = [P(C.c_float), P(u64), u64, u32, P(C.c_float), u32, u64, P(u64),
+                                      P(dbl), P(u32)]
     L.or_confidence.argtypes = [P(dbl), u32, C.c_int, dbl]
     L.or_confidence.restype = dbl
     L.or_k_star.argtypes = [dbl, dbl]
@@ -182,6 +184,24 @@ class OracleBridge:
         if k == 0:
             n[:] = 0
         return ids, sc, n, post
+
+
+def dense_topk(data, ids, queries, k):
+    """CPU restatement of dense_topk (src/dense.cpp:86-101) per query row.
+    -> (ids[nq,k], scores[nq,k], n[nq])"""
+    data = np.ascontiguousarray(data, np.float32)
+    ids = np.ascontiguousarray(ids, np.uint64)
+    queries = np.ascontiguousarray(queries, np.float32)
+    nq, dim = queries.shape
+    kk = max(int(k), 1)
+    o_ids = np.zeros((nq, kk), np.uint64)
+    o_sc = np.zeros((nq, kk))
+    n = np.zeros(nq, np.uint32)
+    if lib().or_dense_topk_batch(_p(data, C.c_float), _p(ids, C.c_uint64), len(ids), dim,
+                                 _p(queries, C.c_float), nq, k, _p(o_ids, C.c_uint64), _p(o_sc, C.c_double),
+                                 _p(n, C.c_uint32)) != 0:
+        raise MemoryError("oracle allocation failed")
+    return o_ids, o_sc, n
 
 
 def confidence(scores, proxy=0, eps=1e-9):

@@ -1,0 +1,215 @@
+// Dense escalate channel on sm_100a: brute-force inner-product top-k over an
+// EmbeddingMatrix, bit-identical to hybrid::dense_topk (src/dense.cpp:86-101).
+//
+// The reference scores every row as dot = sum_j double(r_j) * q_j in fp64,
+// j ascending, then ranks ALL rows by (score desc, DocId asc) (no score
+// filter: RankedList::sort_and_truncate, include/hybrid/types.hpp:21-30).
+// double(float) * double(float) is exact in fp64 (24 + 24 < 53 significant
+// bits), so fma(r_j, q_j, acc) rounds exactly like acc + r_j * q_j: the
+// kernel evaluates each dot as the same sequential fp64 chain, with DFMA.
+//
+//   dense_q64_kernel     queries -> fp64 once per batch
+//   dense_exact_kernel   grid (query tile of 8, document slab); a thread owns
+//                        one row of a 256-row tile and carries 8 dot chains
+//                        (row loads float4, query values broadcast); the
+//                        8 queries' candidate lists live in shared memory:
+//                        a row joins when it reaches the list's k-th score,
+//                        full lists are bitonic-sorted to their best k
+//   dense_merge_kernel   per query: the slabs' sorted lists merged by rank
+#include <cstdint>
+
+#include "hm_dense.h"
+
+namespace hm {
+namespace {
+
+constexpr int kDT = 256;       // threads = rows per tile
+constexpr int kQT = 8;         // queries per CTA
+constexpr int kDW = 512;       // list capacity (>= k + kDT, a power of two)
+constexpr uint32_t kDenseMaxK = kDW - kDT;
+
+__device__ __forceinline__ bool better(double sa, uint64_t ia, double sb, uint64_t ib) {
+    return sa > sb || (sa == sb && ia < ib);
+}
+
+struct DenseSmem {
+    double s[kQT][kDW];
+    uint64_t id[kQT][kDW];
+    uint32_t n[kQT];
+    double L[kQT];  // admission bound: the list's k-th score once it holds k
+};
+
+__global__ void dense_q64_kernel(const float* q, double* q64, uint64_t n) {
+    for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<uint64_t>(gridDim.x) * blockDim.x)
+        q64[i] = static_cast<double>(q[i]);
+}
+
+// sort list (s, id)[0..W) in place by rank (warp-cooperative bitonic network;
+// entries past n are padded with -inf sentinels)
+__device__ void sort_list(double* s, uint64_t* id, uint32_t n, int lane) {
+    for (uint32_t i = n + lane; i < static_cast<uint32_t>(kDW); i += 32) {
+        s[i] = -__longlong_as_double(0x7ff0000000000000ll);
+        id[i] = ~0ull;
+    }
+    __syncwarp();
+    for (uint32_t size = 2; size <= static_cast<uint32_t>(kDW); size <<= 1)
+        for (uint32_t stride = size >> 1; stride > 0; stride >>= 1) {
+            for (uint32_t t = lane; t < static_cast<uint32_t>(kDW) / 2; t += 32) {
+                const uint32_t i = 2 * t - (t & (stride - 1)), j = i + stride;
+                const double si = s[i], sj = s[j];
+                const uint64_t ii = id[i], ij = id[j];
+                if ((i & size) == 0 ? better(sj, ij, si, ii) : better(si, ii, sj, ij)) {
+                    s[i] = sj;
+                    s[j] = si;
+                    id[i] = ij;
+                    id[j] = ii;
+                }
+            }
+            __syncwarp();
+        }
+}
+
+__global__ void __launch_bounds__(kDT) dense_exact_kernel(DenseDev ix, DenseArgs a) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    DenseSmem& S = *reinterpret_cast<DenseSmem*>(smem_raw);
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const uint32_t q0 = blockIdx.x * kQT;
+    const uint32_t nqt = min(static_cast<uint32_t>(kQT), a.nq - q0);
+    const uint32_t slab = blockIdx.y;
+    const uint32_t r_lo = static_cast<uint32_t>((static_cast<uint64_t>(ix.n) * slab) / a.n_slabs);
+    const uint32_t r_hi = static_cast<uint32_t>((static_cast<uint64_t>(ix.n) * (slab + 1)) / a.n_slabs);
+    const uint32_t k = a.k, dim = ix.dim;
+    if (tid < kQT) {
+        S.n[tid] = 0;
+        S.L[tid] = -__longlong_as_double(0x7ff0000000000000ll);
+    }
+    __syncthreads();
+    const double* qb = a.q64 + static_cast<uint64_t>(q0) * dim;
+    for (uint32_t t0 = r_lo; t0 < r_hi; t0 += kDT) {
+        const uint32_t row = t0 + tid;
+        double acc[kQT];
+#pragma unroll
+        for (int u = 0; u < kQT; ++u) acc[u] = 0.0;
+        if (row < r_hi) {
+            const float* r = ix.E + static_cast<uint64_t>(row) * dim;
+            if ((dim & 3u) == 0) {
+                const float4* r4 = reinterpret_cast<const float4*>(r);
+                for (uint32_t j4 = 0; j4 < dim / 4; ++j4) {
+                    const float4 x = __ldg(r4 + j4);
+                    const float xv[4] = {x.x, x.y, x.z, x.w};
+#pragma unroll
+                    for (int h = 0; h < 4; ++h) {
+                        const double rd = static_cast<double>(xv[h]);
+                        const uint32_t j = 4 * j4 + h;
+#pragma unroll
+                        for (int u = 0; u < kQT; ++u)
+                            acc[u] = __fma_rn(rd, __ldg(qb + static_cast<uint64_t>(u) * dim + j), acc[u]);
+                    }
+                }
+            } else {
+                for (uint32_t j = 0; j < dim; ++j) {
+                    const double rd = static_cast<double>(__ldg(r + j));
+#pragma unroll
+                    for (int u = 0; u < kQT; ++u)
+                        acc[u] = __fma_rn(rd, __ldg(qb + static_cast<uint64_t>(u) * dim + j), acc[u]);
+                }
+            }
+        }
+        // admission: every row is ranked (no score filter), so a row joins
+        // list u while the list holds fewer than k or it reaches the k-th score
+        if (row < r_hi) {
+            const uint64_t id = __ldg(ix.ids + row);
+#pragma unroll
+            for (int u = 0; u < kQT; ++u)
+                if (static_cast<uint32_t>(u) < nqt && acc[u] >= S.L[u]) {
+                    const uint32_t p = atomicAdd(&S.n[u], 1u);
+                    S.s[u][p] = acc[u];
+                    S.id[u][p] = id;
+                }
+        }
+        __syncthreads();
+        // lists that cannot take another full tile: sort, keep the best k
+        for (uint32_t u = warp; u < nqt; u += kDT / 32) {
+            const uint32_t n = S.n[u];
+            if (n + kDT > static_cast<uint32_t>(kDW) || t0 + kDT >= r_hi) {
+                sort_list(S.s[u], S.id[u], n, lane);
+                if (lane == 0) {
+                    S.n[u] = min(n, k);
+                    if (n >= k) S.L[u] = S.s[u][k - 1];
+                }
+            }
+        }
+        __syncthreads();
+    }
+    // this slab's sorted best k per query
+    for (uint32_t u = 0; u < nqt; ++u) {
+        const uint32_t n = S.n[u];
+        const uint64_t o = (static_cast<uint64_t>(slab) * a.nq + q0 + u) * k;
+        for (uint32_t i = tid; i < n; i += kDT) {
+            a.part_ids[o + i] = S.id[u][i];
+            a.part_scores[o + i] = S.s[u][i];
+        }
+        if (tid == 0) a.part_n[static_cast<uint64_t>(slab) * a.nq + q0 + u] = n;
+    }
+}
+
+__global__ void __launch_bounds__(256) dense_merge_kernel(DenseArgs a) {
+    const uint32_t q = blockIdx.x, k = a.k, G = a.n_slabs;
+    auto at = [&](uint32_t g, uint32_t i) { return (static_cast<uint64_t>(g) * a.nq + q) * k + i; };
+    uint32_t total = 0;
+    for (uint32_t g = 0; g < G; ++g) total += a.part_n[static_cast<uint64_t>(g) * a.nq + q];
+    for (uint32_t g = 0; g < G; ++g) {
+        const uint32_t ng = a.part_n[static_cast<uint64_t>(g) * a.nq + q];
+        for (uint32_t i = threadIdx.x; i < ng; i += blockDim.x) {
+            const double s = a.part_scores[at(g, i)];
+            const uint64_t id = a.part_ids[at(g, i)];
+            uint32_t rank = i;
+            for (uint32_t h = 0; h < G; ++h) {
+                if (h == g) continue;
+                uint32_t lo = 0, hi = a.part_n[static_cast<uint64_t>(h) * a.nq + q];
+                while (lo < hi) {
+                    const uint32_t mid = (lo + hi) >> 1;
+                    if (better(a.part_scores[at(h, mid)], a.part_ids[at(h, mid)], s, id)) lo = mid + 1;
+                    else hi = mid;
+                }
+                rank += lo;
+            }
+            if (rank < k) {
+                a.out_ids[static_cast<uint64_t>(q) * k + rank] = id;
+                a.out_scores[static_cast<uint64_t>(q) * k + rank] = s;
+            }
+        }
+    }
+    if (threadIdx.x == 0) a.out_n[q] = min(total, k);
+}
+
+}  // namespace
+
+uint32_t dense_max_k() { return kDenseMaxK; }
+
+uint32_t dense_slabs(uint32_t nq, uint32_t n_rows, int sms) {
+    // enough CTAs for every SM twice, slabs of at least a few tiles
+    const uint32_t qtiles = (nq + kQT - 1) / kQT;
+    uint32_t s = (2u * static_cast<uint32_t>(sms) + qtiles - 1) / qtiles;
+    s = min(s, max(1u, n_rows / (4u * kDT)));
+    return max(1u, min(s, 64u));
+}
+
+cudaError_t launch_dense(const DenseDev& ix, const DenseArgs& a, cudaStream_t st) {
+    if (a.nq == 0) return cudaSuccess;
+    const uint64_t nq_el = static_cast<uint64_t>(a.nq) * ix.dim;
+    const uint64_t blocks = (nq_el + 255) / 256 < 4096 ? (nq_el + 255) / 256 : 4096;
+    dense_q64_kernel<<<static_cast<unsigned>(blocks), 256, 0, st>>>(a.q_in, a.q64, nq_el);
+    const size_t smem = sizeof(DenseSmem);
+    cudaError_t e = cudaFuncSetAttribute(dense_exact_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(smem));
+    if (e != cudaSuccess) return e;
+    const dim3 grid((a.nq + kQT - 1) / kQT, a.n_slabs);
+    dense_exact_kernel<<<grid, kDT, smem, st>>>(ix, a);
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    dense_merge_kernel<<<a.nq, 256, 0, st>>>(a);
+    return cudaGetLastError();
+}
+
+}  // namespace hm

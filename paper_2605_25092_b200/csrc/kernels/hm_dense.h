@@ -1,0 +1,35 @@
+// Device layout and launcher of the dense escalate channel (kernels/dense.cu;
+// C ABI in host/hm_dense.cpp).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace hm {
+
+// hybrid::EmbeddingMatrix (include/hybrid/dense.hpp:13-22) in HBM, the
+// reference's own layout: row-major fp32 [n x dim] plus the DocIds.
+struct DenseDev {
+    const float* E;
+    const uint64_t* ids;
+    uint32_t n, dim;
+};
+
+struct DenseArgs {
+    uint32_t nq;
+    const float* q_in;     // [nq x dim] fp32 queries
+    double* q64;           // [nq x dim] scratch: the queries widened once
+    uint32_t k;
+    uint32_t n_slabs;      // document slabs (grid.y); partial lists per slab
+    uint64_t* part_ids;    // [n_slabs][nq][k]
+    double* part_scores;   // [n_slabs][nq][k]
+    uint32_t* part_n;      // [n_slabs][nq]
+    uint64_t* out_ids;     // [nq * k]
+    double* out_scores;    // [nq * k]
+    uint32_t* out_n;       // [nq]
+};
+
+uint32_t dense_max_k();
+uint32_t dense_slabs(uint32_t nq, uint32_t n_rows, int sms);
+cudaError_t launch_dense(const DenseDev& ix, const DenseArgs& a, cudaStream_t st);
+
+}  // namespace hm

@@ -9,6 +9,9 @@ Reference interfaces mirrored (paths under /root/reference/proj):
   the cmd_search batch loop       tools/hybridmem.cpp:227-313  -> search_batch
   SparseVector, bridge_ingest, bridge_export, bridge_topk(_maxscore)
                                   include/hybrid/bridge.hpp:12-40 -> BridgeIndex
+  EmbeddingMatrix, dense_topk     include/hybrid/dense.hpp:13-34  -> DenseIndex
+  rrf, agent_rrf, FusionParams    include/hybrid/fusion.hpp:17-49
+  CascadeConfig, cascade_retrieve include/hybrid/cascade.hpp:19-61 (+ cascade_batch)
 
 Every search runs on the GPU through libhm_b200.so; there is no CPU path.
 Errors map to the reference's exception types (RuntimeError for
@@ -67,7 +70,18 @@ class BridgeBatch(C.Structure):
                 ("row_hi", C.c_uint32), ("max_nnz", C.c_uint32), ("flags", C.c_uint32)]
 
 
-EXPORTS = ["hm_bridge_create", "hm_bridge_destroy", "hm_bridge_search_batch",
+class DenseView(C.Structure):
+    _fields_ = [("dim", C.c_uint32), ("count", C.c_uint32), ("data", C.c_void_p), ("doc_ids", C.c_void_p)]
+
+
+class DenseBatch(C.Structure):
+    _fields_ = [("n_queries", C.c_uint32), ("dim", C.c_uint32), ("queries", C.c_void_p), ("k", C.c_uint32),
+                ("flags", C.c_uint32)]
+
+
+EXPORTS = ["hm_dense_create", "hm_dense_destroy", "hm_dense_search_batch", "hm_dense_search_batch_device",
+           "hm_dense_last_timing",
+           "hm_bridge_create", "hm_bridge_destroy", "hm_bridge_search_batch",
            "hm_bridge_search_batch_device", "hm_bridge_last_timing",
            "hm_index_create", "hm_index_destroy", "hm_index_device_bytes", "hm_index_format",
            "hm_search_batch", "hm_search_batch_device", "hm_last_batch_stats",
@@ -116,6 +130,11 @@ def lib():
                                          C.c_double, P(Results), C.c_void_p]
     L.hm_margin.argtypes = [P(C.c_double), C.c_uint32, C.c_double]
     L.hm_margin.restype = C.c_double
+    L.hm_dense_create.argtypes = [P(DenseView), C.c_int, P(C.c_void_p)]
+    L.hm_dense_destroy.argtypes = [C.c_void_p]
+    L.hm_dense_search_batch.argtypes = [C.c_void_p, P(DenseBatch), P(Results)]
+    L.hm_dense_search_batch_device.argtypes = [C.c_void_p, P(DenseBatch), P(Results), C.c_void_p]
+    L.hm_dense_last_timing.argtypes = [P(C.c_float)]
     L.hm_bridge_create.argtypes = [P(BridgeView), C.c_int, P(C.c_void_p)]
     L.hm_bridge_destroy.argtypes = [C.c_void_p]
     L.hm_bridge_search_batch.argtypes = [C.c_void_p, P(BridgeBatch), P(Results)]
@@ -384,12 +403,12 @@ class CsrIndex:
     bm25_topk_maxscore = bm25_topk
 
     def search_batch(self, queries, k, p=None, tau=None, tau_default=0.10, row_lo=0, row_hi=0,
-                     flags=0):
+                     flags=0, epsilon_guard=1e-9):
         """Batch of string queries (the cmd_search loop, hybridmem.cpp:227-313)."""
         p = p or Bm25Params()
         return self.dev().search_lists([self.resolve(q) for q in queries], k, k1=p.k1, b=p.b,
-                                       tau=tau, tau_default=tau_default, row_lo=row_lo,
-                                       row_hi=row_hi, flags=flags)
+                                       tau=tau, tau_default=tau_default, epsilon_guard=epsilon_guard,
+                                       row_lo=row_lo, row_hi=row_hi, flags=flags)
 
 
 class Hidx:
@@ -762,3 +781,187 @@ def bridge_export(idx):
     t, w = tids[order], idx.posting_weights[order]
     return [(int(idx.doc_ids[d]), SparseVector(t[cuts[d]:cuts[d + 1]], w[cuts[d]:cuts[d + 1]]))
             for d in range(n)]
+
+
+# ------------------------------------------------------------------ dense
+DENSE_MAX_K = 256
+
+
+class DenseIndex:
+    """An HBM-resident hybrid::EmbeddingMatrix (dense.hpp:13-22): row-major
+    fp32 unit vectors + DocIds.  dense_topk runs on the GPU, bit-identical to
+    the reference (src/dense.cpp:86-101)."""
+
+    def __init__(self, data, doc_ids, device=0):
+        data = np.ascontiguousarray(data, np.float32)
+        doc_ids = np.ascontiguousarray(doc_ids, np.uint64)
+        if data.ndim != 2 or data.shape[0] != len(doc_ids):
+            raise ValueError("embedding dimension mismatch")
+        self.dim, self.count = int(data.shape[1]), int(data.shape[0])
+        v = DenseView(self.dim, self.count, _ptr(data), _ptr(doc_ids))
+        h = C.c_void_p()
+        _check(lib().hm_dense_create(C.byref(v), device, C.byref(h)))
+        self._h, self.device = h, device
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib().hm_dense_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        self.close()
+
+    def search_batch(self, queries, k, flags=0):
+        """queries [nq x dim] fp32 -> dict(ids[nq,k], scores[nq,k], n[nq])"""
+        q = np.ascontiguousarray(queries, np.float32)
+        if q.ndim == 1:
+            q = q[None, :]
+        nq = q.shape[0]
+        kk = max(int(k), 1)
+        out = dict(ids=np.zeros((nq, kk), np.uint64), scores=np.zeros((nq, kk)), n=np.zeros(nq, np.uint32))
+        b = DenseBatch(nq, q.shape[1], _ptr(q), int(k), flags)
+        r = Results(_ptr(out["ids"]), _ptr(out["scores"]), _ptr(out["n"]), None, None, None)
+        _check(lib().hm_dense_search_batch(self._h, C.byref(b), C.byref(r)))
+        return out
+
+    def search_batch_device(self, queries, out, k, flags=0, stream=None):
+        """Device-resident batch (torch CUDA tensors: queries [nq,dim] f32;
+        out ids int64 / scores f64 [nq,k], n int32 [nq])."""
+        import torch
+        st = stream if stream is not None else torch.cuda.current_stream(queries.device)
+        b = DenseBatch(queries.shape[0], queries.shape[1], queries.data_ptr(), int(k), flags)
+        r = Results(out["ids"].data_ptr(), out["scores"].data_ptr(), out["n"].data_ptr(), None, None, None)
+        _check(lib().hm_dense_search_batch_device(self._h, C.byref(b), C.byref(r), st.cuda_stream))
+        if flags & HM_FLAG_TIMING:
+            t = C.c_float()
+            lib().hm_dense_last_timing(C.byref(t))
+            return t.value
+
+    def dense_topk(self, query_vec, k):
+        """hybrid::dense_topk: -> [(DocId, score)] over every row (ties by DocId)."""
+        q = np.asarray(query_vec, np.float32)
+        if q.shape != (self.dim,):
+            raise ValueError("query dimension mismatch")
+        r = self.search_batch(q[None, :], min(int(k), self.count))
+        n = int(r["n"][0])
+        return [(int(i), float(s)) for i, s in zip(r["ids"][0, :n], r["scores"][0, :n])]
+
+
+# ------------------------------------------------------------------ fusion
+@dataclass
+class FusionParams:
+    """hybrid::FusionParams (fusion.hpp:17-33)."""
+    k_rrf: float = 60.0
+    alpha: float = 0.005
+    tau_ms: int = 30 * 24 * 3600 * 1000
+    tau_overrides_ms: dict = None
+    beta: float = 0.0
+    recency_qtypes: set = None
+    apply_bonus_when_qtype_unknown: bool = True
+
+    def tau_for(self, qtype):
+        if qtype is not None and self.tau_overrides_ms and qtype in self.tau_overrides_ms:
+            return self.tau_overrides_ms[qtype]
+        return self.tau_ms
+
+
+def _ranked(scores):
+    """RankedList::sort_and_truncate over all entries: (score desc, DocId asc)."""
+    return sorted(scores.items(), key=lambda e: (-e[1], e[0]))
+
+
+def rrf(lists, k_rrf):
+    """Reciprocal rank fusion (fusion.cpp:8-21), same operation order."""
+    if not k_rrf > 0.0:
+        raise ValueError("k_rrf must be > 0")
+    score = {}
+    for lst in lists:
+        for r, (doc, _) in enumerate(lst):
+            score[doc] = score.get(doc, 0.0) + 1.0 / (k_rrf + float(r + 1))
+    return _ranked(score)
+
+
+def agent_rrf(sparse, dense, records, query_ts_ms, qtype, p):
+    """agent_rrf (fusion.cpp:23-50): RRF + alpha*exp(-dt/tau) + beta*w.
+    records: callable DocId -> object with ts_ms / weight, or None."""
+    fused = dict(rrf([sparse, dense], p.k_rrf))
+    if not p.recency_qtypes:
+        bonus_on = qtype is not None or p.apply_bonus_when_qtype_unknown
+    elif qtype is not None:
+        bonus_on = qtype in p.recency_qtypes
+    else:
+        bonus_on = p.apply_bonus_when_qtype_unknown
+    tau = float(p.tau_for(qtype))
+    for doc in list(fused):
+        rec = records(doc)
+        if rec is None:
+            raise RuntimeError(f"record missing from lookup: {doc}")
+        if bonus_on and p.alpha > 0.0:
+            dt = float(max(0, query_ts_ms - rec.ts_ms))
+            fused[doc] += p.alpha * math.exp(-dt / tau)
+        if p.beta != 0.0:
+            fused[doc] += p.beta * rec.weight
+    return _ranked(fused)
+
+
+@dataclass
+class CascadeConfig:
+    """hybrid::CascadeConfig (cascade.hpp:19-27), Margin proxy."""
+    conf_threshold: float = 0.10
+    per_qtype_thresholds: dict = None
+    skip_cost_ms: float = 0.4
+    escalate_cost_ms: float = 53.2
+    epsilon_guard: float = 1e-9
+
+
+@dataclass
+class CascadeDecision:
+    results: list
+    escalated: bool
+    confidence: float
+    accounted_cost_ms: float
+
+
+def cascade_retrieve(k, cfg, bm25_fn, dense_fn, records, query_ts_ms, fusion, qtype=None):
+    """cascade_retrieve (cascade.cpp:44-101) with the Margin proxy: BM25
+    always; skip dense when the confidence clears tau, else agent_rrf."""
+    sparse = bm25_fn(k)
+    conf = margin([s for _, s in sparse], cfg.epsilon_guard)
+    tau = cfg.conf_threshold
+    if qtype is not None and cfg.per_qtype_thresholds and qtype in cfg.per_qtype_thresholds:
+        tau = cfg.per_qtype_thresholds[qtype]
+    if conf >= tau:
+        return CascadeDecision(sparse, False, conf, cfg.skip_cost_ms)
+    fused = agent_rrf(sparse, dense_fn(k), records, query_ts_ms, qtype, fusion)[:k]
+    return CascadeDecision(fused, True, conf, cfg.escalate_cost_ms)
+
+
+def cascade_batch(csr, dense, query_terms, query_vecs, k, records, query_ts_ms, fusion=None, cfg=None,
+                  p=None):
+    """The cascade over a whole batch on the GPU: one BM25 batch (Margin +
+    skip computed on the device), one dense batch over the escalated
+    queries only, agent_rrf on the host (O(k) per query).  Per query it
+    equals cascade_retrieve with bm25_fn = bm25_topk, dense_fn = dense_topk.
+    -> list[CascadeDecision]"""
+    fusion = fusion or FusionParams()
+    cfg = cfg or CascadeConfig()
+    p = p or Bm25Params()
+    r = csr.search_batch(query_terms, k, p, tau_default=cfg.conf_threshold, epsilon_guard=cfg.epsilon_guard)
+    esc = [i for i in range(len(query_terms)) if not r["skip"][i]]
+    dres = dense.search_batch(np.asarray(query_vecs, np.float32)[esc], min(int(k), dense.count)) if esc else None
+    out = []
+    ei = {q: j for j, q in enumerate(esc)}
+    for i in range(len(query_terms)):
+        n = int(r["n"][i])
+        sparse = [(int(d), float(x)) for d, x in zip(r["ids"][i, :n], r["scores"][i, :n])]
+        conf = float(r["conf"][i])
+        if i not in ei:
+            out.append(CascadeDecision(sparse, False, conf, cfg.skip_cost_ms))
+            continue
+        j = ei[i]
+        m = int(dres["n"][j])
+        dl = [(int(d), float(x)) for d, x in zip(dres["ids"][j, :m], dres["scores"][j, :m])]
+        ts = query_ts_ms[i] if np.ndim(query_ts_ms) else query_ts_ms
+        out.append(CascadeDecision(agent_rrf(sparse, dl, records, ts, None, fusion)[:k], True, conf,
+                                   cfg.escalate_cost_ms))
+    return out
