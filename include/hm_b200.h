@@ -242,7 +242,8 @@ int hm_bridge_last_timing(float* ms_kernel);
  * vectors, row-major fp32, one DocId per row) held in HBM.  Scores are
  * sum_j double(r_j) * q_j in fp64, j ascending, every row ranked by
  * (score desc, DocId asc) -- bit-identical to hybrid::dense_topk
- * (src/dense.cpp:86-101).  k <= 256 (HM_ERR_INVALID beyond); a query whose
+ * (src/dense.cpp:86-101).  k <= 256 runs the fused list kernel; larger k
+ * scores every row and sorts on the device per query.  A query whose
  * dim differs from the matrix's fails with the reference's
  * "query dimension mismatch" (HM_ERR_INVALID).  Results as hm_results
  * (conf, skip, postings unused).  Replaces: hybrid::dense_topk per query. */

@@ -24,7 +24,8 @@ thread_local float g_ms_dense = 0.f;
 struct DenseWs {
     cudaStream_t st = nullptr;
     cudaEvent_t ev[2] = {nullptr, nullptr};
-    uint64_t q_cap = 0, part_cap = 0, lists_cap = 0, out_cap = 0, nq_cap = 0;
+    uint64_t q_cap = 0, part_cap = 0, lists_cap = 0, out_cap = 0, nq_cap = 0, big_cap = 0;
+    void* big = nullptr;  // large-k scratch (scores, sort keys, CUB temp)
     float* q_in = nullptr;
     double *q64 = nullptr, *part_scores = nullptr, *out_scores = nullptr;
     uint64_t *part_ids = nullptr, *out_ids = nullptr;
@@ -36,7 +37,7 @@ struct DenseWs {
         ck(cudaEventCreate(&ev[1]), "event");
     }
     ~DenseWs() {
-        void* ps[] = {q_in, q64, part_scores, out_scores, part_ids, out_ids, part_n, out_n};
+        void* ps[] = {q_in, q64, part_scores, out_scores, part_ids, out_ids, part_n, out_n, big};
         for (void* p : ps)
             if (p) cudaFree(p);
         cudaEventDestroy(ev[0]);
@@ -121,30 +122,49 @@ const T* upload(hm_dense* X, const T* host, uint64_t n) {
 
 void check_batch(const hm_dense* X, const hm_dense_batch* b) {
     if (b->dim != X->dev.dim) throw std::invalid_argument("query dimension mismatch");  // dense.cpp:88-89
-    if (b->k > hm::dense_max_k())
-        throw std::invalid_argument("k exceeds the supported maximum of " + std::to_string(hm::dense_max_k()));
 }
 
 // one batch on the workspace's device buffers (queries already in w->q_in
 // or at q_dev); results into w->out_* or the caller's device buffers
 void run(hm_dense* X, DenseWs* w, uint32_t nq, uint32_t k, const float* q_dev, uint64_t* out_ids, double* out_scores,
          uint32_t* out_n, cudaStream_t st, bool timing) {
-    hm::DenseArgs a{};
-    a.nq = nq;
-    a.k = k;
-    a.n_slabs = hm::dense_slabs(nq, X->dev.n, X->sms);
-    w->ensure(static_cast<uint64_t>(nq) * X->dev.dim, static_cast<uint64_t>(a.n_slabs) * nq * k,
-              static_cast<uint64_t>(a.n_slabs) * nq, static_cast<uint64_t>(nq) * k, nq);
-    a.q_in = q_dev;
-    a.q64 = w->q64;
-    a.part_ids = w->part_ids;
-    a.part_scores = w->part_scores;
-    a.part_n = w->part_n;
-    a.out_ids = out_ids;
-    a.out_scores = out_scores;
-    a.out_n = out_n;
     if (timing) ck(cudaEventRecord(w->ev[0], st), "event");
-    ck(hm::launch_dense(X->dev, a, st), "dense kernels");
+    if (k > hm::dense_max_k()) {
+        // k beyond the shared-memory lists: per query, every row scored and
+        // sorted on the device (rare: the reference callers use k = 10)
+        const uint32_t kk = std::min<uint32_t>(k, X->dev.n);
+        const size_t bytes = hm::dense_large_k_bytes(X->dev.n);
+        w->ensure(static_cast<uint64_t>(nq) * X->dev.dim, 0, 0, 0, 0);
+        if (bytes > w->big_cap) {
+            if (w->big) cudaFree(w->big);
+            w->big = nullptr;
+            ck(cudaMalloc(&w->big, bytes), "cudaMalloc(dense large-k scratch)");
+            w->big_cap = bytes;
+        }
+        for (uint32_t q = 0; q < nq; ++q) {
+            double* q64 = w->q64 + static_cast<uint64_t>(q) * X->dev.dim;
+            ck(hm::launch_dense_widen(q_dev + static_cast<uint64_t>(q) * X->dev.dim, q64, X->dev.dim, st), "widen");
+            ck(hm::launch_dense_large_k(X->dev, q64, kk, w->big, bytes, out_ids + static_cast<uint64_t>(q) * k,
+                                        out_scores + static_cast<uint64_t>(q) * k, out_n + q, st),
+               "dense large-k");
+        }
+    } else {
+        hm::DenseArgs a{};
+        a.nq = nq;
+        a.k = k;
+        a.n_slabs = hm::dense_slabs(nq, X->dev.n, X->sms);
+        w->ensure(static_cast<uint64_t>(nq) * X->dev.dim, static_cast<uint64_t>(a.n_slabs) * nq * k,
+                  static_cast<uint64_t>(a.n_slabs) * nq, 0, 0);
+        a.q_in = q_dev;
+        a.q64 = w->q64;
+        a.part_ids = w->part_ids;
+        a.part_scores = w->part_scores;
+        a.part_n = w->part_n;
+        a.out_ids = out_ids;
+        a.out_scores = out_scores;
+        a.out_n = out_n;
+        ck(hm::launch_dense(X->dev, a, st), "dense kernels");
+    }
     if (timing) ck(cudaEventRecord(w->ev[1], st), "event");
 }
 

@@ -16,7 +16,12 @@
 //                        a row joins when it reaches the list's k-th score,
 //                        full lists are bitonic-sorted to their best k
 //   dense_merge_kernel   per query: the slabs' sorted lists merged by rank
+//   large k (> 256: the lists would not fit shared memory): every row's
+//   exact score, then two stable radix sorts -- by DocId, then by score
+//   descending -- which is exactly the (score desc, DocId asc) order
 #include <cstdint>
+
+#include <cub/cub.cuh>
 
 #include "hm_dense.h"
 
@@ -184,6 +189,38 @@ __global__ void __launch_bounds__(256) dense_merge_kernel(DenseArgs a) {
     if (threadIdx.x == 0) a.out_n[q] = min(total, k);
 }
 
+
+// ------------------------------------------------------------ large k
+__global__ void dense_scores_kernel(DenseDev ix, const double* q64, uint64_t* skey, uint32_t* rows) {
+    const uint32_t row = blockIdx.x * blockDim.x + threadIdx.x;
+    if (row >= ix.n) return;
+    const float* r = ix.E + static_cast<uint64_t>(row) * ix.dim;
+    double acc = 0.0;
+    for (uint32_t j = 0; j < ix.dim; ++j) acc = __fma_rn(static_cast<double>(__ldg(r + j)), q64[j], acc);
+    // order-preserving map to u64, complemented: ascending key = descending score
+    const uint64_t b = static_cast<uint64_t>(__double_as_longlong(acc));
+    const uint64_t ord = (b >> 63) ? ~b : (b | 0x8000000000000000ull);
+    skey[row] = ~ord;
+    rows[row] = row;
+}
+
+__global__ void dense_gather_kernel(uint32_t n, const uint64_t* skey, const uint32_t* rows_by_id, uint64_t* key2) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) key2[i] = skey[rows_by_id[i]];
+}
+
+__global__ void dense_emit_kernel(DenseDev ix, uint32_t k, const uint32_t* rows, const uint64_t* key_sorted,
+                                  uint64_t* out_ids, double* out_scores, uint32_t* out_n) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < k) {
+        const uint64_t ord = ~key_sorted[i];
+        const uint64_t b = (ord >> 63) ? (ord & 0x7fffffffffffffffull) : ~ord;
+        out_ids[i] = ix.ids[rows[i]];
+        out_scores[i] = __longlong_as_double(static_cast<long long>(b));
+    }
+    if (i == 0) *out_n = k;
+}
+
 }  // namespace
 
 uint32_t dense_max_k() { return kDenseMaxK; }
@@ -209,6 +246,62 @@ cudaError_t launch_dense(const DenseDev& ix, const DenseArgs& a, cudaStream_t st
     dense_exact_kernel<<<grid, kDT, smem, st>>>(ix, a);
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
     dense_merge_kernel<<<a.nq, 256, 0, st>>>(a);
+    return cudaGetLastError();
+}
+
+}  // namespace hm
+
+namespace hm {
+
+size_t dense_large_k_bytes(uint32_t n) {
+    size_t a = 0, b = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, a, (const uint64_t*)nullptr, (uint64_t*)nullptr, (const uint32_t*)nullptr,
+                                    (uint32_t*)nullptr, static_cast<int>(n));
+    b = a;
+    const size_t el = static_cast<size_t>(n);
+    return b + el * (8 + 8 + 8 + 4 + 4 + 4) + 6 * 256;
+}
+
+cudaError_t launch_dense_large_k(const DenseDev& ix, const double* q64, uint32_t k, void* scratch, size_t bytes,
+                                 uint64_t* out_ids, double* out_scores, uint32_t* out_n, cudaStream_t st) {
+    const uint32_t n = ix.n;
+    auto carve = [&](size_t sz) {
+        void* p = scratch;
+        const size_t a = (sz + 255) & ~size_t(255);
+        scratch = static_cast<char*>(scratch) + a;
+        bytes -= a;
+        return p;
+    };
+    uint64_t* skey = static_cast<uint64_t*>(carve(8ull * n));
+    uint64_t* ids_sorted = static_cast<uint64_t*>(carve(8ull * n));
+    uint64_t* key2 = static_cast<uint64_t*>(carve(8ull * n));
+    uint32_t* rows = static_cast<uint32_t*>(carve(4ull * n));
+    uint32_t* rows_by_id = static_cast<uint32_t*>(carve(4ull * n));
+    uint32_t* rows_final = static_cast<uint32_t*>(carve(4ull * n));
+    uint64_t* key_final = skey;  // reused after the gather
+    size_t temp = bytes;
+    const unsigned blocks = (n + 255) / 256;
+    dense_scores_kernel<<<blocks, 256, 0, st>>>(ix, q64, skey, rows);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    e = cub::DeviceRadixSort::SortPairs(scratch, temp, ix.ids, ids_sorted, rows, rows_by_id, static_cast<int>(n), 0, 64,
+                                        st);
+    if (e != cudaSuccess) return e;
+    dense_gather_kernel<<<blocks, 256, 0, st>>>(n, skey, rows_by_id, key2);
+    temp = bytes;
+    e = cub::DeviceRadixSort::SortPairs(scratch, temp, key2, key_final, rows_by_id, rows_final, static_cast<int>(n), 0,
+                                        64, st);
+    if (e != cudaSuccess) return e;
+    dense_emit_kernel<<<(k + 255) / 256, 256, 0, st>>>(ix, k, rows_final, key_final, out_ids, out_scores, out_n);
+    return cudaGetLastError();
+}
+
+__global__ void dense_q64_one(const float* q, double* q64, uint32_t n) {
+    for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) q64[i] = static_cast<double>(q[i]);
+}
+
+cudaError_t launch_dense_widen(const float* q, double* q64, uint32_t n, cudaStream_t st) {
+    dense_q64_one<<<1, 256, 0, st>>>(q, q64, n);
     return cudaGetLastError();
 }
 

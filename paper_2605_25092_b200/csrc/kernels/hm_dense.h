@@ -31,5 +31,10 @@ struct DenseArgs {
 uint32_t dense_max_k();
 uint32_t dense_slabs(uint32_t nq, uint32_t n_rows, int sms);
 cudaError_t launch_dense(const DenseDev& ix, const DenseArgs& a, cudaStream_t st);
+// k > dense_max_k(): one query, every row scored, two stable radix sorts
+size_t dense_large_k_bytes(uint32_t n_rows);
+cudaError_t launch_dense_widen(const float* q, double* q64, uint32_t dim, cudaStream_t st);
+cudaError_t launch_dense_large_k(const DenseDev& ix, const double* q64, uint32_t k, void* scratch, size_t bytes,
+                                 uint64_t* out_ids, double* out_scores, uint32_t* out_n, cudaStream_t st);
 
 }  // namespace hm

@@ -12,7 +12,9 @@
 #include <vector>
 
 #include "hybrid/bridge.hpp"
+#include "hybrid/cascade.hpp"
 #include "hybrid/csr_index.hpp"
+#include "hybrid/dense.hpp"
 #include "hybrid/temporal_index.hpp"
 
 using namespace hybrid;
@@ -51,6 +53,10 @@ int main() {
     CsrIndex idx, bidx;
     TemporalIndex tidx;
     std::vector<std::pair<DocId, SparseVector>> bdocs;
+    EmbeddingMatrix emb;
+    std::uint32_t emb_dim = 0;
+    std::uint64_t emb_seed = 0;
+    std::vector<MemoryRecord> drecs;
     std::string line;
     while (std::getline(std::cin, line)) {
         std::istringstream in(line);
@@ -165,6 +171,50 @@ int main() {
             } else if (cmd == "BONBM25") {
                 bridge_topk(idx, SparseVector{{0}, {1.0}}, 5);
                 std::cout << "OK\n";
+            } else if (cmd == "EMBDOCS") {  // dim seed: hash_embed every DOCS text
+                in >> emb_dim >> emb_seed;
+                emb = EmbeddingMatrix{};
+                emb.dim = emb_dim;
+                drecs.clear();
+                for (const auto& [id, text] : docs) {
+                    emb.add(id, hash_embed(text, emb_dim, emb_seed));
+                    MemoryRecord r;
+                    r.id = id;
+                    r.ts_ms = static_cast<std::int64_t>(id) * 1000;
+                    drecs.push_back(r);
+                }
+                std::cout << "OK " << emb.count() << '\n';
+            } else if (cmd == "DQUERY") {  // k text...
+                std::size_t k;
+                in >> k;
+                std::string text, t;
+                while (in >> t) text += (text.empty() ? "" : " ") + t;
+                print_list(dense_topk(emb, hash_embed(text, emb_dim, emb_seed), k), " 0");
+            } else if (cmd == "DBADDIM") {
+                dense_topk(emb, std::vector<float>(emb_dim + 1, 0.0f), 3);
+                std::cout << "OK\n";
+            } else if (cmd == "CASCADE") {  // k tau query_ts terms...
+                std::size_t k;
+                double tau;
+                std::int64_t qts;
+                in >> k >> tau >> qts;
+                std::vector<std::string> q;
+                for (std::string t; in >> t;) q.push_back(t);
+                std::string text;
+                for (const auto& t : q) text += (text.empty() ? "" : " ") + t;
+                CascadeConfig cfg;
+                cfg.conf_threshold = tau;
+                RetrieveFn bm25_fn = [&](std::size_t kk) { return idx.bm25_topk_maxscore(q, kk, Bm25Params{}); };
+                RetrieveFn dense_fn = [&](std::size_t kk) {
+                    return dense_topk(emb, hash_embed(text, emb_dim, emb_seed), kk);
+                };
+                RecordLookup lookup = [&](DocId d) -> const MemoryRecord* {
+                    for (const auto& r : drecs)
+                        if (r.id == d) return &r;
+                    return nullptr;
+                };
+                auto d = cascade_retrieve(k, cfg, bm25_fn, dense_fn, lookup, qts, FusionParams{});
+                print_list(d.results, std::string(" ") + (d.escalated ? "1" : "0"));
             } else if (cmd == "KSTAR") {
                 double e, l;
                 in >> e >> l;

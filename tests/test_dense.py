@@ -102,8 +102,9 @@ def test_dense_gpu_large_random_and_errors(gpu):
         assert_dense(dev.search_batch(q, 10), want, f"random {n}x{dim}")
     with pytest.raises(ValueError, match="query dimension mismatch"):
         dev.search_batch(np.zeros((1, 32), np.float32), 5)
-    with pytest.raises(ValueError, match="supported maximum"):
-        dev.search_batch(q[:1], 257)
+    # k beyond the shared-memory lists: the sort path, same bits
+    want = ref.dense_topk_batch(m, ids, q[:3], 1000, workers=16)
+    assert_dense(dev.search_batch(q[:3], 1000), want, "large k")
 
 
 @pytest.mark.gpu

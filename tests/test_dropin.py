@@ -152,3 +152,46 @@ def test_bridge_dropin_matches_reference(gpu):
     d.send(["BDOCS 2", "3 1 1:0x1p+0", "3 1 2:0x1p+0"], expect=0)
     assert d.send(["BINGEST"])[0] == "THROW runtime_error duplicate doc id: 3"
     d.close()
+
+
+def test_dense_and_cascade_dropin_match_reference(gpu):
+    """hybrid::dense_topk through the drop-in (csrc/dropin/dense_b200.cpp; the
+    reference's dense.o keeps hash_embed with its dense_topk weakened), and
+    the reference's own cascade_retrieve driving both GPU channels."""
+    rng = np.random.default_rng(8)
+    docs, _ = random_instance(rng)
+    docs = [(i, "t%d t%d t%d z%d" % (i % 7, i % 11, i % 5, i)) for i in range(300)]
+    d = Driver()
+    d.send([f"DOCS {len(docs)}"] + [f"{i}\t{t}" for i, t in docs], expect=0)
+    assert d.send(["INDEX 0 1.2 0.75"])[0].startswith("OK")
+    assert d.send(["EMBDOCS 32 42"])[0] == "OK 300"
+    emb = np.stack([ref.hash_embed(t, 32, 42) for _, t in docs])
+    ids = np.array([i for i, _ in docs], np.uint64)
+    ri = ref.RefIndex.from_texts(docs, ref.TOK_MINIMAL)
+    recs = {i: (i * 1000, 0.0) for i, _ in docs}
+    n_esc = 0
+    for trial in range(40):
+        q = ["t%d" % int(rng.integers(0, 12)) for _ in range(1 + int(rng.integers(0, 3)))]
+        k = int(rng.choice([1, 3, 10, 400]))
+        text = " ".join(q)
+        got_ids, got_sc, _ = parse(d.send([f"DQUERY {k} {text}"])[0])
+        w = ref.dense_topk_batch(emb, ids, ref.hash_embed(text, 32, 42)[None, :], min(k, 300))
+        n = int(w["n"][0])
+        assert got_ids == w["ids"][0, :n].tolist() and bits(got_sc) == bits(w["scores"][0, :n])
+        # cascade_retrieve (cascade.cpp:44-101) with both channels on the GPU
+        tau = float(rng.choice([0.0, 0.1, 0.5, 1e300]))  # 1e300: always escalate (istream has no "inf")
+        kk = min(k, 50)
+        c_ids, c_sc, esc = parse(d.send([f"CASCADE {kk} {tau} 500000 {text}"])[0])
+        s_ids, s_sc, _ = ri.search(q, kk, maxscore=True)
+        sparse = list(zip(s_ids.tolist(), s_sc.tolist()))
+        if ref.confidence(s_sc) >= tau:
+            assert esc == 0 and c_ids == s_ids.tolist() and bits(c_sc) == bits(s_sc)
+        else:
+            n_esc += 1
+            dl = ref.dense_topk_batch(emb, ids, ref.hash_embed(text, 32, 42)[None, :], kk)
+            dense = list(zip(dl["ids"][0, :dl["n"][0]].tolist(), dl["scores"][0, :dl["n"][0]].tolist()))
+            want = ref.agent_rrf(sparse, dense, recs, 500000)[:kk]
+            assert esc == 1 and c_ids == [x for x, _ in want] and bits(c_sc) == bits([s for _, s in want])
+    assert n_esc > 5
+    assert d.send(["DBADDIM"])[0] == "THROW invalid_argument query dimension mismatch"
+    d.close()
