@@ -242,8 +242,10 @@ int hm_bridge_last_timing(float* ms_kernel);
  * vectors, row-major fp32, one DocId per row) held in HBM.  Scores are
  * sum_j double(r_j) * q_j in fp64, j ascending, every row ranked by
  * (score desc, DocId asc) -- bit-identical to hybrid::dense_topk
- * (src/dense.cpp:86-101).  k <= 256 runs the fused list kernel; larger k
- * scores every row and sorts on the device per query.  A query whose
+ * (src/dense.cpp:86-101).  When dim % 32 == 0 and k <= 32 the tensor cores
+ * (tcgen05, TF32) select candidates within a proven error bound and fp64
+ * rescoring ranks them; otherwise k <= 256 runs the fp64 list kernel and
+ * larger k scores every row and sorts on the device.  A query whose
  * dim differs from the matrix's fails with the reference's
  * "query dimension mismatch" (HM_ERR_INVALID).  Results as hm_results
  * (conf, skip, postings unused).  Replaces: hybrid::dense_topk per query. */
@@ -272,6 +274,13 @@ int hm_dense_search_batch_device(hm_dense* dense, const hm_dense_batch* batch_de
                                  hm_results* out_dev, void* stream);
 /* Device time (ms) of the last HM_FLAG_TIMING dense batch on this thread. */
 int hm_dense_last_timing(float* ms_kernels);
+/* Last dense batch on this thread: path (1 = tensor-core TF32 candidates +
+ * fp64 rescoring, the default when dim % 32 == 0 and k <= 32; 2 = fp64
+ * shared-memory lists, also forced by HM_FLAG_FORCE_EXACT; 3 = fp64 + device
+ * sort for k > 256) and, for HM_FLAG_TIMING tensor-core batches, queries
+ * whose candidate list overflowed (rescored over every row) and the total
+ * number of candidates. */
+int hm_dense_last_stats(uint32_t* path, uint32_t* n_overflow, uint64_t* n_candidates);
 
 /* Margin confidence over a ranked score list (src/cascade.cpp:10-21). */
 double hm_margin(const double* scores, uint32_t n, double epsilon_guard);

@@ -8,6 +8,10 @@
 #include <string>
 #include <vector>
 
+#include <cmath>
+
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 
 #include "hm_b200.h"
@@ -20,11 +24,44 @@ using hm_host::guard;
 namespace {
 
 thread_local float g_ms_dense = 0.f;
+thread_local uint32_t g_dense_overflow = 0;
+thread_local uint64_t g_dense_candidates = 0;
+thread_local uint32_t g_dense_path = 0;  // 1 tensor cores, 2 fp64 lists, 3 fp64 sort (large k)
+constexpr uint32_t kCandCap = 8192;  // tensor-core path: candidates per query (= rescoring capacity)
+
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q{};
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+    });
+    if (!fn) throw std::runtime_error("cuTensorMapEncodeTiled is unavailable");
+    return fn;
+}
+
+// fp32 [rows x dim] row-major as a 2-D TMA map: 32-element (128 B) K boxes,
+// box_rows rows, 128-byte swizzle (the UMMA K-major SW128 layout)
+void encode_map(CUtensorMap* m, const float* ptr, uint32_t rows, uint32_t dim, uint32_t box_rows) {
+    const cuuint64_t gdim[2] = {dim, rows};
+    const cuuint64_t gstride[1] = {static_cast<cuuint64_t>(dim) * 4};
+    const cuuint32_t box[2] = {32, box_rows};
+    const cuuint32_t es[2] = {1, 1};
+    const CUresult r = encode_fn()(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(ptr), gdim, gstride, box,
+                                   es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) throw std::runtime_error("cuTensorMapEncodeTiled failed: " + std::to_string(r));
+}
 
 struct DenseWs {
     cudaStream_t st = nullptr;
     cudaEvent_t ev[2] = {nullptr, nullptr};
-    uint64_t q_cap = 0, part_cap = 0, lists_cap = 0, out_cap = 0, nq_cap = 0, big_cap = 0;
+    uint64_t q_cap = 0, part_cap = 0, lists_cap = 0, out_cap = 0, nq_cap = 0, big_cap = 0, cand_cap = 0;
+    uint32_t *cand_n = nullptr, *cand_rows = nullptr;
+    int* thr_key = nullptr;
     void* big = nullptr;  // large-k scratch (scores, sort keys, CUB temp)
     float* q_in = nullptr;
     double *q64 = nullptr, *part_scores = nullptr, *out_scores = nullptr;
@@ -37,7 +74,8 @@ struct DenseWs {
         ck(cudaEventCreate(&ev[1]), "event");
     }
     ~DenseWs() {
-        void* ps[] = {q_in, q64, part_scores, out_scores, part_ids, out_ids, part_n, out_n, big};
+        void* ps[] = {q_in, q64, part_scores, out_scores, part_ids, out_ids, part_n, out_n, big, cand_n, cand_rows,
+                      thr_key};
         for (void* p : ps)
             if (p) cudaFree(p);
         cudaEventDestroy(ev[0]);
@@ -82,6 +120,9 @@ struct DenseWs {
 struct hm_dense {
     int device = 0, sms = 0;
     hm::DenseDev dev{};
+    bool tc = false;            // dim % 32 == 0: the tensor-core candidate path applies
+    alignas(64) CUtensorMap map_e{};
+    float err_scale = 0.f;      // TF32 selection bound per unit ||q|| (dense_tc.cu)
     std::vector<void*> allocs;
     std::mutex mu;
     std::vector<DenseWs*> pool;
@@ -127,9 +168,49 @@ void check_batch(const hm_dense* X, const hm_dense_batch* b) {
 // one batch on the workspace's device buffers (queries already in w->q_in
 // or at q_dev); results into w->out_* or the caller's device buffers
 void run(hm_dense* X, DenseWs* w, uint32_t nq, uint32_t k, const float* q_dev, uint64_t* out_ids, double* out_scores,
-         uint32_t* out_n, cudaStream_t st, bool timing) {
+         uint32_t* out_n, cudaStream_t st, bool timing, uint32_t flags) {
     if (timing) ck(cudaEventRecord(w->ev[0], st), "event");
-    if (k > hm::dense_max_k()) {
+    if (X->tc && k <= hm::dense_tc_max_k() && !(flags & HM_FLAG_FORCE_EXACT)) {
+        // tensor cores select candidates (TF32), fp64 rescoring decides
+        if (static_cast<uint64_t>(nq) > w->cand_cap) {
+            DenseWs::grow(w->cand_n, nq);
+            DenseWs::grow(w->cand_rows, static_cast<uint64_t>(nq) * kCandCap);
+            DenseWs::grow(w->thr_key, nq);
+            w->cand_cap = nq;
+        }
+        alignas(64) CUtensorMap map_q{};
+        encode_map(&map_q, q_dev, nq, X->dev.dim, 128);
+        ck(cudaMemsetAsync(w->cand_n, 0, nq * 4ull, st), "memset candidates");
+        ck(cudaMemsetAsync(w->thr_key, 0x80, nq * 4ull, st), "memset bounds");
+        hm::DenseTcArgs a{};
+        a.nq = nq;
+        a.dim = X->dev.dim;
+        a.n_rows = X->dev.n;
+        a.k = k;
+        a.n_slabs = hm::dense_tc_slabs(nq, X->dev.n, X->sms);
+        a.q = q_dev;
+        a.err_scale = X->err_scale;
+        a.cand_n = w->cand_n;
+        a.thr_key = w->thr_key;
+        a.cand_rows = w->cand_rows;
+        a.cand_cap = kCandCap;
+        a.out_ids = out_ids;
+        a.out_scores = out_scores;
+        a.out_n = out_n;
+        ck(hm::launch_dense_tc(X->dev, &map_q, &X->map_e, a, X->sms, st), "dense tensor-core kernels");
+        g_dense_path = 1;
+        if (timing) {  // candidate statistics (test / bench evidence of the selection's tightness)
+            std::vector<uint32_t> cn(nq);
+            ck(cudaMemcpyAsync(cn.data(), w->cand_n, nq * 4ull, cudaMemcpyDeviceToHost, st), "D2H candidates");
+            ck(cudaStreamSynchronize(st), "sync");
+            g_dense_overflow = 0;
+            g_dense_candidates = 0;
+            for (uint32_t c : cn) {
+                g_dense_candidates += c;
+                g_dense_overflow += c > kCandCap;
+            }
+        }
+    } else if (k > hm::dense_max_k()) {
         // k beyond the shared-memory lists: per query, every row scored and
         // sorted on the device (rare: the reference callers use k = 10)
         const uint32_t kk = std::min<uint32_t>(k, X->dev.n);
@@ -148,6 +229,7 @@ void run(hm_dense* X, DenseWs* w, uint32_t nq, uint32_t k, const float* q_dev, u
                                         out_scores + static_cast<uint64_t>(q) * k, out_n + q, st),
                "dense large-k");
         }
+        g_dense_path = 3;
     } else {
         hm::DenseArgs a{};
         a.nq = nq;
@@ -164,6 +246,7 @@ void run(hm_dense* X, DenseWs* w, uint32_t nq, uint32_t k, const float* q_dev, u
         a.out_scores = out_scores;
         a.out_n = out_n;
         ck(hm::launch_dense(X->dev, a, st), "dense kernels");
+        g_dense_path = 2;
     }
     if (timing) ck(cudaEventRecord(w->ev[1], st), "event");
 }
@@ -188,6 +271,20 @@ int hm_dense_create(const hm_dense_view* view, int device, hm_dense** out) {
             X->dev.ids = upload(X, view->doc_ids, view->count);
             X->dev.n = view->count;
             X->dev.dim = view->dim;
+            if (view->dim % 32 == 0 && view->count > 0) {
+                // selection bound: 1.25 (2^-9 + 2^-20 + dim 2^-22) max_r ||r|| (dense_tc.cu)
+                double mx = 0.0;
+                for (uint64_t r = 0; r < view->count; ++r) {
+                    double s2 = 0.0;
+                    const float* row = view->data + r * view->dim;
+                    for (uint32_t j = 0; j < view->dim; ++j) s2 += static_cast<double>(row[j]) * row[j];
+                    mx = std::max(mx, s2);
+                }
+                const double c = 1.25 * (std::ldexp(1.0, -9) + std::ldexp(1.0, -20) + view->dim * std::ldexp(1.0, -22));
+                X->err_scale = static_cast<float>(c * std::sqrt(mx) * 1.0001);
+                encode_map(&X->map_e, X->dev.E, view->count, view->dim, 256);
+                X->tc = std::isfinite(X->err_scale);
+            }
         } catch (...) {
             delete X;
             throw;
@@ -220,7 +317,7 @@ int hm_dense_search_batch(hm_dense* X, const hm_dense_batch* b, hm_results* out)
             cudaStream_t st = w->st;
             ck(cudaMemcpyAsync(w->q_in, b->queries, q_el * 4, cudaMemcpyHostToDevice, st), "H2D queries");
             const bool timing = (b->flags & HM_FLAG_TIMING) != 0;
-            run(X, w, nq, b->k, w->q_in, w->out_ids, w->out_scores, w->out_n, st, timing);
+            run(X, w, nq, b->k, w->q_in, w->out_ids, w->out_scores, w->out_n, st, timing, b->flags);
             ck(cudaMemcpyAsync(out->ids, w->out_ids, static_cast<uint64_t>(nq) * b->k * 8, cudaMemcpyDeviceToHost, st),
                "D2H ids");
             ck(cudaMemcpyAsync(out->scores, w->out_scores, static_cast<uint64_t>(nq) * b->k * 8,
@@ -250,7 +347,7 @@ int hm_dense_search_batch_device(hm_dense* X, const hm_dense_batch* b, hm_result
             w->ensure(static_cast<uint64_t>(nq) * X->dev.dim, 0, 0, 0, 0);
             cudaStream_t st = static_cast<cudaStream_t>(stream);
             const bool timing = (b->flags & HM_FLAG_TIMING) != 0;
-            run(X, w, nq, b->k, b->queries, out->ids, out->scores, out->n, st, timing);
+            run(X, w, nq, b->k, b->queries, out->ids, out->scores, out->n, st, timing, b->flags);
             ck(cudaStreamSynchronize(st), "dense sync");  // the workspace is reusable afterwards
             if (timing) ck(cudaEventElapsedTime(&g_ms_dense, w->ev[0], w->ev[1]), "elapsed");
         } catch (...) {
@@ -263,6 +360,13 @@ int hm_dense_search_batch_device(hm_dense* X, const hm_dense_batch* b, hm_result
 
 int hm_dense_last_timing(float* ms) {
     if (ms) *ms = g_ms_dense;
+    return HM_OK;
+}
+
+int hm_dense_last_stats(uint32_t* path, uint32_t* n_overflow, uint64_t* n_candidates) {
+    if (path) *path = g_dense_path;
+    if (n_overflow) *n_overflow = g_dense_overflow;
+    if (n_candidates) *n_candidates = g_dense_candidates;
     return HM_OK;
 }
 

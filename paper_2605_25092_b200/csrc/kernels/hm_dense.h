@@ -28,6 +28,25 @@ struct DenseArgs {
     uint32_t* out_n;       // [nq]
 };
 
+// tensor-core candidate path (kernels/dense_tc.cu)
+struct DenseTcArgs {
+    uint32_t nq, dim, n_rows, k, n_slabs;
+    const float* q;          // [nq x dim] fp32 queries (device)
+    float err_scale;         // 1.25 (2^-9 + 2^-20 + dim 2^-22) max_r ||r||
+    uint32_t* cand_n;        // [nq] (zeroed before the launch)
+    int* thr_key;            // [nq] shared selection bound, order-preserving int (0x80808080 = -huge)
+    uint32_t* cand_rows;     // [nq x cand_cap]
+    uint32_t cand_cap;
+    uint64_t* out_ids;       // [nq * k]
+    double* out_scores;
+    uint32_t* out_n;
+};
+uint32_t dense_tc_max_k();
+uint32_t dense_tc_slabs(uint32_t nq, uint32_t n_rows, int sms);
+// map_q / map_e: CUtensorMap (fp32, K-major, 32 x {128, 256} boxes, 128B swizzle)
+cudaError_t launch_dense_tc(const DenseDev& ix, const void* map_q, const void* map_e, const DenseTcArgs& a, int sms,
+                            cudaStream_t st);
+
 uint32_t dense_max_k();
 uint32_t dense_slabs(uint32_t nq, uint32_t n_rows, int sms);
 cudaError_t launch_dense(const DenseDev& ix, const DenseArgs& a, cudaStream_t st);

@@ -80,7 +80,7 @@ class DenseBatch(C.Structure):
 
 
 EXPORTS = ["hm_dense_create", "hm_dense_destroy", "hm_dense_search_batch", "hm_dense_search_batch_device",
-           "hm_dense_last_timing",
+           "hm_dense_last_timing", "hm_dense_last_stats",
            "hm_bridge_create", "hm_bridge_destroy", "hm_bridge_search_batch",
            "hm_bridge_search_batch_device", "hm_bridge_last_timing",
            "hm_index_create", "hm_index_destroy", "hm_index_device_bytes", "hm_index_format",
@@ -135,6 +135,7 @@ def lib():
     L.hm_dense_search_batch.argtypes = [C.c_void_p, P(DenseBatch), P(Results)]
     L.hm_dense_search_batch_device.argtypes = [C.c_void_p, P(DenseBatch), P(Results), C.c_void_p]
     L.hm_dense_last_timing.argtypes = [P(C.c_float)]
+    L.hm_dense_last_stats.argtypes = [P(C.c_uint32), P(C.c_uint32), P(C.c_uint64)]
     L.hm_bridge_create.argtypes = [P(BridgeView), C.c_int, P(C.c_void_p)]
     L.hm_bridge_destroy.argtypes = [C.c_void_p]
     L.hm_bridge_search_batch.argtypes = [C.c_void_p, P(BridgeBatch), P(Results)]
@@ -836,6 +837,14 @@ class DenseIndex:
             t = C.c_float()
             lib().hm_dense_last_timing(C.byref(t))
             return t.value
+
+    @staticmethod
+    def last_stats():
+        """(path, n_overflow, n_candidates) of this thread's last dense batch
+        (hm_dense_last_stats; candidates only for HM_FLAG_TIMING batches)."""
+        p, o, c = C.c_uint32(), C.c_uint32(), C.c_uint64()
+        lib().hm_dense_last_stats(C.byref(p), C.byref(o), C.byref(c))
+        return p.value, o.value, c.value
 
     def dense_topk(self, query_vec, k):
         """hybrid::dense_topk: -> [(DocId, score)] over every row (ties by DocId)."""

@@ -89,6 +89,40 @@ def test_dense_gpu_bit_identical_on_tied_hash_embeddings(gpu):
 
 
 @pytest.mark.gpu
+def test_dense_tensor_core_path_selects_exactly(gpu):
+    """The tcgen05 TF32 candidate path (dim % 32 == 0, k <= 32) against the
+    reference and against the fp64 path, with the candidate statistics:
+    the selection must be tight (few candidates, no overflow) on random data
+    and must still be exact on heavily tied hash embeddings."""
+    rng = np.random.default_rng(12)
+    for n, dim, nq in ((100_000, 64, 300), (30_001, 128, 77), (5_000, 32, 129), (300, 64, 5)):
+        m = unit_rows(rng, n, dim)
+        ids = rng.permutation(n).astype(np.uint64) * 3
+        dev = search.DenseIndex(m, ids)
+        q = unit_rows(rng, nq, dim)
+        for k in (1, 10, 32):
+            want = ref.dense_topk_batch(m, ids, q, min(k, n), workers=16)
+            got = dev.search_batch(q, min(k, n), flags=search.HM_FLAG_TIMING)
+            path, overflow, cands = search.DenseIndex.last_stats()
+            assert path == 1, path
+            assert_dense(got, want, f"tc {n}x{dim} k={k}")
+            # each row slab starts its own bound: at most ~k per slab plus the band
+            assert overflow == 0 and cands < nq * (160 * k + 512), (overflow, cands)
+            exact = dev.search_batch(q, min(k, n), flags=search.HM_FLAG_FORCE_EXACT)
+            assert search.DenseIndex.last_stats()[0] == 2
+            assert_dense(exact, want, f"fp64 {n}x{dim} k={k}")
+    # ties: duplicate-heavy hash embeddings (overflowing lists fall back to a full rescoring)
+    m = np.concatenate([hash_matrix(2000, 32, 3, "w%d")] * 6)
+    m[1000:11000] = m[7]
+    ids = np.arange(len(m), dtype=np.uint64)
+    dev = search.DenseIndex(m, ids)
+    q = np.stack([m[7], m[8], ref.hash_embed("w7 w8", 32, 3)])
+    want = ref.dense_topk_batch(m, ids, q, 10)
+    assert_dense(dev.search_batch(q, 10, flags=search.HM_FLAG_TIMING), want, "tc ties")
+    assert search.DenseIndex.last_stats()[1] >= 1  # 10,001 exact ties overflow the candidate list
+
+
+@pytest.mark.gpu
 def test_dense_gpu_large_random_and_errors(gpu):
     rng = np.random.default_rng(4)
     for n, dim in ((200_003, 64), (50_000, 384)):
