@@ -91,6 +91,9 @@ __global__ void __launch_bounds__(kDT) dense_exact_kernel(DenseDev ix, DenseArgs
     }
     __syncthreads();
     const double* qb = a.q64 + static_cast<uint64_t>(q0) * dim;
+    uint32_t qu[kQT];  // the tile's query rows (a short last tile repeats its last query)
+#pragma unroll
+    for (int u = 0; u < kQT; ++u) qu[u] = static_cast<uint32_t>(u) < nqt ? u : nqt - 1;
     for (uint32_t t0 = r_lo; t0 < r_hi; t0 += kDT) {
         const uint32_t row = t0 + tid;
         double acc[kQT];
@@ -109,7 +112,7 @@ __global__ void __launch_bounds__(kDT) dense_exact_kernel(DenseDev ix, DenseArgs
                         const uint32_t j = 4 * j4 + h;
 #pragma unroll
                         for (int u = 0; u < kQT; ++u)
-                            acc[u] = __fma_rn(rd, __ldg(qb + static_cast<uint64_t>(u) * dim + j), acc[u]);
+                            acc[u] = __fma_rn(rd, __ldg(qb + static_cast<uint64_t>(qu[u]) * dim + j), acc[u]);
                     }
                 }
             } else {
@@ -117,7 +120,7 @@ __global__ void __launch_bounds__(kDT) dense_exact_kernel(DenseDev ix, DenseArgs
                     const double rd = static_cast<double>(__ldg(r + j));
 #pragma unroll
                     for (int u = 0; u < kQT; ++u)
-                        acc[u] = __fma_rn(rd, __ldg(qb + static_cast<uint64_t>(u) * dim + j), acc[u]);
+                        acc[u] = __fma_rn(rd, __ldg(qb + static_cast<uint64_t>(qu[u]) * dim + j), acc[u]);
                 }
             }
         }
