@@ -606,7 +606,7 @@ void run_batch(hm_index* X, Workspace* w, const hm_query_batch& hb, const uint32
     if (seeded) {
         a.fb_list = w->fb_list;
         ck(cudaMemsetAsync(w->fb_list, 0, nq * sizeof(uint32_t), st), "memset hand-over flags");
-        ck(hm::launch_search_seed(X->dev, a, X->grid_search, st), "seeded search kernel");
+        ck(hm::launch_search_seed(X->dev, a, 2 * X->grid_search, st), "seeded search kernel");
     }
     if (timing) ck(cudaEventRecord(w->ev[4], st), "event");
     ck(hm::launch_search(X->dev, a, X->grid_search, st), "search kernel");

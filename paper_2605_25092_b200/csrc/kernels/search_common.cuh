@@ -23,9 +23,12 @@ struct FastCfg {
     static constexpr int kStages = 2;  // staged steps (1 applied + kStages - 1 in flight)
 };
 
-template <int CAPW>
-struct __align__(16) FastSmem {
-    float acc[kTile];                      // first member: bk offsets are byte offsets into it
+// Shared-memory layout.  ACC floats of accumulators (the tile sweep: kTile;
+// the seeded pass only needs the epilogue's gather/survivor scratch) and,
+// when STG, the sweep's cp.async staging.
+template <int CAPW, int ACC, int STG>
+struct __align__(16) SmemT {
+    float acc[ACC];                        // first member: bk offsets are byte offsets into it
     float w32s[kShortCodes];               // impacts of the short-term codes
     uint32_t cl_row[kConsWarps][CAPW];     // per-warp candidate lists
     float cl_val[kConsWarps][CAPW];
@@ -34,7 +37,7 @@ struct __align__(16) FastSmem {
     uint32_t t_mult[kFastTerms];
     float t_c32[kFastTerms];
     int32_t t_slot[kFastTerms];
-    uint4 stg[kConsWarps][FastCfg<CAPW>::kStages][FastCfg<CAPW>::kC * 32];  // per-warp cp.async staging of baked postings
+    uint4 stg[kConsWarps][STG ? FastCfg<CAPW>::kStages : 1][STG ? FastCfg<CAPW>::kC * 32 : 1];  // per-warp cp.async staging of baked postings
     uint64_t t_bkb[kFastTerms];            // long terms: start of the term's baked ranges in bk
     uint4 rdesc[kConsWarps][kFastTerms];  // per warp: the unit's nonempty long-term ranges in this tile
                                           // {bk address lo, hi, chunks, c bits}, df descending
@@ -54,6 +57,12 @@ struct __align__(16) FastSmem {
     float ubne_q;                          // sum of the non-essential terms' bounds
 };
 
+template <int CAPW>
+using FastSmem = SmemT<CAPW, kTile, 1>;
+// the seeded pass: epilogue scratch only (gather lists 8 B x 8 warps x CAPW >= survivors)
+template <int CAPW>
+using SeedSmem = SmemT<CAPW, 16 * CAPW, 0>;
+
 struct SurvView {
     double* E;
     uint64_t* id;
@@ -72,8 +81,8 @@ __device__ __forceinline__ float esc_w(const DevIndex& ix, uint64_t gidx, uint32
 // binary search over the float bit pattern, values are >= 0), keep the
 // admissible entries (>= max(Lw, Lg) * slack, stable compaction), publish the
 // bound to the CTA-wide Lg.  Warp-synchronous; returns the new list length.
-template <int CAPW>
-__device__ uint32_t warp_prune(FastSmem<CAPW>& S, int w, uint32_t n, uint32_t k, float& Lw, float slack) {
+template <int CAPW, int ACC, int STG>
+__device__ uint32_t warp_prune(SmemT<CAPW, ACC, STG>& S, int w, uint32_t n, uint32_t k, float& Lw, float slack) {
     const int lane = threadIdx.x & 31;
     uint32_t* rows = S.cl_row[w];
     float* vals = S.cl_val[w];
@@ -226,8 +235,8 @@ __device__ __forceinline__ void step_apply(float* __restrict__ acc, uint32_t wba
 // Margin confidence + skip (src/cascade.cpp:15-21, 79-84).  A near-tie flood
 // (> kSurvCap survivors) hands the query to the exact kernel.  Leaves the
 // accumulator area zero.
-template <int CAPW>
-__device__ __forceinline__ void finish_query(const DevIndex& ix, const BatchArgs& a, FastSmem<CAPW>& S, uint32_t q,
+template <int CAPW, int ACC, int STG>
+__device__ __forceinline__ void finish_query(const DevIndex& ix, const BatchArgs& a, SmemT<CAPW, ACC, STG>& S, uint32_t q,
                                              uint32_t m, uint32_t k, uint32_t nw, float f_slack, double k1,
                                              double bb) {
     constexpr int kGatherBytes = 8 * kConsWarps * CAPW;

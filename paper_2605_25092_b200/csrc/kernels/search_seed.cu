@@ -44,7 +44,7 @@ template <int CAPW>
 struct SeedCtx {
     const DevIndex& ix;
     const BatchArgs& a;
-    FastSmem<CAPW>& S;
+    SeedSmem<CAPW>& S;
     const uint32_t* stab;
     uint32_t stride, j0, cb;
     double k1, b;
@@ -235,8 +235,12 @@ __device__ __forceinline__ void hand_over(const BatchArgs& a, uint32_t q) {
 }
 
 template <int CAPW>
-__global__ void __launch_bounds__(kCons, 2) search_seed_kernel(DevIndex ix, BatchArgs a) {
-    using Smem = FastSmem<CAPW>;
+#ifndef HM_SEED_MINB
+#define HM_SEED_MINB 2
+#endif
+__global__ void __launch_bounds__(kCons, HM_SEED_MINB) search_seed_kernel(DevIndex ix, BatchArgs a) {
+    using Smem = SeedSmem<CAPW>;
+    static_assert(16 * CAPW * 4 >= kSurvBytes, "epilogue scratch fits");
     extern __shared__ __align__(16) unsigned char smem_raw[];
     Smem& S = *reinterpret_cast<Smem*>(smem_raw);
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -248,7 +252,7 @@ __global__ void __launch_bounds__(kCons, 2) search_seed_kernel(DevIndex ix, Batc
     float* sA = reinterpret_cast<float*>(a.seed_scratch + static_cast<uint64_t>(blockIdx.x) * kSeedScratch);  // seed scores
     const uint32_t kmax = FastCfg<CAPW>::kMaxKServed;
 
-    for (int i = tid; i < kTile; i += kCons) S.acc[i] = 0.f;
+    for (int i = tid; i < 16 * CAPW; i += kCons) S.acc[i] = 0.f;
     for (int i = tid; i < kShortCodes; i += kCons) S.w32s[i] = a.w32[i];
     if (tid < kConsWarps) S.n_w[tid] = 0;
     if (tid == 0) S.Lg = 0u;
@@ -587,22 +591,31 @@ static cudaError_t seed_attr() {
     static bool done = false;
     if (done) return cudaSuccess;
     const cudaError_t e = cudaFuncSetAttribute(search_seed_kernel<CAPW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                               static_cast<int>(sizeof(FastSmem<CAPW>)));
+                                               static_cast<int>(sizeof(SeedSmem<CAPW>)));
     if (e == cudaSuccess) done = true;
     return e;
 }
 
-cudaError_t launch_search_seed(const DevIndex& ix, const BatchArgs& a, int sms, cudaStream_t st) {
-    if (a.k <= FastCfg<192>::kMaxKServed) {
-        const cudaError_t e = seed_attr<192>();
-        if (e != cudaSuccess) return e;
-        search_seed_kernel<192><<<2 * sms, kCons, sizeof(FastSmem<192>), st>>>(ix, a);
-    } else {
-        const cudaError_t e = seed_attr<320>();
-        if (e != cudaSuccess) return e;
-        search_seed_kernel<320><<<2 * sms, kCons, sizeof(FastSmem<320>), st>>>(ix, a);
-    }
+// `cap`: CTAs the per-CTA scratch (a.seed_scratch, a.stab) was sized for.
+// The pass is latency-bound (dependent probe chains): as many resident CTAs
+// as registers allow, one wave.
+template <int CAPW>
+static cudaError_t launch_seed_w(const DevIndex& ix, const BatchArgs& a, int cap, cudaStream_t st) {
+    cudaError_t e = seed_attr<CAPW>();
+    if (e != cudaSuccess) return e;
+    int dev = 0, sms = 0, per_sm = 0;
+    if ((e = cudaGetDevice(&dev)) != cudaSuccess) return e;
+    if ((e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev)) != cudaSuccess) return e;
+    if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, search_seed_kernel<CAPW>, kCons,
+                                                             sizeof(SeedSmem<CAPW>))) != cudaSuccess)
+        return e;
+    const int grid = per_sm * sms < cap ? per_sm * sms : cap;
+    search_seed_kernel<CAPW><<<grid, kCons, sizeof(SeedSmem<CAPW>), st>>>(ix, a);
     return cudaGetLastError();
+}
+
+cudaError_t launch_search_seed(const DevIndex& ix, const BatchArgs& a, int cap, cudaStream_t st) {
+    return a.k <= FastCfg<192>::kMaxKServed ? launch_seed_w<192>(ix, a, cap, st) : launch_seed_w<320>(ix, a, cap, st);
 }
 
 }  // namespace hm
