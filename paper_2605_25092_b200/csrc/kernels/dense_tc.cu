@@ -24,7 +24,8 @@
 //            256-row B tile (fp32, 128B-swizzled K-major) into a 4-stage ring
 //   warp 1   TMEM owner + MMA issuer: 4 x tcgen05.mma.kind::tf32 (M128 N256
 //            K8) per chunk into one of two 256-column TMEM accumulators
-//   warps 2-5  epilogue: tcgen05.ld 32x32b.x32, filter, candidate emission
+//   warps 2-9  epilogue (two per TMEM lane quarter, each on half of the 256
+//            columns): tcgen05.ld 32x32b.x32, filter, candidate emission
 #include <cstdint>
 
 #include <cuda.h>
@@ -39,7 +40,9 @@ constexpr int kTcM = 128, kTcN = 256, kTcKc = 32;  // tile rows, tile columns, K
 constexpr int kTcStages = 4;
 constexpr uint32_t kABytes = kTcM * 128;  // 16 KB: 128 rows x 128 B
 constexpr uint32_t kBBytes = kTcN * 128;  // 32 KB
-constexpr int kTcThreads = 192;
+constexpr int kEpiWarps = 8;  // two warps per TMEM lane quarter, each on half the columns
+constexpr int kTcThreads = 64 + 32 * kEpiWarps;
+constexpr int kEpiCols = kTcN * 4 / kEpiWarps;  // accumulator columns per epilogue warp
 constexpr uint32_t kTmemCols = 2 * kTcN;  // double-buffered accumulator
 
 struct __align__(1024) TcSmem {
@@ -135,7 +138,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         }
         for (int s = 0; s < 2; ++s) {
             mbar_init(&S.tfull[s], 1);
-            mbar_init(&S.tempty[s], 4 * 32);
+            mbar_init(&S.tempty[s], kEpiWarps * 32);
         }
         mbar_init_fence();
     }
@@ -209,6 +212,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         // ================= epilogue: one query row per thread
         const uint32_t quarter = static_cast<uint32_t>(warp & 3);  // TMEM lanes 32*quarter .. +31
         const uint32_t row = quarter * 32 + lane;
+        const uint32_t col0 = static_cast<uint32_t>((warp - 2) / 4) * kEpiCols;  // my half of the columns
         uint32_t acc = 0, aphase = 0;
         for (uint32_t it = blockIdx.x; it < n_items; it += gridDim.x) {
             const uint32_t qt = it % n_qt, slab = it / n_qt;
@@ -230,19 +234,19 @@ __global__ void __launch_bounds__(kTcThreads, 1)
             for (uint32_t t = t0; t < t1; ++t) {
                 mbar_wait(&S.tfull[acc], aphase);
                 tc_fence_after();
-                const uint32_t taddr = tmem + ((quarter * 32) << 16) + acc * kTcN;
+                const uint32_t taddr = tmem + ((quarter * 32) << 16) + acc * kTcN + col0;
                 // pass 1: each 32-column chunk's maximum (FMNMX3 tree); only a
                 // chunk that beats the running KT-th value is walked to update
                 // the running best KT (and so the bound) -- rare after the
                 // first tiles, so a tile costs ~25 instructions per chunk
-                const bool tail = (t + 1) * kTcN > a.n_rows;
-                float cmax[kTcN / 32];
+                const bool tail = t * kTcN + col0 + kEpiCols > a.n_rows;
+                float cmax[kEpiCols / 32];
 #pragma unroll 1
-                for (uint32_t c = 0; c < static_cast<uint32_t>(kTcN / 32); ++c) {
+                for (uint32_t c = 0; c < static_cast<uint32_t>(kEpiCols / 32); ++c) {
                     uint32_t v[32];
                     tmem_ld32(taddr + 32 * c, v);
                     if (tail) {
-                        const uint32_t base = t * kTcN + 32 * c;
+                        const uint32_t base = t * kTcN + col0 + 32 * c;
 #pragma unroll
                         for (int i = 0; i < 32; ++i)
                             if (base + i >= a.n_rows) v[i] = 0xff800000u;  // -inf: past the last row
@@ -285,11 +289,11 @@ __global__ void __launch_bounds__(kTcThreads, 1)
                 }
                 // pass 2: candidates, from the chunks whose maximum reaches the bound
 #pragma unroll 1
-                for (uint32_t c = 0; c < static_cast<uint32_t>(kTcN / 32); ++c) {
+                for (uint32_t c = 0; c < static_cast<uint32_t>(kEpiCols / 32); ++c) {
                     if (!__any_sync(0xffffffffu, valid && cmax[c] >= thr)) continue;
                     uint32_t v[32];
                     tmem_ld32(taddr + 32 * c, v);
-                    const uint32_t base = t * kTcN + 32 * c;
+                    const uint32_t base = t * kTcN + col0 + 32 * c;
                     if (valid && cmax[c] >= thr) {
 #pragma unroll
                         for (int i = 0; i < 32; ++i) {
