@@ -106,7 +106,10 @@ struct DevIndex {
 };
 constexpr uint16_t kDenseAbsent = 0xFFFF;
 constexpr uint16_t kDenseEscape = 0xFFFE;
-constexpr uint32_t kSeedScratch = 2 * 57344;  // words per CTA (search_seed.cu: kSeedMaxDf scores + rows)
+#ifndef HM_SEED_SCRATCH
+#define HM_SEED_SCRATCH (2 * 131072)
+#endif
+constexpr uint32_t kSeedScratch = HM_SEED_SCRATCH;  // words per CTA (search_seed.cu: kSeedMaxDf scores + rows)
 constexpr int kMaxDense = 128;             // dense arrays: long terms with df >= n_docs / 32, largest first
 constexpr int kDenseMinDiv = 32;
 
