@@ -34,8 +34,14 @@
 
 namespace hm {
 
-constexpr uint64_t kProbeCost = 32;  // seeds: a probe (short dependent-load chain) ~ 32 streamed postings
-constexpr uint64_t kEMax = 65536;    // essential (non-seed) postings served here (best measured on C2)
+#ifndef HM_SEED_PCOST
+#define HM_SEED_PCOST 32
+#endif
+constexpr uint64_t kProbeCost = HM_SEED_PCOST;  // seeds: a probe (short dependent-load chain) ~ 32 streamed postings
+#ifndef HM_SEED_EMAX
+#define HM_SEED_EMAX 131072
+#endif
+constexpr uint64_t kEMax = HM_SEED_EMAX;    // essential (non-seed) postings served here (best measured on C2)
 constexpr uint32_t kSeedMaxTerms = 16;  // longer plans go straight to the exhaustive kernel
 constexpr uint64_t kSeedMaxDf = kSeedScratch / 2;  // seed term: the strongest bound among terms with fewer postings
 constexpr uint64_t kSeedMinPostings = 65536;  // cheaper queries too (e.g. a recency window)
