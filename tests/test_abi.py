@@ -53,6 +53,24 @@ def test_no_cpu_fallback_without_gpu():
     hx = synth.HostIndex(synth.Corpus(n_records=100))
     with pytest.raises(RuntimeError, match="no CUDA device"):
         search.DeviceIndex.from_host(hx)
+    # the bridge and dense channels fail the same way (no CPU scoring path)
+    bi = search.bridge_ingest([(1, search.SparseVector([0, 3], [0.5, 1.0]))])
+    with pytest.raises(RuntimeError, match="no CUDA device"):
+        bi.bridge_topk(search.SparseVector([0], [1.0]), 5)
+    with pytest.raises(RuntimeError, match="no CUDA device"):
+        search.DenseIndex(np.ones((4, 8), np.float32), np.arange(4, dtype=np.uint64))
+
+
+def test_bridge_and_dense_argument_errors_before_any_device_work():
+    """Malformed inputs are rejected with the reference's messages by the host
+    side of the ABI (SparseVector::validate, bridge.cpp:10-20; EmbeddingMatrix
+    shape checks, dense.cpp:44-52) -- no GPU needed to see them."""
+    with pytest.raises(ValueError, match="strictly increasing"):
+        search.SparseVector([2, 2], [1.0, 1.0]).validate()
+    with pytest.raises(ValueError, match="must be > 0"):
+        search.bridge_ingest([(1, search.SparseVector([0], [0.0]))])
+    with pytest.raises(ValueError, match="embedding dimension mismatch"):
+        search.DenseIndex(np.ones((4, 8), np.float32), np.arange(3, dtype=np.uint64))
 
 
 def test_sm100a_cubin_present():

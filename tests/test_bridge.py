@@ -252,3 +252,16 @@ def test_bridge_concurrent_batches(gpu):
     for t in th:
         t.join()
     assert not errs, errs[0]
+
+
+@pytest.mark.gpu
+def test_bridge_gpu_degenerate_indexes(gpu):
+    """Empty index, no postings, all-unknown queries, k larger than the index."""
+    empty = search.bridge_ingest([])
+    assert empty.num_docs() == 0
+    r = empty.dev.search_batch([search.SparseVector([0], [1.0])], 5)
+    assert r["n"][0] == 0 and r["postings"][0] == 0
+    nopost = search.bridge_ingest([(5, search.SparseVector()), (6, search.SparseVector())])
+    assert nopost.bridge_topk(search.SparseVector([0, 1], [1.0, 2.0]), 3) == []
+    one = search.bridge_ingest([(9, search.SparseVector([2], [0.25]))])
+    assert one.bridge_topk(search.SparseVector([0, 1, 2, 7], [1.0, 1.0, 4.0, 1.0]), 100) == [(9, 1.0)]

@@ -180,3 +180,20 @@ def test_cascade_batch_equals_reference_cascade(gpu):
         want = ref.agent_rrf(sparse, dl, recs, int(qts[i]))[:10]
         assert got[i].escalated and got[i].results == want, i
     assert n_esc > 10
+
+
+@pytest.mark.gpu
+def test_dense_gpu_degenerate_matrices(gpu):
+    """Single row, fewer rows than k, zero query, all-equal rows (every score
+    tied: DocId order), on both the tensor-core and fp64 paths."""
+    for dim in (32, 24):
+        one = search.DenseIndex(np.ones((1, dim), np.float32) / np.sqrt(dim), np.array([42], np.uint64))
+        assert [d for d, _ in one.dense_topk(np.ones(dim, np.float32), 10)] == [42]
+        m = np.tile(np.linspace(-1, 1, dim, dtype=np.float32), (700, 1))
+        ids = (np.arange(700, dtype=np.uint64) * 7919) % 1009
+        dev = search.DenseIndex(m, ids)
+        q = np.stack([np.zeros(dim, np.float32), m[0]])
+        for flags in (0, search.HM_FLAG_FORCE_EXACT):
+            got = dev.search_batch(q, 10, flags=flags)
+            want = ref.dense_topk_batch(m, ids, q, 10)
+            assert_dense(got, want, f"ties dim={dim} flags={flags}")
