@@ -155,6 +155,9 @@ __global__ void __launch_bounds__(kCons, 2) search_fast_kernel(DevIndex ix, Batc
             S.bad = bad;
             S.flood = 0;
             if (!(a.flags & 2u)) S.Lg = 0u;  // HM_FLAG_DEBUG_NO_RESET skips the sentinel reset
+            // a query handed over by the seeded pass may carry a lower bound on
+            // the k-th selection score (search_seed.cu: hand_over)
+            if (a.fb_list && a.fb_list[q] > 1u) S.Lg = max(S.Lg, a.fb_list[q]);
         }
         if (!(a.flags & 2u)) {
             if (tid < kConsWarps) S.n_w[tid] = 0;

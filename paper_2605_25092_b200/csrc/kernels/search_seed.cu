@@ -234,9 +234,12 @@ __device__ __noinline__ ValsN<N> seed_probeN(const SeedCtx<CAPW>& c, uint32_t i,
     return out;
 }
 
-// leave query q to the exhaustive kernel (which walks the LPT order itself)
-__device__ __forceinline__ void hand_over(const BatchArgs& a, uint32_t q) {
-    a.fb_list[q] = 1u;
+// leave query q to the exhaustive kernel (which walks the LPT order itself).
+// lb > 0: a lower bound, in the exhaustive kernel's selection domain, on the
+// k-th largest selection score -- its starting Lg (fb_list holds its bits;
+// positive floats order like their bit patterns; 1 = no bound)
+__device__ __forceinline__ void hand_over(const BatchArgs& a, uint32_t q, float lb = 0.f) {
+    a.fb_list[q] = lb > 0.f ? max(__float_as_uint(lb), 1u) : 1u;
     atomicAdd(&a.counters[4], 1u);
 }
 
@@ -472,7 +475,10 @@ __global__ void __launch_bounds__(kCons, HM_SEED_MINB) search_seed_kernel(DevInd
         }
         __syncthreads();
         if (S.flood == 2u) {  // too many essential postings: the exhaustive kernel
-            if (tid == 0) hand_over(a, q);
+            // k seeds have complete scores S >= L here; in the sweep's domain
+            // (baked impacts) each has A >= (1-delta) E >= S (1-delta)/(1+delta)
+            // >= L (1 - 2 delta): a valid starting bound for its admission
+            if (tid == 0) hand_over(a, q, L * (1.0f - 2.0f * delta - 1e-6f));
             continue;
         }
         const uint32_t ne = S.sel[0];
