@@ -28,6 +28,7 @@ thread_local uint32_t g_dense_overflow = 0;
 thread_local uint64_t g_dense_candidates = 0;
 thread_local uint32_t g_dense_path = 0;  // 1 tensor cores, 2 fp64 lists, 3 fp64 sort (large k)
 constexpr uint32_t kCandCap = 8192;  // tensor-core path: candidates per query (= rescoring capacity)
+constexpr uint32_t kTcChunk = 16384;  // queries per tensor-core launch (candidate lists: 512 MB)
 
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
     static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
@@ -171,45 +172,53 @@ void run(hm_dense* X, DenseWs* w, uint32_t nq, uint32_t k, const float* q_dev, u
          uint32_t* out_n, cudaStream_t st, bool timing, uint32_t flags) {
     if (timing) ck(cudaEventRecord(w->ev[0], st), "event");
     if (X->tc && k <= hm::dense_tc_max_k() && !(flags & HM_FLAG_FORCE_EXACT)) {
-        // tensor cores select candidates (TF32), fp64 rescoring decides
-        if (static_cast<uint64_t>(nq) > w->cand_cap) {
-            DenseWs::grow(w->cand_n, nq);
-            DenseWs::grow(w->cand_rows, static_cast<uint64_t>(nq) * kCandCap);
-            DenseWs::grow(w->thr_key, nq);
-            w->cand_cap = nq;
+        // tensor cores select candidates (TF32), fp64 rescoring decides; the
+        // candidate lists (8,192 rows per query) bound a launch to kTcChunk queries
+        const uint32_t chunk = std::min<uint32_t>(nq, kTcChunk);
+        if (static_cast<uint64_t>(chunk) > w->cand_cap) {
+            DenseWs::grow(w->cand_n, chunk);
+            DenseWs::grow(w->cand_rows, static_cast<uint64_t>(chunk) * kCandCap);
+            DenseWs::grow(w->thr_key, chunk);
+            w->cand_cap = chunk;
         }
-        alignas(64) CUtensorMap map_q{};
-        encode_map(&map_q, q_dev, nq, X->dev.dim, 128);
-        ck(cudaMemsetAsync(w->cand_n, 0, nq * 4ull, st), "memset candidates");
-        ck(cudaMemsetAsync(w->thr_key, 0x80, nq * 4ull, st), "memset bounds");
-        hm::DenseTcArgs a{};
-        a.nq = nq;
-        a.dim = X->dev.dim;
-        a.n_rows = X->dev.n;
-        a.k = k;
-        a.n_slabs = hm::dense_tc_slabs(nq, X->dev.n, X->sms);
-        a.q = q_dev;
-        a.err_scale = X->err_scale;
-        a.cand_n = w->cand_n;
-        a.thr_key = w->thr_key;
-        a.cand_rows = w->cand_rows;
-        a.cand_cap = kCandCap;
-        a.out_ids = out_ids;
-        a.out_scores = out_scores;
-        a.out_n = out_n;
-        ck(hm::launch_dense_tc(X->dev, &map_q, &X->map_e, a, X->sms, st), "dense tensor-core kernels");
-        g_dense_path = 1;
-        if (timing) {  // candidate statistics (test / bench evidence of the selection's tightness)
-            std::vector<uint32_t> cn(nq);
-            ck(cudaMemcpyAsync(cn.data(), w->cand_n, nq * 4ull, cudaMemcpyDeviceToHost, st), "D2H candidates");
-            ck(cudaStreamSynchronize(st), "sync");
+        if (timing) {
             g_dense_overflow = 0;
             g_dense_candidates = 0;
-            for (uint32_t c : cn) {
-                g_dense_candidates += c;
-                g_dense_overflow += c > kCandCap;
+        }
+        for (uint32_t q0 = 0; q0 < nq; q0 += chunk) {
+            const uint32_t nc = std::min(chunk, nq - q0);
+            const float* qd = q_dev + static_cast<uint64_t>(q0) * X->dev.dim;
+            alignas(64) CUtensorMap map_q{};
+            encode_map(&map_q, qd, nc, X->dev.dim, 128);
+            ck(cudaMemsetAsync(w->cand_n, 0, nc * 4ull, st), "memset candidates");
+            ck(cudaMemsetAsync(w->thr_key, 0x80, nc * 4ull, st), "memset bounds");
+            hm::DenseTcArgs a{};
+            a.nq = nc;
+            a.dim = X->dev.dim;
+            a.n_rows = X->dev.n;
+            a.k = k;
+            a.n_slabs = hm::dense_tc_slabs(nc, X->dev.n, X->sms);
+            a.q = qd;
+            a.err_scale = X->err_scale;
+            a.cand_n = w->cand_n;
+            a.thr_key = w->thr_key;
+            a.cand_rows = w->cand_rows;
+            a.cand_cap = kCandCap;
+            a.out_ids = out_ids + static_cast<uint64_t>(q0) * k;
+            a.out_scores = out_scores + static_cast<uint64_t>(q0) * k;
+            a.out_n = out_n + q0;
+            ck(hm::launch_dense_tc(X->dev, &map_q, &X->map_e, a, X->sms, st), "dense tensor-core kernels");
+            if (timing) {  // candidate statistics (test / bench evidence of the selection's tightness)
+                std::vector<uint32_t> cn(nc);
+                ck(cudaMemcpyAsync(cn.data(), w->cand_n, nc * 4ull, cudaMemcpyDeviceToHost, st), "D2H candidates");
+                ck(cudaStreamSynchronize(st), "sync");
+                for (uint32_t c : cn) {
+                    g_dense_candidates += c;
+                    g_dense_overflow += c > kCandCap;
+                }
             }
         }
+        g_dense_path = 1;
     } else if (k > hm::dense_max_k()) {
         // k beyond the shared-memory lists: per query, every row scored and
         // sorted on the device (rare: the reference callers use k = 10)

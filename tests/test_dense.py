@@ -197,3 +197,16 @@ def test_dense_gpu_degenerate_matrices(gpu):
             got = dev.search_batch(q, 10, flags=flags)
             want = ref.dense_topk_batch(m, ids, q, 10)
             assert_dense(got, want, f"ties dim={dim} flags={flags}")
+
+
+@pytest.mark.gpu
+def test_dense_tensor_core_batches_larger_than_a_launch(gpu):
+    """More queries than one tensor-core launch takes (16,384): chunked."""
+    rng = np.random.default_rng(21)
+    m = unit_rows(rng, 1500, 32)
+    ids = rng.permutation(1500).astype(np.uint64)
+    q = unit_rows(rng, 16_500, 32)
+    dev = search.DenseIndex(m, ids)
+    got = dev.search_batch(q, 5, flags=search.HM_FLAG_TIMING)
+    assert search.DenseIndex.last_stats()[:2] == (1, 0)
+    assert_dense(got, ref.dense_topk_batch(m, ids, q, 5, workers=16), "chunked")
