@@ -291,7 +291,7 @@ int hm_dense_create(const hm_dense_view* view, int device, hm_dense** out) {
                 }
                 const double c = 1.25 * (std::ldexp(1.0, -9) + std::ldexp(1.0, -20) + view->dim * std::ldexp(1.0, -22));
                 X->err_scale = static_cast<float>(c * std::sqrt(mx) * 1.0001);
-                encode_map(&X->map_e, X->dev.E, view->count, view->dim, 256);
+                encode_map(&X->map_e, X->dev.E, view->count, view->dim, hm::dense_tc_tile_rows());
                 X->tc = std::isfinite(X->err_scale);
             }
         } catch (...) {

@@ -36,19 +36,23 @@
 namespace hm {
 namespace {
 
-constexpr int kTcM = 128, kTcN = 256, kTcKc = 32;  // tile rows, tile columns, K elements per stage
-constexpr int kTcStages = 4;
+#ifndef HM_TC_N
+#define HM_TC_N 256
+#endif
+constexpr int kTcM = 128, kTcN = HM_TC_N, kTcKc = 32;  // tile rows, tile columns, K elements per stage
+constexpr int kTcAcc = 512 / kTcN;                   // TMEM accumulators (512 columns)
+constexpr int kTcStages = 192 * 1024 / (kTcM * 128 + kTcN * 128);
 constexpr uint32_t kABytes = kTcM * 128;  // 16 KB: 128 rows x 128 B
 constexpr uint32_t kBBytes = kTcN * 128;  // 32 KB
 constexpr int kEpiWarps = 8;  // two warps per TMEM lane quarter, each on half the columns
 constexpr int kTcThreads = 64 + 32 * kEpiWarps;
 constexpr int kEpiCols = kTcN * 4 / kEpiWarps;  // accumulator columns per epilogue warp
-constexpr uint32_t kTmemCols = 2 * kTcN;  // double-buffered accumulator
+constexpr uint32_t kTmemCols = 512;  // kTcAcc accumulators of kTcN columns
 
 struct __align__(1024) TcSmem {
     uint8_t a[kTcStages][kABytes];
     uint8_t b[kTcStages][kBBytes];
-    uint64_t full[kTcStages], empty[kTcStages], tfull[2], tempty[2];
+    uint64_t full[kTcStages], empty[kTcStages], tfull[kTcAcc], tempty[kTcAcc];
     uint32_t tmem_base;
 };
 
@@ -136,7 +140,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
             mbar_init(&S.full[s], 1);
             mbar_init(&S.empty[s], 1);
         }
-        for (int s = 0; s < 2; ++s) {
+        for (int s = 0; s < kTcAcc; ++s) {
             mbar_init(&S.tfull[s], 1);
             mbar_init(&S.tempty[s], kEpiWarps * 32);
         }
@@ -201,7 +205,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
                         }
                     }
                     mma_commit(&S.tfull[acc]);
-                    if (++acc == 2) {
+                    if (++acc == kTcAcc) {
                         acc = 0;
                         aphase ^= 1;
                     }
@@ -307,7 +311,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
                 }
                 tc_fence_before();
                 mbar_arrive(&S.tempty[acc]);
-                if (++acc == 2) {
+                if (++acc == kTcAcc) {
                     acc = 0;
                     aphase ^= 1;
                 }
@@ -429,6 +433,7 @@ cudaError_t launch_tc(const CUtensorMap& mq, const CUtensorMap& me, const DenseT
 }  // namespace
 
 uint32_t dense_tc_max_k() { return 32; }
+uint32_t dense_tc_tile_rows() { return kTcN; }
 
 cudaError_t launch_dense_tc(const DenseDev& ix, const void* map_q, const void* map_e, const DenseTcArgs& a, int sms,
                             cudaStream_t st) {

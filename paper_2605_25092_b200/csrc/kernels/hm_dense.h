@@ -42,6 +42,7 @@ struct DenseTcArgs {
     uint32_t* out_n;
 };
 uint32_t dense_tc_max_k();
+uint32_t dense_tc_tile_rows();  // rows per B tile (the E map's box)
 uint32_t dense_tc_slabs(uint32_t nq, uint32_t n_rows, int sms);
 // map_q / map_e: CUtensorMap (fp32, K-major, 32 x {128, 256} boxes, 128B swizzle)
 cudaError_t launch_dense_tc(const DenseDev& ix, const void* map_q, const void* map_e, const DenseTcArgs& a, int sms,
