@@ -133,6 +133,11 @@ int hm_last_batch_stats(uint32_t* n_exact_fallback, uint32_t* n_launches);
  * LPT sort, the fused selection kernel, the exact fallback kernel. */
 int hm_last_batch_timing(float* ms_plan, float* ms_search, float* ms_exact);
 
+/* How the last batch on this thread was launched: 0 stream operations
+ * (first sighting of these arguments, or HM_FLAG_TIMING), 1 captured into a
+ * CUDA graph (second identical batch on the workspace), 2 replayed from it. */
+int hm_last_batch_graph(uint32_t* mode);
+
 /* The seeded MaxScore pre-pass of the last batch on this thread: its device
  * time (HM_FLAG_TIMING batches) and how many queries it handed to the
  * exhaustive kernel (0 with HM_FLAG_EXHAUSTIVE). */

@@ -32,7 +32,7 @@
 
 namespace {
 
-thread_local uint32_t g_last_exact = 0, g_last_launches = 0, g_last_handed = 0;
+thread_local uint32_t g_last_exact = 0, g_last_launches = 0, g_last_handed = 0, g_last_graph = 0;
 thread_local float g_ms_plan = 0.f, g_ms_search = 0.f, g_ms_exact = 0.f, g_ms_seed = 0.f;
 
 using hm_host::ck;
@@ -89,8 +89,19 @@ struct Workspace {
     // pinned host staging
     unsigned char* pin = nullptr;
     size_t pin_bytes = 0;
+    // CUDA graph of the batch's launch sequence, replayed while a batch's
+    // arguments repeat (serving loops): captured on the second identical batch
+    cudaGraphExec_t gexec = nullptr;
+    unsigned char gkey[512] = {}, pkey[512] = {};
+    bool gvalid = false, pvalid = false;
+    void drop_graph() {
+        if (gexec) cudaGraphExecDestroy(gexec);
+        gexec = nullptr;
+        gvalid = pvalid = false;
+    }
 
     void free_dev() {
+        drop_graph();
         void* ps[] = {q_off, q_tid, plan_tid, plan_mult, plan_len, order_in, order, counters,
                       exact_list, fb_list, out_n, cost, cost_sorted, out_ids, out_post, tau, out_scores,
                       out_conf, w32, out_skip, sort_tmp};
@@ -105,6 +116,7 @@ struct Workspace {
         sort_tmp = nullptr;
     }
     ~Workspace() {
+        drop_graph();
         free_dev();
         if (stab) cudaFree(stab);
         if (seed_scratch) cudaFree(seed_scratch);
@@ -586,34 +598,90 @@ void run_batch(hm_index* X, Workspace* w, const hm_query_batch& hb, const uint32
     a.out_post = out.postings;
     fill_w32(X, hb.k1, hb.b, pin_w32);
     cudaStream_t st = w->stream;
-    ck(cudaMemcpyAsync(w->w32, pin_w32, hm::kMaxCodes * sizeof(float), cudaMemcpyHostToDevice, st),
-       "upload w32");
     const bool timing = (hb.flags & HM_FLAG_TIMING) != 0;
     if (timing && !w->ev[0])
         for (auto& e : w->ev) ck(cudaEventCreate(&e), "event");
-    ck(cudaMemsetAsync(w->counters, 0, 8 * sizeof(uint32_t), st), "memset counters");
-    if (timing) ck(cudaEventRecord(w->ev[0], st), "event");
-    ck(hm::launch_plan(X->dev, a, w->order_in, st), "plan kernel");
-    ck(hm::launch_lpt_sort(w->sort_tmp, w->sort_bytes, a, w->cost_sorted, w->order_in, st),
-       "lpt sort");
-    if (timing) ck(cudaEventRecord(w->ev[1], st), "event");
     // seeded MaxScore first (exact; serves the queries with a rare term), the
     // exhaustive kernel for the rest; HM_FLAG_EXHAUSTIVE skips the seeded pass
     // (a narrow row window -- a recency window of the temporal index -- keeps
     // every query cheap on the exhaustive kernel: no seeded pass)
     const bool seeded = !(a.flags & (HM_FLAG_EXHAUSTIVE | HM_FLAG_FORCE_EXACT)) &&
                         ((a.flags & HM_FLAG_SEED_ALL) || 4ull * (a.row_hi - a.row_lo) >= X->dev.n_docs);
-    if (seeded) {
-        a.fb_list = w->fb_list;
-        ck(cudaMemsetAsync(w->fb_list, 0, nq * sizeof(uint32_t), st), "memset hand-over flags");
-        ck(hm::launch_search_seed(X->dev, a, 2 * X->grid_search, st), "seeded search kernel");
-    }
-    if (timing) ck(cudaEventRecord(w->ev[4], st), "event");
-    ck(hm::launch_search(X->dev, a, X->grid_search, st), "search kernel");
-    if (timing) ck(cudaEventRecord(w->ev[2], st), "event");
-    ck(hm::launch_exact(X->dev, a, X->grid_exact, st), "exact kernel");
-    if (timing) ck(cudaEventRecord(w->ev[3], st), "event");
+    if (seeded) a.fb_list = w->fb_list;
     g_last_launches = seeded ? 4 : 3;  // ours: plan, seeded, exhaustive, exact (plus CUB's sort + a memset)
+    auto enqueue = [&] {
+        ck(cudaMemcpyAsync(w->w32, pin_w32, hm::kMaxCodes * sizeof(float), cudaMemcpyHostToDevice, st),
+           "upload w32");
+        ck(cudaMemsetAsync(w->counters, 0, 8 * sizeof(uint32_t), st), "memset counters");
+        if (timing) ck(cudaEventRecord(w->ev[0], st), "event");
+        ck(hm::launch_plan(X->dev, a, w->order_in, st), "plan kernel");
+        ck(hm::launch_lpt_sort(w->sort_tmp, w->sort_bytes, a, w->cost_sorted, w->order_in, st), "lpt sort");
+        if (timing) ck(cudaEventRecord(w->ev[1], st), "event");
+        if (seeded) {
+            ck(cudaMemsetAsync(w->fb_list, 0, nq * sizeof(uint32_t), st), "memset hand-over flags");
+            ck(hm::launch_search_seed(X->dev, a, 2 * X->grid_search, st), "seeded search kernel");
+        }
+        if (timing) ck(cudaEventRecord(w->ev[4], st), "event");
+        ck(hm::launch_search(X->dev, a, X->grid_search, st), "search kernel");
+        if (timing) ck(cudaEventRecord(w->ev[2], st), "event");
+        ck(hm::launch_exact(X->dev, a, X->grid_exact, st), "exact kernel");
+        if (timing) ck(cudaEventRecord(w->ev[3], st), "event");
+    };
+    g_last_graph = 0;
+    if (timing) {  // per-kernel events: run eagerly
+        enqueue();
+        return;
+    }
+    // the launch sequence depends only on the arguments below: a batch equal
+    // to the previous one is captured into a graph, later equal batches
+    // replay it (one launch instead of eight stream operations)
+    unsigned char key[512] = {};
+    static_assert(sizeof(hm::BatchArgs) + 4 * sizeof(int) + 2 * sizeof(void*) + sizeof(size_t) <= sizeof(key),
+                  "graph key");
+    {
+        unsigned char* k = key;
+        std::memcpy(k, &a, sizeof a);  // value-initialised: padding is zero
+        k += sizeof a;
+        const int ints[4] = {seeded ? 1 : 0, X->grid_search, X->grid_exact, static_cast<int>(nq)};
+        std::memcpy(k, ints, sizeof ints);
+        k += sizeof ints;
+        std::memcpy(k, &w->sort_tmp, sizeof(void*));
+        k += sizeof(void*);
+        std::memcpy(k, &pin_w32, sizeof(void*));
+        k += sizeof(void*);
+        std::memcpy(k, &w->sort_bytes, sizeof(size_t));
+    }
+    if (w->gvalid && std::memcmp(key, w->gkey, sizeof key) == 0) {
+        ck(cudaGraphLaunch(w->gexec, st), "graph launch");
+        g_last_graph = 2;
+        return;
+    }
+    if (!(w->pvalid && std::memcmp(key, w->pkey, sizeof key) == 0)) {  // first sighting: eager
+        enqueue();
+        std::memcpy(w->pkey, key, sizeof key);
+        w->pvalid = true;
+        return;
+    }
+    ck(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal), "begin capture");
+    cudaGraph_t g = nullptr;
+    try {
+        enqueue();
+    } catch (...) {
+        cudaStreamEndCapture(st, &g);
+        if (g) cudaGraphDestroy(g);
+        throw;
+    }
+    ck(cudaStreamEndCapture(st, &g), "end capture");
+    if (w->gexec) cudaGraphExecDestroy(w->gexec);
+    w->gexec = nullptr;
+    w->gvalid = false;
+    const cudaError_t ie = cudaGraphInstantiate(&w->gexec, g, 0);
+    cudaGraphDestroy(g);
+    ck(ie, "graph instantiate");
+    std::memcpy(w->gkey, key, sizeof key);
+    w->gvalid = true;
+    ck(cudaGraphLaunch(w->gexec, st), "graph launch");
+    g_last_graph = 1;
 }
 
 void read_timing(Workspace* w) {
@@ -858,6 +926,11 @@ int hm_search_batch_device(hm_index* X, const hm_query_batch* b, hm_results* out
 int hm_last_batch_stats(uint32_t* n_exact, uint32_t* n_launches) {
     if (n_exact) *n_exact = g_last_exact;
     if (n_launches) *n_launches = g_last_launches;
+    return HM_OK;
+}
+
+int hm_last_batch_graph(uint32_t* mode) {
+    if (mode) *mode = g_last_graph;
     return HM_OK;
 }
 

@@ -85,7 +85,7 @@ EXPORTS = ["hm_dense_create", "hm_dense_destroy", "hm_dense_search_batch", "hm_d
            "hm_bridge_search_batch_device", "hm_bridge_last_timing",
            "hm_index_create", "hm_index_destroy", "hm_index_device_bytes", "hm_index_format",
            "hm_search_batch", "hm_search_batch_device", "hm_last_batch_stats",
-           "hm_last_batch_timing", "hm_last_batch_seed",
+           "hm_last_batch_timing", "hm_last_batch_seed", "hm_last_batch_graph",
            "hm_hidx_load", "hm_hidx_last_error", "hm_hidx_view", "hm_hidx_term", "hm_hidx_maxscores",
            "hm_hidx_free", "hm_htix_load", "hm_htix_flat", "hm_htix_partitions", "hm_htix_params",
            "hm_htix_free",
@@ -110,6 +110,7 @@ def lib():
     L.hm_last_batch_stats.argtypes = [P(C.c_uint32), P(C.c_uint32)]
     L.hm_last_batch_timing.argtypes = [P(C.c_float), P(C.c_float), P(C.c_float)]
     L.hm_last_batch_seed.argtypes = [P(C.c_float), P(C.c_uint32)]
+    L.hm_last_batch_graph.argtypes = [P(C.c_uint32)]
     L.hm_hidx_load.argtypes = [C.c_char_p, P(C.c_void_p)]
     L.hm_hidx_last_error.restype = C.c_char_p
     L.hm_hidx_view.argtypes = [C.c_void_p, P(CsrView), P(C.c_uint32), P(C.c_double), P(C.c_double)]
@@ -296,6 +297,13 @@ def last_timing():
     a, b, c = C.c_float(), C.c_float(), C.c_float()
     lib().hm_last_batch_timing(C.byref(a), C.byref(b), C.byref(c))
     return a.value, b.value, c.value
+
+
+def last_graph():
+    """0 eager, 1 captured into a CUDA graph, 2 replayed (this thread's last batch)."""
+    m = C.c_uint32()
+    lib().hm_last_batch_graph(C.byref(m))
+    return m.value
 
 
 def last_seed():

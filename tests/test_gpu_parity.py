@@ -237,3 +237,25 @@ def test_empty_index(gpu):
     ri = ref.RefIndex.from_texts([], ref.TOK_MINIMAL)
     idx = export_to_csr(ri)
     assert idx.bm25_topk(["cat"], 5) == []
+
+
+def test_repeated_batches_replay_a_cuda_graph(c1):
+    """A batch repeated on a workspace is captured into a CUDA graph on its
+    second run and replayed afterwards; results stay the oracle's, and a
+    changed argument (k, parameters, window) falls back to a fresh sequence."""
+    tids = c1["tids"][:300]
+    ids, sc, n, post = c1["orc"].topk(tids, 10)
+    modes = []
+    for _ in range(4):
+        got = c1["dev"].search_lists(tids, 10)
+        modes.append(search.last_graph())
+        check_batch(got, ids, sc, n, post, what="graph replay")
+    assert modes[-2:] == [2, 2] and 1 in modes, modes
+    i5, s5, n5, p5 = c1["orc"].topk(tids, 5)
+    got = c1["dev"].search_lists(tids, 5)
+    assert search.last_graph() == 0
+    check_batch(got, i5, s5, n5, p5, what="new k after replay")
+    for _ in range(3):
+        got = c1["dev"].search_lists(tids, 10, k1=0.9, b=0.4)
+    w = c1["orc"].topk(tids, 10, k1=0.9, b=0.4)
+    check_batch(got, *w, what="other params, replayed")
