@@ -58,9 +58,15 @@ def gather_and_merge(local, k, world, group=None, tau=None, tau_default=0.10,
         g_ids = torch.empty((world, nq, k), dtype=torch.int64, device=dev)
         g_sc = torch.empty((world, nq, k), dtype=torch.float64, device=dev)
         g_n = torch.empty((world, nq), dtype=torch.int32, device=dev)
-        dist.all_gather_into_tensor(g_ids, local["ids"].contiguous(), group=group)
-        dist.all_gather_into_tensor(g_sc, local["scores"].contiguous(), group=group)
-        dist.all_gather_into_tensor(g_n, local["n"].contiguous(), group=group)
+        if dist.get_backend(group) == "gloo":  # CPU transport (tests: ranks sharing one GPU)
+            for g, x in ((g_ids, local["ids"]), (g_sc, local["scores"]), (g_n, local["n"])):
+                parts = [torch.empty_like(x, device="cpu") for _ in range(world)]
+                dist.all_gather(parts, x.contiguous().cpu(), group=group)
+                g.copy_(torch.stack(parts))
+        else:  # NCCL over NVLink: one all-gather per field, device to device
+            dist.all_gather_into_tensor(g_ids, local["ids"].contiguous(), group=group)
+            dist.all_gather_into_tensor(g_sc, local["scores"].contiguous(), group=group)
+            dist.all_gather_into_tensor(g_n, local["n"].contiguous(), group=group)
     else:
         g_ids, g_sc, g_n = local["ids"][None], local["scores"][None], local["n"][None]
     out = dict(ids=torch.zeros((nq, k), dtype=torch.int64, device=dev),

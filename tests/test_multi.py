@@ -118,3 +118,45 @@ def test_device_merge_of_simulated_shards(gpu, G):
     got["postings"] = post
     check_batch(got, full["ids"], full["scores"], full["n"], full["postings"], what=f"G={G}")
     assert out["n"].shape[0] == nq
+
+
+def _gpu_worker(rank, world, port, out_q):
+    """One rank of the sharded path on a shared GPU: ShardedIndex (this rank's
+    shard, global statistics), device search, all-gather (gloo transport),
+    device merge."""
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    torch.cuda.set_device(0)
+    _, _, hx, tids = synth_setup(60000, 5000, 5, 30, 200)
+    sh = shard.ShardedIndex(hx, rank, world, device=0)
+    off = np.zeros(len(tids) + 1, np.uint32)
+    off[1:] = np.cumsum([len(t) for t in tids])
+    flat = np.concatenate([np.asarray(t, np.uint32) for t in tids])
+    res = sh.search_batch(off, flat, K)
+    if rank == 0:
+        out_q.put({k: v for k, v in res.items()})
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("world", [2, 3])
+def test_sharded_index_ranks_on_one_gpu_equal_unsharded(gpu, world):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = 29600 + world * 7 + (os.getpid() % 500)
+    procs = [ctx.Process(target=_gpu_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = q.get(timeout=600)
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    _, _, hx, tids = synth_setup(60000, 5000, 5, 30, 200)
+    ids, sc, n, _ = restate.OracleIndex.from_host(hx).topk(tids, K)
+    assert (res["n"].astype(np.uint32) == n).all()
+    for i in range(len(n)):
+        assert (res["ids"][i, :n[i]].view(np.uint64) == ids[i, :n[i]]).all()
+        assert (res["scores"][i, :n[i]].view(np.uint64) == sc[i, :n[i]].view(np.uint64)).all()
+        assert res["conf"][i] == restate.margin(sc[i, :n[i]])
