@@ -335,6 +335,48 @@ def merge_shards_device(shard_ids, shard_scores, shard_n, out, k, tau=None, tau_
                                         epsilon_guard, C.byref(r), st.cuda_stream))
 
 
+def bm25_score(tf, idf, doc_len, avgdl, p=None):
+    """csr_index.cpp:10-15, the reference's operation order."""
+    p = p or Bm25Params()
+    norm = doc_len / avgdl if avgdl > 0.0 else 1.0
+    return idf * tf * (p.k1 + 1.0) / (tf + p.k1 * (1.0 - p.b + p.b * norm))
+
+
+MARGIN, TOP1_FRACTION, ENTROPY_COMPLEMENT, CLASSIFIER = 0, 1, 2, 3
+
+
+def confidence(scores, proxy=MARGIN, epsilon_guard=1e-9):
+    """cascade::confidence (cascade.cpp:10-38) for every proxy, same
+    operation order (the device computes Margin in the batch epilogue)."""
+    if proxy == CLASSIFIER:
+        raise ValueError("Classifier proxy has no score-based confidence")
+    s = [float(x) for x in scores]
+    if not s or s[0] <= 0.0:
+        return 0.0
+    if proxy == MARGIN:
+        return 0.0 if len(s) < 2 else (s[0] - s[1]) / max(s[0], epsilon_guard)
+    if proxy == TOP1_FRACTION:
+        tot = 0.0
+        for x in s:
+            tot += x
+        return s[0] / max(tot, epsilon_guard)
+    if proxy == ENTROPY_COMPLEMENT:
+        if len(s) < 2:
+            return 0.0
+        tot = 0.0
+        for x in s:
+            tot += x
+        if tot <= 0.0:
+            return 0.0
+        h = 0.0
+        for x in s:
+            pi = x / tot
+            if pi > 0.0:
+                h -= pi * math.log(pi)
+        return 1.0 - h / math.log(float(len(s)))
+    return 0.0
+
+
 def margin(scores, epsilon_guard=1e-9):
     """Margin confidence (src/cascade.cpp:15-21)."""
     s = np.ascontiguousarray(scores, np.float64)
@@ -410,6 +452,45 @@ class CsrIndex:
     # MaxScore's output is identical to the exhaustive path (csr_index.hpp:77-79,
     # acceptance.cpp:144-171); the GPU path serves both with the same kernel.
     bm25_topk_maxscore = bm25_topk
+
+    def bm25_term_score(self, term_id, posting_index, p=None):
+        """csr_index.cpp:61-75: one posting's score (IndexError on ranges)."""
+        p = p or Bm25Params()
+        if term_id >= len(self.terms):
+            raise IndexError("term_id out of range")
+        lo, hi = int(self.term_offsets[term_id]), int(self.term_offsets[term_id + 1])
+        if posting_index >= hi - lo:
+            raise IndexError("posting_index out of term range")
+        i = lo + posting_index
+        return bm25_score(float(self.posting_weights[i]), float(self.term_idfs[term_id]),
+                          float(self.doc_lens[self.posting_rows[i]]), self.avgdl, p)
+
+    def compute_term_maxscores(self, p=None):
+        """Per-term maximum posting score (csr_index.hpp:81-82), host-side,
+        in bm25_score's operation order (vectorised over the postings)."""
+        p = p or Bm25Params()
+        df = np.diff(self.term_offsets.astype(np.int64))
+        idf = np.repeat(self.term_idfs, df)
+        tf = self.posting_weights
+        dl = self.doc_lens[self.posting_rows].astype(np.float64)
+        norm = dl / self.avgdl if self.avgdl > 0.0 else np.ones_like(dl)
+        sc = idf * tf * (p.k1 + 1.0) / (tf + p.k1 * (1.0 - p.b + p.b * norm))
+        out = np.zeros(len(self.terms))
+        nz = df > 0
+        if len(sc):
+            out[nz] = np.maximum.reduceat(sc, self.term_offsets[:-1][nz].astype(np.int64))
+        return out
+
+    def query_upper_bound(self, query_terms, term_maxscores=None):
+        """Sum of the known query terms' maxscores, duplicates counted
+        (csr_index.hpp:84-86)."""
+        ms = self.compute_term_maxscores(self.build_params) if term_maxscores is None else term_maxscores
+        ub = 0.0
+        for t in query_terms:
+            i = self.vocab.get(t)
+            if i is not None:
+                ub += float(ms[i])
+        return ub
 
     def search_batch(self, queries, k, p=None, tau=None, tau_default=0.10, row_lo=0, row_hi=0,
                      flags=0, epsilon_guard=1e-9):

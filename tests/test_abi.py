@@ -92,3 +92,36 @@ def test_k_star_and_temporal_budget_host_logic():
     assert t.num_partitions() == 4 and t.budget() == 3 and t.window() == (5, 20)
     t.params.k_max_partitions = 1
     assert t.window() == (9, 20)
+
+
+def test_confidence_proxies_and_term_scores_mirror_reference():
+    """The host-side pieces of the mirror: every confidence proxy
+    (cascade.cpp:10-38), bm25_score, bm25_term_score, compute_term_maxscores
+    and query_upper_bound against the reference library, bit for bit."""
+    from oracle import ref
+    rng = np.random.default_rng(3)
+    lists = [[8.74, 2.13, 1.40, 0.91, 0.83], [4.21, 3.97, 3.48, 3.11, 2.96], [5.0], [], [0.0, 0.0],
+             list(np.sort(rng.random(10))[::-1] * 7)]
+    for sc in lists:
+        for proxy in (0, 1, 2):
+            assert search.confidence(sc, proxy) == ref.confidence(sc, proxy), (sc, proxy)
+    with pytest.raises(ValueError):
+        search.confidence([1.0, 0.5], search.CLASSIFIER)
+    from _util import export_to_csr, toy_docs
+    ri = ref.RefIndex.from_texts(toy_docs(), ref.TOK_MINIMAL)
+    csr = export_to_csr(ri)
+    e = ri.export()
+    for t in range(len(e["terms"])):
+        for j in range(int(e["term_offsets"][t + 1] - e["term_offsets"][t])):
+            i = int(e["term_offsets"][t]) + j
+            want = ref.bm25_score(float(e["posting_weights"][i]), float(e["idf"][t]),
+                                  float(e["doc_lens"][e["posting_rows"][i]]), e["avgdl"])
+            assert csr.bm25_term_score(t, j) == want
+    assert (csr.compute_term_maxscores().view(np.uint64) == e["maxscore"].view(np.uint64)).all()
+    q = ["cat", "dog", "cat", "unicorn"]
+    assert csr.query_upper_bound(q, e["maxscore"]) == sum(float(e["maxscore"][e["terms"].index(t)]) for t in q
+                                                          if t in e["terms"])
+    with pytest.raises(IndexError, match="term_id out of range"):
+        csr.bm25_term_score(len(e["terms"]), 0)
+    with pytest.raises(IndexError, match="posting_index out of term range"):
+        csr.bm25_term_score(0, 99)
