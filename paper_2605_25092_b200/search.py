@@ -603,7 +603,7 @@ class Htix:
         idx = CsrIndex(self.flat.terms(), a["term_offsets"], a["posting_rows"], a["posting_weights"],
                        a["idf"], a["order_key"], a["doc_lens"], a["doc_ids"], a["avgdl"],
                        self.flat.build_params, device)
-        return TemporalIndex(self.flat.device_index(device), self.part_row, self.params), idx
+        return TemporalIndex(self.flat.device_index(device), self.part_row, self.params, host=idx), idx
 
     def close(self):
         if getattr(self, "_h", None):
@@ -633,6 +633,14 @@ class TemporalParams:
     k_max_partitions: int = 4
 
 
+@dataclass
+class TemporalStats:
+    """hybrid::TemporalStats (temporal_index.hpp:33-37)."""
+    partitions_searched: int = 0
+    postings_touched: int = 0
+    early_stopped: bool = False
+
+
 class TemporalIndex:
     """Time-partitioned index on one device (temporal_index.hpp:40-72).
 
@@ -643,10 +651,85 @@ class TemporalIndex:
     The result equals the reference's greedy most-recent-first merge
     (temporal_index.cpp:72-123; SPEC.md:203)."""
 
-    def __init__(self, flat_dev, part_row, params=None):
+    def __init__(self, flat_dev, part_row, params=None, host=None):
         self.dev = flat_dev
         self.part_row = np.asarray(part_row, np.uint32)
         self.params = params or TemporalParams()
+        self.host = host  # CsrIndex mirror of the flat arrays (vocabulary, partition bounds)
+
+    def partition_upper_bound(self, i, query_terms):
+        """temporal_index.cpp:58-70: sum of partition i's term maxscores over
+        the query terms (duplicates counted).  A partition's maxscores are the
+        build-parameter scores of its own postings under the shared flat
+        statistics (temporal_index.cpp:136-142)."""
+        if i >= self.num_partitions():
+            raise IndexError("partition index out of range")
+        h = self.host
+        lo, hi = int(self.part_row[i]), int(self.part_row[i + 1])
+        bp = h.build_params
+        ub = 0.0
+        cache = {}
+        for t in query_terms:
+            tid = h.vocab.get(t)
+            if tid is None:
+                continue
+            if tid not in cache:
+                a, b = int(h.term_offsets[tid]), int(h.term_offsets[tid + 1])
+                rows = h.posting_rows[a:b]
+                s0 = a + int(np.searchsorted(rows, lo))
+                s1 = a + int(np.searchsorted(rows, hi))
+                ms = 0.0
+                if s1 > s0:
+                    tf = h.posting_weights[s0:s1]
+                    dl = h.doc_lens[h.posting_rows[s0:s1]].astype(np.float64)
+                    norm = dl / h.avgdl if h.avgdl > 0.0 else np.ones_like(dl)
+                    sc = h.term_idfs[tid] * tf * (bp.k1 + 1.0) / (tf + bp.k1 * (1.0 - bp.b + bp.b * norm))
+                    ms = float(sc.max())
+                cache[tid] = ms
+            ub += cache[tid]
+        return ub
+
+    def topk(self, query_terms, k, p=None, stats=None, use_ub_stop=True):
+        """TemporalIndex::topk (temporal_index.cpp:72-123): the newest
+        min(k*, k_max, K) partitions, newest first, each searched on the
+        device (a row window), merged greedily, with the admissible
+        upper-bound stop.  -> [(DocId, score)]; stats: TemporalStats
+        (partitions_searched / early_stopped as the reference; postings in the
+        exhaustive accounting of hm_results.postings)."""
+        p = p or Bm25Params()
+        cur = []
+        K = self.num_partitions()
+        if K == 0 or k == 0:
+            return cur
+        first = K - self.budget()
+        bp = self.host.build_params
+        ub_valid = p.k1 == bp.k1 and p.b == bp.b
+        tids = self.host.resolve(query_terms)
+        better = lambda e: (-e[1], e[0])  # noqa: E731  (RankedList::better order)
+        for i in range(K - 1, first - 1, -1):
+            if stats is not None:
+                stats.partitions_searched += 1
+            r = self.dev.search_lists([tids], k, k1=p.k1, b=p.b, row_lo=int(self.part_row[i]),
+                                      row_hi=int(self.part_row[i + 1]))
+            if stats is not None:
+                stats.postings_touched += int(r["postings"][0])
+            for j in range(int(r["n"][0])):
+                e = (int(r["ids"][0, j]), float(r["scores"][0, j]))
+                if len(cur) < k or better(e) < better(cur[-1]):
+                    cur.append(e)
+                    cur.sort(key=better)
+                    del cur[k:]
+                else:
+                    break
+            if use_ub_stop and ub_valid and i > first and len(cur) == k:
+                ub_rest = 0.0
+                for j in range(first, i):
+                    ub_rest = max(ub_rest, self.partition_upper_bound(j, query_terms))
+                if cur[-1][1] > ub_rest:
+                    if stats is not None:
+                        stats.early_stopped = True
+                    break
+        return cur
 
     def num_partitions(self):
         return len(self.part_row) - 1

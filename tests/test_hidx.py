@@ -184,3 +184,28 @@ def test_htix_temporal_search_like_reference(gpu, tmp_path):
         n = int(got["n"][i])
         assert got["ids"][i, :n].tolist() == list(want_ids), q
         assert (got["scores"][i, :n].view(np.uint64) == np.asarray(want_sc).view(np.uint64)).all(), q
+
+
+@pytest.mark.gpu
+def test_htix_temporal_topk_with_ub_stop_like_reference(gpu, tmp_path):
+    """TemporalIndex.topk per query (temporal_index.cpp:72-123), newest
+    partition first with the upper-bound stop: same list, same
+    partitions_searched and early_stopped as the reference."""
+    ids, ts, texts = _records(13, n=2500, vocab=120, span_days=90)
+    for eps, kmax in ((0.05, 4), (1e-9, 64)):
+        rt = ref.RefTemporal.from_records(ids, ts, texts, epsilon=eps, k_max=kmax)
+        p = tmp_path / f"t{kmax}.htix"
+        rt.save(p)
+        tix, idx = search.Htix(p).temporal_index()
+        rng = np.random.default_rng(kmax)
+        for _ in range(40):
+            q = ["w%d" % rng.integers(0, 130) for _ in range(rng.integers(1, 4))]
+            k = int(rng.integers(1, 12))
+            for ub in (True, False):
+                st = search.TemporalStats()
+                got = tix.topk(q, k, stats=st, use_ub_stop=ub)
+                w_ids, w_sc, w_srch, _ = rt.topk(q, k, use_ub_stop=ub)
+                assert [d for d, _ in got] == w_ids.tolist(), (q, k, ub)
+                assert np.array([s for _, s in got]).view(np.uint64).tolist() == \
+                    np.asarray(w_sc).view(np.uint64).tolist()
+                assert st.partitions_searched == w_srch, (q, k, ub)
