@@ -398,7 +398,10 @@ __global__ void __launch_bounds__(kCons, HM_SEED_MINB) search_seed_kernel(DevInd
         const uint64_t sw0 = S.t_wlo[ts];
         const uint32_t n_seed = static_cast<uint32_t>(S.t_end[ts] - sw0);
         uint32_t* sR = reinterpret_cast<uint32_t*>(sA) + kSeedMaxDf;  // seed rows
-        constexpr int kP = 4;  // rows per lane, probed together
+#ifndef HM_SEED_KP
+#define HM_SEED_KP 4
+#endif
+        constexpr int kP = HM_SEED_KP;  // rows per lane, probed together
         auto score_rows = [&](const RowsN<kP>& rw, uint32_t vm, uint64_t g0, uint32_t step) {
             if (!vm) return;  // seed_probeN needs at least one real row
             float A[kP] = {};
