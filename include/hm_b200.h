@@ -91,6 +91,8 @@ typedef struct {
                                     measurement of bench.py) */
 #define HM_FLAG_SEED_ALL 32u      /* test-only: the seeded pre-pass tries every query that
                                     has a short term, whatever its cost estimate or window */
+#define HM_FLAG_NO_SPLIT 64u     /* keep one CTA per query in small batches (no intra-query row
+                                    slabs; same results -- a test / measurement switch) */
 #define HM_FLAG_TIMING 4u         /* time each kernel with CUDA events on the
                                     launching stream (the call then synchronises);
                                     read back with hm_last_batch_timing */

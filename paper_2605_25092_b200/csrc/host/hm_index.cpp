@@ -89,6 +89,11 @@ struct Workspace {
     // pinned host staging
     unsigned char* pin = nullptr;
     size_t pin_bytes = 0;
+    // slab-query results of a split batch (merged into the caller's outputs)
+    uint64_t *v_ids = nullptr, *v_post = nullptr;
+    double* v_scores = nullptr;
+    uint32_t* v_n = nullptr;
+    uint64_t v_cap = 0, vk_cap = 0;
     // CUDA graph of the batch's launch sequence, replayed while a batch's
     // arguments repeat (serving loops): captured on the second identical batch
     cudaGraphExec_t gexec = nullptr;
@@ -118,6 +123,9 @@ struct Workspace {
     ~Workspace() {
         drop_graph();
         free_dev();
+        void* vs[] = {v_ids, v_post, v_scores, v_n};
+        for (void* p : vs)
+            if (p) cudaFree(p);
         if (stab) cudaFree(stab);
         if (seed_scratch) cudaFree(seed_scratch);
         for (auto e : ev)
@@ -553,6 +561,25 @@ void fill_w32(const hm_index* X, double k1, double b, float* w) {
 }
 
 // enqueue the whole batch on w->stream; batch arrays already on the device
+// Small batches leave most CTAs idle (one CTA per query): each query is then
+// split into row slabs served as separate "slab queries" -- exact per-slab
+// top-k lists, merged by merge_kernel exactly like doc shards (§4).  The
+// intra-query data parallelism of PAPER.md:616.
+uint32_t split_for(const hm_index* X, const hm_query_batch& hb) {
+    if ((hb.flags & (HM_FLAG_NO_SPLIT | HM_FLAG_FORCE_EXACT)) || needs_exact(hb.k1, hb.b) || hb.n_queries == 0 ||
+        hb.k == 0)
+        return 1;  // (the fp64 fallback path keeps one CTA per query)
+    const uint32_t nq = hb.n_queries, k = hb.k;
+    if (2ull * nq > static_cast<uint64_t>(X->grid_search)) return 1;
+    const uint32_t hi = hb.row_hi == 0 ? X->dev.n_docs : std::min(hb.row_hi, X->dev.n_docs);
+    const uint32_t span = hi > hb.row_lo ? hi - hb.row_lo : 0;
+    uint32_t S = static_cast<uint32_t>(X->grid_search) / nq;
+    S = std::min<uint32_t>(S, 2048 / k);  // merge_kernel holds split x k candidates
+    S = std::min<uint32_t>(S, 64);
+    S = std::min<uint32_t>(S, span / hm::kTile);  // at least a tile per slab
+    return S >= 2 ? S : 1;
+}
+
 void run_batch(hm_index* X, Workspace* w, const hm_query_batch& hb, const uint32_t* d_off,
                const uint32_t* d_tid, const double* d_tau, const hm_results& out, float* pin_w32) {
     const uint32_t nq = hb.n_queries;
@@ -596,6 +623,34 @@ void run_batch(hm_index* X, Workspace* w, const hm_query_batch& hb, const uint32
     a.out_conf = out.conf;
     a.out_skip = out.skip;
     a.out_post = out.postings;
+    const uint32_t split = split_for(X, hb);
+    a.split = split;
+    a.nq_real = nq;
+    if (split > 1) {  // slab queries: results into the workspace, decisions at the merge
+        const uint64_t nv = static_cast<uint64_t>(nq) * split;
+        if (nv > w->v_cap || hb.k > w->vk_cap) {
+            ck(cudaStreamSynchronize(w->stream), "sync");
+            void* vs[] = {w->v_ids, w->v_post, w->v_scores, w->v_n};
+            for (void* p : vs)
+                if (p) cudaFree(p);
+            const uint64_t NV = std::max(nv, w->v_cap);
+            const uint64_t K = std::max<uint64_t>(hb.k, w->vk_cap);
+            dalloc(w->v_ids, NV * K);
+            dalloc(w->v_scores, NV * K);
+            dalloc(w->v_n, NV);
+            dalloc(w->v_post, NV);
+            w->v_cap = NV;
+            w->vk_cap = K;
+        }
+        a.nq = static_cast<uint32_t>(nv);
+        a.tau = nullptr;
+        a.out_ids = w->v_ids;
+        a.out_scores = w->v_scores;
+        a.out_n = w->v_n;
+        a.out_conf = nullptr;
+        a.out_skip = nullptr;
+        a.out_post = w->v_post;
+    }
     fill_w32(X, hb.k1, hb.b, pin_w32);
     cudaStream_t st = w->stream;
     const bool timing = (hb.flags & HM_FLAG_TIMING) != 0;
@@ -608,23 +663,39 @@ void run_batch(hm_index* X, Workspace* w, const hm_query_batch& hb, const uint32
     const bool seeded = !(a.flags & (HM_FLAG_EXHAUSTIVE | HM_FLAG_FORCE_EXACT)) &&
                         ((a.flags & HM_FLAG_SEED_ALL) || 4ull * (a.row_hi - a.row_lo) >= X->dev.n_docs);
     if (seeded) a.fb_list = w->fb_list;
-    g_last_launches = seeded ? 4 : 3;  // ours: plan, seeded, exhaustive, exact (plus CUB's sort + a memset)
+    g_last_launches = (seeded ? 4 : 3) + (split > 1 ? 3 : 0);  // ours: plan, [seeded,] exhaustive, exact
+                                                             // [+ expand, merge, postings] (plus CUB's sort)
     auto enqueue = [&] {
         ck(cudaMemcpyAsync(w->w32, pin_w32, hm::kMaxCodes * sizeof(float), cudaMemcpyHostToDevice, st),
            "upload w32");
         ck(cudaMemsetAsync(w->counters, 0, 8 * sizeof(uint32_t), st), "memset counters");
         if (timing) ck(cudaEventRecord(w->ev[0], st), "event");
-        ck(hm::launch_plan(X->dev, a, w->order_in, st), "plan kernel");
-        ck(hm::launch_lpt_sort(w->sort_tmp, w->sort_bytes, a, w->cost_sorted, w->order_in, st), "lpt sort");
+        if (split > 1) {  // plan + LPT over the real queries, then every slab of each
+            hm::BatchArgs ap = a;
+            ap.nq = nq;
+            ap.order = w->exact_list;  // scratch until the sweep appends to it
+            ck(hm::launch_plan(X->dev, ap, w->order_in, st), "plan kernel");
+            ck(hm::launch_lpt_sort(w->sort_tmp, w->sort_bytes, ap, w->cost_sorted, w->order_in, st), "lpt sort");
+            ck(hm::launch_expand_order(nq, split, w->exact_list, w->order, st), "expand order");
+        } else {
+            ck(hm::launch_plan(X->dev, a, w->order_in, st), "plan kernel");
+            ck(hm::launch_lpt_sort(w->sort_tmp, w->sort_bytes, a, w->cost_sorted, w->order_in, st), "lpt sort");
+        }
         if (timing) ck(cudaEventRecord(w->ev[1], st), "event");
         if (seeded) {
-            ck(cudaMemsetAsync(w->fb_list, 0, nq * sizeof(uint32_t), st), "memset hand-over flags");
+            ck(cudaMemsetAsync(w->fb_list, 0, static_cast<uint64_t>(a.nq) * sizeof(uint32_t), st), "memset hand-over flags");
             ck(hm::launch_search_seed(X->dev, a, 2 * X->grid_search, st), "seeded search kernel");
         }
         if (timing) ck(cudaEventRecord(w->ev[4], st), "event");
         ck(hm::launch_search(X->dev, a, X->grid_search, st), "search kernel");
         if (timing) ck(cudaEventRecord(w->ev[2], st), "event");
         ck(hm::launch_exact(X->dev, a, X->grid_exact, st), "exact kernel");
+        if (split > 1) {  // the slabs' exact lists -> the real queries' top-k, Margin, skip
+            ck(hm::launch_merge(split, nq, hb.k, w->v_ids, w->v_scores, w->v_n, d_tau, hb.tau_default,
+                                hb.epsilon_guard, out.ids, out.scores, out.n, out.conf, out.skip, st),
+               "slab merge");
+            ck(hm::launch_sum_slab_postings(nq, split, w->v_post, out.postings, st), "slab postings");
+        }
         if (timing) ck(cudaEventRecord(w->ev[3], st), "event");
     };
     g_last_graph = 0;
@@ -808,7 +879,7 @@ int hm_search_batch(hm_index* X, const hm_query_batch* b, hm_results* out) {
         Workspace* w = acquire(X);
         try {
             const uint32_t k = std::max(b->k, 1u);
-            ensure(w, nq, std::max(ntid, 1u), k, true);
+            ensure(w, nq * split_for(X, *b), std::max(ntid, 1u), k, true);
             unsigned char* p = w->pin;
             auto take = [&](size_t bytes) {
                 unsigned char* r = p;
@@ -891,7 +962,7 @@ int hm_search_batch_device(hm_index* X, const hm_query_batch* b, hm_results* out
         ck(cudaStreamSynchronize(ust), "sync");
         Workspace* w = acquire(X);
         try {
-            ensure(w, nq, std::max(ntid, 1u), std::max(b->k, 1u), false);
+            ensure(w, nq * split_for(X, *b), std::max(ntid, 1u), std::max(b->k, 1u), false);
             // order the workspace stream after the caller's stream and back
             cudaEvent_t ev;
             ck(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming), "event");

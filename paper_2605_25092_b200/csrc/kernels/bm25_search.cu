@@ -126,7 +126,6 @@ __global__ void __launch_bounds__(kExactThreads, 1) exact_kernel(DevIndex ix, Ba
     ExactSmem& S = *reinterpret_cast<ExactSmem*>(smem_raw);
     const int tid = threadIdx.x, lane = tid & 31;
     const uint32_t cb = ix.code_bits;
-    const uint32_t row_lo = a.row_lo, row_hi = a.row_hi;
     const double k1 = a.k1, bb = a.b;
     for (int i = tid; i < kTile; i += kExactThreads) S.acc[i] = 0.0;
     for (int i = tid; i < kMaxCodes; i += kExactThreads) {
@@ -142,8 +141,10 @@ __global__ void __launch_bounds__(kExactThreads, 1) exact_kernel(DevIndex ix, Ba
         __syncthreads();
         const uint32_t q = S.q;
         if (q == kNoTerm) break;
-        const uint32_t poff = a.q_off[q];
-        const uint32_t m = a.plan_len[q];
+        uint32_t qr, row_lo, row_hi;  // the real query and this (slab) query's rows
+        query_window(a, q, qr, row_lo, row_hi);
+        const uint32_t poff = a.q_off[qr];
+        const uint32_t m = a.plan_len[qr];
         const uint32_t k = a.k;
         if (tid < static_cast<int>(m)) {
             const uint32_t t = a.plan_tid[poff + tid];
@@ -365,11 +366,45 @@ __global__ void __launch_bounds__(kMergeThreads) merge_kernel(
     }
 }
 
+// ============================================================ split batches
+// LPT order of slab queries: every slab of the i-th most expensive real query
+__global__ void expand_order_kernel(uint32_t nq_real, uint32_t split, const uint32_t* order_real, uint32_t* order) {
+    const uint32_t v = blockIdx.x * blockDim.x + threadIdx.x;
+    if (v >= nq_real * split) return;
+    const uint32_t i = v / split, s = v % split;
+    order[v] = s * nq_real + order_real[i];
+}
+
+// postings_touched of a real query = the sum over its slab queries
+__global__ void sum_slab_postings_kernel(uint32_t nq_real, uint32_t split, const uint64_t* v_post,
+                                         uint64_t* out_post) {
+    const uint32_t q = blockIdx.x * blockDim.x + threadIdx.x;
+    if (q >= nq_real) return;
+    uint64_t t = 0;
+    for (uint32_t s = 0; s < split; ++s) t += v_post[static_cast<uint64_t>(s) * nq_real + q];
+    out_post[q] = t;
+}
+
 // ============================================================ launchers
 cudaError_t launch_plan(const DevIndex& ix, const BatchArgs& a, uint32_t* order_in,
                         cudaStream_t st) {
     if (a.nq == 0) return cudaSuccess;
     plan_kernel<<<(a.nq + 127) / 128, 128, 0, st>>>(ix, a, order_in);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_expand_order(uint32_t nq_real, uint32_t split, const uint32_t* order_real, uint32_t* order,
+                                cudaStream_t st) {
+    const uint32_t n = nq_real * split;
+    if (n == 0) return cudaSuccess;
+    expand_order_kernel<<<(n + 255) / 256, 256, 0, st>>>(nq_real, split, order_real, order);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_sum_slab_postings(uint32_t nq_real, uint32_t split, const uint64_t* v_post, uint64_t* out_post,
+                                     cudaStream_t st) {
+    if (nq_real == 0 || !out_post) return cudaSuccess;
+    sum_slab_postings_kernel<<<(nq_real + 255) / 256, 256, 0, st>>>(nq_real, split, v_post, out_post);
     return cudaGetLastError();
 }
 

@@ -218,6 +218,22 @@ __device__ void block_bitonic(double* sc, uint64_t* id, Row* row, uint32_t n, Sy
     }
 }
 
+// The real query and the row window of (slab) query q (BatchArgs::split).
+__device__ __forceinline__ void query_window(const BatchArgs& a, uint32_t q, uint32_t& qr, uint32_t& lo,
+                                             uint32_t& hi) {
+    if (a.split <= 1) {
+        qr = q;
+        lo = a.row_lo;
+        hi = a.row_hi;
+        return;
+    }
+    qr = q % a.nq_real;
+    const uint32_t s = q / a.nq_real;
+    const uint64_t span = a.row_hi - a.row_lo;
+    lo = a.row_lo + static_cast<uint32_t>(span * s / a.split);
+    hi = a.row_lo + static_cast<uint32_t>(span * (s + 1) / a.split);
+}
+
 // Margin confidence (src/cascade.cpp:15-21) and skip (:79-84), fp64.
 __device__ __forceinline__ void write_decision(const BatchArgs& a, uint32_t q, const double* s,
                                                uint32_t n) {

@@ -16,6 +16,12 @@ cudaError_t lpt_sort_bytes(uint32_t nq, size_t* bytes);
 cudaError_t launch_lpt_sort(void* temp, size_t bytes, const BatchArgs& a,
                             uint64_t* cost_sorted, const uint32_t* order_in,
                             cudaStream_t st);
+// small batches split each query into row slabs (BatchArgs::split): slab
+// queries in the real LPT order, and their postings summed per real query
+cudaError_t launch_expand_order(uint32_t nq_real, uint32_t split, const uint32_t* order_real, uint32_t* order,
+                                cudaStream_t st);
+cudaError_t launch_sum_slab_postings(uint32_t nq_real, uint32_t split, const uint64_t* v_post, uint64_t* out_post,
+                                     cudaStream_t st);
 // persistent fused kernel: TAAT scoring + selection + exact rescoring + margin
 cudaError_t launch_search(const DevIndex& ix, const BatchArgs& a, int grid, cudaStream_t st);
 // seeded MaxScore pre-pass (kernels/search_seed.cu); hands the queries it

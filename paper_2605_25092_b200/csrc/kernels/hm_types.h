@@ -130,6 +130,11 @@ struct BatchArgs {
     double tau_default, eps;
     uint32_t row_lo, row_hi;
     uint32_t flags;
+    // intra-query split (small batches): split > 1 makes query q a slab
+    // query -- real query q % nq_real over the split's (q / nq_real)-th of
+    // [row_lo, row_hi); plan arrays are per real query, results per slab
+    // query (merged afterwards by merge_kernel)
+    uint32_t split, nq_real;
     const float* w32;          // [kMaxCodes] idf-free impacts for (k1, b)
     // planner scratch (device)
     uint32_t* plan_tid;        // [q_off[nq]] plan of query i at q_off[i]

@@ -55,7 +55,6 @@ __global__ void __launch_bounds__(kCons, 2) search_fast_kernel(DevIndex ix, Batc
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     auto csync = [] { __syncthreads(); };
     const uint32_t cb = ix.code_bits;
-    const uint32_t row_lo = a.row_lo, row_hi = a.row_hi;
     const double k1 = a.k1, bb = a.b;
     const uint32_t stride = a.stab_stride;
     uint32_t* stab = a.stab + static_cast<uint64_t>(blockIdx.x) * kMaxTerms * stride;
@@ -87,8 +86,10 @@ __global__ void __launch_bounds__(kCons, 2) search_fast_kernel(DevIndex ix, Batc
         __syncthreads();
         const uint32_t q = S.q;
         if (q == kNoTerm) break;
-        const uint32_t poff = a.q_off[q];
-        const uint32_t m = a.plan_len[q];
+        uint32_t qr, row_lo, row_hi;  // the real query and this (slab) query's rows
+        query_window(a, q, qr, row_lo, row_hi);
+        const uint32_t poff = a.q_off[qr];
+        const uint32_t m = a.plan_len[qr];
         const uint32_t k = a.k;
         if (m > kMaxTerms) {
             if (tid == 0) {

@@ -254,7 +254,6 @@ __global__ void __launch_bounds__(kCons, HM_SEED_MINB) search_seed_kernel(DevInd
     Smem& S = *reinterpret_cast<Smem*>(smem_raw);
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const uint32_t cb = ix.code_bits;
-    const uint32_t row_lo = a.row_lo, row_hi = a.row_hi;
     const double k1 = a.k1, bb = a.b;
     const uint32_t stride = a.stab_stride;
     uint32_t* stab = a.stab + static_cast<uint64_t>(blockIdx.x) * kMaxTerms * stride;
@@ -275,8 +274,10 @@ __global__ void __launch_bounds__(kCons, HM_SEED_MINB) search_seed_kernel(DevInd
         __syncthreads();
         const uint32_t q = S.q;
         if (q == kNoTerm) break;
-        const uint32_t poff = a.q_off[q];
-        const uint32_t m = a.plan_len[q];
+        uint32_t qr, row_lo, row_hi;  // the real query and this (slab) query's rows
+        query_window(a, q, qr, row_lo, row_hi);
+        const uint32_t poff = a.q_off[qr];
+        const uint32_t m = a.plan_len[qr];
         const uint32_t k = a.k;
         // anything unusual goes to the exhaustive kernel, which routes it on
         if (m == 0 || m > kFastTerms || k == 0 || k > kmax || (a.flags & 1u) || row_hi <= row_lo) {

@@ -31,6 +31,7 @@ HM_FLAG_DEBUG_NO_RESET = 2
 HM_FLAG_TIMING = 4
 HM_FLAG_EXHAUSTIVE = 16
 HM_FLAG_SEED_ALL = 32
+HM_FLAG_NO_SPLIT = 64
 NO_TERM = 0xFFFFFFFF
 MAX_K = 256
 

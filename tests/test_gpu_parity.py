@@ -259,3 +259,20 @@ def test_repeated_batches_replay_a_cuda_graph(c1):
         got = c1["dev"].search_lists(tids, 10, k1=0.9, b=0.4)
     w = c1["orc"].topk(tids, 10, k1=0.9, b=0.4)
     check_batch(got, *w, what="other params, replayed")
+
+
+@pytest.mark.parametrize("nq,k", [(1, 10), (3, 1), (17, 10), (60, 100), (140, 5)])
+def test_small_batches_split_into_row_slabs(c1, nq, k):
+    """Small batches run each query as row-slab queries (intra-query
+    parallelism) merged like doc shards: ids, score bits, conf, skip and
+    postings equal the oracle and the unsplit run, with and without a row
+    window and for other BM25 parameters."""
+    tids = c1["tids"][5:5 + nq]
+    n_docs = len(c1["hx"].doc_ids)
+    for (lo, hi), (k1, b) in [((0, 0), (1.2, 0.75)), ((1234, n_docs - 777), (1.2, 0.75)), ((0, 0), (0.9, 0.4))]:
+        w = c1["orc"].topk(tids, k, k1=k1, b=b, row_lo=lo, row_hi=hi if hi else n_docs)
+        got = c1["dev"].search_lists(tids, k, k1=k1, b=b, row_lo=lo, row_hi=hi)
+        check_batch(got, *w, what=f"split nq={nq} k={k} window=({lo},{hi})")
+        ref_run = c1["dev"].search_lists(tids, k, k1=k1, b=b, row_lo=lo, row_hi=hi, flags=search.HM_FLAG_NO_SPLIT)
+        for key in ("ids", "scores", "n", "conf", "skip", "postings"):
+            assert (np.asarray(got[key]).view(np.uint8) == np.asarray(ref_run[key]).view(np.uint8)).all(), key
