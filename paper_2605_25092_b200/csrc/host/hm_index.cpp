@@ -1,3 +1,4 @@
+#include <cstdlib>
 // C-ABI implementation (include/hm_b200.h): device index build/upload, the
 // per-call workspace pool, batch orchestration and error mapping.
 //
@@ -570,10 +571,18 @@ uint32_t split_for(const hm_index* X, const hm_query_batch& hb) {
         hb.k == 0)
         return 1;  // (the fp64 fallback path keeps one CTA per query)
     const uint32_t nq = hb.n_queries, k = hb.k;
-    if (2ull * nq > static_cast<uint64_t>(X->grid_search)) return 1;
+    // resident sweep CTAs (launch_search runs 2 per unit of grid_search); the
+    // batch is split while the heaviest query, not the total work, would set
+    // the time
+    const uint64_t resident = 2ull * static_cast<uint64_t>(X->grid_search);
     const uint32_t hi = hb.row_hi == 0 ? X->dev.n_docs : std::min(hb.row_hi, X->dev.n_docs);
     const uint32_t span = hi > hb.row_lo ? hi - hb.row_lo : 0;
-    uint32_t S = static_cast<uint32_t>(X->grid_search) / nq;
+    // (tiny batches: one slab per CTA -- per-slab overheads dominate thin
+    // slabs; larger ones: two per CTA, so LPT can even out the heavy queries)
+    // (measured on C2: B = 1..30 best near one slab per CTA, B >= 100 near two;
+    // caps 16 / 32 and half a slab per CTA measured slower for B <= 3 / B = 30)
+    const uint64_t target = nq >= 32 ? 2 * resident : resident;
+    uint32_t S = static_cast<uint32_t>(std::min<uint64_t>(target / nq, 64));
     S = std::min<uint32_t>(S, 2048 / k);  // merge_kernel holds split x k candidates
     S = std::min<uint32_t>(S, 64);
     S = std::min<uint32_t>(S, span / hm::kTile);  // at least a tile per slab

@@ -34,7 +34,7 @@ def main():
     strs = hx.term_strings()
     vocab = {w: i for i, w in enumerate(strs)}  # the reference's CsrIndex::vocab
     rows = []
-    for B in (1, 10, 100, 1000, 10000, 50000):
+    for B in [int(x) for x in os.environ.get('HM_LAT_SIZES', '1,10,100,1000,10000,50000').split(',')]:
         k = 10
         out = dict(ids=torch.zeros(B, k, dtype=torch.int64, device="cuda"),
                    scores=torch.zeros(B, k, dtype=torch.float64, device="cuda"),
