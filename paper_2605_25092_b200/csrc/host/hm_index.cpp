@@ -577,11 +577,10 @@ uint32_t split_for(const hm_index* X, const hm_query_batch& hb) {
     const uint64_t resident = 2ull * static_cast<uint64_t>(X->grid_search);
     const uint32_t hi = hb.row_hi == 0 ? X->dev.n_docs : std::min(hb.row_hi, X->dev.n_docs);
     const uint32_t span = hi > hb.row_lo ? hi - hb.row_lo : 0;
-    // (tiny batches: one slab per CTA -- per-slab overheads dominate thin
-    // slabs; larger ones: two per CTA, so LPT can even out the heavy queries)
-    // (measured on C2: B = 1..30 best near one slab per CTA, B >= 100 near two;
-    // caps 16 / 32 and half a slab per CTA measured slower for B <= 3 / B = 30)
-    const uint64_t target = nq >= 32 ? 2 * resident : resident;
+    // slab queries per resident CTA, measured on C2 (profiles/r01_latency.md):
+    // tiny batches one (per-slab overheads dominate thin slabs), 32-255
+    // queries four, 256+ eight (LPT then evens out the heaviest queries)
+    const uint64_t target = nq < 32 ? resident : nq < 256 ? 4 * resident : 8 * resident;
     uint32_t S = static_cast<uint32_t>(std::min<uint64_t>(target / nq, 64));
     S = std::min<uint32_t>(S, 2048 / k);  // merge_kernel holds split x k candidates
     S = std::min<uint32_t>(S, 64);
