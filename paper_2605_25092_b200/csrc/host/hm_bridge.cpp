@@ -17,6 +17,7 @@
 #include "hm_b200.h"
 #include "hm_bridge.h"
 #include "hm_host.h"
+#include "hm_launch.h"
 
 using hm_host::ck;
 using hm_host::guard;
@@ -34,6 +35,11 @@ struct BridgeWs {
     uint64_t *q_off = nullptr, *out_ids = nullptr, *out_post = nullptr, *scratch = nullptr;
     uint32_t *q_idx = nullptr, *out_n = nullptr, *counters = nullptr;
     double *q_val = nullptr, *out_scores = nullptr;
+    // slab-query results of a split batch (merged into the final outputs)
+    uint64_t *v_ids = nullptr, *v_post = nullptr;
+    double* v_scores = nullptr;
+    uint32_t* v_n = nullptr;
+    uint64_t v_cap = 0, vk_cap = 0;
 
     BridgeWs() {
         ck(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking), "bridge stream");
@@ -42,7 +48,8 @@ struct BridgeWs {
         ck(cudaMalloc(&counters, 4 * sizeof(uint32_t)), "cudaMalloc(counters)");
     }
     ~BridgeWs() {
-        void* ps[] = {q_off, out_ids, out_post, scratch, q_idx, out_n, counters, q_val, out_scores};
+        void* ps[] = {q_off, out_ids, out_post, scratch, q_idx, out_n, counters, q_val, out_scores,
+                      v_ids, v_post, v_scores, v_n};
         for (void* p : ps)
             if (p) cudaFree(p);
         cudaEventDestroy(ev[0]);
@@ -54,6 +61,16 @@ struct BridgeWs {
         if (p) cudaFree(p);
         p = nullptr;
         ck(cudaMalloc(&p, std::max<uint64_t>(n, 1) * sizeof(T)), "cudaMalloc(bridge workspace)");
+    }
+    void ensure_slabs(uint64_t nv, uint32_t k) {
+        if (nv <= v_cap && k <= vk_cap) return;
+        const uint64_t NV = std::max(nv, v_cap), K = std::max<uint64_t>(k, vk_cap);
+        grow(v_ids, NV * K);
+        grow(v_scores, NV * K);
+        grow(v_n, NV);
+        grow(v_post, NV);
+        v_cap = NV;
+        vk_cap = K;
     }
     void ensure(uint32_t nq, uint64_t nnz, uint32_t k, uint64_t scratch_words) {
         if (nq > nq_cap || k > k_cap) {
@@ -175,10 +192,46 @@ uint64_t scratch_words(const hm_bridge* X, uint32_t k, uint32_t m_max) {
     return static_cast<uint64_t>(hm::bridge_grid(k, X->sms)) * (3 + 2 * 8) * std::max(m_max, 1u);
 }
 
-void run(hm_bridge* X, const hm::BridgeArgs& a, BridgeWs* w, cudaStream_t st, bool timing) {
+// Small batches: each query split into row slabs (the BM25 path's policy,
+// hm_index.cpp split_for): slab queries in one launch, merged like doc shards.
+uint32_t bridge_split(const hm_bridge* X, const hm::BridgeArgs& a, uint32_t flags) {
+    if ((flags & HM_FLAG_NO_SPLIT) || a.k == 0 || a.nq == 0) return 1;
+    const uint64_t resident = hm::bridge_grid(a.k, X->sms);
+    const uint64_t target = a.nq < 32 ? resident : a.nq < 256 ? 4 * resident : 8 * resident;
+    const uint32_t span = a.row_hi > a.row_lo ? a.row_hi - a.row_lo : 0;
+    uint64_t S = std::min<uint64_t>(target / a.nq, 64);
+    S = std::min<uint64_t>(S, 2048 / a.k);  // merge_kernel holds split x k candidates
+    S = std::min<uint64_t>(S, span / 8192);  // >= one 1,024-row unit per warp
+    return S >= 2 ? static_cast<uint32_t>(S) : 1;
+}
+
+// one batch: a.out_* are the final outputs; split batches write slab results
+// to the workspace and merge them there
+void run(hm_bridge* X, hm::BridgeArgs a, BridgeWs* w, cudaStream_t st, bool timing, uint32_t flags) {
+    const uint32_t nq = a.nq, split = bridge_split(X, a, flags);
+    uint64_t* fin_ids = a.out_ids;
+    double* fin_scores = a.out_scores;
+    uint32_t* fin_n = a.out_n;
+    uint64_t* fin_post = a.out_post;
+    if (split > 1) {
+        w->ensure_slabs(static_cast<uint64_t>(nq) * split, a.k);
+        a.nq = nq * split;
+        a.split = split;
+        a.nq_real = nq;
+        a.out_ids = w->v_ids;
+        a.out_scores = w->v_scores;
+        a.out_n = w->v_n;
+        a.out_post = w->v_post;
+    }
     ck(cudaMemsetAsync(w->counters, 0, 4 * sizeof(uint32_t), st), "memset counters");
     if (timing) ck(cudaEventRecord(w->ev[0], st), "event");
     ck(hm::launch_bridge(X->dev, a, X->sms, st), "bridge kernel");
+    if (split > 1) {
+        ck(hm::launch_merge(split, nq, a.k, w->v_ids, w->v_scores, w->v_n, nullptr, 0.0, 1e-9, fin_ids, fin_scores,
+                            fin_n, nullptr, nullptr, st),
+           "slab merge");
+        ck(hm::launch_sum_slab_postings(nq, split, w->v_post, fin_post, st), "slab postings");
+    }
     if (timing) ck(cudaEventRecord(w->ev[1], st), "event");
 }
 
@@ -249,7 +302,7 @@ int hm_bridge_search_batch(hm_bridge* X, const hm_bridge_batch* b, hm_results* o
             a.out_post = w->out_post;
             // row stride of the results is k (the caller's layout)
             const bool timing = (b->flags & HM_FLAG_TIMING) != 0;
-            run(X, a, w, st, timing);
+            run(X, a, w, st, timing, b->flags);
             if (b->k) {
                 ck(cudaMemcpyAsync(out->ids, w->out_ids, static_cast<uint64_t>(nq) * b->k * 8, cudaMemcpyDeviceToHost, st),
                    "D2H ids");
@@ -293,7 +346,7 @@ int hm_bridge_search_batch_device(hm_bridge* X, const hm_bridge_batch* b, hm_res
             a.out_n = out->n;
             a.out_post = out->postings;
             const bool timing = (b->flags & HM_FLAG_TIMING) != 0;
-            run(X, a, w, st, timing);
+            run(X, a, w, st, timing, b->flags);
             // the workspace (scratch, counters) is reusable once the kernel ends
             ck(cudaStreamSynchronize(st), "bridge sync");
             if (timing) ck(cudaEventElapsedTime(&g_ms_bridge, w->ev[0], w->ev[1]), "elapsed");

@@ -119,9 +119,18 @@ __global__ void __launch_bounds__(kBrThreads) bridge_kernel(BridgeDev ix, Bridge
         __syncthreads();
         const uint32_t q = S.q;
         if (q >= a.nq) break;
+        // small batches: query q is the (q / nq_real)-th row slab of real
+        // query q % nq_real (merged afterwards like doc shards)
+        const uint32_t qr = a.split > 1 ? q % a.nq_real : q;
+        uint32_t row_lo = a.row_lo, row_hi = a.row_hi;
+        if (a.split > 1) {
+            const uint64_t sp = a.row_hi - a.row_lo, s = q / a.nq_real;
+            row_lo = a.row_lo + static_cast<uint32_t>(sp * s / a.split);
+            row_hi = a.row_lo + static_cast<uint32_t>(sp * (s + 1) / a.split);
+        }
         // ---- the query's known terms, in its (ascending) order (bridge.cpp:120-123)
         if (warp == 0) {
-            const uint64_t o0 = a.q_off[q], o1 = a.q_off[q + 1];
+            const uint64_t o0 = a.q_off[qr], o1 = a.q_off[qr + 1];
             uint32_t cnt = 0;
             // (device batches: a query longer than m_max is refused, n = 0 and
             // postings = ~0; the host entry point sizes m_max itself)
@@ -145,7 +154,7 @@ __global__ void __launch_bounds__(kBrThreads) bridge_kernel(BridgeDev ix, Bridge
         }
         __syncthreads();
         const uint32_t m = S.m;
-        if (m == 0 || m == kNone || a.row_hi <= a.row_lo) {
+        if (m == 0 || m == kNone || row_hi <= row_lo) {
             if (tid == 0) {
                 a.out_n[q] = 0;
                 if (a.out_post) a.out_post[q] = m == kNone ? ~0ull : 0ull;
@@ -153,9 +162,9 @@ __global__ void __launch_bounds__(kBrThreads) bridge_kernel(BridgeDev ix, Bridge
             continue;
         }
         // ---- my span of the window, and each term's cursor at its start
-        const uint32_t span = a.row_hi - a.row_lo;
-        const uint32_t lo_w = a.row_lo + static_cast<uint32_t>((static_cast<uint64_t>(span) * warp) / kBrWarps);
-        const uint32_t hi_w = a.row_lo + static_cast<uint32_t>((static_cast<uint64_t>(span) * (warp + 1)) / kBrWarps);
+        const uint32_t span = row_hi - row_lo;
+        const uint32_t lo_w = row_lo + static_cast<uint32_t>((static_cast<uint64_t>(span) * warp) / kBrWarps);
+        const uint32_t hi_w = row_lo + static_cast<uint32_t>((static_cast<uint64_t>(span) * (warp + 1)) / kBrWarps);
         auto lower_bound = [&](uint64_t lo, uint64_t hi, uint32_t row) {
             while (lo < hi) {
                 const uint64_t mid = (lo + hi) >> 1;

@@ -24,6 +24,7 @@ struct BridgeArgs {
     const double* q_val;
     uint32_t k;
     uint32_t row_lo, row_hi;
+    uint32_t split, nq_real;   // split > 1: query q = slab q / nq_real of real query q % nq_real
     uint32_t m_max;            // >= every query's nnz (scratch stride)
     uint64_t* scratch;         // [grid][(3 + 2 * 8) * m_max]
     uint32_t* counters;        // [0] query cursor

@@ -265,3 +265,22 @@ def test_bridge_gpu_degenerate_indexes(gpu):
     assert nopost.bridge_topk(search.SparseVector([0, 1], [1.0, 2.0]), 3) == []
     one = search.bridge_ingest([(9, search.SparseVector([2], [0.25]))])
     assert one.bridge_topk(search.SparseVector([0, 1, 2, 7], [1.0, 1.0, 4.0, 1.0]), 100) == [(9, 1.0)]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("nq,k", [(1, 10), (7, 3), (40, 50)])
+def test_bridge_small_batches_split_into_row_slabs(gpu, nq, k):
+    """Small bridge batches run as row-slab queries merged like doc shards:
+    identical to the unsplit run and to the reference (ids, bits, postings)."""
+    rng = np.random.default_rng(nq * 100 + k)
+    docs = random_vectors(rng, 80000, 800, 0.01)
+    ids = rng.permutation(200000)[:80000].astype(np.uint64)
+    rb = ref.RefBridge.from_vectors(ids, docs)
+    bi = _dev(ids, docs)
+    qs = random_queries(rng, nq, 800, 0.05)
+    want = rb.topk_batch(qs, k)
+    got = bi.search_batch(to_sv(qs), k)
+    assert_same(got, want, f"split nq={nq} k={k}")
+    one = bi.dev.search_batch(to_sv(qs), k, flags=search.HM_FLAG_NO_SPLIT)
+    for key in ("ids", "scores", "n", "postings"):
+        assert (np.asarray(got[key]).view(np.uint8) == np.asarray(one[key]).view(np.uint8)).all(), key
