@@ -262,18 +262,33 @@ __global__ void __launch_bounds__(kTcThreads, 1)
                     m = fmaxf(m, __uint_as_float(v[31]));
                     cmax[c] = m;
                     if (valid && m > top[KT - 1]) {
+                        if (t - t0 < 2) {  // warm-up tiles: every value (a tight bound early)
 #pragma unroll
-                        for (int i = 0; i < 32; ++i) {
-                            float x = __uint_as_float(v[i]);
-                            if (x > top[KT - 1]) {
+                            for (int i = 0; i < 32; ++i) {
+                                float x = __uint_as_float(v[i]);
+                                if (x > top[KT - 1]) {
 #pragma unroll
-                                for (int j = 0; j < KT; ++j)
-                                    if (x > top[j]) {
-                                        const float y = top[j];
-                                        top[j] = x;
-                                        x = y;
-                                    }
+                                    for (int j = 0; j < KT; ++j)
+                                        if (x > top[j]) {
+                                            const float y = top[j];
+                                            top[j] = x;
+                                            x = y;
+                                        }
+                                }
                             }
+                        } else {  // then only the chunk maximum: still real rows' values
+                            // (a valid bound; the top-k values of a slab almost never
+                            // share a 32-row chunk), and the insertion network runs once
+                            // per chunk instead of per value -- per value it cost ~2x the
+                            // epilogue, since some lane of the warp nearly always inserts
+                            float x = m;
+#pragma unroll
+                            for (int j = 0; j < KT; ++j)
+                                if (x > top[j]) {
+                                    const float y = top[j];
+                                    top[j] = x;
+                                    x = y;
+                                }
                         }
                     }
                 }
