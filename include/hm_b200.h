@@ -73,7 +73,7 @@ typedef struct {
     uint32_t n_queries;
     const uint32_t* q_off;     /* [n_queries + 1] */
     const uint32_t* q_tid;     /* [q_off[n_queries]] */
-    uint32_t k;                /* top-k; 0 gives empty results */
+    uint32_t k;                /* top-k, any value; 0 gives empty results */
     double k1, b;              /* hybrid::Bm25Params */
     const double* tau;         /* [n_queries] per-query skip threshold, or NULL */
     double tau_default;        /* CascadeConfig::conf_threshold (0.10) */
@@ -125,6 +125,13 @@ int hm_search_batch(hm_index* index, const hm_query_batch* batch, hm_results* ou
  * synchronisation.  `n_queries` etc. are read from the host struct. */
 int hm_search_batch_device(hm_index* index, const hm_query_batch* batch_dev,
                            hm_results* out_dev, void* stream);
+
+/* Queries of the last batch on this thread that ran on the wide path
+ * (kernels/wide.cu): every query when k > 256, else those whose plan has more
+ * than 256 distinct terms.  The wide path scores exhaustively in fp64 in plan
+ * order and ranks by an exact radix select + sort: any k, any query length,
+ * the reference's bits (csr_index.hpp:72-79 has no cap on either). */
+int hm_last_batch_wide(uint32_t* n_wide);
 
 /* Statistics of the last batch on this thread: queries that fell back to the
  * exact fp64 kernel (candidate overflow or non-positive impacts), kernel

@@ -33,7 +33,7 @@
 
 namespace {
 
-thread_local uint32_t g_last_exact = 0, g_last_launches = 0, g_last_handed = 0, g_last_graph = 0;
+thread_local uint32_t g_last_exact = 0, g_last_launches = 0, g_last_handed = 0, g_last_graph = 0, g_last_wide = 0;
 thread_local float g_ms_plan = 0.f, g_ms_search = 0.f, g_ms_exact = 0.f, g_ms_seed = 0.f;
 
 using hm_host::ck;
@@ -77,7 +77,7 @@ struct Workspace {
     // device
     uint32_t *q_off = nullptr, *q_tid = nullptr, *plan_tid = nullptr, *plan_mult = nullptr,
              *plan_len = nullptr, *order_in = nullptr, *order = nullptr, *counters = nullptr,
-             *exact_list = nullptr, *out_n = nullptr, *fb_list = nullptr;
+             *exact_list = nullptr, *out_n = nullptr, *fb_list = nullptr, *wide_list = nullptr;
     uint64_t *cost = nullptr, *cost_sorted = nullptr, *out_ids = nullptr, *out_post = nullptr;
     double *tau = nullptr, *out_scores = nullptr, *out_conf = nullptr;
     float* w32 = nullptr;
@@ -95,6 +95,18 @@ struct Workspace {
     double* v_scores = nullptr;
     uint32_t* v_n = nullptr;
     uint64_t v_cap = 0, vk_cap = 0;
+    // the wide path (kernels/wide.cu): k > 256 or > 256 distinct terms
+    double* wd_scores = nullptr;
+    uint64_t wd_scores_cap = 0;
+    uint32_t* wd_hist = nullptr;
+    hm::WideState* wd_st = nullptr;
+    uint32_t wd_g_cap = 0;
+    hm::WideCand* wd_cand = nullptr;
+    uint64_t wd_cand_cap = 0;
+    void* wd_sort = nullptr;
+    size_t wd_sort_bytes = 0;
+    uint32_t* wd_iota = nullptr;
+    uint32_t wd_iota_cap = 0;
     // CUDA graph of the batch's launch sequence, replayed while a batch's
     // arguments repeat (serving loops): captured on the second identical batch
     cudaGraphExec_t gexec = nullptr;
@@ -109,12 +121,12 @@ struct Workspace {
     void free_dev() {
         drop_graph();
         void* ps[] = {q_off, q_tid, plan_tid, plan_mult, plan_len, order_in, order, counters,
-                      exact_list, fb_list, out_n, cost, cost_sorted, out_ids, out_post, tau, out_scores,
-                      out_conf, w32, out_skip, sort_tmp};
+                      exact_list, fb_list, wide_list, out_n, cost, cost_sorted, out_ids, out_post, tau,
+                      out_scores, out_conf, w32, out_skip, sort_tmp};
         for (void* p : ps)
             if (p) cudaFree(p);
         q_off = q_tid = plan_tid = plan_mult = plan_len = order_in = order = counters = exact_list =
-            out_n = fb_list = nullptr;
+            out_n = fb_list = wide_list = nullptr;
         cost = cost_sorted = out_ids = out_post = nullptr;
         tau = out_scores = out_conf = nullptr;
         w32 = nullptr;
@@ -124,7 +136,7 @@ struct Workspace {
     ~Workspace() {
         drop_graph();
         free_dev();
-        void* vs[] = {v_ids, v_post, v_scores, v_n};
+        void* vs[] = {v_ids, v_post, v_scores, v_n, wd_scores, wd_hist, wd_st, wd_cand, wd_sort, wd_iota};
         for (void* p : vs)
             if (p) cudaFree(p);
         if (stab) cudaFree(stab);
@@ -512,6 +524,7 @@ void ensure(Workspace* w, uint32_t nq, uint32_t ntid, uint32_t k, bool need_io) 
         dalloc(w->counters, 8);
         dalloc(w->exact_list, NQ);
         dalloc(w->fb_list, NQ);
+        dalloc(w->wide_list, NQ);
         dalloc(w->cost, NQ);
         dalloc(w->cost_sorted, NQ);
         dalloc(w->tau, NQ);
@@ -612,6 +625,7 @@ void run_batch(hm_index* X, Workspace* w, const hm_query_batch& hb, const uint32
     a.order = w->order;
     a.counters = w->counters;
     a.exact_list = w->exact_list;
+    a.wide_list = w->wide_list;
     a.stab_stride = X->dev.n_tiles + 2;
     const uint64_t words = 2ull * X->grid_search * hm::kMaxTerms * a.stab_stride;  // up to 2 CTAs per SM
     if (w->stab_words < words) {
@@ -763,6 +777,110 @@ void run_batch(hm_index* X, Workspace* w, const hm_query_batch& hb, const uint32
     g_last_graph = 1;
 }
 
+// Arguments of the wide path for a planned batch (plan arrays in w).
+hm::BatchArgs wide_args(const hm_index* X, const Workspace* w, const hm_query_batch& hb, const uint32_t* d_off,
+                        const uint32_t* d_tid, const double* d_tau, const hm_results& out) {
+    hm::BatchArgs a{};
+    a.nq = hb.n_queries;
+    a.k = hb.k;
+    a.q_off = d_off;
+    a.q_tid = d_tid;
+    a.k1 = hb.k1;
+    a.b = hb.b;
+    a.tau = d_tau;
+    a.tau_default = hb.tau_default;
+    a.eps = hb.epsilon_guard;
+    a.row_lo = hb.row_lo;
+    a.row_hi = hb.row_hi == 0 ? X->dev.n_docs : std::min(hb.row_hi, X->dev.n_docs);
+    a.flags = hb.flags;
+    a.split = 1;
+    a.nq_real = hb.n_queries;
+    a.plan_tid = w->plan_tid;
+    a.plan_mult = w->plan_mult;
+    a.plan_len = w->plan_len;
+    a.cost = w->cost;
+    a.order = w->order;
+    a.counters = w->counters;
+    a.out_ids = out.ids;
+    a.out_scores = out.scores;
+    a.out_n = out.n;
+    a.out_conf = out.conf;
+    a.out_skip = out.skip;
+    a.out_post = out.postings;
+    return a;
+}
+
+// The wide path over queries d_qlist[0..n) of a planned batch: groups of G
+// queries whose fp64 score rows fit a 1 GiB budget (kernels/wide.cu).
+void run_wide(hm_index* X, Workspace* w, const hm::BatchArgs& a, const uint32_t* d_qlist, uint32_t n) {
+    if (n == 0) return;
+    cudaStream_t st = w->stream;
+    const uint64_t span = a.row_hi > a.row_lo ? a.row_hi - a.row_lo : 0;
+    const uint64_t k = std::max<uint32_t>(a.k, 1u);
+    uint64_t G = 64;
+    if (span) G = std::min<uint64_t>(G, std::max<uint64_t>(1, (1ull << 30) / (span * 8ull)));
+    G = std::min<uint64_t>(G, std::max<uint64_t>(1, (256ull << 20) / (k * sizeof(hm::WideCand))));
+    G = std::min<uint64_t>(G, n);
+    const size_t sb = hm::wide_sort_bytes(G * k);
+    if (G * span > w->wd_scores_cap || G > w->wd_g_cap || G * k > w->wd_cand_cap || sb > w->wd_sort_bytes) {
+        ck(cudaStreamSynchronize(st), "sync");
+        void* ps[] = {w->wd_scores, w->wd_hist, w->wd_st, w->wd_cand, w->wd_sort};
+        for (void* p : ps)
+            if (p) cudaFree(p);
+        w->wd_scores = nullptr;
+        w->wd_hist = nullptr;
+        w->wd_st = nullptr;
+        w->wd_cand = nullptr;
+        w->wd_sort = nullptr;
+        w->wd_scores_cap = std::max(G * span, w->wd_scores_cap);
+        w->wd_g_cap = static_cast<uint32_t>(std::max<uint64_t>(G, w->wd_g_cap));
+        w->wd_cand_cap = std::max(G * k, w->wd_cand_cap);
+        w->wd_sort_bytes = std::max(sb, w->wd_sort_bytes);
+        dalloc(w->wd_scores, w->wd_scores_cap);
+        dalloc(w->wd_hist, w->wd_g_cap * 256ull);
+        dalloc(w->wd_st, w->wd_g_cap);
+        dalloc(w->wd_cand, w->wd_cand_cap);
+        unsigned char* t = nullptr;
+        dalloc(t, std::max<size_t>(w->wd_sort_bytes, 16));
+        w->wd_sort = t;
+    }
+    for (uint64_t g0 = 0; g0 < n; g0 += G) {
+        hm::WideArgs wa{};
+        wa.G = static_cast<uint32_t>(std::min<uint64_t>(G, n - g0));
+        wa.qlist = d_qlist + g0;
+        wa.span = static_cast<uint32_t>(span);
+        wa.scores = w->wd_scores;
+        wa.hist = w->wd_hist;
+        wa.st = w->wd_st;
+        wa.cand = w->wd_cand;
+        ck(hm::launch_wide_group(X->dev, a, wa, w->wd_sort, w->wd_sort_bytes, st), "wide path");
+    }
+    g_last_wide += n;
+}
+
+// A batch with k > kMaxK: plan, then every query on the wide path.
+void run_wide_batch(hm_index* X, Workspace* w, const hm_query_batch& hb, const uint32_t* d_off, const uint32_t* d_tid,
+                    const double* d_tau, const hm_results& out) {
+    const uint32_t nq = hb.n_queries;
+    cudaStream_t st = w->stream;
+    if (nq > w->wd_iota_cap) {
+        ck(cudaStreamSynchronize(st), "sync");
+        if (w->wd_iota) cudaFree(w->wd_iota);
+        w->wd_iota = nullptr;
+        dalloc(w->wd_iota, nq);
+        std::vector<uint32_t> io(nq);
+        for (uint32_t i = 0; i < nq; ++i) io[i] = i;
+        ck(cudaMemcpy(w->wd_iota, io.data(), nq * 4ull, cudaMemcpyHostToDevice), "iota");
+        w->wd_iota_cap = nq;
+    }
+    hm::BatchArgs a = wide_args(X, w, hb, d_off, d_tid, d_tau, out);
+    ck(cudaMemsetAsync(w->counters, 0, 8 * sizeof(uint32_t), st), "memset counters");
+    ck(hm::launch_plan(X->dev, a, w->order_in, st), "plan kernel");
+    g_last_launches = 1;
+    g_last_graph = 0;
+    run_wide(X, w, a, w->wd_iota, nq);
+}
+
 void read_timing(Workspace* w) {
     ck(cudaEventSynchronize(w->ev[3]), "event sync");
     ck(cudaEventElapsedTime(&g_ms_plan, w->ev[0], w->ev[1]), "elapsed");
@@ -815,10 +933,16 @@ bool ensure_baked(hm_index* X, double k1, double b, std::shared_lock<std::shared
 
 void validate(const hm_index* X, const hm_query_batch* b) {
     if (!b) throw std::invalid_argument("null batch");
-    if (b->k > static_cast<uint32_t>(hm::kMaxK))
-        throw std::invalid_argument("k exceeds the supported maximum of 256");
     if (b->n_queries && (!b->q_off)) throw std::invalid_argument("q_off is required");
     (void)X;
+}
+
+// the batch's longest query (raw term count): plans longer than kMaxTerms
+// distinct terms are only possible above it
+uint32_t max_query_len(const uint32_t* q_off, uint32_t nq) {
+    uint32_t m = 0;
+    for (uint32_t i = 0; i < nq; ++i) m = std::max(m, q_off[i + 1] - q_off[i]);
+    return m;
 }
 
 }  // namespace
@@ -882,12 +1006,21 @@ int hm_search_batch(hm_index* X, const hm_query_batch* b, hm_results* out) {
             if (b->q_tid[i] != hm::kNoTerm && b->q_tid[i] >= X->dev.n_terms)
                 throw std::out_of_range("term id out of range");
         ck(cudaSetDevice(X->device), "cudaSetDevice");
+        // k > 256: the wide path for the whole batch; queries longer than 256
+        // terms: no row slabs, and the ones whose plans exceed 256 distinct
+        // terms are served by the wide path after the batch
+        const bool wide_all = b->k > static_cast<uint32_t>(hm::kMaxK);
+        const bool long_any = max_query_len(b->q_off, nq) > static_cast<uint32_t>(hm::kMaxTerms);
+        g_last_wide = 0;
         std::shared_lock<std::shared_mutex> bake_lk;
-        const bool baked = ensure_baked(X, b->k1, b->b, bake_lk);
+        const bool baked = wide_all ? false : ensure_baked(X, b->k1, b->b, bake_lk);
         Workspace* w = acquire(X);
         try {
             const uint32_t k = std::max(b->k, 1u);
-            ensure(w, nq * split_for(X, *b), std::max(ntid, 1u), k, true);
+            hm_query_batch hb = *b;
+            if (!baked) hb.flags |= HM_FLAG_FORCE_EXACT;
+            if (long_any) hb.flags |= HM_FLAG_NO_SPLIT;
+            ensure(w, nq * (wide_all ? 1 : split_for(X, hb)), std::max(ntid, 1u), k, true);
             unsigned char* p = w->pin;
             auto take = [&](size_t bytes) {
                 unsigned char* r = p;
@@ -912,11 +1045,20 @@ int hm_search_batch(hm_index* X, const hm_query_batch* b, hm_results* out) {
             ck(cudaMemcpyAsync(w->q_off, poff, (nq + 1ull) * 4, cudaMemcpyHostToDevice, st), "H2D");
             if (ntid) ck(cudaMemcpyAsync(w->q_tid, ptid, ntid * 4ull, cudaMemcpyHostToDevice, st), "H2D");
             if (b->tau) ck(cudaMemcpyAsync(w->tau, ptau, nq * 8ull, cudaMemcpyHostToDevice, st), "H2D");
-            hm_query_batch hb = *b;
-            if (!baked) hb.flags |= HM_FLAG_FORCE_EXACT;
             hm_results dout{w->out_ids, w->out_scores, w->out_n, w->out_conf, w->out_skip, w->out_post};
             // the k used on device must match the output stride
-            run_batch(X, w, hb, w->q_off, w->q_tid, b->tau ? w->tau : nullptr, dout, pw);
+            if (wide_all) {
+                run_wide_batch(X, w, hb, w->q_off, w->q_tid, b->tau ? w->tau : nullptr, dout);
+            } else {
+                run_batch(X, w, hb, w->q_off, w->q_tid, b->tau ? w->tau : nullptr, dout, pw);
+                if (long_any) {  // plans beyond 256 distinct terms: the wide path
+                    ck(cudaMemcpyAsync(rcnt, w->counters, 32, cudaMemcpyDeviceToHost, st), "D2H");
+                    ck(cudaStreamSynchronize(st), "batch");
+                    if (b->flags & HM_FLAG_TIMING) read_timing(w);
+                    run_wide(X, w, wide_args(X, w, hb, w->q_off, w->q_tid, b->tau ? w->tau : nullptr, dout),
+                             w->wide_list, rcnt[6]);
+                }
+            }
             const size_t kk = b->k;
             if (kk) {
                 ck(cudaMemcpyAsync(rids, w->out_ids, nq * kk * 8, cudaMemcpyDeviceToHost, st), "D2H");
@@ -928,7 +1070,7 @@ int hm_search_batch(hm_index* X, const hm_query_batch* b, hm_results* out) {
             ck(cudaMemcpyAsync(rpost, w->out_post, nq * 8ull, cudaMemcpyDeviceToHost, st), "D2H");
             ck(cudaMemcpyAsync(rcnt, w->counters, 32, cudaMemcpyDeviceToHost, st), "D2H");
             ck(cudaStreamSynchronize(st), "batch");
-            if (b->flags & HM_FLAG_TIMING) read_timing(w);
+            if ((b->flags & HM_FLAG_TIMING) && !wide_all && !long_any) read_timing(w);
             g_last_exact = rcnt[1];
             g_last_handed = rcnt[4];
             if (rcnt[3] & hm::kErrTooManyTerms)
@@ -963,22 +1105,39 @@ int hm_search_batch_device(hm_index* X, const hm_query_batch* b, hm_results* out
         // the batch's tid count is unknown on the host: plan scratch is sized
         // from q_off[nq] read back once (a 4-byte D2H on the caller's stream)
         cudaStream_t ust = static_cast<cudaStream_t>(stream);
-        std::shared_lock<std::shared_mutex> bake_lk;
-        const bool baked = ensure_baked(X, b->k1, b->b, bake_lk);
-        uint32_t ntid = 0;
-        ck(cudaMemcpyAsync(&ntid, b->q_off + nq, 4, cudaMemcpyDeviceToHost, ust), "D2H q_off");
+        // (q_off is read back whole: a query longer than kMaxTerms terms
+        // disables row slabs and may need the wide path)
+        std::vector<uint32_t> hoff(nq + 1ull);
+        ck(cudaMemcpyAsync(hoff.data(), b->q_off, (nq + 1ull) * 4, cudaMemcpyDeviceToHost, ust), "D2H q_off");
         ck(cudaStreamSynchronize(ust), "sync");
+        const uint32_t ntid = hoff[nq];
+        const bool wide_all = b->k > static_cast<uint32_t>(hm::kMaxK);
+        const bool long_any = max_query_len(hoff.data(), nq) > static_cast<uint32_t>(hm::kMaxTerms);
+        g_last_wide = 0;
+        std::shared_lock<std::shared_mutex> bake_lk;
+        const bool baked = wide_all ? false : ensure_baked(X, b->k1, b->b, bake_lk);
         Workspace* w = acquire(X);
         try {
-            ensure(w, nq * split_for(X, *b), std::max(ntid, 1u), std::max(b->k, 1u), false);
+            hm_query_batch hb = *b;
+            if (!baked) hb.flags |= HM_FLAG_FORCE_EXACT;
+            if (long_any) hb.flags |= HM_FLAG_NO_SPLIT;
+            ensure(w, nq * (wide_all ? 1 : split_for(X, hb)), std::max(ntid, 1u), std::max(b->k, 1u), false);
             // order the workspace stream after the caller's stream and back
             cudaEvent_t ev;
             ck(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming), "event");
             ck(cudaEventRecord(ev, ust), "event record");
             ck(cudaStreamWaitEvent(w->stream, ev, 0), "wait");
-            hm_query_batch hb = *b;
-            if (!baked) hb.flags |= HM_FLAG_FORCE_EXACT;
-            run_batch(X, w, hb, b->q_off, b->q_tid, b->tau, *out, reinterpret_cast<float*>(w->pin));
+            if (wide_all) {
+                run_wide_batch(X, w, hb, b->q_off, b->q_tid, b->tau, *out);
+            } else {
+                run_batch(X, w, hb, b->q_off, b->q_tid, b->tau, *out, reinterpret_cast<float*>(w->pin));
+                if (long_any) {
+                    uint32_t* rc = reinterpret_cast<uint32_t*>(w->pin) + hm::kMaxCodes;
+                    ck(cudaMemcpyAsync(rc, w->counters, 32, cudaMemcpyDeviceToHost, w->stream), "D2H counters");
+                    ck(cudaStreamSynchronize(w->stream), "sync");
+                    run_wide(X, w, wide_args(X, w, hb, b->q_off, b->q_tid, b->tau, *out), w->wide_list, rc[6]);
+                }
+            }
             ck(cudaEventRecord(ev, w->stream), "event record");
             ck(cudaStreamWaitEvent(ust, ev, 0), "wait");
             if (b->flags & HM_FLAG_TIMING) {  // plus the batch counters (32 B D2H)
@@ -991,7 +1150,7 @@ int hm_search_batch_device(hm_index* X, const hm_query_batch* b, hm_results* out
             // pinned w32 staging is reused by the next call on this workspace:
             // make sure the async upload finished before handing it back
             ck(cudaStreamSynchronize(w->stream), "sync");
-            if (b->flags & HM_FLAG_TIMING) read_timing(w);
+            if ((b->flags & HM_FLAG_TIMING) && !wide_all) read_timing(w);
             cudaEventDestroy(ev);
         } catch (...) {
             cudaStreamSynchronize(w->stream);
@@ -1005,6 +1164,11 @@ int hm_search_batch_device(hm_index* X, const hm_query_batch* b, hm_results* out
 int hm_last_batch_stats(uint32_t* n_exact, uint32_t* n_launches) {
     if (n_exact) *n_exact = g_last_exact;
     if (n_launches) *n_launches = g_last_launches;
+    return HM_OK;
+}
+
+int hm_last_batch_wide(uint32_t* n_wide) {
+    if (n_wide) *n_wide = g_last_wide;
     return HM_OK;
 }
 

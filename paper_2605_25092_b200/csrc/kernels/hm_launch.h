@@ -40,6 +40,11 @@ cudaError_t launch_merge(uint32_t n_shards, uint32_t nq, uint32_t k, const uint6
 uint32_t bake_ks(double k1);
 cudaError_t launch_bake(const DevIndex& ix, const uint32_t* long_terms, uint32_t n_long, double k1,
                         double b, uint32_t ks, uint32_t* bk, uint32_t* err, cudaStream_t st);
+// the wide path (wide.cu): one group of w.G queries, any k and plan length;
+// plan arrays of `a` must be filled (launch_plan)
+size_t wide_sort_bytes(uint64_t n_items);
+cudaError_t launch_wide_group(const DevIndex& ix, const BatchArgs& a, const WideArgs& w, void* sort_tmp,
+                              size_t sort_bytes, cudaStream_t st);
 // resident CTAs per SM of the two persistent kernels
 cudaError_t search_occupancy(int* search_blocks_per_sm, int* exact_blocks_per_sm);
 cudaError_t search_occupancy_fast(int* blocks);

@@ -146,6 +146,9 @@ struct BatchArgs {
                                // [2]=work cursor exact, [3]=error flags,
                                // [4]=queries handed over, [5]=exhaustive cursor after the seeded pass
     uint32_t* exact_list;      // [nq]
+    uint32_t* wide_list;       // [nq] queries with more than kMaxTerms distinct terms
+                               // (counters[6] entries) for the wide path (wide.cu);
+                               // null: such a query sets kErrTooManyTerms
     uint32_t* fb_list;         // [nq] 1 = the seeded kernel handed the query to the
                                // exhaustive kernel (which walks `order` with cursor
                                // counters[5] and skips the others); null: every query
@@ -159,6 +162,29 @@ struct BatchArgs {
     double* out_conf;
     uint8_t* out_skip;
     uint64_t* out_post;
+};
+
+// The wide path (kernels/wide.cu): any k, any plan length, fp64 exhaustive.
+struct WideState {
+    uint64_t pre_hi, pre_lo;   // key prefix of the k-th document found so far
+    uint64_t post;             // postings_touched of the query
+    uint32_t kr;               // rank of the k-th document inside the prefix group
+    uint32_t done, take_all;   // selection finished; every positive document qualifies
+    uint32_t n_c;              // candidates emitted
+};
+struct WideCand {
+    uint32_t g;                // query slot in the group (sort key 1)
+    uint64_t bits;             // score bits (desc), 0 = padding
+    uint64_t id;               // DocId (asc)
+};
+struct WideArgs {
+    uint32_t G;                // queries in the group
+    const uint32_t* qlist;     // [G] batch query indices
+    uint32_t span;             // rows of the window
+    double* scores;            // [G][span] fp64 scores
+    uint32_t* hist;            // [G][256]
+    WideState* st;             // [G]
+    WideCand* cand;            // [G][k]
 };
 
 constexpr uint32_t kErrTooManyTerms = 1u;

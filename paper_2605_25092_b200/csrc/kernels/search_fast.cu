@@ -91,8 +91,10 @@ __global__ void __launch_bounds__(kCons, 2) search_fast_kernel(DevIndex ix, Batc
         const uint32_t poff = a.q_off[qr];
         const uint32_t m = a.plan_len[qr];
         const uint32_t k = a.k;
-        if (m > kMaxTerms) {
-            if (tid == 0) {
+        if (m > kMaxTerms) {  // the wide path (wide.cu) serves it after the batch
+            if (tid == 0 && a.wide_list) {
+                a.wide_list[atomicAdd(&a.counters[6], 1u)] = q;
+            } else if (tid == 0) {
                 atomicOr(&a.counters[3], kErrTooManyTerms);
                 a.out_n[q] = 0;
                 if (a.out_post) a.out_post[q] = 0;

@@ -465,7 +465,12 @@ __global__ void __launch_bounds__(kCons, HM_SEED_MINB) search_seed_kernel(DevInd
                 if (lane >= o) v += nb;
             }
             const bool isne = static_cast<uint32_t>(lane) < m && v * f_ub < te;
-            const uint32_t ne = __reduce_or_sync(0xffffffffu, isne ? 1u << S.msorder[lane] : 0u);
+            // t* is never non-essential: its postings are the seeds, and the
+            // candidate pass recognises seed rows only by probing t* (a term
+            // tied with t*'s bound can sort after it and stay essential).
+            // The bound sum still includes t*: an over-estimate, safe.
+            const uint32_t ne =
+                __reduce_or_sync(0xffffffffu, isne ? 1u << S.msorder[lane] : 0u) & ~(1u << S.n_long);
             const uint32_t bal = __ballot_sync(0xffffffffu, isne);
             const float ub = bal ? __shfl_sync(0xffffffffu, v, 31 - __clz(bal)) : 0.f;
             if (lane == 0) S.ubne_q = ub;

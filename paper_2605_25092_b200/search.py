@@ -112,6 +112,7 @@ def lib():
     L.hm_last_batch_timing.argtypes = [P(C.c_float), P(C.c_float), P(C.c_float)]
     L.hm_last_batch_seed.argtypes = [P(C.c_float), P(C.c_uint32)]
     L.hm_last_batch_graph.argtypes = [P(C.c_uint32)]
+    L.hm_last_batch_wide.argtypes = [P(C.c_uint32)]
     L.hm_hidx_load.argtypes = [C.c_char_p, P(C.c_void_p)]
     L.hm_hidx_last_error.restype = C.c_char_p
     L.hm_hidx_view.argtypes = [C.c_void_p, P(CsrView), P(C.c_uint32), P(C.c_double), P(C.c_double)]
@@ -307,6 +308,14 @@ def last_graph():
     return m.value
 
 
+def last_wide():
+    """Queries of this thread's last batch served by the wide path (k > 256 or
+    plans of more than 256 distinct terms; kernels/wide.cu)."""
+    n = C.c_uint32()
+    lib().hm_last_batch_wide(C.byref(n))
+    return n.value
+
+
 def last_seed():
     """(ms_seed, n_handed_over): the seeded MaxScore pass of this thread's last
     batch (its time on HM_FLAG_TIMING batches; queries left to the exhaustive kernel)."""
@@ -406,6 +415,7 @@ class CsrIndex:
         self.build_params = build_params or Bm25Params()
         self.device = device
         self._dev = None
+        self._maxscores = {}
 
     @classmethod
     def load(cls, path, device=0):
@@ -485,7 +495,12 @@ class CsrIndex:
     def query_upper_bound(self, query_terms, term_maxscores=None):
         """Sum of the known query terms' maxscores, duplicates counted
         (csr_index.hpp:84-86)."""
-        ms = self.compute_term_maxscores(self.build_params) if term_maxscores is None else term_maxscores
+        if term_maxscores is None:  # cached per build parameters (one pass over P)
+            key = (self.build_params.k1, self.build_params.b)
+            if key not in self._maxscores:
+                self._maxscores[key] = self.compute_term_maxscores(self.build_params)
+            term_maxscores = self._maxscores[key]
+        ms = term_maxscores
         ub = 0.0
         for t in query_terms:
             i = self.vocab.get(t)

@@ -276,3 +276,80 @@ def test_small_batches_split_into_row_slabs(c1, nq, k):
         ref_run = c1["dev"].search_lists(tids, k, k1=k1, b=b, row_lo=lo, row_hi=hi, flags=search.HM_FLAG_NO_SPLIT)
         for key in ("ids", "scores", "n", "conf", "skip", "postings"):
             assert (np.asarray(got[key]).view(np.uint8) == np.asarray(ref_run[key]).view(np.uint8)).all(), key
+
+
+def test_seed_term_tied_with_another_term(gpu):
+    """Two terms that always appear together (same df, same max impact) tie on
+    the MaxScore bound.  The seeded pass picks the first as its seed t*; the
+    bound-ascending prefix may then cover t* but not its twin, and the seed
+    rows reached again through the twin's postings must still be recognised
+    as seen (duplicates in the top-k otherwise).  The reference's
+    bm25_topk / bm25_topk_maxscore on its own build are the oracle."""
+    rng = np.random.default_rng(99)
+    docs = []
+    for d in range(3000):
+        words = ["f%d" % int(rng.integers(0, 400)) for _ in range(5)]
+        if d % 50 == 7:
+            words[:2] = ["qa", "qb"]          # 60 docs: the twins, always together
+        if d % 3 == 0:
+            words[4] = "cc"                   # a frequent third term, lower bound
+        docs.append((d, " ".join(words)))
+    ri = ref.RefIndex.from_texts(docs, ref.TOK_MINIMAL)
+    idx = export_to_csr(ri)
+    for q in (["qa", "qb", "cc"], ["qb", "qa"], ["cc", "qa", "qb", "f3"]):
+        for k in (1, 10, 50):
+            want_ids, want_sc, _ = ri.search(q, k)
+            for flags in (0, search.HM_FLAG_SEED_ALL):
+                got = idx.bm25_topk(q, k, flags=flags)
+                ids = [g[0] for g in got]
+                assert len(set(ids)) == len(ids), f"{q} k={k}: duplicate DocIds {ids}"
+                assert_same(ids, [g[1] for g in got], want_ids, want_sc, f"{q} k={k} flags={flags}")
+
+
+@pytest.mark.parametrize("k", [257, 1000, 5000])
+def test_k_above_256_wide_path(c1, k):
+    """The reference's bm25_topk takes any k (csr_index.hpp:72-79; collect_topk
+    has no cap, csr_index.cpp:50-59): k > 256 runs on the wide path
+    (kernels/wide.cu) -- bit-identical ids, scores, counts, conf, skip and
+    postings, including queries with fewer than k positive documents and a
+    row window."""
+    tids = c1["tids"][:40]
+    got = c1["dev"].search_lists(tids, k)
+    assert search.last_wide() == len(tids)
+    ids, sc, n, post = c1["orc"].topk(tids, k)
+    check_batch(got, ids, sc, n, post, what=f"wide k={k}")
+    n_docs = len(c1["hx"].doc_ids)
+    got = c1["dev"].search_lists(tids, k, row_lo=777, row_hi=n_docs - 12345, k1=0.9, b=0.4)
+    w = c1["orc"].topk(tids, k, row_lo=777, row_hi=n_docs - 12345, k1=0.9, b=0.4)
+    check_batch(got, *w, what=f"wide k={k} window")
+
+
+def test_more_than_256_distinct_terms(c1):
+    """make_plan accepts any query length (csr_index.cpp:31-48): plans of more
+    than 256 distinct terms are served by the wide path inside an ordinary
+    batch; the other queries of the batch keep the fast kernels."""
+    rng = np.random.default_rng(5)
+    V = len(c1["hx"].idf)
+    longq = [rng.choice(V, size=n, replace=False).astype(np.uint32) for n in (257, 300, 1000)]
+    longq.append(np.concatenate([longq[0], longq[0][:50], [search.NO_TERM] * 3]).astype(np.uint32))
+    tids = list(c1["tids"][:30]) + longq + list(c1["tids"][30:60])
+    for k in (10, 100):
+        got = c1["dev"].search_lists(tids, k)
+        assert search.last_wide() == 4
+        ids, sc, n, post = c1["orc"].topk(tids, k)
+        check_batch(got, ids, sc, n, post, what=f"long plans k={k}")
+    got = c1["dev"].search_lists(longq, 10, tau=np.full(len(longq), 0.0))
+    assert (got["skip"] == 1).all()
+
+
+def test_many_ties_at_the_kth_score(gpu):
+    """A single-term query over documents with equal (tf, len) ties on its
+    score everywhere: the k-th document is decided by DocId alone
+    (types.hpp:21-25).  DocIds run against the row order."""
+    docs = [(10_000 - d, " ".join(["aa"] + ["z%d" % (d % 7)] * 4)) for d in range(3000)]
+    ri = ref.RefIndex.from_texts(docs, ref.TOK_MINIMAL)
+    idx = export_to_csr(ri)
+    for k in (5, 256, 300, 2999, 3000, 4000):
+        want_ids, want_sc, _ = ri.search(["aa"], k)
+        got = idx.bm25_topk(["aa"], k)
+        assert_same([g[0] for g in got], [g[1] for g in got], want_ids, want_sc, f"ties k={k}")
