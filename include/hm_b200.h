@@ -120,6 +120,19 @@ typedef struct {
  * cascade::confidence + the skip decision (src/cascade.cpp:10-21, 67-92). */
 int hm_search_batch(hm_index* index, const hm_query_batch* batch, hm_results* out);
 
+/* The batch searched inside each of n_parts contiguous row ranges
+ * [part_row[p], part_row[p+1]) separately (part_row ascending, <= n_docs; the
+ * batch's row_lo/row_hi are ignored): one launch sequence whose (query, part)
+ * pairs are scheduled together.  Results are per part, row-major
+ * [n_parts][n_queries][k] (ids, scores), [n_parts][n_queries] (n, postings);
+ * conf and skip are not written.  Replaces: the per-partition loop of
+ * TemporalIndex::topk (src/temporal_index.cpp:72-123) -- every partition of
+ * the budget at once over a partition-ordered flat index, the caller merging
+ * the per-partition lists in the reference's order (its upper-bound stop
+ * only decides which of them it keeps). */
+int hm_search_batch_parts(hm_index* index, const hm_query_batch* batch, uint32_t n_parts,
+                          const uint32_t* part_row, hm_results* out_parts);
+
 /* Same with DEVICE buffers (batch arrays and results on the index's device),
  * enqueued on `stream` (a cudaStream_t, NULL = legacy default) without host
  * synchronisation.  `n_queries` etc. are read from the host struct. */
@@ -295,6 +308,23 @@ int hm_dense_last_timing(float* ms_kernels);
  * whose candidate list overflowed (rescored over every row) and the total
  * number of candidates. */
 int hm_dense_last_stats(uint32_t* path, uint32_t* n_overflow, uint64_t* n_candidates);
+
+/* ---------------------------------------------------------------- strings
+ * Query strings -> term ids (the vocabulary lookup of make_plan,
+ * src/csr_index.cpp:31-48, and the whitespace split of load_queries_tsv,
+ * src/io.cpp:389-391).  hm_vocab_create copies terms[tid] (the CsrIndex's
+ * alphabetical `terms`; lens NULL = NUL-terminated).  hm_vocab_resolve splits
+ * query i = text[text_off[i] .. text_off[i+1]) on C-locale whitespace and
+ * writes q_off[n_queries + 1] and q_tid (0xFFFFFFFF for an unknown term) --
+ * exactly hm_query_batch's q_off / q_tid; HM_ERR_RANGE when the tokens exceed
+ * tid_cap (*n_tids holds the count).  n_threads 0 = hardware concurrency
+ * (batches under 4,096 queries resolve on the calling thread). */
+typedef struct hm_vocab hm_vocab;
+int hm_vocab_create(const char* const* terms, const uint32_t* lens, uint32_t n_terms, hm_vocab** out);
+void hm_vocab_destroy(hm_vocab* vocab);
+uint32_t hm_vocab_size(const hm_vocab* vocab);
+int hm_vocab_resolve(const hm_vocab* vocab, uint32_t n_queries, const char* text, const uint64_t* text_off,
+                     uint32_t* q_off, uint32_t* q_tid, uint64_t tid_cap, uint64_t* n_tids, uint32_t n_threads);
 
 /* Margin confidence over a ranked score list (src/cascade.cpp:10-21). */
 double hm_margin(const double* scores, uint32_t n, double epsilon_guard);

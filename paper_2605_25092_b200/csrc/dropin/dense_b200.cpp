@@ -15,6 +15,7 @@
 #include <unordered_map>
 #include <vector>
 
+#include "dropin_common.hpp"
 #include "hm_b200.h"
 #include "hybrid/dense.hpp"
 
@@ -22,40 +23,29 @@ namespace hybrid {
 
 namespace {
 
-void throw_on(int rc) {
-    if (rc == HM_OK) return;
-    const std::string msg = hm_last_error();
-    if (rc == HM_ERR_INVALID) throw std::invalid_argument(msg);
-    if (rc == HM_ERR_RANGE) throw std::out_of_range(msg);
-    throw std::runtime_error(msg);
-}
+using hm_dropin::throw_on;
 
-// one device copy per EmbeddingMatrix, uploaded on first search; the
-// fingerprint catches a matrix that was modified (add) or re-created
+// one device copy per EmbeddingMatrix (LRU); the fingerprint catches a matrix
+// that was modified (add) or re-created
 struct DenseEntry {
+    const void* key = nullptr;
+    uint64_t fp = 0;
     hm_dense* h = nullptr;
-    const void* data = nullptr;
-    const void* ids = nullptr;
-    std::size_t n = 0;
-    std::uint32_t dim = 0;
-};
-
-hm_dense* device_matrix(const EmbeddingMatrix& m) {
-    static std::mutex mu;
-    static std::unordered_map<const EmbeddingMatrix*, DenseEntry> cache;
-    std::lock_guard<std::mutex> lk(mu);
-    DenseEntry& e = cache[&m];
-    if (e.h && e.data == m.data.data() && e.ids == m.doc_ids.data() && e.n == m.count() && e.dim == m.dim)
-        return e.h;
-    if (e.h) {
-        hm_dense_destroy(e.h);
-        e.h = nullptr;
+    ~DenseEntry() {
+        if (h) hm_dense_destroy(h);
     }
-    hm_dense_view v{m.dim, static_cast<uint32_t>(m.count()), m.data.data(), m.doc_ids.data()};
-    hm_dense* h = nullptr;
-    throw_on(hm_dense_create(&v, 0, &h));
-    e = DenseEntry{h, m.data.data(), m.doc_ids.data(), m.count(), m.dim};
-    return h;
+};
+using Cache = hm_dropin::LruCache<DenseEntry>;
+
+Cache::Ptr device_matrix(const EmbeddingMatrix& m) {
+    static Cache cache(4);
+    uint64_t fp = hm_dropin::mix(11, m.dim);
+    fp = hm_dropin::sample(fp, m.data);
+    fp = hm_dropin::sample(fp, m.doc_ids);
+    return cache.get(&m, fp, [&](DenseEntry& e) {
+        hm_dense_view v{m.dim, static_cast<uint32_t>(m.count()), m.data.data(), m.doc_ids.data()};
+        throw_on(hm_dense_create(&v, 0, &e.h));
+    });
 }
 
 }  // namespace
@@ -70,7 +60,8 @@ RankedList dense_topk(const EmbeddingMatrix& matrix, const std::vector<float>& q
     std::vector<double> sc(kk);
     uint32_t n = 0;
     hm_results r{ids.data(), sc.data(), &n, nullptr, nullptr, nullptr};
-    throw_on(hm_dense_search_batch(device_matrix(matrix), &b, &r));
+    auto e = device_matrix(matrix);
+    throw_on(hm_dense_search_batch(e->h, &b, &r));
     out.entries.reserve(n);
     for (uint32_t i = 0; i < n; ++i) out.entries.emplace_back(ids[i], sc[i]);
     return out;

@@ -87,6 +87,8 @@ struct Workspace {
     uint32_t* stab = nullptr;  // per-CTA short-term tile tables
     uint64_t stab_words = 0;
     uint32_t* seed_scratch = nullptr;  // per-CTA seeded-pass scratch
+    uint32_t* slab_row = nullptr;      // part boundaries of hm_search_batch_parts
+    uint32_t slab_cap = 0;
     // pinned host staging
     unsigned char* pin = nullptr;
     size_t pin_bytes = 0;
@@ -141,6 +143,7 @@ struct Workspace {
             if (p) cudaFree(p);
         if (stab) cudaFree(stab);
         if (seed_scratch) cudaFree(seed_scratch);
+        if (slab_row) cudaFree(slab_row);
         for (auto e : ev)
             if (e) cudaEventDestroy(e);
         if (pin) cudaFreeHost(pin);
@@ -601,8 +604,12 @@ uint32_t split_for(const hm_index* X, const hm_query_batch& hb) {
     return S >= 2 ? S : 1;
 }
 
+// d_slab_row (n_parts + 1 device boundaries): every query is searched inside
+// each part separately; the per-part lists stay in the workspace's v_* arrays
+// ([part][query][k]) instead of being merged (hm_search_batch_parts)
 void run_batch(hm_index* X, Workspace* w, const hm_query_batch& hb, const uint32_t* d_off,
-               const uint32_t* d_tid, const double* d_tau, const hm_results& out, float* pin_w32) {
+               const uint32_t* d_tid, const double* d_tau, const hm_results& out, float* pin_w32,
+               uint32_t n_parts = 0, const uint32_t* d_slab_row = nullptr) {
     const uint32_t nq = hb.n_queries;
     hm::BatchArgs a{};
     a.nq = nq;
@@ -637,18 +644,20 @@ void run_batch(hm_index* X, Workspace* w, const hm_query_batch& hb, const uint32
         w->stab_words = words;
     }
     a.stab = w->stab;
-    if (!w->seed_scratch) dalloc(w->seed_scratch, 2ull * X->grid_search * hm::kSeedScratch);  // up to 2 CTAs per SM
-    a.seed_scratch = w->seed_scratch;
+    a.seed_half = std::max<uint32_t>(1, std::min<uint32_t>(hm::kSeedScratch / 2, X->dev.n_docs));
+    a.seed_scratch = w->seed_scratch;  // allocated below when the seeded pass runs
     a.out_ids = out.ids;
     a.out_scores = out.scores;
     a.out_n = out.n;
     a.out_conf = out.conf;
     a.out_skip = out.skip;
     a.out_post = out.postings;
-    const uint32_t split = split_for(X, hb);
+    const uint32_t split = d_slab_row ? n_parts : split_for(X, hb);
     a.split = split;
     a.nq_real = nq;
-    if (split > 1) {  // slab queries: results into the workspace, decisions at the merge
+    a.slab_row = d_slab_row;
+    const bool merge = split > 1 && !d_slab_row;
+    if (split > 1 || d_slab_row) {  // slab queries: results into the workspace, decisions at the merge
         const uint64_t nv = static_cast<uint64_t>(nq) * split;
         if (nv > w->v_cap || hb.k > w->vk_cap) {
             ck(cudaStreamSynchronize(w->stream), "sync");
@@ -684,8 +693,12 @@ void run_batch(hm_index* X, Workspace* w, const hm_query_batch& hb, const uint32
     // every query cheap on the exhaustive kernel: no seeded pass)
     const bool seeded = !(a.flags & (HM_FLAG_EXHAUSTIVE | HM_FLAG_FORCE_EXACT)) &&
                         ((a.flags & HM_FLAG_SEED_ALL) || 4ull * (a.row_hi - a.row_lo) >= X->dev.n_docs);
-    if (seeded) a.fb_list = w->fb_list;
-    g_last_launches = (seeded ? 4 : 3) + (split > 1 ? 3 : 0);  // ours: plan, [seeded,] exhaustive, exact
+    if (seeded) {
+        a.fb_list = w->fb_list;
+        if (!w->seed_scratch) dalloc(w->seed_scratch, 2ull * X->grid_search * 2ull * a.seed_half);  // up to 2 CTAs per SM
+        a.seed_scratch = w->seed_scratch;
+    }
+    g_last_launches = (seeded ? 4 : 3) + (split > 1 ? 1 : 0) + (merge ? 2 : 0);  // ours: plan, [seeded,] exhaustive, exact
                                                              // [+ expand, merge, postings] (plus CUB's sort)
     auto enqueue = [&] {
         ck(cudaMemcpyAsync(w->w32, pin_w32, hm::kMaxCodes * sizeof(float), cudaMemcpyHostToDevice, st),
@@ -712,7 +725,7 @@ void run_batch(hm_index* X, Workspace* w, const hm_query_batch& hb, const uint32
         ck(hm::launch_search(X->dev, a, X->grid_search, st), "search kernel");
         if (timing) ck(cudaEventRecord(w->ev[2], st), "event");
         ck(hm::launch_exact(X->dev, a, X->grid_exact, st), "exact kernel");
-        if (split > 1) {  // the slabs' exact lists -> the real queries' top-k, Margin, skip
+        if (merge) {  // the slabs' exact lists -> the real queries' top-k, Margin, skip
             ck(hm::launch_merge(split, nq, hb.k, w->v_ids, w->v_scores, w->v_n, d_tau, hb.tau_default,
                                 hb.epsilon_guard, out.ids, out.scores, out.n, out.conf, out.skip, st),
                "slab merge");
@@ -991,8 +1004,16 @@ int hm_index_format(const hm_index* X, uint32_t* row_bits, uint32_t* code_bits, 
     });
 }
 
-int hm_search_batch(hm_index* X, const hm_query_batch* b, hm_results* out) {
-    return guard([&] {
+}  // extern "C"
+
+namespace {
+
+// The host-buffer batch (hm_search_batch), or with n_parts > 0 the batch
+// searched inside each of the parts [part_row[p], part_row[p+1]) separately
+// (hm_search_batch_parts): outputs [n_parts][n_queries][k], no conf / skip.
+void search_host(hm_index* X, const hm_query_batch* b, hm_results* out, uint32_t n_parts,
+                 const uint32_t* part_row) {
+    {
         if (!X || !out) throw std::invalid_argument("null argument");
         validate(X, b);
         const uint32_t nq = b->n_queries;
@@ -1011,6 +1032,34 @@ int hm_search_batch(hm_index* X, const hm_query_batch* b, hm_results* out) {
         // terms are served by the wide path after the batch
         const bool wide_all = b->k > static_cast<uint32_t>(hm::kMaxK);
         const bool long_any = max_query_len(b->q_off, nq) > static_cast<uint32_t>(hm::kMaxTerms);
+        if (n_parts) {
+            if (!part_row) throw std::invalid_argument("part_row is required");
+            for (uint32_t p = 0; p < n_parts; ++p)
+                if (part_row[p + 1] < part_row[p]) throw std::invalid_argument("part_row not ascending");
+            if (part_row[n_parts] > X->dev.n_docs) throw std::out_of_range("part_row beyond the index's rows");
+            const uint64_t kk = b->k;
+            if (wide_all || long_any || part_row[n_parts] == part_row[0]) {  // part by part
+                uint32_t wide = 0;
+                for (uint32_t p = 0; p < n_parts; ++p) {
+                    const uint64_t o = static_cast<uint64_t>(p) * nq;
+                    hm_results r{out->ids + o * kk, out->scores + o * kk, out->n + o, nullptr, nullptr,
+                                 out->postings ? out->postings + o : nullptr};
+                    if (part_row[p] == part_row[p + 1]) {  // (row_hi = 0 would mean "every row")
+                        std::fill(r.n, r.n + nq, 0u);
+                        if (r.postings) std::fill(r.postings, r.postings + nq, 0ull);
+                        continue;
+                    }
+                    hm_query_batch hb = *b;
+                    hb.row_lo = part_row[p];
+                    hb.row_hi = part_row[p + 1];
+                    search_host(X, &hb, &r, 0, nullptr);
+                    wide += g_last_wide;
+                }
+                g_last_wide = wide;
+                return;
+            }
+        }
+        const uint32_t nv = nq * std::max(n_parts, 1u);  // result rows
         g_last_wide = 0;
         std::shared_lock<std::shared_mutex> bake_lk;
         const bool baked = wide_all ? false : ensure_baked(X, b->k1, b->b, bake_lk);
@@ -1020,7 +1069,11 @@ int hm_search_batch(hm_index* X, const hm_query_batch* b, hm_results* out) {
             hm_query_batch hb = *b;
             if (!baked) hb.flags |= HM_FLAG_FORCE_EXACT;
             if (long_any) hb.flags |= HM_FLAG_NO_SPLIT;
-            ensure(w, nq * (wide_all ? 1 : split_for(X, hb)), std::max(ntid, 1u), k, true);
+            if (n_parts) {
+                hb.row_lo = part_row[0];
+                hb.row_hi = part_row[n_parts];
+            }
+            ensure(w, n_parts ? nv : nq * (wide_all ? 1 : split_for(X, hb)), std::max(ntid, 1u), k, true);
             unsigned char* p = w->pin;
             auto take = [&](size_t bytes) {
                 unsigned char* r = p;
@@ -1031,13 +1084,14 @@ int hm_search_batch(hm_index* X, const hm_query_batch* b, hm_results* out) {
             uint32_t* poff = reinterpret_cast<uint32_t*>(take((nq + 1ull) * 4));
             uint32_t* ptid = reinterpret_cast<uint32_t*>(take(ntid * 4ull));
             double* ptau = reinterpret_cast<double*>(take(nq * 8ull));
-            uint64_t* rids = reinterpret_cast<uint64_t*>(take(static_cast<size_t>(nq) * k * 8));
-            double* rsc = reinterpret_cast<double*>(take(static_cast<size_t>(nq) * k * 8));
-            uint32_t* rn = reinterpret_cast<uint32_t*>(take(nq * 4ull));
+            uint64_t* rids = reinterpret_cast<uint64_t*>(take(static_cast<size_t>(nv) * k * 8));
+            double* rsc = reinterpret_cast<double*>(take(static_cast<size_t>(nv) * k * 8));
+            uint32_t* rn = reinterpret_cast<uint32_t*>(take(nv * 4ull));
             double* rconf = reinterpret_cast<double*>(take(nq * 8ull));
             uint8_t* rskip = take(nq);
-            uint64_t* rpost = reinterpret_cast<uint64_t*>(take(nq * 8ull));
+            uint64_t* rpost = reinterpret_cast<uint64_t*>(take(nv * 8ull));
             uint32_t* rcnt = reinterpret_cast<uint32_t*>(take(32));
+            uint32_t* prow = reinterpret_cast<uint32_t*>(take((n_parts + 1ull) * 4));
             std::memcpy(poff, b->q_off, (nq + 1ull) * 4);
             if (ntid) std::memcpy(ptid, b->q_tid, ntid * 4ull);
             if (b->tau) std::memcpy(ptau, b->tau, nq * 8ull);
@@ -1047,7 +1101,19 @@ int hm_search_batch(hm_index* X, const hm_query_batch* b, hm_results* out) {
             if (b->tau) ck(cudaMemcpyAsync(w->tau, ptau, nq * 8ull, cudaMemcpyHostToDevice, st), "H2D");
             hm_results dout{w->out_ids, w->out_scores, w->out_n, w->out_conf, w->out_skip, w->out_post};
             // the k used on device must match the output stride
-            if (wide_all) {
+            if (n_parts) {  // every part a slab of each query, lists left in v_*
+                if (n_parts + 1 > w->slab_cap) {
+                    ck(cudaStreamSynchronize(st), "sync");
+                    if (w->slab_row) cudaFree(w->slab_row);
+                    w->slab_row = nullptr;
+                    dalloc(w->slab_row, n_parts + 1ull);
+                    w->slab_cap = n_parts + 1;
+                }
+                std::memcpy(prow, part_row, (n_parts + 1ull) * 4);
+                ck(cudaMemcpyAsync(w->slab_row, prow, (n_parts + 1ull) * 4, cudaMemcpyHostToDevice, st), "H2D");
+                run_batch(X, w, hb, w->q_off, w->q_tid, nullptr, dout, pw, n_parts, w->slab_row);
+                dout = hm_results{w->v_ids, w->v_scores, w->v_n, nullptr, nullptr, w->v_post};
+            } else if (wide_all) {
                 run_wide_batch(X, w, hb, w->q_off, w->q_tid, b->tau ? w->tau : nullptr, dout);
             } else {
                 run_batch(X, w, hb, w->q_off, w->q_tid, b->tau ? w->tau : nullptr, dout, pw);
@@ -1061,13 +1127,15 @@ int hm_search_batch(hm_index* X, const hm_query_batch* b, hm_results* out) {
             }
             const size_t kk = b->k;
             if (kk) {
-                ck(cudaMemcpyAsync(rids, w->out_ids, nq * kk * 8, cudaMemcpyDeviceToHost, st), "D2H");
-                ck(cudaMemcpyAsync(rsc, w->out_scores, nq * kk * 8, cudaMemcpyDeviceToHost, st), "D2H");
+                ck(cudaMemcpyAsync(rids, dout.ids, nv * kk * 8, cudaMemcpyDeviceToHost, st), "D2H");
+                ck(cudaMemcpyAsync(rsc, dout.scores, nv * kk * 8, cudaMemcpyDeviceToHost, st), "D2H");
             }
-            ck(cudaMemcpyAsync(rn, w->out_n, nq * 4ull, cudaMemcpyDeviceToHost, st), "D2H");
-            ck(cudaMemcpyAsync(rconf, w->out_conf, nq * 8ull, cudaMemcpyDeviceToHost, st), "D2H");
-            ck(cudaMemcpyAsync(rskip, w->out_skip, nq, cudaMemcpyDeviceToHost, st), "D2H");
-            ck(cudaMemcpyAsync(rpost, w->out_post, nq * 8ull, cudaMemcpyDeviceToHost, st), "D2H");
+            ck(cudaMemcpyAsync(rn, dout.n, nv * 4ull, cudaMemcpyDeviceToHost, st), "D2H");
+            if (!n_parts) {
+                ck(cudaMemcpyAsync(rconf, dout.conf, nq * 8ull, cudaMemcpyDeviceToHost, st), "D2H");
+                ck(cudaMemcpyAsync(rskip, dout.skip, nq, cudaMemcpyDeviceToHost, st), "D2H");
+            }
+            ck(cudaMemcpyAsync(rpost, dout.postings, nv * 8ull, cudaMemcpyDeviceToHost, st), "D2H");
             ck(cudaMemcpyAsync(rcnt, w->counters, 32, cudaMemcpyDeviceToHost, st), "D2H");
             ck(cudaStreamSynchronize(st), "batch");
             if ((b->flags & HM_FLAG_TIMING) && !wide_all && !long_any) read_timing(w);
@@ -1076,22 +1144,38 @@ int hm_search_batch(hm_index* X, const hm_query_batch* b, hm_results* out) {
             if (rcnt[3] & hm::kErrTooManyTerms)
                 throw std::invalid_argument("a query has more than 256 distinct terms");
             if (rcnt[3] & 2u) throw std::runtime_error("exact kernel failed to converge");
-            for (uint32_t i = 0; i < nq; ++i) {
+            for (uint32_t i = 0; i < nv; ++i) {
                 out->n[i] = rn[i];
                 for (uint32_t j = 0; j < rn[i]; ++j) {
                     out->ids[i * kk + j] = rids[i * kk + j];
                     out->scores[i * kk + j] = rsc[i * kk + j];
                 }
             }
-            if (out->conf) std::memcpy(out->conf, rconf, nq * 8ull);
-            if (out->skip) std::memcpy(out->skip, rskip, nq);
-            if (out->postings) std::memcpy(out->postings, rpost, nq * 8ull);
+            if (out->conf && !n_parts) std::memcpy(out->conf, rconf, nq * 8ull);
+            if (out->skip && !n_parts) std::memcpy(out->skip, rskip, nq);
+            if (out->postings) std::memcpy(out->postings, rpost, nv * 8ull);
         } catch (...) {
             cudaStreamSynchronize(w->stream);
             release(X, w);
             throw;
         }
         release(X, w);
+    }
+}
+
+}  // namespace
+
+extern "C" {
+
+int hm_search_batch(hm_index* X, const hm_query_batch* b, hm_results* out) {
+    return guard([&] { search_host(X, b, out, 0, nullptr); });
+}
+
+int hm_search_batch_parts(hm_index* X, const hm_query_batch* b, uint32_t n_parts, const uint32_t* part_row,
+                          hm_results* out) {
+    return guard([&] {
+        if (n_parts == 0) throw std::invalid_argument("n_parts must be >= 1");
+        search_host(X, b, out, n_parts, part_row);
     });
 }
 

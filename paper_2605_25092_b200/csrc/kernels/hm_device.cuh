@@ -229,6 +229,11 @@ __device__ __forceinline__ void query_window(const BatchArgs& a, uint32_t q, uin
     }
     qr = q % a.nq_real;
     const uint32_t s = q / a.nq_real;
+    if (a.slab_row) {
+        lo = a.slab_row[s];
+        hi = a.slab_row[s + 1];
+        return;
+    }
     const uint64_t span = a.row_hi - a.row_lo;
     lo = a.row_lo + static_cast<uint32_t>(span * s / a.split);
     hi = a.row_lo + static_cast<uint32_t>(span * (s + 1) / a.split);

@@ -135,6 +135,8 @@ struct BatchArgs {
     // [row_lo, row_hi); plan arrays are per real query, results per slab
     // query (merged afterwards by merge_kernel)
     uint32_t split, nq_real;
+    const uint32_t* slab_row;  // [split + 1] explicit slab boundaries (partitions), or null:
+                               // equal slabs of [row_lo, row_hi)
     const float* w32;          // [kMaxCodes] idf-free impacts for (k1, b)
     // planner scratch (device)
     uint32_t* plan_tid;        // [q_off[nq]] plan of query i at q_off[i]
@@ -153,7 +155,8 @@ struct BatchArgs {
                                // exhaustive kernel (which walks `order` with cursor
                                // counters[5] and skips the others); null: every query
     uint32_t* stab;            // per-CTA short-term tile tables
-    uint32_t* seed_scratch;    // per-CTA seeded-pass scratch: kSeedScratch words (scores, rows)
+    uint32_t* seed_scratch;    // per-CTA seeded-pass scratch: 2 * seed_half words (scores, rows)
+    uint32_t seed_half;        // min(kSeedScratch / 2, n_docs): the largest seed set of the index
     uint32_t stab_stride;      // words per short term (>= n_tiles + 2)
     // results (device)
     uint64_t* out_ids;

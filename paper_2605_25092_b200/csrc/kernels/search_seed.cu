@@ -257,7 +257,8 @@ __global__ void __launch_bounds__(kCons, HM_SEED_MINB) search_seed_kernel(DevInd
     const double k1 = a.k1, bb = a.b;
     const uint32_t stride = a.stab_stride;
     uint32_t* stab = a.stab + static_cast<uint64_t>(blockIdx.x) * kMaxTerms * stride;
-    float* sA = reinterpret_cast<float*>(a.seed_scratch + static_cast<uint64_t>(blockIdx.x) * kSeedScratch);  // seed scores
+    // seed scores, then seed rows (n_seed <= min(kSeedMaxDf, n_docs) = seed_half)
+    float* sA = reinterpret_cast<float*>(a.seed_scratch + static_cast<uint64_t>(blockIdx.x) * 2u * a.seed_half);
     const uint32_t kmax = FastCfg<CAPW>::kMaxKServed;
 
     for (int i = tid; i < 16 * CAPW; i += kCons) S.acc[i] = 0.f;
@@ -398,7 +399,7 @@ __global__ void __launch_bounds__(kCons, HM_SEED_MINB) search_seed_kernel(DevInd
         // and complete score land at the posting's index in the scratch
         const uint64_t sw0 = S.t_wlo[ts];
         const uint32_t n_seed = static_cast<uint32_t>(S.t_end[ts] - sw0);
-        uint32_t* sR = reinterpret_cast<uint32_t*>(sA) + kSeedMaxDf;  // seed rows
+        uint32_t* sR = reinterpret_cast<uint32_t*>(sA) + a.seed_half;  // seed rows
 #ifndef HM_SEED_KP
 #define HM_SEED_KP 4
 #endif

@@ -90,7 +90,9 @@ EXPORTS = ["hm_dense_create", "hm_dense_destroy", "hm_dense_search_batch", "hm_d
            "hm_hidx_load", "hm_hidx_last_error", "hm_hidx_view", "hm_hidx_term", "hm_hidx_maxscores",
            "hm_hidx_free", "hm_htix_load", "hm_htix_flat", "hm_htix_partitions", "hm_htix_params",
            "hm_htix_free",
-           "hm_merge_shards_device", "hm_margin", "hm_last_error"]
+           "hm_merge_shards_device", "hm_margin", "hm_last_error", "hm_search_batch_parts",
+           "hm_last_batch_wide", "hm_vocab_create", "hm_vocab_destroy", "hm_vocab_size",
+           "hm_vocab_resolve"]
 
 
 def lib():
@@ -113,6 +115,13 @@ def lib():
     L.hm_last_batch_seed.argtypes = [P(C.c_float), P(C.c_uint32)]
     L.hm_last_batch_graph.argtypes = [P(C.c_uint32)]
     L.hm_last_batch_wide.argtypes = [P(C.c_uint32)]
+    L.hm_search_batch_parts.argtypes = [C.c_void_p, P(QueryBatch), C.c_uint32, C.c_void_p, P(Results)]
+    L.hm_vocab_create.argtypes = [C.c_void_p, C.c_void_p, C.c_uint32, P(C.c_void_p)]
+    L.hm_vocab_destroy.argtypes = [C.c_void_p]
+    L.hm_vocab_size.argtypes = [C.c_void_p]
+    L.hm_vocab_size.restype = C.c_uint32
+    L.hm_vocab_resolve.argtypes = [C.c_void_p, C.c_uint32, C.c_char_p, C.c_void_p, C.c_void_p,
+                                   C.c_void_p, C.c_uint64, P(C.c_uint64), C.c_uint32]
     L.hm_hidx_load.argtypes = [C.c_char_p, P(C.c_void_p)]
     L.hm_hidx_last_error.restype = C.c_char_p
     L.hm_hidx_view.argtypes = [C.c_void_p, P(CsrView), P(C.c_uint32), P(C.c_double), P(C.c_double)]
@@ -267,6 +276,24 @@ class DeviceIndex:
             out["scores"] = out["scores"][:, :0]
         return out
 
+    def search_parts(self, q_off, q_tid, k, part_row, k1=1.2, b=0.75, flags=0):
+        """hm_search_batch_parts: every query searched inside each row range
+        [part_row[p], part_row[p+1]) separately.  Returns dict(ids[P,nq,k],
+        scores[P,nq,k], n[P,nq], postings[P,nq])."""
+        q_off = np.ascontiguousarray(q_off, np.uint32)
+        q_tid = np.ascontiguousarray(q_tid, np.uint32)
+        part_row = np.ascontiguousarray(part_row, np.uint32)
+        nq, P = len(q_off) - 1, len(part_row) - 1
+        kk = max(int(k), 1)
+        out = dict(ids=np.zeros((P, nq, kk), np.uint64), scores=np.zeros((P, nq, kk), np.float64),
+                   n=np.zeros((P, nq), np.uint32), postings=np.zeros((P, nq), np.uint64))
+        qb = QueryBatch(nq, _ptr(q_off), _ptr(q_tid) if len(q_tid) else None, int(k), k1, b,
+                        None, 0.10, 1e-9, 0, 0, flags)
+        r = Results(_ptr(out["ids"]), _ptr(out["scores"]), _ptr(out["n"]), None, None,
+                    _ptr(out["postings"]))
+        _check(lib().hm_search_batch_parts(self._h, C.byref(qb), P, _ptr(part_row), C.byref(r)))
+        return out
+
     def search_lists(self, tid_lists, k, **kw):
         off = np.zeros(len(tid_lists) + 1, np.uint32)
         off[1:] = np.cumsum([len(t) for t in tid_lists])
@@ -306,6 +333,50 @@ def last_graph():
     m = C.c_uint32()
     lib().hm_last_batch_graph(C.byref(m))
     return m.value
+
+
+class Vocab:
+    """hm_vocab: term strings -> term ids for whole batches of query strings
+    (make_plan's lookup, csr_index.cpp:31-48; the whitespace split of
+    load_queries_tsv, io.cpp:389-391), resolved by native threads."""
+
+    def __init__(self, terms):
+        enc = [t.encode() for t in terms]
+        arr = (C.c_char_p * max(len(enc), 1))(*enc)
+        lens = np.array([len(e) for e in enc] or [0], np.uint32)
+        h = C.c_void_p()
+        _check(lib().hm_vocab_create(arr, _ptr(lens), len(enc), C.byref(h)))
+        self._h = h
+
+    def __len__(self):
+        return lib().hm_vocab_size(self._h)
+
+    def resolve_text(self, text, text_off, n_threads=0):
+        """text: bytes of all queries; text_off[nq+1] byte offsets -> (q_off, q_tid)."""
+        text_off = np.ascontiguousarray(text_off, np.uint64)
+        nq = len(text_off) - 1
+        q_off = np.zeros(nq + 1, np.uint32)
+        cap = max(len(text) // 2 + 1, 1)  # a token takes >= 1 byte + 1 separator
+        q_tid = np.zeros(cap, np.uint32)
+        n = C.c_uint64()
+        _check(lib().hm_vocab_resolve(self._h, nq, text, _ptr(text_off), _ptr(q_off), _ptr(q_tid),
+                                      cap, C.byref(n), n_threads))
+        return q_off, q_tid[:n.value]
+
+    def resolve(self, queries, n_threads=0):
+        """list of query strings -> (q_off, q_tid)."""
+        enc = [q.encode() for q in queries]
+        off = np.zeros(len(enc) + 1, np.uint64)
+        off[1:] = np.cumsum([len(e) for e in enc])
+        return self.resolve_text(b"".join(enc), off, n_threads)
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib().hm_vocab_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        self.close()
 
 
 def last_wide():

@@ -16,6 +16,7 @@
 #include "hybrid/csr_index.hpp"
 #include "hybrid/dense.hpp"
 #include "hybrid/temporal_index.hpp"
+#include "hybrid_b200.hpp"
 
 using namespace hybrid;
 
@@ -130,6 +131,32 @@ int main() {
                 TemporalStats st;
                 RankedList r = tidx.topk(q, k, Bm25Params{}, &st, ub != 0);
                 print_list(r, " " + std::to_string(st.partitions_searched));
+            } else if (cmd == "QBATCH" || cmd == "TBATCH") {  // k ub n, then n query lines: one GPU batch
+                std::size_t k, n;
+                int ub;
+                in >> k >> ub >> n;
+                std::vector<std::vector<std::string>> qs(n);
+                for (auto& q : qs) {
+                    std::getline(std::cin, line);
+                    std::istringstream ql(line);
+                    for (std::string t; ql >> t;) q.push_back(t);
+                }
+                if (cmd == "QBATCH") {
+                    std::vector<SearchStats> st;
+                    std::vector<hybrid_b200::Decision> dec;
+                    auto r = hybrid_b200::bm25_topk_batch(idx, qs, k, Bm25Params{}, &st, &dec, 0.10);
+                    for (std::size_t i = 0; i < n; ++i)
+                        print_list(r[i], " " + std::to_string(st[i].postings_touched) + " " + hexd(dec[i].conf) +
+                                             " " + std::to_string(dec[i].skip ? 1 : 0));
+                } else {
+                    std::vector<TemporalStats> st;
+                    auto r = hybrid_b200::temporal_topk_batch(tidx, qs, k, Bm25Params{}, &st, ub != 0);
+                    for (std::size_t i = 0; i < n; ++i)
+                        print_list(r[i], " " + std::to_string(st[i].partitions_searched) + " " +
+                                             std::to_string(st[i].early_stopped ? 1 : 0));
+                }
+            } else if (cmd == "NCACHED") {
+                std::cout << "V " << hybrid_b200::cached_device_indexes() << '\n';
             } else if (cmd == "BDOCS") {  // n lines of "id nnz i:v ..."
                 std::size_t n;
                 in >> n;

@@ -39,6 +39,16 @@ def parse(line):
     return ids, sc, extra
 
 
+def parse_ext(line, n_extra):
+    """R n x1 .. x_{n_extra} id:score ... -> (ids, scores, [x1 ..])"""
+    parts = line.split()
+    assert parts[0] == "R", line
+    n = int(parts[1])
+    extra = parts[2:2 + n_extra]
+    ent = parts[2 + n_extra:2 + n_extra + n]
+    return [int(x.split(":")[0]) for x in ent], [float.fromhex(x.split(":")[1]) for x in ent], extra
+
+
 def bits(xs):
     return np.asarray(xs, np.float64).view(np.uint64).tolist()
 
@@ -194,4 +204,53 @@ def test_dense_and_cascade_dropin_match_reference(gpu):
             assert esc == 1 and c_ids == [x for x, _ in want] and bits(c_sc) == bits([s for _, s in want])
     assert n_esc > 5
     assert d.send(["DBADDIM"])[0] == "THROW invalid_argument query dimension mismatch"
+    d.close()
+
+
+def test_batch_entries_match_reference_and_cache_is_bounded(gpu):
+    """hybrid_b200::bm25_topk_batch / temporal_topk_batch (include/hybrid_b200.hpp):
+    one GPU batch per call, result i == the reference's per-query call on
+    query i (ids, score bits, postings, Margin/skip, partitions searched); the
+    drop-in's device cache stays bounded (LRU) however many indexes are built."""
+    rng = np.random.default_rng(41)
+    d = Driver()
+    for trial in range(12):
+        docs, _ = random_instance(rng)
+        d.send([f"DOCS {len(docs)}"] + [f"{i}\t{t}" for i, t in docs], expect=0)
+        assert d.send(["INDEX 0 1.2 0.75"])[0].startswith("OK")
+        ri = ref.RefIndex.from_texts(docs, ref.TOK_MINIMAL)
+        qs = [random_instance(rng)[1] for _ in range(25)] + [[], ["zz_unknown"]]
+        k = 1 + int(rng.integers(0, 12))
+        lines = d.send([f"QBATCH {k} 1 {len(qs)}"] + [" ".join(q) for q in qs], expect=len(qs))
+        for q, line in zip(qs, lines):
+            ids, sc, (post, conf, skip) = parse_ext(line, 3)
+            post, conf, skip = int(post), float.fromhex(conf), int(skip)
+            w_ids, w_sc, w_post = ri.search(q, k)
+            assert ids == w_ids.tolist() and bits(sc) == bits(w_sc) and post == w_post, (q, k)
+            assert conf == ref.confidence(w_sc) and skip == int(conf >= 0.10)
+    n_cached = int(d.send(["NCACHED"])[0].split()[1])
+    assert 1 <= n_cached <= 6
+    # temporal batches
+    day = 24 * 3600 * 1000
+    n = 400
+    ts = [int(rng.integers(0, 50 * day)) for _ in range(n)]
+    texts = [" ".join("t%d" % int(rng.integers(0, 30)) for _ in range(2 + int(rng.integers(0, 10))))
+             for _ in range(n)]
+    d.send([f"RECORDS {n}"] + [f"{i} {ts[i]} {texts[i]}" for i in range(n)], expect=0)
+    for eps, kmax in [(0.05, 4), (1e-9, 64)]:
+        assert d.send([f"TEMPORAL {7 * day} {eps} 1.4 {kmax} 0"])[0].startswith("OK")
+        rt = ref.RefTemporal.from_records(list(range(n)), ts, texts, epsilon=eps, k_max=kmax,
+                                          tok_mode=ref.TOK_MINIMAL)
+        budget = min(ref.k_star(eps, 1.4), kmax, len(rt.partitions()[0]))
+        qs = [["t%d" % int(rng.integers(0, 30)) for _ in range(1 + int(rng.integers(0, 4)))] for _ in range(60)]
+        for k in (1, 5, 50):
+            for ub in (1, 0):
+                lines = d.send([f"TBATCH {k} {ub} {len(qs)}"] + [" ".join(q) for q in qs], expect=len(qs))
+                for q, line in zip(qs, lines):
+                    ids, sc, (searched, stopped) = parse_ext(line, 2)
+                    searched, stopped = int(searched), int(stopped)
+                    w_ids, w_sc, w_searched, _ = rt.topk(q, k, use_ub_stop=bool(ub))
+                    assert ids == w_ids.tolist() and bits(sc) == bits(w_sc), (q, k, ub)
+                    assert searched == w_searched
+                    assert stopped == int(w_searched < budget)
     d.close()

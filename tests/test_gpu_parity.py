@@ -353,3 +353,23 @@ def test_many_ties_at_the_kth_score(gpu):
         want_ids, want_sc, _ = ri.search(["aa"], k)
         got = idx.bm25_topk(["aa"], k)
         assert_same([g[0] for g in got], [g[1] for g in got], want_ids, want_sc, f"ties k={k}")
+
+
+@pytest.mark.parametrize("k", [10, 300])
+def test_search_parts_equal_per_window_search(c1, k):
+    """hm_search_batch_parts: each (query, part) list equals the oracle's search
+    restricted to that row range -- including an empty part, a part inside
+    one tile, and parts cut mid-tile (the temporal drop-in's partitions)."""
+    tids = c1["tids"][:150]
+    N = len(c1["hx"].doc_ids)
+    parts = np.array([0, 1000, 1000, 1500, 30000, 77777, N], np.uint32)
+    off = np.zeros(len(tids) + 1, np.uint32)
+    off[1:] = np.cumsum([len(t) for t in tids])
+    got = c1["dev"].search_parts(off, np.concatenate(tids).astype(np.uint32), k, parts)
+    for p in range(len(parts) - 1):
+        ids, sc, n, post = c1["orc"].topk(tids, k, row_lo=int(parts[p]), row_hi=int(parts[p + 1]))
+        assert (got["n"][p] == n).all(), p
+        assert (got["postings"][p] == post).all(), p
+        for i in range(len(tids)):
+            m = int(n[i])
+            assert_same(got["ids"][p, i, :m], got["scores"][p, i, :m], ids[i, :m], sc[i, :m], f"part {p} q{i}")
