@@ -107,6 +107,21 @@ const double* hm_synth_index_order_key(const hm_synth_index* x);     /* [V'] */
 const uint32_t* hm_synth_index_doc_lens(const hm_synth_index* x);    /* [N] */
 const uint64_t* hm_synth_index_doc_ids(const hm_synth_index* x);     /* [N] */
 
+/* Doc-range shard [row_lo, row_hi) of the flat index, built by the rank that
+ * serves it: phase 1 counts the shard's document frequencies
+ * (df[vocab_size], by Zipf rank) and length sum; the caller sums them over the
+ * ranks (an all-reduce); phase 2 builds the shard's postings (rows
+ * renumbered from 0, doc ids global) with the GLOBAL idf and avgdl -- the
+ * reference's SharedStats (csr_index.hpp:28-35), so shard scores are the flat
+ * scores bit for bit.  Term ids are the flat index's (every term with a
+ * global df).  The shard's maxscore is its LOCAL maximum: order keys are the
+ * max over the ranks (a MAX all-reduce), set by the caller. */
+int hm_synth_shard_counts(const hm_synth_corpus* c, uint64_t row_lo, uint64_t row_hi, int threads,
+                          uint64_t* df, uint64_t* len_sum);
+int hm_synth_build_shard(const hm_synth_corpus* c, double k1, double b, uint64_t row_lo, uint64_t row_hi,
+                         const uint64_t* global_df, uint64_t n_global, uint64_t len_sum_global, int threads,
+                         hm_synth_index** out);
+
 /* Temporal partitioning of a corpus (temporal_index.cpp:144-167):
  * window index of each record, partition count K, and the row order that lays
  * records out partition by partition (stable insertion order inside a

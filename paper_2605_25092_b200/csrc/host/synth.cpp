@@ -298,124 +298,188 @@ const uint64_t* hm_synth_queries_gold(const hm_synth_queries* q) { return q->gol
 const int64_t* hm_synth_queries_ts(const hm_synth_queries* q) { return q->ts.data(); }
 const uint8_t* hm_synth_queries_paraphrased(const hm_synth_queries* q) { return q->para.data(); }
 
+}  // extern "C"
+
+namespace {
+
+// Distinct token ranks of record rec, sorted (the tf runs of its postings).
+inline void distinct_tokens(const hm_synth_corpus* c, std::uint64_t rec, std::vector<std::uint32_t>& buf) {
+    buf.assign(c->tokens.begin() + static_cast<std::ptrdiff_t>(c->offsets[rec]),
+               c->tokens.begin() + static_cast<std::ptrdiff_t>(c->offsets[rec + 1]));
+    std::sort(buf.begin(), buf.end());
+}
+
+// Document frequency per rank over rows [lo, hi) of the row order, per thread.
+std::vector<std::vector<std::uint32_t>> count_df(const hm_synth_corpus* c, const std::vector<std::uint64_t>& recs,
+                                                 int T) {
+    const std::uint32_t V = c->spec.vocab_size;
+    std::vector<std::vector<std::uint32_t>> dfl(T);
+    parallel_ranges(recs.size(), T, [&](int t, std::size_t a, std::size_t e) {
+        dfl[t].assign(V, 0);
+        std::vector<std::uint32_t> buf;
+        for (std::size_t row = a; row < e; ++row) {
+            distinct_tokens(c, recs[row], buf);
+            for (std::size_t i = 0; i < buf.size(); ++i)
+                if (i == 0 || buf[i] != buf[i - 1]) {
+                    if (buf[i] >= V) throw std::runtime_error("token rank >= vocab_size");
+                    ++dfl[t][buf[i]];
+                }
+        }
+    });
+    return dfl;
+}
+
+// The CSR of the records recs[0..n) (row r = recs[r]); the statistics come
+// from global_df / n_global / avgdl_global when given (a doc-range shard of a
+// larger corpus: SharedStats, csr_index.hpp:28-35), else from these records.
+hm_synth_index* build_rows(const hm_synth_corpus* c, double k1, double b, const std::vector<std::uint64_t>& recs,
+                           const std::uint64_t* global_df, std::uint64_t n_global, double avgdl_global, int T) {
+    const std::uint64_t n = recs.size();
+    if (n >= (1ull << 32)) throw std::invalid_argument("too many records for u32 rows");
+    const std::uint32_t V = c->spec.vocab_size;
+    auto x = std::make_unique<hm_synth_index>();
+    x->doc_lens.resize(n);
+    x->doc_ids.resize(n);
+    for (std::uint64_t r = 0; r < n; ++r) {
+        x->doc_ids[r] = recs[r];
+        x->doc_lens[r] = static_cast<std::uint32_t>(c->offsets[recs[r] + 1] - c->offsets[recs[r]]);
+    }
+    std::vector<std::vector<std::uint32_t>> dfl = count_df(c, recs, T);
+    std::vector<std::uint64_t> df(V, 0);  // postings per rank in these rows
+    for (int t = 0; t < T; ++t)
+        if (!dfl[t].empty())
+            for (std::uint32_t r = 0; r < V; ++r) df[r] += dfl[t][r];
+    // alphabetical term ids over present ranks (csr_index.cpp:272-274); a
+    // shard keeps every term of the corpus, so term ids agree across shards
+    const std::uint64_t* present = global_df ? global_df : df.data();
+    std::vector<std::pair<std::string, std::uint32_t>> names;
+    for (std::uint32_t r = 0; r < V; ++r)
+        if (present[r]) names.emplace_back("w" + std::to_string(r), r);
+    std::sort(names.begin(), names.end());
+    const std::uint32_t NT = static_cast<std::uint32_t>(names.size());
+    x->term_rank.resize(NT);
+    x->rank_to_tid.assign(V, ~0u);
+    x->term_offsets.resize(NT + 1);
+    std::uint64_t off = 0;
+    for (std::uint32_t t = 0; t < NT; ++t) {
+        std::uint32_t r = names[t].second;
+        x->term_rank[t] = r;
+        x->rank_to_tid[r] = t;
+        x->term_offsets[t] = off;
+        off += df[r];
+    }
+    x->term_offsets[NT] = off;
+    names.clear();
+    names.shrink_to_fit();
+    x->posting_rows.resize(off);
+    x->posting_tf.resize(off);
+    // per-thread cursors: tid start + rows owned by earlier threads
+    std::vector<std::uint64_t> base(V, 0);
+    for (std::uint32_t t = 0; t < NT; ++t) base[x->term_rank[t]] = x->term_offsets[t];
+    std::vector<std::vector<std::uint64_t>> cur(T);
+    for (int t = 0; t < T; ++t) {
+        if (dfl[t].empty()) continue;
+        cur[t].resize(V);
+        for (std::uint32_t r = 0; r < V; ++r) {
+            cur[t][r] = base[r];
+            base[r] += dfl[t][r];
+        }
+        std::vector<std::uint32_t>().swap(dfl[t]);
+    }
+    parallel_ranges(n, T, [&](int t, std::size_t a, std::size_t e) {
+        std::vector<std::uint32_t> buf;
+        auto& cu = cur[t];
+        for (std::size_t row = a; row < e; ++row) {
+            distinct_tokens(c, recs[row], buf);
+            for (std::size_t i = 0; i < buf.size();) {
+                std::size_t j = i;
+                while (j < buf.size() && buf[j] == buf[i]) ++j;
+                std::uint64_t p = cu[buf[i]]++;
+                x->posting_rows[p] = static_cast<std::uint32_t>(row);
+                x->posting_tf[p] = static_cast<std::uint32_t>(j - i);
+                i = j;
+            }
+        }
+    });
+    // statistics (csr_index.cpp:283-322)
+    double len_sum = 0.0;
+    for (auto l : x->doc_lens) len_sum += l;
+    x->avgdl = global_df ? avgdl_global : n ? len_sum / static_cast<double>(n) : 0.0;
+    x->idf.resize(NT);
+    x->maxscore.assign(NT, 0.0);
+    const std::uint32_t N32 = static_cast<std::uint32_t>(global_df ? n_global : n);
+    const double avgdl = x->avgdl;
+    parallel_ranges(NT, T, [&](int, std::size_t a, std::size_t e) {
+        for (std::size_t t = a; t < e; ++t) {
+            std::uint64_t lo = x->term_offsets[t], hi = x->term_offsets[t + 1];
+            std::uint32_t dfv = static_cast<std::uint32_t>(global_df ? global_df[x->term_rank[t]] : hi - lo);
+            double idf = std::log(1.0 + (static_cast<double>(N32) - dfv + 0.5) / (dfv + 0.5));
+            x->idf[t] = idf;
+            double ms = 0.0;
+            for (std::uint64_t i = lo; i < hi; ++i) {
+                double tf = static_cast<double>(x->posting_tf[i]);
+                double dl = static_cast<double>(x->doc_lens[x->posting_rows[i]]);
+                double norm = avgdl > 0.0 ? dl / avgdl : 1.0;
+                double denom = tf + k1 * (1.0 - b + b * norm);
+                double s = idf * tf * (k1 + 1.0) / denom;
+                if (s > ms) ms = s;
+            }
+            x->maxscore[t] = ms;
+        }
+    });
+    x->order_key = x->maxscore;  // a shard's caller replaces them by the global maxima
+    return x.release();
+}
+
+}  // namespace
+
+extern "C" {
+
 int hm_synth_build(const hm_synth_corpus* c, double k1, double b,
                    const uint32_t* row_order, int threads, hm_synth_index** out) {
     return guard([&] {
         const std::uint64_t n = c->ts.size();
-        if (n >= (1ull << 32)) throw std::invalid_argument("too many records for u32 rows");
-        const std::uint32_t V = c->spec.vocab_size;
-        const int T = n_threads(threads);
-        auto x = std::make_unique<hm_synth_index>();
-        x->doc_lens.resize(n);
-        x->doc_ids.resize(n);
+        std::vector<std::uint64_t> recs(n);
         for (std::uint64_t r = 0; r < n; ++r) {
-            std::uint64_t rec = row_order ? row_order[r] : r;
-            if (rec >= n) throw std::invalid_argument("row_order out of range");
-            x->doc_ids[r] = rec;
-            x->doc_lens[r] = static_cast<std::uint32_t>(c->offsets[rec + 1] - c->offsets[rec]);
+            recs[r] = row_order ? row_order[r] : r;
+            if (recs[r] >= n) throw std::invalid_argument("row_order out of range");
         }
-        // per-thread document frequencies over contiguous row ranges
-        std::vector<std::vector<std::uint32_t>> dfl(T);
-        auto distinct = [&](std::uint64_t row, std::vector<std::uint32_t>& buf) {
-            std::uint64_t rec = x->doc_ids[row];
-            buf.assign(c->tokens.begin() + static_cast<std::ptrdiff_t>(c->offsets[rec]),
-                       c->tokens.begin() + static_cast<std::ptrdiff_t>(c->offsets[rec + 1]));
-            std::sort(buf.begin(), buf.end());
-        };
-        parallel_ranges(n, T, [&](int t, std::size_t a, std::size_t e) {
-            dfl[t].assign(V, 0);
-            std::vector<std::uint32_t> buf;
-            for (std::size_t row = a; row < e; ++row) {
-                distinct(row, buf);
-                for (std::size_t i = 0; i < buf.size(); ++i)
-                    if (i == 0 || buf[i] != buf[i - 1]) {
-                        if (buf[i] >= V) throw std::runtime_error("token rank >= vocab_size");
-                        ++dfl[t][buf[i]];
-                    }
-            }
-        });
-        std::vector<std::uint64_t> df(V, 0);
-        for (int t = 0; t < T; ++t)
-            if (!dfl[t].empty())
-                for (std::uint32_t r = 0; r < V; ++r) df[r] += dfl[t][r];
-        // alphabetical term ids over present ranks (csr_index.cpp:272-274)
-        std::vector<std::pair<std::string, std::uint32_t>> names;
-        for (std::uint32_t r = 0; r < V; ++r)
-            if (df[r]) names.emplace_back("w" + std::to_string(r), r);
-        std::sort(names.begin(), names.end());
-        const std::uint32_t NT = static_cast<std::uint32_t>(names.size());
-        x->term_rank.resize(NT);
-        x->rank_to_tid.assign(V, ~0u);
-        x->term_offsets.resize(NT + 1);
-        std::uint64_t off = 0;
-        for (std::uint32_t t = 0; t < NT; ++t) {
-            std::uint32_t r = names[t].second;
-            x->term_rank[t] = r;
-            x->rank_to_tid[r] = t;
-            x->term_offsets[t] = off;
-            off += df[r];
-        }
-        x->term_offsets[NT] = off;
-        names.clear();
-        names.shrink_to_fit();
-        x->posting_rows.resize(off);
-        x->posting_tf.resize(off);
-        // per-thread cursors: tid start + rows owned by earlier threads
-        std::vector<std::uint64_t> base(V, 0);
-        for (std::uint32_t t = 0; t < NT; ++t) base[x->term_rank[t]] = x->term_offsets[t];
-        std::vector<std::vector<std::uint64_t>> cur(T);
-        for (int t = 0; t < T; ++t) {
-            if (dfl[t].empty()) continue;
-            cur[t].resize(V);
-            for (std::uint32_t r = 0; r < V; ++r) {
-                cur[t][r] = base[r];
-                base[r] += dfl[t][r];
-            }
-            std::vector<std::uint32_t>().swap(dfl[t]);
-        }
-        parallel_ranges(n, T, [&](int t, std::size_t a, std::size_t e) {
-            std::vector<std::uint32_t> buf;
-            auto& cu = cur[t];
-            for (std::size_t row = a; row < e; ++row) {
-                distinct(row, buf);
-                for (std::size_t i = 0; i < buf.size();) {
-                    std::size_t j = i;
-                    while (j < buf.size() && buf[j] == buf[i]) ++j;
-                    std::uint64_t p = cu[buf[i]]++;
-                    x->posting_rows[p] = static_cast<std::uint32_t>(row);
-                    x->posting_tf[p] = static_cast<std::uint32_t>(j - i);
-                    i = j;
-                }
-            }
-        });
-        // statistics (csr_index.cpp:283-322)
-        double len_sum = 0.0;
-        for (auto l : x->doc_lens) len_sum += l;
-        x->avgdl = n ? len_sum / static_cast<double>(n) : 0.0;
-        x->idf.resize(NT);
-        x->maxscore.assign(NT, 0.0);
-        const std::uint32_t N32 = static_cast<std::uint32_t>(n);
-        const double avgdl = x->avgdl;
-        parallel_ranges(NT, T, [&](int, std::size_t a, std::size_t e) {
-            for (std::size_t t = a; t < e; ++t) {
-                std::uint64_t lo = x->term_offsets[t], hi = x->term_offsets[t + 1];
-                std::uint32_t dfv = static_cast<std::uint32_t>(hi - lo);
-                double idf = std::log(1.0 + (static_cast<double>(N32) - dfv + 0.5) / (dfv + 0.5));
-                x->idf[t] = idf;
-                double ms = 0.0;
-                for (std::uint64_t i = lo; i < hi; ++i) {
-                    double tf = static_cast<double>(x->posting_tf[i]);
-                    double dl = static_cast<double>(x->doc_lens[x->posting_rows[i]]);
-                    double norm = avgdl > 0.0 ? dl / avgdl : 1.0;
-                    double denom = tf + k1 * (1.0 - b + b * norm);
-                    double s = idf * tf * (k1 + 1.0) / denom;
-                    if (s > ms) ms = s;
-                }
-                x->maxscore[t] = ms;
-            }
-        });
-        x->order_key = x->maxscore;
-        *out = x.release();
+        *out = build_rows(c, k1, b, recs, nullptr, 0, 0.0, n_threads(threads));
+    });
+}
+
+int hm_synth_shard_counts(const hm_synth_corpus* c, uint64_t row_lo, uint64_t row_hi, int threads,
+                          uint64_t* df, uint64_t* len_sum) {
+    return guard([&] {
+        const std::uint64_t n = c->ts.size();
+        if (row_lo > row_hi || row_hi > n) throw std::invalid_argument("shard rows out of range");
+        std::vector<std::uint64_t> recs(row_hi - row_lo);
+        for (std::uint64_t r = row_lo; r < row_hi; ++r) recs[r - row_lo] = r;
+        const auto dfl = count_df(c, recs, n_threads(threads));
+        const std::uint32_t V = c->spec.vocab_size;
+        std::fill(df, df + V, 0ull);
+        for (const auto& d : dfl)
+            if (!d.empty())
+                for (std::uint32_t r = 0; r < V; ++r) df[r] += d[r];
+        std::uint64_t s = 0;
+        for (std::uint64_t r = row_lo; r < row_hi; ++r) s += c->offsets[r + 1] - c->offsets[r];
+        *len_sum = s;
+    });
+}
+
+int hm_synth_build_shard(const hm_synth_corpus* c, double k1, double b, uint64_t row_lo, uint64_t row_hi,
+                         const uint64_t* global_df, uint64_t n_global, uint64_t len_sum_global, int threads,
+                         hm_synth_index** out) {
+    return guard([&] {
+        const std::uint64_t n = c->ts.size();
+        if (row_lo > row_hi || row_hi > n) throw std::invalid_argument("shard rows out of range");
+        if (!global_df) throw std::invalid_argument("global_df is required");
+        std::vector<std::uint64_t> recs(row_hi - row_lo);
+        for (std::uint64_t r = row_lo; r < row_hi; ++r) recs[r - row_lo] = r;
+        // the reference's avgdl: a double sum of the integral lengths (exact
+        // below 2^53) over the flat corpus, divided by N
+        const double avgdl = n_global ? static_cast<double>(len_sum_global) / static_cast<double>(n_global) : 0.0;
+        *out = build_rows(c, k1, b, recs, global_df, n_global, avgdl, n_threads(threads));
     });
 }
 

@@ -777,46 +777,54 @@ class TemporalIndex:
         return ub
 
     def topk(self, query_terms, k, p=None, stats=None, use_ub_stop=True):
-        """TemporalIndex::topk (temporal_index.cpp:72-123): the newest
-        min(k*, k_max, K) partitions, newest first, each searched on the
-        device (a row window), merged greedily, with the admissible
-        upper-bound stop.  -> [(DocId, score)]; stats: TemporalStats
-        (partitions_searched / early_stopped as the reference; postings in the
-        exhaustive accounting of hm_results.postings)."""
+        """TemporalIndex::topk (temporal_index.cpp:72-123) for one query:
+        -> [(DocId, score)]; stats: TemporalStats (partitions_searched /
+        early_stopped as the reference; postings in the exhaustive accounting
+        of hm_results.postings)."""
+        lists, st = self.topk_many([query_terms], k, p, use_ub_stop)
+        if stats is not None:
+            stats.partitions_searched += st[0].partitions_searched
+            stats.postings_touched += st[0].postings_touched
+            stats.early_stopped = stats.early_stopped or st[0].early_stopped
+        return lists[0]
+
+    def topk_many(self, queries, k, p=None, use_ub_stop=True):
+        """TemporalIndex::topk for a batch of string queries: every partition of
+        the budget min(k*, k_max, K) searched for every query in ONE device call
+        (hm_search_batch_parts), the per-partition lists merged newest first
+        with the reference's admissible upper-bound stop.
+        -> (lists of [(DocId, score)], [TemporalStats])."""
         p = p or Bm25Params()
-        cur = []
+        nq = len(queries)
+        out = [[] for _ in range(nq)]
+        stats = [TemporalStats() for _ in range(nq)]
         K = self.num_partitions()
-        if K == 0 or k == 0:
-            return cur
+        if K == 0 or k == 0 or nq == 0:
+            return out, stats
         first = K - self.budget()
         bp = self.host.build_params
         ub_valid = p.k1 == bp.k1 and p.b == bp.b
-        tids = self.host.resolve(query_terms)
-        better = lambda e: (-e[1], e[0])  # noqa: E731  (RankedList::better order)
-        for i in range(K - 1, first - 1, -1):
-            if stats is not None:
-                stats.partitions_searched += 1
-            r = self.dev.search_lists([tids], k, k1=p.k1, b=p.b, row_lo=int(self.part_row[i]),
-                                      row_hi=int(self.part_row[i + 1]))
-            if stats is not None:
-                stats.postings_touched += int(r["postings"][0])
-            for j in range(int(r["n"][0])):
-                e = (int(r["ids"][0, j]), float(r["scores"][0, j]))
-                if len(cur) < k or better(e) < better(cur[-1]):
-                    cur.append(e)
-                    cur.sort(key=better)
-                    del cur[k:]
-                else:
-                    break
-            if use_ub_stop and ub_valid and i > first and len(cur) == k:
-                ub_rest = 0.0
-                for j in range(first, i):
-                    ub_rest = max(ub_rest, self.partition_upper_bound(j, query_terms))
-                if cur[-1][1] > ub_rest:
-                    if stats is not None:
-                        stats.early_stopped = True
-                    break
-        return cur
+        tids = [self.host.resolve(q) for q in queries]
+        off = np.zeros(nq + 1, np.uint32)
+        off[1:] = np.cumsum([len(t) for t in tids])
+        flat = np.array([x for t in tids for x in t], np.uint32)
+        r = self.dev.search_parts(off, flat, k, self.part_row[first:], k1=p.k1, b=p.b)
+        key = lambda e: (-e[1], e[0])  # noqa: E731  (RankedList::better order)
+        for q in range(nq):
+            cur, st = out[q], stats[q]
+            for i in range(K - 1, first - 1, -1):
+                c = i - first
+                st.partitions_searched += 1
+                st.postings_touched += int(r["postings"][c, q])
+                m = int(r["n"][c, q])
+                new = list(zip(r["ids"][c, q, :m].tolist(), r["scores"][c, q, :m].tolist()))
+                cur[:] = sorted(cur + new, key=key)[:k]  # partitions hold disjoint documents
+                if use_ub_stop and ub_valid and i > first and len(cur) == k:
+                    rest = max([0.0] + [self.partition_upper_bound(j, queries[q]) for j in range(first, i)])
+                    if cur[-1][1] > rest:
+                        st.early_stopped = True
+                        break
+        return out, stats
 
     def num_partitions(self):
         return len(self.part_row) - 1

@@ -43,6 +43,46 @@ def shard_host_index(hx, rank, world):
     return d
 
 
+def _allreduce(x, op, group=None):
+    """In-place all-reduce of a CPU numpy array over the default group (NCCL
+    needs device tensors: the array travels through this rank's GPU)."""
+    import torch
+    import torch.distributed as dist
+    t = torch.from_numpy(x)
+    if dist.get_backend(group) == "nccl":
+        d = t.cuda()
+        dist.all_reduce(d, op=op, group=group)
+        t.copy_(d.cpu())
+    else:
+        dist.all_reduce(t, op=op, group=group)
+    return x
+
+
+def build_shard(corpus, rank, world, group=None, k1=1.2, b=0.75, threads=0):
+    """Rank `rank`'s shard built by this rank alone (no rank builds the whole
+    index): its document frequencies and length sum are summed over the ranks
+    (all-reduce), the shard's postings are built with the resulting GLOBAL
+    idf / avgdl, and the order keys are the global per-term maxima (a MAX
+    all-reduce of the shards' maxscores) -- bit-identical to shard_host_index
+    of the flat build (tests/test_multi.py)."""
+    import torch.distributed as dist
+    from . import synth
+    n = corpus.n
+    lo, hi = shard_bounds(n, world)[rank]
+    df, ls = synth.shard_counts(corpus, lo, hi, threads)
+    if world > 1:
+        df = _allreduce(df.view(np.int64), dist.ReduceOp.SUM, group).view(np.uint64)
+        ls = int(_allreduce(np.array([ls], np.int64), dist.ReduceOp.SUM, group)[0])
+    hx = synth.HostIndex.shard(corpus, lo, hi, df, n, ls, k1=k1, b=b, threads=threads)
+    ms = np.ascontiguousarray(hx.maxscore, np.float64)
+    if world > 1:
+        ms = _allreduce(ms, dist.ReduceOp.MAX, group)
+    hx.maxscore = ms
+    hx.order_key = ms.copy()
+    hx.row_range = (lo, hi)
+    return hx
+
+
 def gather_and_merge(local, k, world, group=None, tau=None, tau_default=0.10,
                      epsilon_guard=1e-9):
     """All-gather per-shard top-k (torch tensors on this rank's device) and merge.
@@ -79,6 +119,20 @@ def gather_and_merge(local, k, world, group=None, tau=None, tau_default=0.10,
     return out
 
 
+def allreduce_postings(local_post, world, group=None):
+    """postings_touched of the merged result: the shards' counts summed."""
+    import torch.distributed as dist
+    tot = local_post.clone()
+    if world > 1:
+        if dist.get_backend(group) == "gloo":
+            t = tot.cpu()
+            dist.all_reduce(t, group=group)
+            tot.copy_(t)
+        else:
+            dist.all_reduce(tot, group=group)
+    return tot
+
+
 def merge_host(shard_ids, shard_scores, shard_n, k, tau_default=0.10, eps=1e-9):
     """Host restatement of the merge (used by the gloo CPU tests of the exchange
     protocol; the product merge is merge_kernel on the device)."""
@@ -110,10 +164,28 @@ class ShardedIndex:
                                       d["order_key"], d["doc_lens"], d["doc_ids"], d["avgdl"],
                                       posting_tf=d["posting_tf"], device=device)
 
+    @classmethod
+    def from_corpus(cls, corpus, rank, world, device=0, group=None, threads=0):
+        """Each rank builds and uploads only its own shard (build_shard).
+        -> (ShardedIndex, the shard's HostIndex: term ids / resolve are global)."""
+        hx = build_shard(corpus, rank, world, group=group, threads=threads)
+        self = cls.__new__(cls)
+        self.rank, self.world = rank, world
+        self.dev = search.DeviceIndex(hx.term_offsets, hx.posting_rows, hx.idf, hx.order_key, hx.doc_lens,
+                                      hx.doc_ids, hx.avgdl, posting_tf=hx.posting_tf, device=device)
+        return self, hx
+
     def search_device(self, q_off, q_tid, k, local_out, **kw):
-        """Device-resident batch: local exact top-k, all-gather, merge."""
+        """Device-resident batch: local exact top-k, all-gather, merge.  The
+        merged skip decision uses the caller's per-query tau / tau_default /
+        epsilon_guard; postings_touched is summed over the shards (every
+        posting lives on exactly one shard, so the sum is the flat count)."""
         self.dev.search_batch_device(q_off, q_tid, local_out, k, **kw)
-        return gather_and_merge(local_out, k, self.world, tau_default=kw.get("tau_default", 0.10))
+        out = gather_and_merge(local_out, k, self.world, tau=kw.get("tau"),
+                               tau_default=kw.get("tau_default", 0.10),
+                               epsilon_guard=kw.get("epsilon_guard", 1e-9))
+        out["postings"] = allreduce_postings(local_out["postings"], self.world)
+        return out
 
     def search_batch(self, q_off, q_tid, k, **kw):
         """Host buffers in, host results out (H2D, search, all-gather, merge, D2H)."""

@@ -42,6 +42,8 @@ def _lib_handle():
     L.hm_synth_build.argtypes = [vp, dbl, dbl, C.POINTER(u32), C.c_int, C.POINTER(vp)]
     L.hm_synth_partition.argtypes = [vp, i64, C.POINTER(u32), C.POINTER(u32),
                                      C.POINTER(u32), C.POINTER(i64)]
+    L.hm_synth_shard_counts.argtypes = [vp, u64, u64, C.c_int, vp, C.POINTER(u64)]
+    L.hm_synth_build_shard.argtypes = [vp, dbl, dbl, u64, u64, vp, u64, u64, C.c_int, C.POINTER(vp)]
     for name in ("hm_synth_corpus_destroy", "hm_synth_queries_destroy", "hm_synth_index_destroy"):
         getattr(L, name).argtypes = [vp]
     for name, rt in [("hm_synth_corpus_n", u64), ("hm_synth_corpus_n_tokens", u64),
@@ -165,14 +167,16 @@ class Queries:
 class HostIndex:
     """build_index output as numpy arrays (the reference CsrIndex fields)."""
 
-    def __init__(self, corpus, k1=1.2, b=0.75, row_order=None, threads=0):
+    def __init__(self, corpus, k1=1.2, b=0.75, row_order=None, threads=0, _handle=None):
         L = _lib_handle()
-        h = C.c_void_p()
-        ro = None
-        if row_order is not None:
-            row_order = np.ascontiguousarray(row_order, dtype=np.uint32)
-            ro = row_order.ctypes.data_as(C.POINTER(C.c_uint32))
-        _check(L.hm_synth_build(corpus._h, k1, b, ro, threads, C.byref(h)))
+        h = _handle
+        if h is None:
+            h = C.c_void_p()
+            ro = None
+            if row_order is not None:
+                row_order = np.ascontiguousarray(row_order, dtype=np.uint32)
+                ro = row_order.ctypes.data_as(C.POINTER(C.c_uint32))
+            _check(L.hm_synth_build(corpus._h, k1, b, ro, threads, C.byref(h)))
         nt, npost, nd = (L.hm_synth_index_n_terms(h), L.hm_synth_index_n_postings(h),
                          L.hm_synth_index_n_docs(h))
         self.build_k1, self.build_b = k1, b
@@ -188,6 +192,16 @@ class HostIndex:
         self.doc_lens = _view(L.hm_synth_index_doc_lens(h), nd, np.uint32)
         self.doc_ids = _view(L.hm_synth_index_doc_ids(h), nd, np.uint64)
         L.hm_synth_index_destroy(h)
+
+    @classmethod
+    def shard(cls, corpus, row_lo, row_hi, global_df, n_global, len_sum_global, k1=1.2, b=0.75, threads=0):
+        """Rows [row_lo, row_hi) of the flat index with the GLOBAL idf / avgdl
+        (hm_synth_build_shard); maxscore is the shard's local maximum."""
+        h = C.c_void_p()
+        gdf = np.ascontiguousarray(global_df, np.uint64)
+        _check(_lib_handle().hm_synth_build_shard(corpus._h, k1, b, row_lo, row_hi, gdf.ctypes.data,
+                                                  n_global, len_sum_global, threads, C.byref(h)))
+        return cls(corpus, k1, b, _handle=h)
 
     @property
     def n_terms(self):
@@ -207,3 +221,12 @@ class HostIndex:
         ok = ranks < len(self.rank_to_tid)
         out[ok] = self.rank_to_tid[ranks[ok]]
         return out
+
+
+def shard_counts(corpus, row_lo, row_hi, threads=0):
+    """(df[vocab_size] by Zipf rank, length sum) of rows [row_lo, row_hi)."""
+    df = np.zeros(corpus.spec.vocab_size, np.uint64)
+    ls = C.c_uint64()
+    _check(_lib_handle().hm_synth_shard_counts(corpus._h, row_lo, row_hi, threads, df.ctypes.data,
+                                               C.byref(ls)))
+    return df, ls.value

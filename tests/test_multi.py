@@ -86,6 +86,49 @@ def test_gloo_world2_shard_exchange_merge_equals_unsharded():
         assert mc[i] == restate.margin(sc[i, :n[i]])
 
 
+def _build_worker(rank, world, port, out_q):
+    """A rank builds only its own shard (shard.build_shard: df / length sums
+    and maxscores all-reduced over gloo)."""
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    corpus = synth.Corpus(n_records=20000, vocab_size=3000, min_doc_tokens=5, max_doc_tokens=30)
+    hx = shard.build_shard(corpus, rank, world, threads=2)
+    out_q.put((rank, dict(term_offsets=hx.term_offsets, posting_rows=hx.posting_rows, posting_tf=hx.posting_tf,
+                          idf=hx.idf, order_key=hx.order_key, doc_lens=hx.doc_lens, doc_ids=hx.doc_ids,
+                          avgdl=hx.avgdl, rank_to_tid=hx.rank_to_tid)))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_per_rank_shard_build_equals_flat_shard(world):
+    """Each rank builds only its rows, with the global statistics from
+    all-reduces: identical to slicing the flat build (shard_host_index) --
+    rows, tf, idf, avgdl, order keys (global maxima), DocIds, term ids."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = 29700 + world * 11 + (os.getpid() % 500)
+    procs = [ctx.Process(target=_build_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    got = dict(q.get(timeout=300) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    corpus = synth.Corpus(n_records=20000, vocab_size=3000, min_doc_tokens=5, max_doc_tokens=30)
+    full = synth.HostIndex(corpus)
+    for r in range(world):
+        want = shard.shard_host_index(full, r, world)
+        g = got[r]
+        assert (g["rank_to_tid"] == full.rank_to_tid).all()
+        for key in ("term_offsets", "posting_rows", "posting_tf", "doc_lens", "doc_ids"):
+            assert (np.asarray(g[key]) == np.asarray(want[key])).all(), key
+        for key in ("idf", "order_key"):
+            assert (np.asarray(g[key]).view(np.uint64) == np.asarray(want[key]).view(np.uint64)).all(), key
+        assert float(g["avgdl"]).hex() == float(want["avgdl"]).hex()
+
+
 @pytest.mark.gpu
 @pytest.mark.parametrize("G", [2, 4, 8])
 def test_device_merge_of_simulated_shards(gpu, G):
@@ -128,12 +171,13 @@ def _gpu_worker(rank, world, port, out_q):
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     torch.cuda.set_device(0)
-    _, _, hx, tids = synth_setup(60000, 5000, 5, 30, 200)
-    sh = shard.ShardedIndex(hx, rank, world, device=0)
+    corpus, _, hx, tids = synth_setup(60000, 5000, 5, 30, 200)
+    sh, _ = shard.ShardedIndex.from_corpus(corpus, rank, world, device=0, threads=2)
     off = np.zeros(len(tids) + 1, np.uint32)
     off[1:] = np.cumsum([len(t) for t in tids])
     flat = np.concatenate([np.asarray(t, np.uint32) for t in tids])
-    res = sh.search_batch(off, flat, K)
+    tau = np.linspace(0.0, 0.4, len(tids))
+    res = sh.search_batch(off, flat, K, tau=torch.from_numpy(tau).cuda())
     if rank == 0:
         out_q.put({k: v for k, v in res.items()})
     dist.barrier()
@@ -154,9 +198,12 @@ def test_sharded_index_ranks_on_one_gpu_equal_unsharded(gpu, world):
         p.join(timeout=120)
         assert p.exitcode == 0
     _, _, hx, tids = synth_setup(60000, 5000, 5, 30, 200)
-    ids, sc, n, _ = restate.OracleIndex.from_host(hx).topk(tids, K)
+    ids, sc, n, post = restate.OracleIndex.from_host(hx).topk(tids, K)
+    tau = np.linspace(0.0, 0.4, len(tids))
     assert (res["n"].astype(np.uint32) == n).all()
+    assert (res["postings"].astype(np.uint64) == post).all()  # summed over the shards
     for i in range(len(n)):
         assert (res["ids"][i, :n[i]].view(np.uint64) == ids[i, :n[i]]).all()
         assert (res["scores"][i, :n[i]].view(np.uint64) == sc[i, :n[i]].view(np.uint64)).all()
         assert res["conf"][i] == restate.margin(sc[i, :n[i]])
+        assert bool(res["skip"][i]) == (res["conf"][i] >= tau[i])  # the caller's per-query tau
