@@ -139,6 +139,12 @@ int hm_search_batch_parts(hm_index* index, const hm_query_batch* batch, uint32_t
 int hm_search_batch_device(hm_index* index, const hm_query_batch* batch_dev,
                            hm_results* out_dev, void* stream);
 
+/* Per query of the last HM_FLAG_TIMING batch on this thread (one without
+ * row slabs): 1 if it was served by the exhaustive tile sweep (handed over
+ * by the seeded MaxScore pass, or the pass did not run), 0 if the seeded pass
+ * served it.  HM_ERR_RANGE when n exceeds the batch. */
+int hm_last_batch_handover(uint32_t* flags, uint32_t n);
+
 /* Queries of the last batch on this thread that ran on the wide path
  * (kernels/wide.cu): every query when k > 256, else those whose plan has more
  * than 256 distinct terms.  The wide path scores exhaustively in fp64 in plan

@@ -64,6 +64,8 @@ def lib():
     L.ref_build_temporal.argtypes = [u64, P(u64), P(i64), P(C.c_char_p), i64, dbl, dbl, u32,
                                      C.c_int, dbl, dbl, P(vp)]
     L.ref_build_temporal_corpus.argtypes = [vp, i64, dbl, dbl, u32, C.c_int, dbl, dbl, P(vp)]
+    L.ref_temporal_from_flat.argtypes = [u32, P(C.c_char_p), P(u64), P(u32), P(dbl), P(dbl), P(dbl), P(u32),
+                                         P(u64), dbl, u32, P(u32), i64, i64, dbl, dbl, u32, dbl, dbl, P(vp)]
     L.ref_temporal_free.argtypes = [vp]
     L.ref_temporal_num_partitions.argtypes = [vp]
     L.ref_temporal_num_partitions.restype = u32
@@ -406,6 +408,24 @@ class RefTemporal:
         _chk(lib().ref_build_temporal(len(ids), _p(ids, C.c_uint64), _p(ts, C.c_int64),
                                       _cstrs(texts), window_ms, epsilon, lambda_hat, k_max,
                                       tok_mode, k1, b, C.byref(h)))
+        return cls(h)
+
+    @classmethod
+    def from_flat(cls, terms, term_offsets, posting_rows, posting_weights, idf, order_key, doc_lens, doc_ids,
+                  avgdl, part_row, t0, window_ms=7 * 24 * 3600 * 1000, epsilon=0.05, lambda_hat=1.4, k_max=4,
+                  k1=1.2, b=0.75):
+        """A reference TemporalIndex assembled from a partition-ordered flat
+        index (ref_temporal_from_flat): partitions share the flat statistics."""
+        keep = [np.ascontiguousarray(term_offsets, np.uint64), np.ascontiguousarray(posting_rows, np.uint32),
+                np.ascontiguousarray(posting_weights, np.float64), np.ascontiguousarray(idf, np.float64),
+                np.ascontiguousarray(order_key, np.float64), np.ascontiguousarray(doc_lens, np.uint32),
+                np.ascontiguousarray(doc_ids, np.uint64), np.ascontiguousarray(part_row, np.uint32)]
+        h = C.c_void_p()
+        _chk(lib().ref_temporal_from_flat(
+            len(terms), _cstrs(terms), _p(keep[0], C.c_uint64), _p(keep[1], C.c_uint32), _p(keep[2], C.c_double),
+            _p(keep[3], C.c_double), _p(keep[4], C.c_double), _p(keep[5], C.c_uint32), _p(keep[6], C.c_uint64),
+            avgdl, len(keep[7]) - 1, _p(keep[7], C.c_uint32), int(t0), window_ms, epsilon, lambda_hat, k_max,
+            k1, b, C.byref(h)))
         return cls(h)
 
     @classmethod

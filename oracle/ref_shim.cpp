@@ -380,6 +380,66 @@ int ref_build_temporal(std::uint64_t n, const std::uint64_t* ids,
         *out = t.release();
     });
 }
+// A reference TemporalIndex over a partition-ordered flat index (rows of
+// partition j are [part_row[j], part_row[j+1])): each partition a CsrIndex of
+// its rows with the flat (shared) idf / order keys / avgdl and its own
+// maxscores from the reference's compute_term_maxscores -- the object
+// build_temporal_index produces (temporal_index.cpp:125-169), without
+// re-tokenising the corpus.  Marshalling only (bench CPU baseline, tests).
+int ref_temporal_from_flat(std::uint32_t n_terms, const char* const* terms,
+                           const std::uint64_t* term_offsets, const std::uint32_t* posting_rows,
+                           const double* posting_weights, const double* idfs, const double* order_keys,
+                           const std::uint32_t* doc_lens, const std::uint64_t* doc_ids, double avgdl,
+                           std::uint32_t n_parts, const std::uint32_t* part_row, std::int64_t t0,
+                           std::int64_t window_ms, double epsilon, double lambda_hat, std::uint32_t k_max,
+                           double build_k1, double build_b, void** out) {
+    return guard([&] {
+        auto t = std::make_unique<Temporal>();
+        TemporalIndex& T = t->t;
+        T.params.window_ms = window_ms;
+        T.params.epsilon = epsilon;
+        T.params.lambda_hat = lambda_hat;
+        T.params.k_max_partitions = k_max;
+        T.total_docs = part_row[n_parts];
+        T.shared.avgdl = avgdl;
+        for (std::uint32_t g = 0; g < n_terms; ++g) {
+            T.shared.idf.emplace(terms[g], idfs[g]);
+            T.shared.order_key.emplace(terms[g], order_keys[g]);
+        }
+        std::vector<std::uint64_t> cur(term_offsets, term_offsets + n_terms);  // per-term cursor
+        T.partitions.resize(n_parts);
+        for (std::uint32_t j = 0; j < n_parts; ++j) {
+            auto& part = T.partitions[j];
+            part.window_start = t0 + static_cast<std::int64_t>(j) * window_ms;
+            part.window_end = part.window_start + window_ms;
+            CsrIndex& x = part.index;
+            x.build_params = Bm25Params{build_k1, build_b};
+            x.avgdl = avgdl;
+            const std::uint32_t lo = part_row[j], hi = part_row[j + 1];
+            x.term_offsets.push_back(0);
+            for (std::uint32_t g = 0; g < n_terms; ++g) {
+                std::uint64_t i = cur[g];
+                const std::uint64_t e = term_offsets[g + 1];
+                if (i == e || posting_rows[i] >= hi) continue;
+                for (; i < e && posting_rows[i] < hi; ++i) {
+                    x.posting_rows.push_back(posting_rows[i] - lo);
+                    x.posting_weights.push_back(posting_weights[i]);
+                }
+                cur[g] = i;
+                x.vocab.emplace(terms[g], static_cast<std::uint32_t>(x.terms.size()));
+                x.terms.emplace_back(terms[g]);
+                x.term_idfs.push_back(idfs[g]);
+                x.term_order_keys.push_back(order_keys[g]);
+                x.term_offsets.push_back(x.posting_rows.size());
+            }
+            x.doc_lens.assign(doc_lens + lo, doc_lens + hi);
+            x.doc_ids.assign(doc_ids + lo, doc_ids + hi);
+            x.term_maxscores = x.compute_term_maxscores(x.build_params);
+        }
+        *out = t.release();
+    });
+}
+
 int ref_build_temporal_corpus(void* corpus, std::int64_t window_ms,
                               double epsilon, double lambda_hat,
                               std::uint32_t k_max, int tok_mode, double k1,

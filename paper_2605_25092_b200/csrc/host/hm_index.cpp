@@ -35,6 +35,9 @@ namespace {
 
 thread_local uint32_t g_last_exact = 0, g_last_launches = 0, g_last_handed = 0, g_last_graph = 0, g_last_wide = 0;
 thread_local float g_ms_plan = 0.f, g_ms_search = 0.f, g_ms_exact = 0.f, g_ms_seed = 0.f;
+thread_local bool g_last_seeded = false;
+thread_local uint32_t g_last_split = 1;
+thread_local std::vector<uint32_t> g_handover;  // HM_FLAG_TIMING batches: fb_list of the seeded pass
 
 using hm_host::ck;
 using hm_host::guard;
@@ -698,6 +701,8 @@ void run_batch(hm_index* X, Workspace* w, const hm_query_batch& hb, const uint32
         if (!w->seed_scratch) dalloc(w->seed_scratch, 2ull * X->grid_search * 2ull * a.seed_half);  // up to 2 CTAs per SM
         a.seed_scratch = w->seed_scratch;
     }
+    g_last_seeded = seeded;
+    g_last_split = split;
     g_last_launches = (seeded ? 4 : 3) + (split > 1 ? 1 : 0) + (merge ? 2 : 0);  // ours: plan, [seeded,] exhaustive, exact
                                                              // [+ expand, merge, postings] (plus CUB's sort)
     auto enqueue = [&] {
@@ -891,7 +896,17 @@ void run_wide_batch(hm_index* X, Workspace* w, const hm_query_batch& hb, const u
     ck(hm::launch_plan(X->dev, a, w->order_in, st), "plan kernel");
     g_last_launches = 1;
     g_last_graph = 0;
+    g_last_seeded = false;
+    g_last_split = 1;
     run_wide(X, w, a, w->wd_iota, nq);
+}
+
+// which queries of the last (synchronised) batch the seeded pass handed to
+// the tile sweep: every query when the pass did not run
+void save_handover(Workspace* w, uint32_t nq) {
+    g_handover.assign(nq, 1u);
+    if (g_last_seeded && g_last_split == 1)
+        ck(cudaMemcpy(g_handover.data(), w->fb_list, nq * 4ull, cudaMemcpyDeviceToHost), "D2H hand-over");
 }
 
 void read_timing(Workspace* w) {
@@ -1141,6 +1156,7 @@ void search_host(hm_index* X, const hm_query_batch* b, hm_results* out, uint32_t
             if ((b->flags & HM_FLAG_TIMING) && !wide_all && !long_any) read_timing(w);
             g_last_exact = rcnt[1];
             g_last_handed = rcnt[4];
+            if ((b->flags & HM_FLAG_TIMING) && !n_parts) save_handover(w, nq);
             if (rcnt[3] & hm::kErrTooManyTerms)
                 throw std::invalid_argument("a query has more than 256 distinct terms");
             if (rcnt[3] & 2u) throw std::runtime_error("exact kernel failed to converge");
@@ -1230,6 +1246,7 @@ int hm_search_batch_device(hm_index* X, const hm_query_batch* b, hm_results* out
                 ck(cudaStreamSynchronize(w->stream), "sync");
                 g_last_exact = rc[1];
                 g_last_handed = rc[4];
+                save_handover(w, nq);
             }
             // pinned w32 staging is reused by the next call on this workspace:
             // make sure the async upload finished before handing it back
@@ -1249,6 +1266,12 @@ int hm_last_batch_stats(uint32_t* n_exact, uint32_t* n_launches) {
     if (n_exact) *n_exact = g_last_exact;
     if (n_launches) *n_launches = g_last_launches;
     return HM_OK;
+}
+
+int hm_last_batch_handover(uint32_t* flags, uint32_t n) {
+    const uint32_t m = std::min<uint32_t>(n, static_cast<uint32_t>(g_handover.size()));
+    for (uint32_t i = 0; i < m; ++i) flags[i] = g_handover[i] ? 1u : 0u;
+    return m == n ? HM_OK : HM_ERR_RANGE;
 }
 
 int hm_last_batch_wide(uint32_t* n_wide) {

@@ -55,6 +55,7 @@ struct __align__(16) SmemT {
     uint8_t msorder[kFastTerms];           // plan indices by t_ms ascending
     uint8_t t_spos[kFastTerms];            // short terms: index among the short terms (stab row)
     float ubne_q;                          // sum of the non-essential terms' bounds
+    float rem_ub[kFastTerms + 1];          // seeds: bound of the ascending-bound prefix without t*
 };
 
 template <int CAPW>

@@ -395,8 +395,10 @@ __global__ void __launch_bounds__(kCons, HM_SEED_MINB) search_seed_kernel(DevInd
             return A;
         };
 
-        // ---------------- 1. seeds: every posting of t* in the window; its row
-        // and complete score land at the posting's index in the scratch
+        // ---------------- 1. seeds: every posting of t* in the window.  sR[e] = the
+        // row of its e-th posting; sA[e] = the row's complete score, or 0 for a
+        // row proven unable to reach the admission threshold (0 never exceeds a
+        // real score, so the k-th largest sA stays a valid lower bound)
         const uint64_t sw0 = S.t_wlo[ts];
         const uint32_t n_seed = static_cast<uint32_t>(S.t_end[ts] - sw0);
         uint32_t* sR = reinterpret_cast<uint32_t*>(sA) + a.seed_half;  // seed rows
@@ -404,55 +406,135 @@ __global__ void __launch_bounds__(kCons, HM_SEED_MINB) search_seed_kernel(DevInd
 #define HM_SEED_KP 4
 #endif
         constexpr int kP = HM_SEED_KP;  // rows per lane, probed together
-        auto score_rows = [&](const RowsN<kP>& rw, uint32_t vm, uint64_t g0, uint32_t step) {
-            if (!vm) return;  // seed_probeN needs at least one real row
-            float A[kP] = {};
-            for (uint32_t i = 0; i < m; ++i) {
-                const ValsN<kP> x = seed_probeN<CAPW, kP>(sc, i, rw, vm);
-#pragma unroll
-                for (int u = 0; u < kP; ++u) A[u] += x.v[u];
-            }
-#pragma unroll
-            for (int u = 0; u < kP; ++u)
-                if ((vm >> u) & 1u) {
-                    const uint32_t e = static_cast<uint32_t>(g0 + u * step - sw0);
-                    sA[e] = A[u];
-                    sR[e] = rw.r[u];
-                }
-        };
         if (S.t_slot[ts] < 0) {
-            for (uint32_t e = tid; e < n_seed; e += kP * kCons) {
-                RowsN<kP> rw;
-                uint32_t vm = 0;
-#pragma unroll
-                for (int u = 0; u < kP; ++u) {
-                    const uint32_t eu = e + u * kCons;
-                    rw.r[u] = eu < n_seed ? __ldg(ix.post + sw0 + eu) >> cb : 0u;
-                    vm |= (eu < n_seed ? 1u : 0u) << u;
-                }
-                score_rows(rw, vm, sw0 + e, kCons);
-            }
-        } else {  // a long seed term: its postings tile by tile (rows from the tile offsets)
+            for (uint32_t e = tid; e < n_seed; e += kCons) sR[e] = __ldg(ix.post + sw0 + e) >> cb;
+        } else {  // a long seed term: rows from the tile offsets, tile by tile
             const uint32_t* tb = tile_row(ix, S.t_slot[ts]);
             const uint64_t s0 = S.t_start[ts], sw1 = S.t_end[ts];
             for (uint32_t j = j0 + warp; j <= j1; j += kConsWarps) {
                 const uint64_t b0 = max(s0 + __ldg(tb + static_cast<uint64_t>(j) * kSubPerTile), sw0);
                 const uint64_t b1 = min(s0 + __ldg(tb + static_cast<uint64_t>(j + 1) * kSubPerTile), sw1);
-                for (uint64_t g0 = b0; g0 < b1; g0 += 32 * kP) {
-                    RowsN<kP> rw;
-                    uint32_t vm = 0;
-#pragma unroll
-                    for (int u = 0; u < kP; ++u) {
-                        const uint64_t gu = g0 + 32 * u + lane;
-                        rw.r[u] = gu < b1 ? (j << kTileShift) + (__ldg(ix.post + gu) >> kCodeBitsLong) : 0u;
-                        vm |= (gu < b1 ? 1u : 0u) << u;
-                    }
-                    score_rows(rw, vm, g0 + lane, 32);
-                }
+                for (uint64_t g = b0 + lane; g < b1; g += 32)
+                    sR[g - sw0] = (j << kTileShift) + (__ldg(ix.post + g) >> kCodeBitsLong);
             }
         }
+        // t*'s own contribution to seed e (its posting's code, no probe)
+        auto seed_imp = [&](uint32_t e) -> float {
+            const uint32_t p = __ldg(ix.post + sw0 + e);
+            const uint32_t row = sR[e];
+            float w;
+            if (S.t_slot[ts] >= 0) {
+                const uint32_t code = p & kEscLong;
+                w = code < ix.n_codes ? code_w(sc, code)
+                                      : impact32(static_cast<double>(__ldg(ix.tf + sw0 + e)),
+                                                 static_cast<double>(__ldg(ix.doc_lens + row)), ix.avgdl, k1, bb);
+            } else {
+                const uint32_t code = p & ix.esc_short;
+                w = code < ix.n_codes_short ? S.w32s[code]
+                                            : impact32(static_cast<double>(__ldg(ix.tf + sw0 + e)),
+                                                       static_cast<double>(__ldg(ix.doc_lens + row)), ix.avgdl, k1,
+                                                       bb);
+            }
+            return S.t_cu[ts] * w;
+        };
+        // bound of the terms other than t* still unprobed: probes run in
+        // bound-descending order, so after the j largest bounds the rest is the
+        // ascending prefix msorder[0 .. m-1-j) without t* (rounded up)
+        if (warp == 0) {
+            const uint32_t i = static_cast<uint32_t>(lane) < m ? S.msorder[lane] : 0u;
+            float v = static_cast<uint32_t>(lane) < m && i != ts ? S.t_ms[i] : 0.f;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const float nb = __shfl_up_sync(0xffffffffu, v, o);
+                if (lane >= o) v += nb;
+            }
+            if (static_cast<uint32_t>(lane) < m) S.rem_ub[lane + 1] = v * 1.00001f;
+            if (lane == 0) S.rem_ub[0] = 0.f;
+        }
         __syncthreads();
+        // score rows e_u (u < kP, bit u of vm): every term (full) or, with
+        // early exit, t*'s impact first and the others by descending bound,
+        // dropping a row once (partial + unprobed bound) (1 + 3 delta) < thr
+        auto score_seeds = [&](const uint32_t (&eu)[kP], uint32_t vm, bool early, float thr) {
+            if (!vm) return;
+            RowsN<kP> rw;
+#pragma unroll
+            for (int u = 0; u < kP; ++u) rw.r[u] = (vm >> u) & 1u ? sR[eu[u]] : 0u;
+            float A[kP] = {};
+            uint32_t live = vm;
+            if (!early) {
+                for (uint32_t i = 0; i < m; ++i) {
+                    const ValsN<kP> x = seed_probeN<CAPW, kP>(sc, i, rw, vm);
+#pragma unroll
+                    for (int u = 0; u < kP; ++u) A[u] += x.v[u];
+                }
+            } else {
+#pragma unroll
+                for (int u = 0; u < kP; ++u)
+                    if ((vm >> u) & 1u) A[u] = seed_imp(eu[u]);
+                for (int j = static_cast<int>(m) - 1; j >= 0 && live; --j) {
+                    const uint32_t i = S.msorder[j];
+                    if (i == ts) continue;
+                    const float rem = S.rem_ub[j + 1];  // bounds of msorder[0..j] but t*
+#pragma unroll
+                    for (int u = 0; u < kP; ++u)
+                        if (((live >> u) & 1u) && (A[u] + rem) * f_ub < thr) live &= ~(1u << u);
+                    if (!live) break;
+                    const ValsN<kP> x = seed_probeN<CAPW, kP>(sc, i, rw, live);
+#pragma unroll
+                    for (int u = 0; u < kP; ++u)
+                        if ((live >> u) & 1u) A[u] += x.v[u];
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < kP; ++u)
+                if ((vm >> u) & 1u) sA[eu[u]] = (live >> u) & 1u ? A[u] : 0.f;
+        };
+        // pass over the seeds: select(e) picks the rows of this pass
+        auto seed_pass = [&](auto select, bool early, float thr) {
+            for (uint32_t e = tid; e < n_seed; e += kP * kCons) {
+                uint32_t eu[kP], vm = 0;
+#pragma unroll
+                for (int u = 0; u < kP; ++u) {
+                    eu[u] = e + u * kCons;
+                    if (eu[u] < n_seed && select(eu[u])) vm |= 1u << u;
+                }
+                score_seeds(eu, vm, early, thr);
+            }
+        };
+#ifndef HM_SEED_FULL
+#define HM_SEED_FULL 2048
+#endif
+        const uint32_t n_full = max(static_cast<uint32_t>(HM_SEED_FULL), 8u * k);
         float L = 0.f;
+        if (n_seed <= n_full) {  // few seeds: every one complete
+            seed_pass([](uint32_t) { return true; }, false, 0.f);
+            __syncthreads();
+        } else {
+            // (a) the n_full seeds with the largest t* impact, complete: L0
+            for (uint32_t e = tid; e < n_seed; e += kCons) sA[e] = seed_imp(e);
+            __syncthreads();
+            const float v0 = block_kth_largest<kCons>(sA, n_seed, n_full, S.hist, S.sel, [] { __syncthreads(); });
+            if (tid == 0) S.total = 0;
+            __syncthreads();
+            // rows left for (b) hold the smallest denormal: below every complete
+            // score (>= n_full >= k complete rows are normal and positive), so
+            // the k-th largest is the complete rows' lower bound L0
+            constexpr uint32_t kTodo = 1u;
+            seed_pass(
+                [&](uint32_t e) {
+                    const bool top = sA[e] >= v0 && atomicAdd(&S.total, 1u) < 2u * n_full;
+                    if (!top) sA[e] = __uint_as_float(kTodo);
+                    return top;
+                },
+                false, 0.f);
+            __syncthreads();
+            const float L0 = block_kth_largest<kCons>(sA, n_seed, k, S.hist, S.sel, [] { __syncthreads(); });
+            const float te0 = fmaxf(L0 * f_slack, kFltMin);
+            // (b) the other seeds with early exit against te0
+            seed_pass([&](uint32_t e) { return __float_as_uint(sA[e]) == kTodo; }, true, te0);
+            __syncthreads();
+        }
         if (n_seed >= k) L = block_kth_largest<kCons>(sA, n_seed, k, S.hist, S.sel, [] { __syncthreads(); });
         const float te = fmaxf(L * f_slack, kFltMin);  // admission threshold (as the exhaustive kernel's)
         if (tid == 0) S.Lg = __float_as_uint(L);

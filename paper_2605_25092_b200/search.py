@@ -91,7 +91,7 @@ EXPORTS = ["hm_dense_create", "hm_dense_destroy", "hm_dense_search_batch", "hm_d
            "hm_hidx_free", "hm_htix_load", "hm_htix_flat", "hm_htix_partitions", "hm_htix_params",
            "hm_htix_free",
            "hm_merge_shards_device", "hm_margin", "hm_last_error", "hm_search_batch_parts",
-           "hm_last_batch_wide", "hm_vocab_create", "hm_vocab_destroy", "hm_vocab_size",
+           "hm_last_batch_wide", "hm_last_batch_handover", "hm_vocab_create", "hm_vocab_destroy", "hm_vocab_size",
            "hm_vocab_resolve"]
 
 
@@ -115,6 +115,7 @@ def lib():
     L.hm_last_batch_seed.argtypes = [P(C.c_float), P(C.c_uint32)]
     L.hm_last_batch_graph.argtypes = [P(C.c_uint32)]
     L.hm_last_batch_wide.argtypes = [P(C.c_uint32)]
+    L.hm_last_batch_handover.argtypes = [C.c_void_p, C.c_uint32]
     L.hm_search_batch_parts.argtypes = [C.c_void_p, P(QueryBatch), C.c_uint32, C.c_void_p, P(Results)]
     L.hm_vocab_create.argtypes = [C.c_void_p, C.c_void_p, C.c_uint32, P(C.c_void_p)]
     L.hm_vocab_destroy.argtypes = [C.c_void_p]
@@ -377,6 +378,14 @@ class Vocab:
 
     def __del__(self):
         self.close()
+
+
+def last_handover(nq):
+    """uint8[nq]: 1 where the last HM_FLAG_TIMING batch's query ran on the tile
+    sweep (handed over by the seeded pass), 0 where the seeded pass served it."""
+    f = np.zeros(nq, np.uint32)
+    _check(lib().hm_last_batch_handover(_ptr(f), nq))
+    return f.astype(np.uint8)
 
 
 def last_wide():

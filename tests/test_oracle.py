@@ -187,3 +187,29 @@ def test_temporal_budget_restatement():
     for c in g["cases"]:
         b = restate.temporal_budget(c["epsilon"], c["lambda_hat"], c["k_max"], c["partitions"])
         assert max(q["searched"] for q in c["queries"]) <= b
+
+
+def test_reference_temporal_from_flat_equals_its_own_build():
+    """ref_temporal_from_flat (the bench's C3 CPU baseline object: partitions
+    cut from a partition-ordered flat index) == the reference's own
+    build_temporal_index on the same corpus: results and partitions searched."""
+    import numpy as np
+    from paper_2605_25092_b200 import synth
+    day = 24 * 3600 * 1000
+    n = 20000
+    span = int(28 * day * n / 4052)
+    corpus = synth.Corpus(n_records=n, time_span_ms=span)
+    queries = synth.Queries(corpus, n_queries=200)
+    K, order, part, t0 = corpus.partition(7 * day)
+    hx = synth.HostIndex(corpus, row_order=order)
+    rf = ref.RefTemporal.from_flat(hx.term_strings(), hx.term_offsets, hx.posting_rows,
+                                   hx.posting_tf.astype(np.float64), hx.idf, hx.order_key, hx.doc_lens,
+                                   hx.doc_ids, hx.avgdl, part, t0)
+    rt = ref.RefTemporal.from_corpus(ref.RefCorpus(n, time_span_ms=span))
+    assert len(rf.partitions()[2]) == len(rt.partitions()[2]) == K
+    assert (rf.partitions()[2] == rt.partitions()[2]).all() and (rf.partitions()[0] == rt.partitions()[0]).all()
+    for i in range(len(queries)):
+        a = rf.topk(queries.terms(i), 10)
+        b = rt.topk(queries.terms(i), 10)
+        assert a[0].tolist() == b[0].tolist() and a[1].view(np.uint64).tolist() == b[1].view(np.uint64).tolist()
+        assert a[2] == b[2] and a[3] == b[3]
