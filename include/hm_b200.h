@@ -93,6 +93,11 @@ typedef struct {
                                     has a short term, whatever its cost estimate or window */
 #define HM_FLAG_NO_SPLIT 64u     /* keep one CTA per query in small batches (no intra-query row
                                     slabs; same results -- a test / measurement switch) */
+#define HM_FLAG_NO_NESKIP 128u   /* test / measurement switch: no essential-term sweep -- the
+                                    tile sweep streams every term of every query (same results) */
+#define HM_FLAG_NE_ALL 256u      /* test / measurement switch: every query the tile sweep serves
+                                    goes through its essential-term variant, whatever its plan
+                                    length (same results) */
 #define HM_FLAG_TIMING 4u         /* time each kernel with CUDA events on the
                                     launching stream (the call then synchronises);
                                     read back with hm_last_batch_timing */

@@ -6,7 +6,8 @@ loudly with the command that builds it.
 import ctypes
 import os
 
-LIB_DIR = os.path.join(os.path.dirname(os.path.abspath(__file__)), "lib")
+# HM_LIB_DIR: an alternative in-tree build (measurement of compile-time variants)
+LIB_DIR = os.environ.get("HM_LIB_DIR") or os.path.join(os.path.dirname(os.path.abspath(__file__)), "lib")
 _cache = {}
 
 

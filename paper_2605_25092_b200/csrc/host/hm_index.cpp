@@ -90,6 +90,7 @@ struct Workspace {
     uint32_t* stab = nullptr;  // per-CTA short-term tile tables
     uint64_t stab_words = 0;
     uint32_t* seed_scratch = nullptr;  // per-CTA seeded-pass scratch
+    uint64_t* ne_pend = nullptr;       // per-CTA/warp pending rows of the essential-term sweep
     uint32_t* slab_row = nullptr;      // part boundaries of hm_search_batch_parts
     uint32_t slab_cap = 0;
     // pinned host staging
@@ -146,6 +147,7 @@ struct Workspace {
             if (p) cudaFree(p);
         if (stab) cudaFree(stab);
         if (seed_scratch) cudaFree(seed_scratch);
+        if (ne_pend) cudaFree(ne_pend);
         if (slab_row) cudaFree(slab_row);
         for (auto e : ev)
             if (e) cudaEventDestroy(e);
@@ -527,7 +529,7 @@ void ensure(Workspace* w, uint32_t nq, uint32_t ntid, uint32_t k, bool need_io) 
         dalloc(w->plan_len, NQ);
         dalloc(w->order_in, NQ);
         dalloc(w->order, NQ);
-        dalloc(w->counters, 8);
+        dalloc(w->counters, 16);
         dalloc(w->exact_list, NQ);
         dalloc(w->fb_list, NQ);
         dalloc(w->wide_list, NQ);
@@ -701,14 +703,20 @@ void run_batch(hm_index* X, Workspace* w, const hm_query_batch& hb, const uint32
         if (!w->seed_scratch) dalloc(w->seed_scratch, 2ull * X->grid_search * 2ull * a.seed_half);  // up to 2 CTAs per SM
         a.seed_scratch = w->seed_scratch;
     }
+    a.ne_pend = nullptr;
+    if (hm::sweep_ne_launched(a)) {  // up to 2 sweep CTAs per SM, 8 warps each
+        if (!w->ne_pend) dalloc(w->ne_pend, 2ull * X->grid_search * 8ull * hm::kNePendCap);
+        a.ne_pend = w->ne_pend;
+    }
     g_last_seeded = seeded;
     g_last_split = split;
-    g_last_launches = (seeded ? 4 : 3) + (split > 1 ? 1 : 0) + (merge ? 2 : 0);  // ours: plan, [seeded,] exhaustive, exact
+    g_last_launches = (seeded ? 4 : 3) + (split > 1 ? 1 : 0) + (merge ? 2 : 0) +  // ours: plan, [seeded,] exhaustive, exact
+                      (hm::sweep_ne_launched(a) ? 1 : 0);                      // [+ essential-term sweep]
                                                              // [+ expand, merge, postings] (plus CUB's sort)
     auto enqueue = [&] {
         ck(cudaMemcpyAsync(w->w32, pin_w32, hm::kMaxCodes * sizeof(float), cudaMemcpyHostToDevice, st),
            "upload w32");
-        ck(cudaMemsetAsync(w->counters, 0, 8 * sizeof(uint32_t), st), "memset counters");
+        ck(cudaMemsetAsync(w->counters, 0, 16 * sizeof(uint32_t), st), "memset counters");
         if (timing) ck(cudaEventRecord(w->ev[0], st), "event");
         if (split > 1) {  // plan + LPT over the real queries, then every slab of each
             hm::BatchArgs ap = a;
@@ -892,7 +900,7 @@ void run_wide_batch(hm_index* X, Workspace* w, const hm_query_batch& hb, const u
         w->wd_iota_cap = nq;
     }
     hm::BatchArgs a = wide_args(X, w, hb, d_off, d_tid, d_tau, out);
-    ck(cudaMemsetAsync(w->counters, 0, 8 * sizeof(uint32_t), st), "memset counters");
+    ck(cudaMemsetAsync(w->counters, 0, 16 * sizeof(uint32_t), st), "memset counters");
     ck(hm::launch_plan(X->dev, a, w->order_in, st), "plan kernel");
     g_last_launches = 1;
     g_last_graph = 0;

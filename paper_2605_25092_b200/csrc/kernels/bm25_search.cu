@@ -67,6 +67,7 @@ __global__ void plan_kernel(DevIndex ix, BatchArgs a, uint32_t* order_in) {
     for (uint32_t i = 0; i < m; ++i) c += ix.term_off[pt[i] + 1] - ix.term_off[pt[i]];
     a.plan_len[q] = m;
     a.cost[q] = c;
+    if (m >= kNeMinTerms && m <= 32) atomicAdd(&a.counters[8], 1u);  // the essential-term sweep has work
     order_in[q] = q;
 }
 

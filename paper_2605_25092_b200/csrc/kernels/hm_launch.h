@@ -24,6 +24,8 @@ cudaError_t launch_sum_slab_postings(uint32_t nq_real, uint32_t split, const uin
                                      cudaStream_t st);
 // persistent fused kernel: TAAT scoring + selection + exact rescoring + margin
 cudaError_t launch_search(const DevIndex& ix, const BatchArgs& a, int grid, cudaStream_t st);
+// launch_search also runs the essential-term variant first (one more launch)
+bool sweep_ne_launched(const BatchArgs& a);
 // seeded MaxScore pre-pass (kernels/search_seed.cu); hands the queries it
 // does not serve to the exhaustive kernel through a.fb_list
 cudaError_t launch_search_seed(const DevIndex& ix, const BatchArgs& a, int grid, cudaStream_t st);

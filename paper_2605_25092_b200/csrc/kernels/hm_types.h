@@ -110,6 +110,11 @@ constexpr uint16_t kDenseEscape = 0xFFFE;
 #define HM_SEED_SCRATCH (2 * 131072)
 #endif
 constexpr uint32_t kSeedScratch = HM_SEED_SCRATCH;  // words per CTA (search_seed.cu: kSeedMaxDf scores + rows)
+constexpr uint32_t kNePendCap = 8192;     // essential-term sweep: pending rows per warp
+#ifndef HM_NE_MIN_TERMS
+#define HM_NE_MIN_TERMS 8
+#endif
+constexpr uint32_t kNeMinTerms = HM_NE_MIN_TERMS;  // plans the essential-term sweep serves
 constexpr int kMaxDense = 128;             // dense arrays: long terms with df >= n_docs / 32, largest first
 constexpr int kDenseMinDiv = 32;
 
@@ -146,7 +151,9 @@ struct BatchArgs {
     uint32_t* order;           // [nq] queries, most expensive first
     uint32_t* counters;        // [0]=work cursor (seeded or exhaustive), [1]=exact list size,
                                // [2]=work cursor exact, [3]=error flags,
-                               // [4]=queries handed over, [5]=exhaustive cursor after the seeded pass
+                               // [4]=queries handed over, [5]=exhaustive cursor after the seeded pass,
+                               // [6]=wide list size, [7]=essential-term sweep cursor,
+                               // [8]=plans of kNeMinTerms..32 terms (16 words)
     uint32_t* exact_list;      // [nq]
     uint32_t* wide_list;       // [nq] queries with more than kMaxTerms distinct terms
                                // (counters[6] entries) for the wide path (wide.cu);
@@ -156,6 +163,8 @@ struct BatchArgs {
                                // counters[5] and skips the others); null: every query
     uint32_t* stab;            // per-CTA short-term tile tables
     uint32_t* seed_scratch;    // per-CTA seeded-pass scratch: 2 * seed_half words (scores, rows)
+    uint64_t* ne_pend;         // essential-term sweep: per CTA and warp kNePendCap rows awaiting
+                               // completion, (score bits << 32) | row
     uint32_t seed_half;        // min(kSeedScratch / 2, n_docs): the largest seed set of the index
     uint32_t stab_stride;      // words per short term (>= n_tiles + 2)
     // results (device)

@@ -13,6 +13,17 @@ constexpr int kFastTerms = 32;            // plan size served by this kernel
 constexpr uint32_t kOffMask = (kUnitRows * 4 - 1) & ~3u;  // bk: impact (19 bits) | byte offset (13 bits)
 constexpr int kImpShift = 2 + kUnitShift - (23 - kBakeMantBits);
 constexpr float kFltMin = 1.17549435e-38f;
+#ifndef HM_NE_ALPHA
+#define HM_NE_ALPHA 0.3f
+#endif
+// essential-term variant of the sweep (search_fast.cu): the left-out terms'
+// bound stays below kNeAlpha * the warp's admission threshold (0.3 measured
+// best on C4 among 0.3-0.5); it serves plans of >= kNeMinTerms terms (C2's
+// 3-6-term plans measured no faster there), every query with
+// HM_FLAG_NE_ALL, none with HM_FLAG_NO_NESKIP
+constexpr float kNeAlpha = HM_NE_ALPHA;
+constexpr uint32_t kFlagNoNeSkip = 128u;
+constexpr uint32_t kFlagNeAll = 256u;
 static_assert(kConsWarps * kUnitRows == kTile, "one warp per 2048-row unit");
 static_assert(2 + kUnitShift + 3 + kBakeMantBits == 32, "bk = 19-bit impact | 13-bit offset");
 
@@ -55,7 +66,11 @@ struct __align__(16) SmemT {
     uint8_t msorder[kFastTerms];           // plan indices by t_ms ascending
     uint8_t t_spos[kFastTerms];            // short terms: index among the short terms (stab row)
     float ubne_q;                          // sum of the non-essential terms' bounds
-    float rem_ub[kFastTerms + 1];          // seeds: bound of the ascending-bound prefix without t*
+    float rem_ub[kFastTerms + 1];          // seeds: bound of the ascending-bound prefix without t*;
+                                           // sweep: bound of the first p terms of msorder (long terms)
+    uint16_t p_lvl[kConsWarps][kFastTerms + 1];  // sweep, per warp: first tile (- j0) whose left-out
+                                                 // prefix is >= l terms (0xFFFF: none yet)
+    uint32_t n_ne, hbase;                  // sweep: long terms in msorder / histogram base bits
 };
 
 template <int CAPW>

@@ -38,12 +38,121 @@
 #include "hm_launch.h"
 #include "hm_ptx.cuh"
 
+#include "probe.cuh"
 #include "search_common.cuh"
 
 namespace hm {
 
 // ---------------------------------------------------------------- kernel
-template <int CAPW>
+#ifdef HM_STATS  // development counters (scratch builds only): hm_dev_stats()
+__device__ unsigned long long g_stats[8];
+#define HM_STAT(i, v) atomicAdd(&g_stats[i], static_cast<unsigned long long>(v))
+#else
+#define HM_STAT(i, v) ((void)0)
+#endif
+// ---------------------------------------------------------------- essential-term mode
+// Completion of a warp's pending rows (gp[0 .. np): (essential score bits <<
+// 32) | row): every row is completed by probes of the terms its tile left out
+// -- msorder[0 .. p) with p = the tile's prefix (p_lvl) -- in bound-descending
+// order, dropped once (partial + unprobed bound)(1 + 3 delta) < te, and the
+// complete fp32 scores A >= te are admitted into the warp's list exactly as
+// the scan admits (prune beyond CAPW - 128 entries; a near-tie flood sets
+// `flood`).  Out of line: the tile loop keeps its registers.
+template <int CAPW, class Smem>
+__device__ __noinline__ uint32_t ne_complete(const ProbeCtx<Smem>& pc, const uint64_t* gp, uint32_t np,
+                                             uint32_t nw, float& Lw, float f_ub, float f_slack, uint32_t k,
+                                             uint32_t j0, uint32_t n_ne, bool& flood) {
+    Smem& S = pc.S;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    float te = fmaxf(fmaxf(Lw, __uint_as_float(S.Lg)) * f_slack, kFltMin);
+    if (lane == 0) HM_STAT(0, np);
+    for (uint32_t b0 = 0; b0 < np && !flood; b0 += 128) {
+        RowsN<4> rw;
+        float A[4];
+        uint32_t pr[4];
+        uint32_t live = 0, pmax = 0;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const uint32_t i = b0 + lane + 32 * u;
+            const uint64_t e = i < np ? gp[i] : 0ull;
+            rw.r[u] = static_cast<uint32_t>(e);
+            A[u] = __uint_as_float(static_cast<uint32_t>(e >> 32));
+            uint32_t pj = 0;  // levels reached by the row's tile (p_lvl is ascending)
+            const uint32_t jt = (rw.r[u] >> kTileShift) - j0;
+            for (uint32_t l = 1; l <= n_ne && S.p_lvl[warp][l] <= jt; ++l) pj = l;
+            pr[u] = pj;
+            if (i < np) {
+                live |= 1u << u;
+                pmax = max(pmax, pj);
+            }
+        }
+        pmax = __reduce_max_sync(0xffffffffu, pmax);
+        for (int j = static_cast<int>(pmax) - 1; j >= 0; --j) {
+            const float rem = S.rem_ub[j + 1];  // msorder[0 .. j] unprobed
+            uint32_t need = 0;
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                if (!((live >> u) & 1u) || pr[u] <= static_cast<uint32_t>(j)) continue;
+                if ((A[u] + rem) * f_ub < te) live &= ~(1u << u);
+                else need |= 1u << u;
+            }
+            if (need) {
+                HM_STAT(2, __popc(need));
+                const ValsN<4> x = seed_probeN<Smem, 4>(pc, S.msorder[j], rw, need);
+#pragma unroll
+                for (int u = 0; u < 4; ++u)
+                    if ((need >> u) & 1u) A[u] += x.v[u];
+            }
+        }
+        uint32_t ok = 0;
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+            if (((live >> u) & 1u) && A[u] >= te) ok |= 1u << u;
+        const uint32_t cnt = __popc(ok);
+        const uint32_t incl = warp_incl_scan(cnt);
+        if (lane == 31) HM_STAT(3, incl);
+        uint32_t slot = nw + incl - cnt;
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+            if ((ok >> u) & 1u) {
+                S.cl_row[warp][slot] = rw.r[u];
+                S.cl_val[warp][slot] = A[u];
+                ++slot;
+            }
+        nw += __shfl_sync(0xffffffffu, incl, 31);
+        __syncwarp();
+        if (nw > static_cast<uint32_t>(CAPW - 128)) {
+            nw = warp_prune(S, warp, nw, k, Lw, f_slack);
+            te = fmaxf(fmaxf(Lw, __uint_as_float(S.Lg)) * f_slack, kFltMin);
+            if (nw > static_cast<uint32_t>(CAPW - 128)) flood = true;  // near-tie flood
+        }
+    }
+    return nw;
+}
+
+#ifndef HM_NE_ALL
+#define HM_NE_ALL 0
+#endif
+// the essential-term variant serves the queries handed over with a bound
+// (HM_NE_ALL: every query of the sweep)
+__host__ __device__ __forceinline__ bool sweep_ne_on(const BatchArgs& a) {
+    return !(a.flags & kFlagNoNeSkip);
+}
+// fb_list values: 0 served by the seeded pass, 1 no bound, else the bound's
+// bits; kFbPlain marks a query the essential-term variant gave back (overflow)
+constexpr uint32_t kFbPlain = 0x80000000u;
+__device__ __forceinline__ bool ne_takes(const BatchArgs& a, uint32_t fb, uint32_t q) {
+    if (fb & kFbPlain) return false;
+    if (HM_NE_ALL || (a.flags & kFlagNeAll)) return true;
+    const uint32_t m = a.plan_len[a.split > 1 ? q % a.nq_real : q];
+    return m >= kNeMinTerms && m <= kFastTerms;  // as counted by plan_kernel (counters[8])
+}
+
+// NE = true: the essential-term variant, launched first over the queries the
+// seeded pass handed over WITH a lower bound; NE = false serves the others
+// (every query without the seeded pass).  Two instantiations keep the plain
+// sweep's register allocation free of the probe code.
+template <int CAPW, bool NE>
 __global__ void __launch_bounds__(kCons, 2) search_fast_kernel(DevIndex ix, BatchArgs a) {
     using Smem = FastSmem<CAPW>;
     constexpr int kGatherBytes = 8 * kConsWarps * CAPW;
@@ -63,6 +172,7 @@ __global__ void __launch_bounds__(kCons, 2) search_fast_kernel(DevIndex ix, Batc
     const uint32_t wbase = static_cast<uint32_t>(warp) * (kUnitRows * 4);  // my unit, bytes into acc
     char* const accw = reinterpret_cast<char*>(S.acc) + wbase;
 
+    if (NE && !HM_NE_ALL && !(a.flags & kFlagNeAll) && a.counters[8] == 0) return;  // no plan for this variant
     for (int i = tid; i < kTile; i += kCons) S.acc[i] = 0.f;
     for (int i = tid; i < kShortCodes; i += kCons) S.w32s[i] = a.w32[i];
     if (tid < kConsWarps) S.n_w[tid] = 0;
@@ -74,12 +184,19 @@ __global__ void __launch_bounds__(kCons, 2) search_fast_kernel(DevIndex ix, Batc
         if (tid == 0) {
             // after the seeded kernel: only the queries it handed over, still in
             // LPT order (the ones it served are skipped)
+            // (NE: those with a bound, cursor counters[7]; the plain variant
+            // leaves them out unless the essential-term mode is off)
+            const bool ne_on = sweep_ne_on(a);
             uint32_t q = kNoTerm;
             for (;;) {
-                const uint32_t w = atomicAdd(&a.counters[a.fb_list ? 5 : 0], 1u);
-                if (w >= a.nq) break;
+                const uint32_t w = atomicAdd(&a.counters[NE ? 7 : a.fb_list ? 5 : 0], 1u);
+                if (w >= a.nq) {
+                    q = kNoTerm;
+                    break;
+                }
                 q = a.order[w];
-                if (!a.fb_list || a.fb_list[q]) break;
+                const uint32_t fb = a.fb_list ? a.fb_list[q] : 1u;  // 0: served by the seeded pass
+                if (fb && (NE ? ne_takes(a, fb, q) : !ne_on || !ne_takes(a, fb, q))) break;
             }
             S.q = q;
         }
@@ -127,10 +244,55 @@ __global__ void __launch_bounds__(kCons, 2) search_fast_kernel(DevIndex ix, Batc
             S.t_slot[tid] = slot;
             S.t_bkb[tid] = slot >= 0 ? ix.bk_base[slot] : 0;
         }
+        if (NE && tid < static_cast<int>(m)) {  // bounds and probe weights of the essential-term mode (below)
+            const uint32_t t = a.plan_tid[poff + tid];
+            const uint32_t mult = a.plan_mult[poff + tid];
+            const double idf = ix.idf[t];
+            const int32_t slot = ix.long_slot[t];
+            const float cu = static_cast<float>(ldexp(static_cast<double>(mult) * idf, -kScoreShift));
+            S.t_cu[tid] = cu;
+            S.t_ms[tid] = cu * ix.tmax[t] * 1.0000010f;  // rounded up: an upper bound
+            S.t_dense[tid] = slot >= 0 ? ix.dense_of_slot[slot] : -1;
+        }
         __syncthreads();
         if (tid == 0) {
             uint64_t post = 0;
             uint32_t nl = 0, ns = 0, bad = 0;
+            // Essential-term mode (MaxScore inside the sweep, csr_index.cpp:
+            // 106-207): the long terms by bound ascending (msorder[0..n_ne))
+            // with the bound of every prefix (rem_ub[p], rounded up).  Each warp
+            // leaves the first p of them out of its stream for a tile, p the
+            // longest prefix whose bound stays below kNeAlpha * (its admission
+            // threshold at that point); a row is then completed by probes only
+            // if its essential score plus that bound can reach the threshold.
+            uint32_t n_ne = 0;
+            if (NE) {
+                float U = 0.f;
+                for (uint32_t i = 0; i < m; ++i) {
+                    U += S.t_ms[i];
+                    S.t_spos[i] = 0xFFu;  // rank among the long terms by bound (reused field)
+                    if (S.t_slot[i] < 0) continue;
+                    uint32_t p = n_ne++;
+                    while (p > 0 && S.t_ms[S.msorder[p - 1]] > S.t_ms[i]) {
+                        S.msorder[p] = S.msorder[p - 1];
+                        --p;
+                    }
+                    S.msorder[p] = static_cast<uint8_t>(i);
+                }
+                float r = 0.f;
+                S.rem_ub[0] = 0.f;
+                for (uint32_t p = 0; p < n_ne; ++p) {
+                    r += S.t_ms[S.msorder[p]];
+                    S.rem_ub[p + 1] = r * 1.00001f;
+                    S.t_spos[S.msorder[p]] = static_cast<uint8_t>(p);
+                }
+                if (a.flags & kFlagNoNeSkip) n_ne = 0;
+                // admission histogram: 32 buckets per binade over the 8 binades
+                // below the query's largest possible score (search_fast: hist_bound)
+                const uint32_t ub = __float_as_uint(U * 1.001f) & 0x7F800000u;
+                S.hbase = ub > (8u << 23) ? ub - (8u << 23) : 0u;
+            }
+            S.n_ne = n_ne;
             for (uint32_t i = 0; i < m; ++i) {
                 post += S.t_end[i] - S.t_wlo[i];
                 const double idf = S.t_idf[i];
@@ -160,12 +322,15 @@ __global__ void __launch_bounds__(kCons, 2) search_fast_kernel(DevIndex ix, Batc
             if (!(a.flags & 2u)) S.Lg = 0u;  // HM_FLAG_DEBUG_NO_RESET skips the sentinel reset
             // a query handed over by the seeded pass may carry a lower bound on
             // the k-th selection score (search_seed.cu: hand_over)
-            if (a.fb_list && a.fb_list[q] > 1u) S.Lg = max(S.Lg, a.fb_list[q]);
+            const uint32_t fbq = a.fb_list ? a.fb_list[q] & ~kFbPlain : 0u;
+            if (fbq > 1u) S.Lg = max(S.Lg, fbq);
         }
         if (!(a.flags & 2u)) {
             if (tid < kConsWarps) S.n_w[tid] = 0;
             Lw = 0.f;
         }
+        if (NE)
+            for (int i = tid; i < 256; i += kCons) S.hist[i] = 0u;
         __syncthreads();
         if (S.bad) {
             if (tid == 0) a.exact_list[atomicAdd(&a.counters[1], 1u)] = q;
@@ -249,9 +414,43 @@ __global__ void __launch_bounds__(kCons, 2) search_fast_kernel(DevIndex ix, Batc
         };
         // tile j's nonempty ranges of my unit as a compact descriptor list (the
         // previous tile's list is no longer read once the pipeline enters j)
+        // essential-term mode: the prefix length p of the bound-ascending long
+        // terms this warp leaves out of tile j, decided when the pipeline enters
+        // j (which may run several empty tiles ahead of the scans) and never
+        // decreasing: p_lvl records the first tile of every level, the scan of
+        // tile j recovers its p from it
+        const uint32_t n_ne = NE ? S.n_ne : 0u;
+        const float f_ub = 1.0f + 3.0f * delta;
+        uint64_t* const gp = NE ? a.ne_pend + (static_cast<uint64_t>(blockIdx.x) * kConsWarps + warp) * kNePendCap
+                                : nullptr;
+        uint32_t np = 0;  // pending rows of this warp (completed after the sweep)
+        bool overflow = false;  // more than kNePendCap pending rows: handed to the plain sweep
+        uint32_t p_inst = 0;
+        if (NE) {
+            S.p_lvl[warp][lane + 1] = 0xFFFFu;
+            __syncwarp();
+        }
+        auto p_of_tile = [&](uint32_t j) -> uint32_t {
+            const bool ok = static_cast<uint32_t>(lane) < n_ne && S.p_lvl[warp][lane + 1] <= j - j0;
+            return __popc(__ballot_sync(0xffffffffu, ok));
+        };
+        const uint32_t my_rank = NE && static_cast<uint32_t>(lane) < n_long ? S.t_spos[S.order_list[lane]] : 0xFFu;
+        auto pick_p = [&]() -> uint32_t {
+            if (!n_ne || np > kNePendCap / 2) return 0u;  // no further growth under buffer pressure
+            const float cap = kNeAlpha * fmaxf(fmaxf(Lw, __uint_as_float(S.Lg)) * f_slack, kFltMin);
+            const bool ok = static_cast<uint32_t>(lane) < n_ne && S.rem_ub[lane + 1] * f_ub < cap;
+            return __popc(__ballot_sync(0xffffffffu, ok));  // rem_ub increases: a prefix
+        };
         auto install = [&](uint32_t j) {
             uint32_t u0, u1;
-            const bool ok = static_cast<uint32_t>(lane) < n_long && pre1 > pre0 && live(j, u0, u1);
+            uint32_t pj = 0;
+            if constexpr (NE) {
+                pj = max(p_inst, pick_p());
+                if (static_cast<uint32_t>(lane) >= p_inst && static_cast<uint32_t>(lane) < pj)
+                    S.p_lvl[warp][lane + 1] = static_cast<uint16_t>(j - j0);
+                p_inst = pj;
+            }
+            const bool ok = static_cast<uint32_t>(lane) < n_long && pre1 > pre0 && live(j, u0, u1) && my_rank >= pj;
             const uint32_t bal = __ballot_sync(0xffffffffu, ok);
             if (ok) {
                 const uint64_t addr = reinterpret_cast<uint64_t>(my_bk + pre0);
@@ -268,6 +467,105 @@ __global__ void __launch_bounds__(kCons, 2) search_fast_kernel(DevIndex ix, Batc
         // the loads of the next step(s) -- possibly ranges of later tiles --
         // are in flight while the current step is applied, and across the
         // short-term pass and the scan.
+        // ---- essential-term mode: scan of a unit whose first p bound-ascending
+        // long terms were not streamed (U = rem_ub[p]).  Rows with
+        // (A_E + U)(1 + 3 delta) >= te are collected at the tail of the warp's
+        // list (<= 128 pending) and completed by probes of the left-out terms
+        // in bound-descending order, each dropped once (partial + unprobed
+        // bound)(1 + 3 delta) < te; the complete fp32 scores are admitted with
+        // the usual rule (A >= te).  A row below the first test cannot reach te:
+        // its score is at most (A_E + U)(1 + 3 delta) -- the seeded pass's
+        // argument.  Admitted scores also go into a CTA-wide histogram whose
+        // k-th bucket floor is a lower bound on the k-th largest score (hist_bound).
+        const ProbeCtx<Smem> pc{ix, a, S, stab, stride, j0, cb, k1, bb};
+        const uint32_t hbase = NE ? S.hbase : 0u;
+        auto hist_add = [&](float A) {
+            const uint32_t u = __float_as_uint(A);
+            atomicAdd(&S.hist[u <= hbase ? 0u : min((u - hbase) >> 18, 255u)], 1u);
+        };
+        // every counted document is distinct (a row is admitted once per query)
+        // and has A >= the floor of its bucket: the floor of the bucket holding
+        // the k-th largest count is a valid Lg (counts only grow: stale reads
+        // give a smaller, still valid bound)
+        auto hist_bound = [&]() {
+            uint32_t loc[8], sum = 0;
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                loc[j] = S.hist[lane * 8 + j];
+                sum += loc[j];
+            }
+            uint32_t incl = sum;  // over lanes >= lane
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t nb = __shfl_down_sync(0xffffffffu, incl, o);
+                if (lane + o < 32) incl += nb;
+            }
+            const uint32_t above = incl - sum;
+            uint32_t bkt = 0;
+            if (above < k && k <= incl) {
+                uint32_t cum = above;
+                for (int j = 7; j >= 0; --j) {
+                    cum += loc[j];
+                    if (cum >= k) {
+                        bkt = static_cast<uint32_t>(lane * 8 + j);
+                        break;
+                    }
+                }
+            }
+            bkt = __reduce_max_sync(0xffffffffu, bkt);
+            if (lane == 0 && bkt > 0) atomicMax(&S.Lg, hbase + (bkt << 18));
+        };
+        auto scan_ne = [&](float4* acc4, uint32_t base, float te, uint32_t pj) {
+            constexpr uint32_t kV = kUnitRows / 4;
+            const float4 z4 = make_float4(0.f, 0.f, 0.f, 0.f);
+            const float ubne = S.rem_ub[pj];
+            auto pend = [&](float4 x4, uint32_t v) {
+                const bool q0 = (x4.x + ubne) * f_ub >= te, q1 = (x4.y + ubne) * f_ub >= te;
+                const bool q2 = (x4.z + ubne) * f_ub >= te, q3 = (x4.w + ubne) * f_ub >= te;
+                const uint32_t cnt = q0 + q1 + q2 + q3;
+                if (!__any_sync(0xffffffffu, cnt != 0)) return;
+                const uint32_t incl = warp_incl_scan(cnt);
+                const uint32_t tot = __shfl_sync(0xffffffffu, incl, 31);
+                if (np + tot > kNePendCap) {  // full: the plain sweep serves the query (below)
+                    overflow = true;
+                    return;
+                }
+                uint64_t* dst = gp + np + incl - cnt;
+                const uint32_t P = wr0 + 4 * v;
+                auto put = [&](bool okp, uint32_t pos, float val) {
+                    if (okp) {
+                        *dst++ = (static_cast<uint64_t>(__float_as_uint(val)) << 32) | (base + swz10(pos));
+                        hist_add(val);  // a partial score: a lower bound of the row's score
+                    }
+                };
+                put(q0, P, x4.x);
+                put(q1, P + 1, x4.y);
+                put(q2, P + 2, x4.z);
+                put(q3, P + 3, x4.w);
+                np += tot;
+            };
+#pragma unroll 1
+            for (uint32_t vb = 0; vb < kV && !overflow; vb += 128) {
+                float4 x[4];
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    x[q] = acc4[vb + 32 * q + lane];
+                    acc4[vb + 32 * q + lane] = z4;
+                }
+                const float m0 = max3f(x[0].x, x[0].y, x[0].z), m1 = max3f(x[0].w, x[1].x, x[1].y);
+                const float m2 = max3f(x[1].z, x[1].w, x[2].x), m3 = max3f(x[2].y, x[2].z, x[2].w);
+                const float m4 = max3f(x[3].x, x[3].y, x[3].z);
+                const float mx = fmaxf(max3f(m0, m1, m2), max3f(m3, m4, x[3].w));
+                if (__any_sync(0xffffffffu, (mx + ubne) * f_ub >= te)) {
+#pragma unroll
+                    for (int q = 0; q < 4; ++q)
+                        if (!overflow) pend(x[q], vb + 32 * q + lane);
+                }
+            }
+            if (overflow)  // the plain sweep takes the query: finish zeroing my rows
+                for (uint32_t z = lane; z < kV; z += 32) acc4[z] = z4;
+            __syncwarp();
+        };
         uint32_t ready = j0;  // the tile whose ranges are in rdesc
         prefetch(j0);
         install(j0);
@@ -370,7 +668,7 @@ __global__ void __launch_bounds__(kCons, 2) search_fast_kernel(DevIndex ix, Batc
             float4* acc4 = reinterpret_cast<float4*>(accw);
             constexpr uint32_t kV = kUnitRows / 4;
             const float4 z4 = make_float4(0.f, 0.f, 0.f, 0.f);
-            if (flood) {  // this query goes to the exact kernel: only keep acc clean
+            if (flood || overflow) {  // this query goes elsewhere: only keep acc clean
                 for (uint32_t z = lane; z < kV; z += 32) acc4[z] = z4;
                 __syncwarp();
                 continue;
@@ -399,6 +697,7 @@ __global__ void __launch_bounds__(kCons, 2) search_fast_kernel(DevIndex ix, Batc
                         S.cl_row[warp][slot] = base + swz10(pos);  // position -> row (involution)
                         S.cl_val[warp][slot] = val;
                         ++slot;
+                        if constexpr (NE) hist_add(val);
                     }
                 };
                 put(q0, P, x4.x);
@@ -408,6 +707,15 @@ __global__ void __launch_bounds__(kCons, 2) search_fast_kernel(DevIndex ix, Batc
                 nw += __shfl_sync(0xffffffffu, incl, 31);
                 __syncwarp();
             };
+            if constexpr (NE) {
+                const uint32_t pj = p_of_tile(j);
+                if (lane == 0) HM_STAT(pj ? 4 : 5, 1);
+                if (pj) {
+                    scan_ne(acc4, base, te, pj);
+                    hist_bound();
+                    continue;
+                }
+            }
 #pragma unroll 1
             for (uint32_t vb = 0; vb < kV && !flood; vb += 128) {  // 4 float4 (16 rows) per lane
                 float4 x[4];
@@ -429,12 +737,29 @@ __global__ void __launch_bounds__(kCons, 2) search_fast_kernel(DevIndex ix, Batc
             if (flood)  // the query goes to the exact kernel: finish zeroing my rows
                 for (uint32_t z = lane; z < kV; z += 32) acc4[z] = z4;
             __syncwarp();
+            if constexpr (NE) {
+                if (n_ne) hist_bound();
+            }
+        }
+        if constexpr (NE) {
+            if (overflow && lane == 0) atomicMax(&S.flood, 2u);
+            if (np && !flood && !overflow) {
+                __syncwarp();  // gp entries of every lane written
+                nw = ne_complete<CAPW>(pc, gp, np, nw, Lw, f_ub, f_slack, k, j0, n_ne, flood);
+            }
         }
         if (lane == 0) {
             S.n_w[warp] = nw;
-            if (flood) S.flood = 1;
+            if (flood) atomicMax(&S.flood, 1u);
         }
         csync();
+        if (NE && S.flood == 2u && a.fb_list) {  // a warp's pending rows overflowed: the plain sweep
+            // (launched next) takes the query, with the seeded pass's bound
+            if (tid == 0) a.fb_list[q] = kFbPlain | (a.fb_list[q] > 1u ? a.fb_list[q] : 1u);
+            csync();
+            if (tid < kConsWarps) S.n_w[tid] = 0;
+            continue;
+        }
         if (S.flood) {
             if (tid == 0) a.exact_list[atomicAdd(&a.counters[1], 1u)] = q;
             csync();
@@ -450,35 +775,40 @@ template <int CAPW>
 static cudaError_t fast_attr() {
     static bool done = false;
     if (done) return cudaSuccess;
-    const cudaError_t e = cudaFuncSetAttribute(search_fast_kernel<CAPW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                               static_cast<int>(sizeof(FastSmem<CAPW>)));
+    cudaError_t e = cudaFuncSetAttribute(search_fast_kernel<CAPW, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(sizeof(FastSmem<CAPW>)));
+    if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(search_fast_kernel<CAPW, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(sizeof(FastSmem<CAPW>)));
     if (e == cudaSuccess) done = true;
     return e;
 }
 
+template <int CAPW>
+static cudaError_t launch_fast_w(const DevIndex& ix, const BatchArgs& a, int sms, cudaStream_t st) {
+    const cudaError_t e = fast_attr<CAPW>();
+    if (e != cudaSuccess) return e;
+    if (sweep_ne_launched(a)) search_fast_kernel<CAPW, true><<<2 * sms, kCons, sizeof(FastSmem<CAPW>), st>>>(ix, a);
+    search_fast_kernel<CAPW, false><<<2 * sms, kCons, sizeof(FastSmem<CAPW>), st>>>(ix, a);
+    return cudaGetLastError();
+}
+
+bool sweep_ne_launched(const BatchArgs& a) { return sweep_ne_on(a); }
+
 // CAPW 192 (k <= 32) or 320 (k <= 128); two 8-warp CTAs per SM either way.
 cudaError_t launch_search(const DevIndex& ix, const BatchArgs& a, int sms, cudaStream_t st) {
-    if (a.k <= FastCfg<192>::kMaxKServed) {
-        const cudaError_t e = fast_attr<192>();
-        if (e != cudaSuccess) return e;
-        search_fast_kernel<192><<<2 * sms, kCons, sizeof(FastSmem<192>), st>>>(ix, a);
-    } else {
-        const cudaError_t e = fast_attr<320>();
-        if (e != cudaSuccess) return e;
-        search_fast_kernel<320><<<2 * sms, kCons, sizeof(FastSmem<320>), st>>>(ix, a);
-    }
-    return cudaGetLastError();
+    return a.k <= FastCfg<192>::kMaxKServed ? launch_fast_w<192>(ix, a, sms, st) : launch_fast_w<320>(ix, a, sms, st);
 }
 
 cudaError_t search_occupancy_fast(int* blocks) {
     int b[2] = {0, 0};
     cudaError_t e = fast_attr<192>();
     if (e == cudaSuccess)
-        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b[0], search_fast_kernel<192>, kCons,
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b[0], search_fast_kernel<192, false>, kCons,
                                                           sizeof(FastSmem<192>));
     if (e == cudaSuccess) e = fast_attr<320>();
     if (e == cudaSuccess)
-        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b[1], search_fast_kernel<320>, kCons,
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b[1], search_fast_kernel<320, false>, kCons,
                                                           sizeof(FastSmem<320>));
     if (e != cudaSuccess) return e;
     if (b[0] < 2 || b[1] < 2) return cudaErrorInvalidConfiguration;
@@ -489,3 +819,14 @@ cudaError_t search_occupancy_fast(int* blocks) {
 size_t search_smem_bytes() { return sizeof(FastSmem<192>); }
 
 }  // namespace hm
+
+#ifdef HM_STATS
+extern "C" int hm_dev_stats(unsigned long long* out, int reset) {
+    if (cudaMemcpyFromSymbol(out, hm::g_stats, sizeof(hm::g_stats)) != cudaSuccess) return -1;
+    if (reset) {
+        static const unsigned long long z[8] = {};
+        cudaMemcpyToSymbol(hm::g_stats, z, sizeof(z));
+    }
+    return 0;
+}
+#endif

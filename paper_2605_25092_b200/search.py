@@ -32,6 +32,8 @@ HM_FLAG_TIMING = 4
 HM_FLAG_EXHAUSTIVE = 16
 HM_FLAG_SEED_ALL = 32
 HM_FLAG_NO_SPLIT = 64
+HM_FLAG_NO_NESKIP = 128
+HM_FLAG_NE_ALL = 256
 NO_TERM = 0xFFFFFFFF
 MAX_K = 256
 

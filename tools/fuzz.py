@@ -42,7 +42,8 @@ def fuzz_bm25(rng):
     b = float(rng.choice([0.75, 0.0, 1.0, 0.3]))
     k = int(rng.integers(1, 40))
     qs = [["t%d" % rng.integers(0, V + 5) for _ in range(rng.integers(1, 8))] for _ in range(int(rng.integers(1, 60)))]
-    flags = int(rng.choice([0, search.HM_FLAG_SEED_ALL, search.HM_FLAG_EXHAUSTIVE, search.HM_FLAG_FORCE_EXACT]))
+    flags = int(rng.choice([0, search.HM_FLAG_SEED_ALL, search.HM_FLAG_NE_ALL, search.HM_FLAG_NE_ALL,
+                               search.HM_FLAG_EXHAUSTIVE, search.HM_FLAG_FORCE_EXACT]))
     lo = hi = 0
     if rng.random() < 0.3:  # a row window (temporal recency / doc shard)
         lo = int(rng.integers(0, n))

@@ -49,7 +49,7 @@ def main():
     for r in data:
         name = r[col["Kernel Name"]].split("(")[0].split("<")[0].split("::")[-1]
         ns = num(r[col["gpu__time_duration.sum"]])
-        scale = {"nsecond": 1e-6, "usecond": 1e-3, "msecond": 1.0}.get(units[col["gpu__time_duration.sum"]], 1e-6)
+        scale = {"nsecond": 1e-6, "usecond": 1e-3, "msecond": 1.0, "ms": 1.0, "us": 1e-3, "ns": 1e-6}.get(units[col["gpu__time_duration.sum"]], 1e-6)
         rd = num(r[col["dram__bytes_read.sum"]]) or 0.0
         wr = num(r[col["dram__bytes_write.sum"]]) or 0.0
         bscale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(units[col["dram__bytes_read.sum"]], 1)
