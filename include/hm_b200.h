@@ -187,6 +187,32 @@ int hm_merge_shards_device(uint32_t n_shards, uint32_t n_queries, uint32_t k,
                            const uint32_t* shard_n, const double* tau, double tau_default,
                            double epsilon_guard, hm_results* out_dev, void* stream);
 
+/* Doc-sharded search over several devices of one process (north_star's
+ * multi-GPU path for C++ callers; the torch.distributed one-rank-per-GPU
+ * path is paper_2605_25092_b200/shard.py).  hm_sharded_create splits the
+ * view's rows into n_shards contiguous ranges [n_docs*g/G, n_docs*(g+1)/G)
+ * and uploads shard g -- its sub-CSR with the flat index's idf, order keys
+ * and avgdl (SharedStats, csr_index.hpp:28-35), so every local score is the
+ * flat score bit for bit -- to devices[g] (a device may be listed more than
+ * once).  n_shards <= 16 and <= n_docs.  Peer access devices[0] -> devices[g]
+ * is enabled where the hardware allows it (NVLink / NVSwitch).
+ * hm_sharded_search_batch takes the hm_search_batch arguments (HOST buffers,
+ * row window in flat rows, any k): every shard searches its part of the
+ * window on its own device concurrently, then ONE kernel on devices[0] reads
+ * the shards' top-k lists over peer memory and merges them (all-gather +
+ * k-way merge fused; shards the root cannot address are copied first) and
+ * writes Margin confidence, skip and postings_touched summed over shards.
+ * Results equal hm_search_batch on the unsharded index.  Calls on one
+ * hm_sharded are serialised.  hm_sharded_info: shard count, first flat row of
+ * each shard ([n_shards + 1]), devices, and a bit per shard read by the
+ * merge over peer memory. */
+typedef struct hm_sharded hm_sharded;
+int hm_sharded_create(const hm_csr_view* view, const int* devices, uint32_t n_shards, hm_sharded** out);
+int hm_sharded_destroy(hm_sharded* sharded);
+int hm_sharded_info(const hm_sharded* sharded, uint32_t* n_shards, uint32_t* shard_row, int* devices,
+                    uint32_t* p2p_mask);
+int hm_sharded_search_batch(hm_sharded* sharded, const hm_query_batch* batch, hm_results* out);
+
 /* The reference's on-disk index, HIDX v1 (proj/src/io.cpp:91-157, 223-232):
  * parsed straight into host arrays, validated with the reference's messages
  * ("not an index file (bad magic)", "unsupported index version N",

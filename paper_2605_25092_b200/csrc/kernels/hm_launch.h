@@ -37,6 +37,12 @@ cudaError_t launch_merge(uint32_t n_shards, uint32_t nq, uint32_t k, const uint6
                          double tau_default, double eps, uint64_t* out_ids,
                          double* out_scores, uint32_t* out_n, double* out_conf,
                          uint8_t* out_skip, cudaStream_t st);
+// doc-sharded search: all-gather of the shards' lists over peer memory fused
+// with the k-way merge (rank by binary search), Margin, skip, postings sum
+cudaError_t launch_gather_merge(const ShardLists& lists, uint32_t nq, uint32_t k, const double* tau,
+                                double tau_default, double eps, uint64_t* out_ids, double* out_scores,
+                                uint32_t* out_n, double* out_conf, uint8_t* out_skip, uint64_t* out_post,
+                                cudaStream_t st);
 // K0: bake the long-term postings into bk[] for (k1, b); *err |= 1 when an
 // impact falls outside the 7 representable binades (kernels/bake.cu)
 uint32_t bake_ks(double k1);

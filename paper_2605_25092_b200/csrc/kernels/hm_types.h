@@ -199,6 +199,18 @@ struct WideArgs {
     WideCand* cand;            // [G][k]
 };
 
+// doc-sharded search (hm_sharded_*): each shard's exact local top-k lists,
+// device pointers readable from the merging device (its own HBM or a peer's
+// over NVLink), for gather_merge_kernel (shard_merge.cu)
+constexpr int kMaxShards = 16;
+struct ShardLists {
+    uint32_t G;
+    const uint64_t* ids[kMaxShards];     // [nq][k]
+    const double* scores[kMaxShards];    // [nq][k]
+    const uint32_t* n[kMaxShards];       // [nq]
+    const uint64_t* post[kMaxShards];    // [nq] or NULL
+};
+
 constexpr uint32_t kErrTooManyTerms = 1u;
 constexpr uint32_t kErrNoConverge = 2u;
 

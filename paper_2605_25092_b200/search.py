@@ -143,6 +143,10 @@ def lib():
     L.hm_merge_shards_device.argtypes = [C.c_uint32, C.c_uint32, C.c_uint32, C.c_void_p,
                                          C.c_void_p, C.c_void_p, C.c_void_p, C.c_double,
                                          C.c_double, P(Results), C.c_void_p]
+    L.hm_sharded_create.argtypes = [P(CsrView), C.c_void_p, C.c_uint32, P(C.c_void_p)]
+    L.hm_sharded_destroy.argtypes = [C.c_void_p]
+    L.hm_sharded_info.argtypes = [C.c_void_p, P(C.c_uint32), C.c_void_p, C.c_void_p, P(C.c_uint32)]
+    L.hm_sharded_search_batch.argtypes = [C.c_void_p, P(QueryBatch), P(Results)]
     L.hm_margin.argtypes = [P(C.c_double), C.c_uint32, C.c_double]
     L.hm_margin.restype = C.c_double
     L.hm_dense_create.argtypes = [P(DenseView), C.c_int, P(C.c_void_p)]
@@ -322,6 +326,82 @@ class DeviceIndex:
         _check(lib().hm_search_batch_device(self._h, C.byref(qb), C.byref(r), st.cuda_stream))
         if flags & HM_FLAG_TIMING:
             return last_timing()
+
+
+class ShardedDeviceIndex:
+    """Doc-sharded index over several devices of this process (hm_sharded_*):
+    shard g = rows [n*g/G, n*(g+1)/G) on devices[g] with the flat statistics;
+    one search call runs every shard concurrently and merges on devices[0]
+    with one kernel reading the shards' lists over peer memory.  Results equal
+    DeviceIndex.search_batch on the unsharded index."""
+
+    def __init__(self, term_offsets, posting_rows, idf, order_key, doc_lens, doc_ids, avgdl,
+                 devices, posting_tf=None, posting_weights=None):
+        keep = dict(
+            term_offsets=np.ascontiguousarray(term_offsets, np.uint64),
+            posting_rows=np.ascontiguousarray(posting_rows, np.uint32),
+            idf=np.ascontiguousarray(idf, np.float64),
+            order_key=np.ascontiguousarray(order_key, np.float64),
+            doc_lens=np.ascontiguousarray(doc_lens, np.uint32),
+            doc_ids=np.ascontiguousarray(doc_ids, np.uint64))
+        if posting_tf is not None:
+            keep["tf"] = np.ascontiguousarray(posting_tf, np.uint32)
+        if posting_weights is not None:
+            keep["w"] = np.ascontiguousarray(posting_weights, np.float64)
+        v = CsrView(len(keep["idf"]), _ptr(keep["term_offsets"]), _ptr(keep["posting_rows"]),
+                    _ptr(keep.get("w")), _ptr(keep.get("tf")), _ptr(keep["idf"]), _ptr(keep["order_key"]),
+                    len(keep["doc_ids"]), _ptr(keep["doc_lens"]), _ptr(keep["doc_ids"]), float(avgdl))
+        devs = np.ascontiguousarray(devices, np.int32)
+        h = C.c_void_p()
+        _check(lib().hm_sharded_create(C.byref(v), _ptr(devs), len(devs), C.byref(h)))
+        self._h = h
+        self.n_docs = len(keep["doc_ids"])
+
+    @classmethod
+    def from_host(cls, hx, devices):
+        return cls(hx.term_offsets, hx.posting_rows, hx.idf, hx.order_key, hx.doc_lens,
+                   hx.doc_ids, hx.avgdl, devices, posting_tf=hx.posting_tf)
+
+    def info(self):
+        """dict(n_shards, shard_row[G+1], devices[G], p2p[G])."""
+        n = C.c_uint32()
+        _check(lib().hm_sharded_info(self._h, C.byref(n), None, None, None))
+        G = n.value
+        rows = np.zeros(G + 1, np.uint32)
+        devs = np.zeros(G, np.int32)
+        mask = C.c_uint32()
+        _check(lib().hm_sharded_info(self._h, C.byref(n), _ptr(rows), _ptr(devs), C.byref(mask)))
+        return dict(n_shards=G, shard_row=rows, devices=devs,
+                    p2p=np.array([(mask.value >> g) & 1 for g in range(G)], bool))
+
+    def search_batch(self, q_off, q_tid, k, k1=1.2, b=0.75, tau=None, tau_default=0.10,
+                     epsilon_guard=1e-9, row_lo=0, row_hi=0, flags=0):
+        """hm_sharded_search_batch; same arguments and outputs as DeviceIndex.search_batch."""
+        q_off = np.ascontiguousarray(q_off, np.uint32)
+        q_tid = np.ascontiguousarray(q_tid, np.uint32)
+        nq = len(q_off) - 1
+        kk = max(int(k), 1)
+        out = dict(ids=np.zeros((nq, kk), np.uint64), scores=np.zeros((nq, kk), np.float64),
+                   n=np.zeros(nq, np.uint32), conf=np.zeros(nq, np.float64),
+                   skip=np.zeros(nq, np.uint8), postings=np.zeros(nq, np.uint64))
+        tau_a = None if tau is None else np.ascontiguousarray(tau, np.float64)
+        qb = QueryBatch(nq, _ptr(q_off), _ptr(q_tid) if len(q_tid) else None, int(k), k1, b,
+                        _ptr(tau_a), tau_default, epsilon_guard, row_lo, row_hi, flags)
+        r = Results(_ptr(out["ids"]), _ptr(out["scores"]), _ptr(out["n"]), _ptr(out["conf"]),
+                    _ptr(out["skip"]), _ptr(out["postings"]))
+        _check(lib().hm_sharded_search_batch(self._h, C.byref(qb), C.byref(r)))
+        if k == 0:
+            out["ids"] = out["ids"][:, :0]
+            out["scores"] = out["scores"][:, :0]
+        return out
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib().hm_sharded_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        self.close()
 
 
 def last_timing():
