@@ -76,8 +76,23 @@ struct __align__(16) SmemT {
 template <int CAPW>
 using FastSmem = SmemT<CAPW, kTile, 1>;
 // the seeded pass: epilogue scratch only (gather lists 8 B x 8 warps x CAPW >= survivors)
+// seeded pass's essential-score hash table (search_seed.cu), in the
+// accumulator area before the epilogue uses it: kHashSlots keys + values
+#ifndef HM_HASH_BITS
+#define HM_HASH_BITS 12
+#endif
+constexpr int kHashBits = HM_HASH_BITS;
+constexpr uint32_t kHashSlots = 1u << kHashBits;
+constexpr uint32_t kHashEmpty = 0xFFFFFFFFu;
+// + the per-chunk segment table (kMaxSeg x (u64 start, u32 prefix, u32 meta) + 1)
+#ifndef HM_MAX_SEG
+#define HM_MAX_SEG 512
+#endif
+constexpr uint32_t kMaxSeg = HM_MAX_SEG;
+constexpr uint32_t kSeedSmemMax = kHashSlots;  // seeds kept in the same area (scores, rows)
+constexpr int kSeedAcc = 2 * static_cast<int>(kHashSlots) + 4 * static_cast<int>(kMaxSeg) + 4;
 template <int CAPW>
-using SeedSmem = SmemT<CAPW, 16 * CAPW, 0>;
+using SeedSmem = SmemT<CAPW, (16 * CAPW > kSeedAcc ? 16 * CAPW : kSeedAcc), 0>;
 
 struct SurvView {
     double* E;

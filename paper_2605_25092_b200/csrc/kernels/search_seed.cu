@@ -14,10 +14,14 @@
 //      bound-ascending order with sum(ms) * (1 + 3 delta) < te = L (1 - 2.5
 //      delta).  A document without t* and without any essential term scores
 //      at most that sum: it cannot be admitted.
-//   3. candidates: every posting of the remaining essential terms E' is scored
-//      completely the same way, unless they are more than kEMax postings --
-//      then the query falls back to the exhaustive kernel; rows already seen
-//      (they contain t* or an earlier E' term) are recognised from the probes.
+//   3. candidates: the postings of the essential terms (t* and the rest, E')
+//      are accumulated per row in a shared-memory hash table (chunks of whole
+//      tiles, fixed-point integer atomics; rows holding t* flagged -- the seeds
+//      scored them), unless E' has more than kEMax postings -- then the query
+//      falls back to the exhaustive kernel with L as its starting bound.  Rows
+//      whose essential score plus the non-essential bound can still reach the
+//      threshold are completed by probing the non-essential terms (bound
+//      descending, early exit);
 //   4. admission into the per-warp candidate lists with the exhaustive
 //      kernel's rule (A >= L (1 - 2.5 delta)), then the common exact epilogue
 //      (finish_query: survivors rescored in fp64 in the reference's order).
@@ -56,6 +60,16 @@ __device__ __forceinline__ void hand_over(const BatchArgs& a, uint32_t q, float 
     atomicAdd(&a.counters[4], 1u);
 }
 
+#ifdef HM_SEED_STATS  // development counters (scratch builds only): hm_seed_stats()
+__device__ unsigned long long g_seed_stats[32];
+#define SST(i, v) atomicAdd(&g_seed_stats[i], static_cast<unsigned long long>(v))
+#define SCNT(var, v) (var += (v))
+#else
+#define SST(i, v) ((void)0)
+#define SCNT(var, v) ((void)0)
+#endif
+
+
 template <int CAPW>
 #ifndef HM_SEED_MINB
 #define HM_SEED_MINB 2
@@ -70,8 +84,10 @@ __global__ void __launch_bounds__(kCons, HM_SEED_MINB) search_seed_kernel(DevInd
     const double k1 = a.k1, bb = a.b;
     const uint32_t stride = a.stab_stride;
     uint32_t* stab = a.stab + static_cast<uint64_t>(blockIdx.x) * kMaxTerms * stride;
-    // seed scores, then seed rows (n_seed <= min(kSeedMaxDf, n_docs) = seed_half)
-    float* sA = reinterpret_cast<float*>(a.seed_scratch + static_cast<uint64_t>(blockIdx.x) * 2u * a.seed_half);
+    // seed scores, then seed rows (n_seed <= min(kSeedMaxDf, n_docs) = seed_half):
+    // in shared memory (the hash table's area, idle until then) up to
+    // kSeedSmemMax seeds, else in the CTA's global scratch
+    float* const gA = reinterpret_cast<float*>(a.seed_scratch + static_cast<uint64_t>(blockIdx.x) * 2u * a.seed_half);
     const uint32_t kmax = FastCfg<CAPW>::kMaxKServed;
 
     for (int i = tid; i < 16 * CAPW; i += kCons) S.acc[i] = 0.f;
@@ -88,6 +104,10 @@ __global__ void __launch_bounds__(kCons, HM_SEED_MINB) search_seed_kernel(DevInd
         __syncthreads();
         const uint32_t q = S.q;
         if (q == kNoTerm) break;
+#ifdef HM_SEED_STATS
+        long long c_t0 = clock64(), c_t1 = 0, c_t2 = 0, c_t3 = 0;
+        uint32_t c_sp = 0, c_ep = 0, c_np = 0, c_en = 0;
+#endif
         uint32_t qr, row_lo, row_hi;  // the real query and this (slab) query's rows
         query_window(a, q, qr, row_lo, row_hi);
         const uint32_t poff = a.q_off[qr];
@@ -198,6 +218,9 @@ __global__ void __launch_bounds__(kCons, HM_SEED_MINB) search_seed_kernel(DevInd
             }
         }
         __syncthreads();
+#ifdef HM_SEED_STATS
+        c_t1 = clock64();
+#endif
         const float delta = static_cast<float>(m + 10) * 5.9604645e-08f + 1.5258789e-05f;  // (m+10) 2^-24 + 2^-16
         const float f_slack = 1.0f - 2.5f * delta;
         const float f_ub = 1.0f + 3.0f * delta;
@@ -214,21 +237,85 @@ __global__ void __launch_bounds__(kCons, HM_SEED_MINB) search_seed_kernel(DevInd
         // real score, so the k-th largest sA stays a valid lower bound)
         const uint64_t sw0 = S.t_wlo[ts];
         const uint32_t n_seed = static_cast<uint32_t>(S.t_end[ts] - sw0);
-        uint32_t* sR = reinterpret_cast<uint32_t*>(sA) + a.seed_half;  // seed rows
+        const bool seed_sm = n_seed <= kSeedSmemMax;
+        float* const sA = seed_sm ? S.acc : gA;
+        uint32_t* const sR = seed_sm ? reinterpret_cast<uint32_t*>(S.acc + kSeedSmemMax)
+                                     : reinterpret_cast<uint32_t*>(gA) + a.seed_half;  // seed rows
 #ifndef HM_SEED_KP
 #define HM_SEED_KP 4
 #endif
         constexpr int kP = HM_SEED_KP;  // rows per lane, probed together
+        // segments of postings (a term's range in one tile, or a short term's
+        // range in a chunk) flattened by an exclusive scan of their lengths:
+        // every posting of a segment list is then one independent load
+        uint64_t* const seg_b = reinterpret_cast<uint64_t*>(S.acc + 2 * kHashSlots);
+        uint32_t* const seg_pref = reinterpret_cast<uint32_t*>(seg_b + kMaxSeg);
+        uint32_t* const seg_meta = seg_pref + kMaxSeg + 1;
+        auto seg_scan = [&](uint32_t nseg) {  // seg_pref: lengths -> exclusive prefix; + total
+            __syncthreads();
+            if (warp == 0) {
+                constexpr uint32_t kPer = kMaxSeg / 32;
+                uint32_t loc = 0;
+                for (uint32_t u = 0; u < kPer; ++u) {
+                    const uint32_t x = lane * kPer + u;
+                    loc += x < nseg ? seg_pref[x] : 0u;
+                }
+                const uint32_t incl = warp_incl_scan(loc);
+                uint32_t run = incl - loc;
+                for (uint32_t u = 0; u < kPer; ++u) {
+                    const uint32_t x = lane * kPer + u;
+                    if (x < nseg) {
+                        const uint32_t l = seg_pref[x];
+                        seg_pref[x] = run;
+                        run += l;
+                    }
+                }
+                if (lane == 31) seg_pref[nseg] = incl;
+            }
+            __syncthreads();
+        };
+        auto seg_find = [&](uint32_t f, uint32_t nseg) {  // largest s with seg_pref[s] <= f
+            uint32_t lo = 0, hi = nseg;
+            while (hi - lo > 1) {
+                const uint32_t mid = (lo + hi) >> 1;
+                if (seg_pref[mid] <= f) lo = mid;
+                else hi = mid;
+            }
+            return lo;
+        };
         if (S.t_slot[ts] < 0) {
+#pragma unroll 4
             for (uint32_t e = tid; e < n_seed; e += kCons) sR[e] = __ldg(ix.post + sw0 + e) >> cb;
-        } else {  // a long seed term: rows from the tile offsets, tile by tile
+        } else {  // a long seed term: rows from the tile offsets, tiles as segments
             const uint32_t* tb = tile_row(ix, S.t_slot[ts]);
             const uint64_t s0 = S.t_start[ts], sw1 = S.t_end[ts];
-            for (uint32_t j = j0 + warp; j <= j1; j += kConsWarps) {
-                const uint64_t b0 = max(s0 + __ldg(tb + static_cast<uint64_t>(j) * kSubPerTile), sw0);
-                const uint64_t b1 = min(s0 + __ldg(tb + static_cast<uint64_t>(j + 1) * kSubPerTile), sw1);
-                for (uint64_t g = b0 + lane; g < b1; g += 32)
-                    sR[g - sw0] = (j << kTileShift) + (__ldg(ix.post + g) >> kCodeBitsLong);
+            for (uint32_t jb = j0; jb <= j1; jb += kMaxSeg) {
+                const uint32_t ns = min(j1 - jb + 1, kMaxSeg);
+                for (uint32_t x = tid; x < ns; x += kCons) {
+                    const uint64_t b = max(s0 + __ldg(tb + static_cast<uint64_t>(jb + x) * kSubPerTile), sw0);
+                    const uint64_t e = min(s0 + __ldg(tb + static_cast<uint64_t>(jb + x + 1) * kSubPerTile), sw1);
+                    seg_b[x] = b;
+                    seg_pref[x] = e > b ? static_cast<uint32_t>(e - b) : 0u;
+                }
+                seg_scan(ns);
+                const uint32_t total = seg_pref[ns];
+                for (uint32_t f0 = tid; f0 < total; f0 += 4 * kCons) {
+                    uint64_t g[4];
+                    uint32_t jt[4], p[4];
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        const uint32_t f = f0 + u * kCons;
+                        const uint32_t sg = seg_find(f, ns);
+                        g[u] = seg_b[sg] + (f - seg_pref[sg]);
+                        jt[u] = jb + sg;
+                    }
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) p[u] = f0 + u * kCons < total ? __ldg(ix.post + g[u]) : 0u;
+#pragma unroll
+                    for (int u = 0; u < 4; ++u)
+                        if (f0 + u * kCons < total) sR[g[u] - sw0] = (jt[u] << kTileShift) + (p[u] >> kCodeBitsLong);
+                }
+                __syncthreads();
             }
         }
         // t*'s own contribution to seed e (its posting's code, no probe)
@@ -277,6 +364,7 @@ __global__ void __launch_bounds__(kCons, HM_SEED_MINB) search_seed_kernel(DevInd
             uint32_t live = vm;
             if (!early) {
                 for (uint32_t i = 0; i < m; ++i) {
+                    SCNT(c_sp, __popc(vm));
                     const ValsN<kP> x = seed_probeN<Smem, kP>(sc, i, rw, vm);
 #pragma unroll
                     for (int u = 0; u < kP; ++u) A[u] += x.v[u];
@@ -293,6 +381,7 @@ __global__ void __launch_bounds__(kCons, HM_SEED_MINB) search_seed_kernel(DevInd
                     for (int u = 0; u < kP; ++u)
                         if (((live >> u) & 1u) && (A[u] + rem) * f_ub < thr) live &= ~(1u << u);
                     if (!live) break;
+                    SCNT(c_sp, __popc(live));
                     const ValsN<kP> x = seed_probeN<Smem, kP>(sc, i, rw, live);
 #pragma unroll
                     for (int u = 0; u < kP; ++u)
@@ -325,9 +414,10 @@ __global__ void __launch_bounds__(kCons, HM_SEED_MINB) search_seed_kernel(DevInd
             __syncthreads();
         } else {
             // (a) the n_full seeds with the largest t* impact, complete: L0
+#pragma unroll 4
             for (uint32_t e = tid; e < n_seed; e += kCons) sA[e] = seed_imp(e);
             __syncthreads();
-            const float v0 = block_kth_largest<kCons>(sA, n_seed, n_full, S.hist, S.sel, [] { __syncthreads(); });
+            const float v0 = block_kth_largest<kCons>(sA, n_seed, n_full, S.hist, S.sel, [] { __syncthreads(); }, 16);
             if (tid == 0) S.total = 0;
             __syncthreads();
             // rows left for (b) hold the smallest denormal: below every complete
@@ -342,15 +432,22 @@ __global__ void __launch_bounds__(kCons, HM_SEED_MINB) search_seed_kernel(DevInd
                 },
                 false, 0.f);
             __syncthreads();
-            const float L0 = block_kth_largest<kCons>(sA, n_seed, k, S.hist, S.sel, [] { __syncthreads(); });
+            const float L0 = block_kth_largest<kCons>(sA, n_seed, k, S.hist, S.sel, [] { __syncthreads(); }, 8);
             const float te0 = fmaxf(L0 * f_slack, kFltMin);
             // (b) the other seeds with early exit against te0
             seed_pass([&](uint32_t e) { return __float_as_uint(sA[e]) == kTodo; }, true, te0);
             __syncthreads();
         }
-        if (n_seed >= k) L = block_kth_largest<kCons>(sA, n_seed, k, S.hist, S.sel, [] { __syncthreads(); });
+        if (n_seed >= k) L = block_kth_largest<kCons>(sA, n_seed, k, S.hist, S.sel, [] { __syncthreads(); }, 8);
         const float te = fmaxf(L * f_slack, kFltMin);  // admission threshold (as the exhaustive kernel's)
         if (tid == 0) S.Lg = __float_as_uint(L);
+#ifdef HM_SEED_STATS
+        c_t2 = clock64();
+        if (tid == 0) {
+            SST(0, 1);
+            SST(1, n_seed);
+        }
+#endif
         // ---------------- 2. non-essential terms: longest bound-ascending prefix
         // whose bound sum cannot reach te; the rest (but t*) must be enumerated
         if (warp == 0) {
@@ -383,7 +480,10 @@ __global__ void __launch_bounds__(kCons, HM_SEED_MINB) search_seed_kernel(DevInd
             // k seeds have complete scores S >= L here; in the sweep's domain
             // (baked impacts) each has A >= (1-delta) E >= S (1-delta)/(1+delta)
             // >= L (1 - 2 delta): a valid starting bound for its admission
-            if (tid == 0) hand_over(a, q, L * (1.0f - 2.0f * delta - 1e-6f));
+            if (tid == 0) {
+                SST(10, 1);
+                hand_over(a, q, L * (1.0f - 2.0f * delta - 1e-6f));
+            }
             continue;
         }
         const uint32_t ne = S.sel[0];
@@ -412,94 +512,297 @@ __global__ void __launch_bounds__(kCons, HM_SEED_MINB) search_seed_kernel(DevInd
             const bool v = e < n_seed;
             admit(v, v ? sR[e] : 0u, v ? sA[e] : 0.f);
         }
-        // essential candidates: warp w enumerates the term's postings of tile w,
-        // w + 8, ... (long terms: rows from the tile offsets, no per-posting search)
-        // kP candidates per lane, probed together; a row already seen (it holds
-        // t* or an earlier essential term) is not admitted twice
-        // Essential terms first (t* and E'); only rows whose essential partial
-        // score plus the non-essential bound can still reach te get the
-        // non-essential probes: (A_E + U_NE) (1 + 3 delta) < te bounds the
-        // full score below te, exactly as for rows without essential terms.
         const float ubne = S.ubne_q;
-        auto candidates = [&](const RowsN<kP>& rw, uint32_t vm, uint32_t i) {
-            float A[kP] = {};
-            if (vm) {
-                for (uint32_t i2 = 0; i2 < m && vm; ++i2) {  // (every row may turn out seen)
-                    if ((ne >> i2) & 1u) continue;
-                    const ValsN<kP> x = seed_probeN<Smem, kP>(sc, i2, rw, vm);
-                    const bool seen = i2 == ts || i2 < i;
+        // ---------------- essential candidates without probes: the postings of
+        // the essential terms (t* and E') are accumulated per row in a
+        // shared-memory hash table (row -> essential score A_E), chunk by chunk
+        // of whole tiles sized to fill it about half; rows holding t* get -inf
+        // (the seeds scored them completely).  A row then needs the
+        // non-essential probes only if (A_E + U_NE)(1 + 3 delta) reaches the
+        // threshold -- those run in bound-descending order with early exit --
+        // and is admitted with the usual rule.  A table overflow hands the
+        // query to the sweep with the seeds' bound.
+        {
+            // key = row, value = the row's essential score in fixed point
+            // (2^-sx units, integer adds are native shared-memory atomics);
+            // bit 31 flags a row holding t*
+            uint32_t* hkey = reinterpret_cast<uint32_t*>(S.acc);
+            uint32_t* hval = reinterpret_cast<uint32_t*>(S.acc) + kHashSlots;
+            // per-chunk segments of the essential terms' postings: one per short
+            // term (rows in the postings), one per (long term, tile) (rows need
+            // the tile); flattened by an exclusive scan of their lengths
+            uint64_t TE = 0;
+            uint32_t n_el = 0, n_es = 0;
+            for (uint32_t i = 0; i < m; ++i)
+                if (!((ne >> i) & 1u)) {
+                    TE += S.t_end[i] - S.t_wlo[i];
+                    if (S.t_slot[i] < 0) ++n_es;
+                    else ++n_el;
+                }
+            uint64_t tpc64 = TE ? (static_cast<uint64_t>(kHashSlots / 2) * nt) / TE : nt;
+            if (n_el && tpc64 > (kMaxSeg - n_es) / n_el) tpc64 = (kMaxSeg - n_es) / n_el;
+            const uint32_t tpc = tpc64 < 1 ? 1u : tpc64 > nt ? nt : static_cast<uint32_t>(tpc64);
+            __syncthreads();  // the seeds (possibly in this area) are admitted
+            for (uint32_t x = tid; x < kHashSlots; x += kCons) {
+                hkey[x] = kHashEmpty;
+                hval[x] = 0u;
+            }
+            __syncthreads();
+            // fixed-point scale: the E' bounds sum to at most 2^30 units, so a
+            // row's sum stays below bit 31; rounding adds at most m/2 units --
+            // read back rounded up by m units (an over-estimate, safe for both
+            // the filter and admission), which must stay far inside the
+            // selection slack: m 2^-sx <= 2^-20 L, else the sweep takes the query
+            float UE = 0.f;
+            uint32_t n_ep = 0;  // E' terms: none -> every candidate holds t* (no work)
+            for (uint32_t i = 0; i < m; ++i)
+                if (!((ne >> i) & 1u) && i != ts) {
+                    UE += S.t_ms[i];
+                    ++n_ep;
+                }
+            int ex = 0;
+            frexpf(fmaxf(UE * 1.0001f, kFltMin), &ex);
+            const int sx = 30 - ex;
+            const float up = ldexpf(1.f, sx), down = ldexpf(1.f, -sx);
+            const bool fix_ok = static_cast<float>(m) * down <= ldexpf(L, -20) && sx < 126 && sx > -126;
+            if (n_ep && !fix_ok && tid == 0) S.flood = 2u;
+            auto insert = [&](uint32_t row, uint32_t v) {
+                uint32_t h = (row * 0x9E3779B1u) >> (32 - kHashBits);
+                for (uint32_t pr = 0; pr < kHashSlots; ++pr) {
+                    const uint32_t old = atomicCAS(hkey + h, kHashEmpty, row);
+                    if (old == kHashEmpty || old == row) {
+                        atomicAdd(hval + h, v);
+                        return;
+                    }
+                    h = (h + 1) & (kHashSlots - 1);
+                }
+                S.flood = 2u;  // full: the sweep serves the query
+            };
+            constexpr uint32_t kPerWarp = kHashSlots / kConsWarps;
+            const uint32_t region = warp * kPerWarp;
+            __syncthreads();
+#ifdef HM_SEED_STATS
+            if (tid == 0 && n_ep) {
+                SST(16, TE);
+                SST(17, 1);
+                SST(18, n_seed);
+            }
+#endif
+            for (uint32_t c0 = j0; n_ep && c0 <= j1 && S.flood != 2u; c0 += tpc) {
+                const uint32_t c1 = min(c0 + tpc - 1, j1);
+                const uint32_t ntc = c1 - c0 + 1;
+#ifdef HM_SEED_STATS
+                long long h_t0 = clock64();
+                if (tid == 0) SST(12, 1);
+#endif
+                // (a) segments [b, e) of every essential term in the chunk
+                const uint32_t nseg = n_es + n_el * ntc;
+                for (uint32_t x = tid; x < nseg; x += kCons) {
+                    uint32_t i = 0, o = 0, tile = c0;
+                    for (; i < m; ++i) {
+                        if ((ne >> i) & 1u) continue;
+                        const uint32_t c = S.t_slot[i] < 0 ? 1u : ntc;
+                        if (x < o + c) {
+                            tile = c0 + (x - o);
+                            break;
+                        }
+                        o += c;
+                    }
+                    const uint64_t w0 = S.t_wlo[i], w1 = S.t_end[i], s0 = S.t_start[i];
+                    uint64_t b, e;
+                    if (S.t_slot[i] < 0) {
+                        const uint32_t* tab = stab + static_cast<uint64_t>(S.t_spos[i]) * stride;
+                        b = max(s0 + tab[c0 - j0], w0);
+                        e = min(s0 + tab[c1 + 1 - j0], w1);
+                    } else {
+                        const uint32_t* tb = tile_row(ix, S.t_slot[i]);
+                        b = max(s0 + __ldg(tb + static_cast<uint64_t>(tile) * kSubPerTile), w0);
+                        e = min(s0 + __ldg(tb + static_cast<uint64_t>(tile + 1) * kSubPerTile), w1);
+                    }
+                    seg_b[x] = b;
+                    seg_pref[x] = e > b ? static_cast<uint32_t>(e - b) : 0u;
+                    seg_meta[x] = (i << 27) | tile;
+                }
+                seg_scan(nseg);
+#ifdef HM_SEED_STATS
+                if (tid == 0) SST(15, clock64() - h_t0);
+#endif
+                // (b) every posting of the chunk into the table: kU postings per
+                // thread located and loaded together, then inserted
+                const uint32_t total = seg_pref[nseg];
+#ifndef HM_SEED_KU
+#define HM_SEED_KU 4
+#endif
+                constexpr int kU = HM_SEED_KU;
+                for (uint32_t f0 = tid; f0 < total; f0 += kU * kCons) {
+                    uint32_t p[kU], meta[kU];
+                    uint64_t g[kU];
 #pragma unroll
-                    for (int u = 0; u < kP; ++u) {
-                        if (seen && x.v[u] != 0.f) vm &= ~(1u << u);
-                        A[u] += x.v[u];
+                    for (int u = 0; u < kU; ++u) {
+                        const uint32_t f = f0 + u * kCons;
+                        const uint32_t lo = seg_find(f, nseg);
+                        g[u] = seg_b[lo] + (f - seg_pref[lo]);
+                        meta[u] = seg_meta[lo];
+                    }
+#pragma unroll
+                    for (int u = 0; u < kU; ++u) p[u] = f0 + u * kCons < total ? __ldg(ix.post + g[u]) : 0u;
+#pragma unroll
+                    for (int u = 0; u < kU; ++u) {
+                        if (f0 + u * kCons >= total) break;
+                        const uint32_t i = meta[u] >> 27;
+                        uint32_t row;
+                        float v = 0.f;
+                        if (S.t_slot[i] < 0) {
+                            row = p[u] >> cb;
+                            if (i != ts) {
+                                const uint32_t code = p[u] & ix.esc_short;
+                                v = S.t_cu[i] * (code < ix.n_codes_short
+                                                     ? S.w32s[code]
+                                                     : impact32(static_cast<double>(__ldg(ix.tf + g[u])),
+                                                                static_cast<double>(__ldg(ix.doc_lens + row)),
+                                                                ix.avgdl, k1, bb));
+                            }
+                        } else {
+                            row = ((meta[u] & 0x7FFFFFFu) << kTileShift) + (p[u] >> kCodeBitsLong);
+                            if (i != ts) {
+                                const uint32_t code = p[u] & kEscLong;
+                                v = S.t_cu[i] * (code < ix.n_codes
+                                                     ? code_w(sc, code)
+                                                     : impact32(static_cast<double>(__ldg(ix.tf + g[u])),
+                                                                static_cast<double>(__ldg(ix.doc_lens + row)),
+                                                                ix.avgdl, k1, bb));
+                            }
+                        }
+                        insert(row, i == ts ? 0x80000000u : __float2uint_rn(v * up));
                     }
                 }
-                uint32_t need = 0;
-                const float tn = fmaxf(fmaxf(Lw, __uint_as_float(S.Lg)) * f_slack, te);
+                __syncthreads();
+#ifdef HM_SEED_STATS
+                long long h_t1 = clock64();
+                if (tid == 0) SST(13, h_t1 - h_t0);
+#endif
+                if (S.flood == 2u) break;
+                // (c) scan of warp w's slots: candidates (rows without t* whose
+                // essential score + U_NE can reach the threshold) compacted to the
+                // front of the region, every slot cleared
+                uint32_t ncand = 0;
+                {
+                    const float tn = fmaxf(fmaxf(Lw, __uint_as_float(S.Lg)) * f_slack, te);
+                    for (uint32_t g0 = 0; g0 < kPerWarp; g0 += 128) {
+                        uint32_t r4[4], v4[4];
 #pragma unroll
-                for (int u = 0; u < kP; ++u)
-                    if (((vm >> u) & 1u) && (A[u] + ubne) * f_ub >= tn) need |= 1u << u;
-                vm = need;
-                if (ne && vm)
-                    for (uint32_t i2 = 0; i2 < m; ++i2) {
-                        if (!((ne >> i2) & 1u)) continue;
-                        const ValsN<kP> x = seed_probeN<Smem, kP>(sc, i2, rw, vm);
+                        for (int u = 0; u < 4; ++u) {
+                            r4[u] = hkey[region + g0 + 32 * u + lane];
+                            v4[u] = hval[region + g0 + 32 * u + lane];
+                        }
+                        __syncwarp();
 #pragma unroll
-                        for (int u = 0; u < kP; ++u) A[u] += x.v[u];
+                        for (int u = 0; u < 4; ++u) {
+                            hkey[region + g0 + 32 * u + lane] = kHashEmpty;
+                            hval[region + g0 + 32 * u + lane] = 0u;
+                        }
+                        __syncwarp();
+#pragma unroll
+                        for (int u = 0; u < 4; ++u) {
+                            // rows with t* (bit 31) were scored as seeds
+                            const float ae = __fmul_ru(__uint2float_ru(v4[u] + m), down);
+                            const bool ok = r4[u] != kHashEmpty && !(v4[u] >> 31) && (ae + ubne) * f_ub >= tn;
+                            const uint32_t bal = __ballot_sync(0xffffffffu, ok);
+                            if (ok) {
+                                const uint32_t pos = region + ncand + __popc(bal & ((1u << lane) - 1u));
+                                hkey[pos] = r4[u];
+                                hval[pos] = __float_as_uint(ae);
+                            }
+                            ncand += __popc(bal);
+                        }
+                        __syncwarp();
                     }
-            }
-#pragma unroll
-            for (int u = 0; u < kP; ++u) admit((vm >> u) & 1u, rw.r[u], A[u]);
-        };
-        for (uint32_t i = 0; i < m && !flood; ++i) {
-            if (i == ts || ((ne >> i) & 1u)) continue;
-            const uint64_t w0 = S.t_wlo[i], w1 = S.t_end[i];
-            if (S.t_slot[i] < 0) {
-                const uint32_t n = static_cast<uint32_t>(w1 - w0);
-                for (uint32_t e0 = warp * 32 * kP; e0 < n && !flood; e0 += kConsWarps * 32 * kP) {
+                }
+                SCNT(c_en, lane == 0 ? ncand : 0u);
+                // (d) the candidates: non-essential terms by bound descending with
+                // early exit, then admission
+                for (uint32_t c = 0; c < ncand; c += 32 * kP) {
                     RowsN<kP> rw;
+                    float A[kP];
                     uint32_t vm = 0;
 #pragma unroll
                     for (int u = 0; u < kP; ++u) {
-                        const uint32_t eu = e0 + 32 * u + lane;
-                        rw.r[u] = eu < n ? __ldg(ix.post + w0 + eu) >> cb : 0u;
-                        vm |= (eu < n ? 1u : 0u) << u;
+                        const uint32_t x = c + 32 * u + lane;
+                        rw.r[u] = x < ncand ? hkey[region + x] : 0u;
+                        A[u] = x < ncand ? __uint_as_float(hval[region + x]) : 0.f;
+                        vm |= (x < ncand ? 1u : 0u) << u;
                     }
-                    candidates(rw, vm, i);
-                }
-            } else {
-                const uint32_t* tb = tile_row(ix, S.t_slot[i]);
-                const uint64_t s0 = S.t_start[i];
-                for (uint32_t j = j0 + warp; j <= j1 && !flood; j += kConsWarps) {
-                    const uint64_t b0 = max(s0 + __ldg(tb + static_cast<uint64_t>(j) * kSubPerTile), w0);
-                    const uint64_t b1 = min(s0 + __ldg(tb + static_cast<uint64_t>(j + 1) * kSubPerTile), w1);
-                    const uint32_t base = j << kTileShift;
-                    for (uint64_t g0 = b0; g0 < b1 && !flood; g0 += 32 * kP) {
-                        RowsN<kP> rw;
-                        uint32_t vm = 0;
+                    const float tn = fmaxf(fmaxf(Lw, __uint_as_float(S.Lg)) * f_slack, te);
+                    uint32_t live = vm;
+                    for (int jn = static_cast<int>(m) - 1; jn >= 0 && live && ne; --jn) {
+                        const uint32_t i2 = S.msorder[jn];
+                        if (!((ne >> i2) & 1u)) continue;
+                        const float rem = S.rem_ub[jn + 1];  // bounds of msorder[0..jn] but t*
 #pragma unroll
-                        for (int u = 0; u < kP; ++u) {
-                            const uint64_t gu = g0 + 32 * u + lane;
-                            rw.r[u] = gu < b1 ? base + (__ldg(ix.post + gu) >> kCodeBitsLong) : 0u;
-                            vm |= (gu < b1 ? 1u : 0u) << u;
-                        }
-                        candidates(rw, vm, i);
+                        for (int u = 0; u < kP; ++u)
+                            if (((live >> u) & 1u) && (A[u] + rem) * f_ub < tn) live &= ~(1u << u);
+                        if (!live) break;
+                        SCNT(c_np, __popc(live));
+                        const ValsN<kP> xv = seed_probeN<Smem, kP>(sc, i2, rw, live);
+#pragma unroll
+                        for (int u = 0; u < kP; ++u)
+                            if ((live >> u) & 1u) A[u] += xv.v[u];
                     }
+#pragma unroll
+                    for (int u = 0; u < kP; ++u) admit((live >> u) & 1u, rw.r[u], A[u]);
+                    if (flood) break;
                 }
+                __syncwarp();
+                for (uint32_t x = lane; x < ncand; x += 32) {
+                    hkey[region + x] = kHashEmpty;
+                    hval[region + x] = 0u;
+                }
+                if (flood && lane == 0) atomicMax(&S.flood, 1u);
+                __syncthreads();
+#ifdef HM_SEED_STATS
+                if (tid == 0) SST(14, clock64() - h_t1);
+#endif
+                if (S.flood) break;
             }
         }
         if (lane == 0) {
             S.n_w[warp] = nw;
-            if (flood) S.flood = 1;
+            if (flood) atomicMax(&S.flood, 1u);
         }
+#ifdef HM_SEED_STATS
+        {
+            const uint32_t vs[4] = {c_sp, c_en, c_ep, c_np};
+            for (int z = 0; z < 4; ++z) {
+                uint32_t v = vs[z];
+                for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+                if (lane == 0) SST(2 + z, v);
+            }
+        }
+#endif
         __syncthreads();
-        if (S.flood) {  // the lists cannot hold the near-ties: the exhaustive kernel
-            if (tid == 0) hand_over(a, q);
+#ifdef HM_SEED_STATS
+        c_t3 = clock64();
+#endif
+        if (S.flood) {  // the lists cannot hold the near-ties (1) or the hash table
+                        // overflowed (2, with the seeds' bound): the exhaustive kernel
+            if (tid == 0) {
+                if (S.flood == 2u) hand_over(a, q, L * (1.0f - 2.0f * delta - 1e-6f));
+                else hand_over(a, q);
+            }
             __syncthreads();
             if (tid < kConsWarps) S.n_w[tid] = 0;
             continue;
         }
         finish_query<CAPW>(ix, a, S, q, m, k, nw, f_slack, k1, bb);
+#ifdef HM_SEED_STATS
+        if (tid == 0) {
+            SST(6, c_t1 - c_t0);
+            SST(7, c_t2 - c_t1);
+            SST(8, c_t3 - c_t2);
+            SST(9, clock64() - c_t3);
+            SST(11, 1);
+        }
+#endif
     }
 }
 
@@ -536,3 +839,14 @@ cudaError_t launch_search_seed(const DevIndex& ix, const BatchArgs& a, int cap, 
 }
 
 }  // namespace hm
+
+#ifdef HM_SEED_STATS
+extern "C" int hm_seed_stats(unsigned long long* out, int reset) {
+    if (cudaMemcpyFromSymbol(out, hm::g_seed_stats, sizeof(hm::g_seed_stats)) != cudaSuccess) return -1;
+    if (reset) {
+        static const unsigned long long z[32] = {};
+        cudaMemcpyToSymbol(hm::g_seed_stats, z, sizeof(z));
+    }
+    return 0;
+}
+#endif

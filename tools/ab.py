@@ -62,6 +62,22 @@ def main():
             st = " stats/query=" + str([round(v / ((reps + 2) * cfg["n_queries"]), 1) for v in arr])
         except AttributeError:
             pass
+        try:
+            import ctypes
+            from paper_2605_25092_b200 import _lib
+            fn = _lib.load("libhm_b200.so").hm_seed_stats
+            arr = (ctypes.c_ulonglong * 32)()
+            fn(arr, 1)
+            v = list(arr)
+            nq_seed = max(v[0], 1)
+            st += (f" seed: queries={v[0]} served={v[11]} emax_handover={v[10]} seeds/q={v[1] / nq_seed:.0f} "
+                   f"seed_probes/q={v[2] / nq_seed:.0f} Eposts/q={v[3] / nq_seed:.0f} Eprobes/q={v[4] / nq_seed:.0f} "
+                   f"NEprobes/q={v[5] / nq_seed:.0f} cycles/q prologue={v[6] / nq_seed:.0f} seeds={v[7] / nq_seed:.0f} "
+                   f"cand={v[8] / max(v[11], 1):.0f} epilogue={v[9] / max(v[11], 1):.0f} "
+                   f"chunks/q={v[12] / nq_seed:.1f} insert={v[13] / nq_seed:.0f} (segments {v[15] / nq_seed:.0f}) scan={v[14] / nq_seed:.0f} "
+                   f"hashed_q={v[17]} TE/hq={v[16] / max(v[17], 1):.0f} seeds/hq={v[18] / max(v[17], 1):.0f}")
+        except AttributeError:
+            pass
         print(f"{name} flags={fl:4d}: {np.median(ts):8.2f} ms  {cfg['n_queries'] / np.median(ts) * 1e3:10.0f} q/s  "
               f"timing={tm} seeded={search.last_seed()} {same}{st}", flush=True)
 
