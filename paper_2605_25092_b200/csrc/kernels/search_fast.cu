@@ -44,6 +44,7 @@
 namespace hm {
 
 // ---------------------------------------------------------------- kernel
+
 #ifdef HM_STATS  // development counters (scratch builds only): hm_dev_stats()
 __device__ unsigned long long g_stats[8];
 #define HM_STAT(i, v) atomicAdd(&g_stats[i], static_cast<unsigned long long>(v))
@@ -566,6 +567,24 @@ __global__ void __launch_bounds__(kCons, 2) search_fast_kernel(DevIndex ix, Batc
                 for (uint32_t z = lane; z < kV; z += 32) acc4[z] = z4;
             __syncwarp();
         };
+        // short terms: lane s holds term s's segment of the next tile to process
+        uint64_t ss_b = 0, ss_e = 0;
+        float my_sc = 0.f;
+        const uint32_t* my_stab = nullptr;
+        uint64_t my_s0 = 0;
+        if (static_cast<uint32_t>(lane) < n_short) {
+            const uint32_t i = S.order_list[n_long + lane];
+            my_sc = S.t_c32[i];
+            my_stab = stab + static_cast<uint64_t>(lane) * stride;
+            my_s0 = S.t_start[i];
+        }
+        auto short_prefetch = [&](uint32_t j) {
+            if (static_cast<uint32_t>(lane) < n_short) {
+                ss_b = my_s0 + my_stab[j - j0];
+                ss_e = my_s0 + my_stab[j - j0 + 1];
+            }
+        };
+        if (NE && n_short) short_prefetch(j0);
         uint32_t ready = j0;  // the tile whose ranges are in rdesc
         prefetch(j0);
         install(j0);
@@ -641,22 +660,86 @@ __global__ void __launch_bounds__(kCons, 2) search_fast_kernel(DevIndex ix, Batc
                 cur = nxt;
                 stage = stage + 1 == static_cast<uint32_t>(kSt) ? 0 : stage + 1;
             }
-            // ---- short terms: the tile segment is small; every warp filters its rows
-            for (uint32_t s = 0; s < n_short; ++s) {
-                const uint32_t i = S.order_list[n_long + s];
-                const float c = S.t_c32[i];
-                const uint32_t* tab = stab + static_cast<uint64_t>(s) * stride;
-                const uint64_t b = S.t_start[i] + tab[j - j0], e = S.t_start[i] + tab[j - j0 + 1];
-                for (uint64_t b0 = b; b0 < e; b0 += 32) {
-                    const uint64_t g = b0 + lane;
-                    if (g < e) {
-                        const uint32_t p = __ldg(ix.post + g);
-                        const uint32_t local = (p >> cb) - base;
-                        if (local - wr0 < static_cast<uint32_t>(kUnitRows)) {
-                            const uint32_t code = p & ix.esc_short;
-                            const float w = code < ix.n_codes_short ? S.w32s[code] : esc_w(ix, g, base + local, k1, bb);
-                            float* acc = reinterpret_cast<float*>(accw) + (swz10(local) & (kUnitRows - 1));
-                            *acc = __fmaf_rn(c, w, *acc);
+            // ---- short terms: the tile segments of all of them (a few postings
+            // each) flattened across the lanes -- lane s holds short term s's
+            // segment (offsets prefetched one tile ahead), a warp scan of the
+            // lengths, then every lane takes postings f = lane, lane + 32, ...
+            // of the concatenation (loads in flight together); every warp
+            // keeps the rows of its own unit.  Two lanes of one step may hold
+            // the same row (a document with two short terms): rows are merged
+            // with a match before the read-modify-write.
+            if (!NE) {  // short terms one after the other: the tile segment is small; every warp filters its rows
+                for (uint32_t st = 0; st < n_short; ++st) {
+                    const uint32_t i = S.order_list[n_long + st];
+                    const float c = S.t_c32[i];
+                    const uint32_t* tab = stab + static_cast<uint64_t>(st) * stride;
+                    const uint64_t b = S.t_start[i] + tab[j - j0], e = S.t_start[i] + tab[j - j0 + 1];
+                    for (uint64_t b0 = b; b0 < e; b0 += 32) {
+                        const uint64_t g = b0 + lane;
+                        if (g < e) {
+                            const uint32_t p = __ldg(ix.post + g);
+                            const uint32_t local = (p >> cb) - base;
+                            if (local - wr0 < static_cast<uint32_t>(kUnitRows)) {
+                                const uint32_t code = p & ix.esc_short;
+                                const float w = code < ix.n_codes_short ? S.w32s[code] : esc_w(ix, g, base + local, k1, bb);
+                                float* acc = reinterpret_cast<float*>(accw) + (swz10(local) & (kUnitRows - 1));
+                                *acc = __fmaf_rn(c, w, *acc);
+                            }
+                        }
+                    }
+                    __syncwarp();
+                }
+            } else if (n_short) {
+                const uint32_t slen = ss_e > ss_b ? static_cast<uint32_t>(ss_e - ss_b) : 0u;
+                const uint64_t sbg = ss_b;
+                const uint32_t incl = warp_incl_scan(slen), spre = incl - slen;
+                const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
+                if (j < j1) short_prefetch(j + 1);
+                constexpr int kSU = 4;
+                for (uint32_t f0 = 0; f0 < total; f0 += 32 * kSU) {
+                    uint64_t g[kSU];
+                    float c[kSU];
+                    uint32_t p[kSU];
+#pragma unroll
+                    for (int u = 0; u < kSU; ++u) {
+                        const uint32_t f = f0 + 32 * u + lane;
+                        uint32_t lo = 0, hi = n_short;  // largest term s with spre_s <= f
+#pragma unroll
+                        for (int it = 0; it < 5; ++it) {
+                            const uint32_t mid = (lo + hi) >> 1;
+                            const uint32_t pm = __shfl_sync(0xffffffffu, spre, mid & 31);
+                            if (hi - lo > 1) {
+                                if (pm <= f) lo = mid;
+                                else hi = mid;
+                            }
+                        }
+                        g[u] = __shfl_sync(0xffffffffu, sbg, lo) + (f - __shfl_sync(0xffffffffu, spre, lo));
+                        c[u] = __shfl_sync(0xffffffffu, my_sc, lo);
+                    }
+#pragma unroll
+                    for (int u = 0; u < kSU; ++u) p[u] = f0 + 32 * u + lane < total ? __ldg(ix.post + g[u]) : 0u;
+#pragma unroll
+                    for (int u = 0; u < kSU; ++u) {
+                        const uint32_t local = (p[u] >> cb) - base;
+                        const bool mine = f0 + 32 * u + lane < total && local - wr0 < static_cast<uint32_t>(kUnitRows);
+                        float v = 0.f;
+                        if (mine) {
+                            const uint32_t code = p[u] & ix.esc_short;
+                            v = c[u] * (code < ix.n_codes_short ? S.w32s[code] : esc_w(ix, g[u], base + local, k1, bb));
+                        }
+                        // lanes holding the same row: the lowest one adds the group's sum
+                        const uint32_t key = mine ? local : 0xFFFFFFFFu;
+                        const uint32_t grp = __match_any_sync(0xffffffffu, key);
+                        if (mine) {
+                            if (__popc(grp) > 1) {
+                                float sum = 0.f;
+                                for (uint32_t mm = grp; mm; mm &= mm - 1) sum += __shfl_sync(grp, v, __ffs(mm) - 1);
+                                v = sum;
+                            }
+                            if ((__ffs(grp) - 1) == lane) {
+                                float* acc = reinterpret_cast<float*>(accw) + (swz10(local) & (kUnitRows - 1));
+                                *acc += v;
+                            }
                         }
                     }
                 }

@@ -4,7 +4,7 @@ final k-th score theta, why a query is handed to the tile sweep, and what
 alternative starting bounds (per-term champion lists: the C postings of each
 plan term with the largest impact, scored completely) would give.
 
-    python tools/c2_study.py [stride] [C]
+    python tools/c2_study.py [stride] [C] [c2|c4]
 """
 import os
 import sys
@@ -18,8 +18,9 @@ from paper_2605_25092_b200 import synth  # noqa: E402
 
 stride = int(sys.argv[1]) if len(sys.argv) > 1 else 50
 CH = int(sys.argv[2]) if len(sys.argv) > 2 else 64
+CFG = {"c2": bench.C2, "c4": bench.C4}[sys.argv[3] if len(sys.argv) > 3 else "c2"]
 t0 = time.time()
-corpus, q = bench.gen(bench.C2)
+corpus, q = bench.gen(CFG)
 hx = synth.HostIndex(corpus)
 print("built", round(time.time() - t0, 1), flush=True)
 off = hx.term_offsets.astype(np.int64)
@@ -33,7 +34,7 @@ Kd = (k1 * (1 - b + b * dl / hx.avgdl)).astype(np.float32)
 tids_all = hx.resolve(q.term_ranks)
 qo = q.offsets
 SEEDMAX, EMAX = 131072, 131072
-K = 10
+K = CFG["k"]
 acc = np.zeros(N, np.float64)
 stats = []
 for qi in range(0, len(qo) - 1, stride):

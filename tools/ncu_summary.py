@@ -63,7 +63,7 @@ def main():
         if name not in kernels or kernels[name]["ms"] < k["ms"]:
             kernels[name] = k
     res = dict(report=rep, note=note, kernels=kernels, launches=launches,
-               step_ms=sum(x["ms"] for x in launches), step_dram_bytes=sum(x["dram_bytes"] for x in launches))
+               step_ms=sum(x["ms"] for x in launches), step_dram_bytes=sum(x["dram_bytes"] for x in launches if x["dram_bytes"] == x["dram_bytes"]))
     with open(out, "w") as f:
         json.dump(res, f, indent=1)
     for n, k in kernels.items():
