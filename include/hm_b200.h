@@ -139,8 +139,13 @@ int hm_search_batch_parts(hm_index* index, const hm_query_batch* batch, uint32_t
                           const uint32_t* part_row, hm_results* out_parts);
 
 /* Same with DEVICE buffers (batch arrays and results on the index's device),
- * enqueued on `stream` (a cudaStream_t, NULL = legacy default) without host
- * synchronisation.  `n_queries` etc. are read from the host struct. */
+ * ordered on `stream` (a cudaStream_t, NULL = legacy default): the launches
+ * run on a pooled workspace stream that waits for `stream`, and `stream`
+ * waits for them.  `n_queries` etc. are read from the host struct.  The call
+ * is NOT fully asynchronous: it reads q_off back (a (n_queries + 1) x 4-byte
+ * D2H on `stream`, synchronised) to size the plan scratch, and synchronises
+ * the workspace stream before returning (the pinned staging of the impact
+ * table is reused by the next call); results are complete on return. */
 int hm_search_batch_device(hm_index* index, const hm_query_batch* batch_dev,
                            hm_results* out_dev, void* stream);
 
