@@ -27,11 +27,17 @@ constexpr uint32_t kFlagNeAll = 256u;
 static_assert(kConsWarps * kUnitRows == kTile, "one warp per 2048-row unit");
 static_assert(2 + kUnitShift + 3 + kBakeMantBits == 32, "bk = 19-bit impact | 13-bit offset");
 
+#ifndef HM_KC320
+#define HM_KC320 2
+#endif
+#ifndef HM_ST320
+#define HM_ST320 2
+#endif
 template <int CAPW>
 struct FastCfg {
     static constexpr int kMaxKServed = CAPW == 192 ? 32 : 128;
-    static constexpr int kC = CAPW == 192 ? 3 : 2;   // 16-byte chunks per lane per pipeline step
-    static constexpr int kStages = 2;  // staged steps (1 applied + kStages - 1 in flight)
+    static constexpr int kC = CAPW == 192 ? 3 : HM_KC320;   // 16-byte chunks per lane per pipeline step
+    static constexpr int kStages = CAPW == 192 ? 2 : HM_ST320;  // staged steps (1 applied + kStages - 1 in flight)
 };
 
 // Shared-memory layout.  ACC floats of accumulators (the tile sweep: kTile;
