@@ -52,6 +52,8 @@ C2 = dict(n_records=8841823, vocab_size=1000000, min_doc_tokens=20, max_doc_toke
           n_queries=10000, min_terms=3, max_terms=6, k=10)
 C4 = dict(n_records=8841823, vocab_size=1000000, min_doc_tokens=40, max_doc_tokens=80,
           n_queries=4096, min_terms=24, max_terms=32, k=100)
+C1 = dict(n_records=100000, vocab_size=5000, min_doc_tokens=5, max_doc_tokens=30,
+          n_queries=1000, min_terms=3, max_terms=6, k=10)
 C3 = dict(n_records=5000000, vocab_size=5000, min_doc_tokens=5, max_doc_tokens=30,
           n_queries=10000, min_terms=3, max_terms=6, k=10,
           time_span_ms=int(28 * DAY * 5000000 / 4052))  # constant arrival (acceptance.cpp:101-104)
@@ -331,6 +333,50 @@ def measure_c4(torch, d, flush, args, peak):
                postings_identical_to_reference_count=bool((got["postings"] == post).all()))
     if not args.no_cpu_baseline:
         res["cpu_baseline"] = cpu_baseline_flat(hx, queries, "C4", args.cpu_sample_c4, C4["k"])
+    del dev, hx
+    torch.cuda.empty_cache()
+    return res
+
+
+def measure_c1(torch, d, flush, args):
+    """BASELINE configs[0] (the reference's CPU-runnable case): 100K docs,
+    1,000 queries, top-10 -- L2-resident and launch-bound, so qps
+    and latency, no roofline; parity on the reference's answers for the first
+    40 queries (tests/golden/c1_sample.json, oracle/make_golden.py)."""
+    from paper_2605_25092_b200 import search, synth
+    corpus, queries = gen(C1)
+    hx = synth.HostIndex(corpus)
+    del corpus
+    dev = search.DeviceIndex.from_host(hx)
+    q_off = queries.offsets.astype(np.uint32)
+    tids = hx.resolve(queries.term_ranks)
+    post = exhaustive_postings(hx, q_off, tids)
+    b = DevBatch(torch, d, q_off, tids, C1["k"])
+    ms, _ = time_device_steps(torch, dev, b, max(5, args.steps), 3, flush, timing=False)
+    got = b.host()
+    t = statistics.mean(ms)
+    with open(os.path.join(ROOT, "tests", "golden", "c1_sample.json")) as f:
+        g = json.load(f)
+    ids_ok = sc_ok = skip_ok = True
+    nd_o, nd_r = [], []
+    for i, qg in enumerate(g["queries"]):
+        m = len(qg["ids"])
+        ids_ok &= int(got["n"][i]) == m and got["ids"][i, :m].tolist() == qg["ids"]
+        sc_ok &= [float(x).hex() for x in got["scores"][i, :m]] == qg["scores"]
+        skip_ok &= bool(got["skip"][i]) == (float.fromhex(qg["margin"]) >= 0.10)
+        nd_o.append(ndcg10(got["ids"][i, :int(got["n"][i])], qg["gold"]))
+        nd_r.append(ndcg10(qg["ids"], qg["gold"]))
+    res = dict(workload="C1: 100,000 docs (V=5,000, 5-30 tokens), 1,000 queries of 3-6 terms, top-10",
+               qps=C1["n_queries"] / (t / 1e3), p50_batch_ms=pct(ms, 0.5), p99_batch_ms=pct(ms, 0.99),
+               steps=len(ms), bound="latency / L2 (SURVEY §8d: the whole index is ~11 MB)",
+               exhaustive_postings=int(post.sum()),
+               parity=dict(sample=len(g["queries"]), reference="tests/golden/c1_sample.json (reference library answers)",
+                           ids_identical=bool(ids_ok), scores_identical=bool(sc_ok), skip_identical=bool(skip_ok),
+                           ndcg10_ours=float(np.mean(nd_o)), ndcg10_reference=float(np.mean(nd_r))),
+               postings_identical_to_reference_count=all(int(got["postings"][i]) == qg["postings"]
+                                                         for i, qg in enumerate(g["queries"])))
+    if not args.no_cpu_baseline:
+        res["cpu_baseline"] = cpu_baseline_flat(hx, queries, "C1", C1["n_queries"], C1["k"])
     del dev, hx
     torch.cuda.empty_cache()
     return res
@@ -657,7 +703,8 @@ def main():
         if not args.c2_only:
             del dev
             torch.cuda.empty_cache()
-            configs = dict(c4=measure_c4(torch, d, flush, args, peak), c3=measure_c3(torch, d, flush, args, peak))
+            configs = dict(c4=measure_c4(torch, d, flush, args, peak), c3=measure_c3(torch, d, flush, args, peak),
+                           c1=measure_c1(torch, d, flush, args))
 
     if rank == 0:
         line = dict(metric=METRIC, value=qps, unit="queries/s", n_gpus=world, steps=args.steps,
