@@ -443,6 +443,7 @@ __global__ void __launch_bounds__(kCons, 2) search_fast_kernel(DevIndex ix, Batc
             return __popc(__ballot_sync(0xffffffffu, ok));  // rem_ub increases: a prefix
         };
         auto install = [&](uint32_t j) {
+            __syncwarp();  // every lane is done reading the previous tile's descriptors
             uint32_t u0, u1;
             uint32_t pj = 0;
             if constexpr (NE) {
@@ -741,6 +742,7 @@ __global__ void __launch_bounds__(kCons, 2) search_fast_kernel(DevIndex ix, Batc
                                 *acc += v;
                             }
                         }
+                        __syncwarp();  // the next step's lanes may hold the same rows
                     }
                 }
                 __syncwarp();

@@ -26,7 +26,8 @@ def main():
     cases = [dict(), dict(flags=search.HM_FLAG_SEED_ALL), dict(flags=search.HM_FLAG_EXHAUSTIVE),
              dict(flags=search.HM_FLAG_FORCE_EXACT), dict(row_lo=3000, row_hi=17000),
              dict(row_lo=3000, row_hi=17000, flags=search.HM_FLAG_SEED_ALL), dict(k=100),
-             dict(k1=0.9, b=0.4, flags=search.HM_FLAG_SEED_ALL)]
+             dict(k1=0.9, b=0.4, flags=search.HM_FLAG_SEED_ALL), dict(flags=search.HM_FLAG_NE_ALL),
+             dict(k=300), dict(flags=search.HM_FLAG_SEED_ALL | search.HM_FLAG_NO_SPLIT)]
     for kw in cases:
         k = kw.pop("k", 10)
         got = dev.search_lists(tids, k, **kw)
@@ -49,7 +50,18 @@ def main():
         assert (got["n"] == n).all()
         for i in range(len(t2)):
             assert (got["ids"][i, :n[i]] == ids[i, :n[i]]).all(), (lo, hi, i)
-    print("sanitize cases ok:", len(cases) + 3)
+    # doc-sharded search behind the C ABI: three shards on this device, the
+    # gather + merge kernel reading their lists (peer memory on a multi-GPU box)
+    sh = search.ShardedDeviceIndex.from_host(hx2, [0, 0, 0])
+    off = np.zeros(len(t2) + 1, np.uint32)
+    off[1:] = np.cumsum([len(t) for t in t2])
+    for k in (10, 300):
+        got = sh.search_batch(off, np.concatenate(t2).astype(np.uint32), k)
+        ids, sc, n, _ = orc2.topk(t2, k)
+        assert (got["n"] == n).all()
+        for i in range(len(t2)):
+            assert (got["ids"][i, :n[i]] == ids[i, :n[i]]).all(), ("sharded", k, i)
+    print("sanitize cases ok:", len(cases) + 5)
 
 
 if __name__ == "__main__":
