@@ -244,7 +244,10 @@ class DeviceIndex:
             self._h = None
 
     def __del__(self):
-        self.close()
+        try:
+            self.close()
+        except TypeError:  # interpreter shutdown: module globals already cleared
+            pass
 
     @property
     def device_bytes(self):
@@ -401,7 +404,10 @@ class ShardedDeviceIndex:
             self._h = None
 
     def __del__(self):
-        self.close()
+        try:
+            self.close()
+        except TypeError:  # interpreter shutdown: module globals already cleared
+            pass
 
 
 def last_timing():
@@ -459,7 +465,10 @@ class Vocab:
             self._h = None
 
     def __del__(self):
-        self.close()
+        try:
+            self.close()
+        except TypeError:  # interpreter shutdown: module globals already cleared
+            pass
 
 
 def last_handover(nq):
@@ -749,7 +758,10 @@ class Hidx:
             self._h = None
 
     def __del__(self):
-        self.close()
+        try:
+            self.close()
+        except TypeError:  # interpreter shutdown: module globals already cleared
+            pass
 
 
 class Htix:
@@ -790,7 +802,10 @@ class Htix:
             self._h = None
 
     def __del__(self):
-        self.close()
+        try:
+            self.close()
+        except TypeError:  # interpreter shutdown: module globals already cleared
+            pass
 
 
 def k_star(epsilon, lam):
@@ -1004,7 +1019,10 @@ class DeviceBridge:
             self._h = None
 
     def __del__(self):
-        self.close()
+        try:
+            self.close()
+        except TypeError:  # interpreter shutdown: module globals already cleared
+            pass
 
     def search_batch(self, queries, k, row_lo=0, row_hi=0, flags=0):
         """Host-buffer batch (hm_bridge_search_batch) over SparseVectors.
@@ -1168,7 +1186,10 @@ class DenseIndex:
             self._h = None
 
     def __del__(self):
-        self.close()
+        try:
+            self.close()
+        except TypeError:  # interpreter shutdown: module globals already cleared
+            pass
 
     def search_batch(self, queries, k, flags=0):
         """queries [nq x dim] fp32 -> dict(ids[nq,k], scores[nq,k], n[nq])"""
