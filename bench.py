@@ -585,7 +585,8 @@ def main():
     kern = nc.get("kernels", {})
 
     def kroof(name, ms, algo):
-        kn = kern.get(name, {})
+        # ncu names the kernel by its demangled base name ("void search_seed_kernel")
+        kn = next((v for kname, v in kern.items() if name in kname), {})
         dram = kn.get("dram_bytes")
         return dict(ms=ms, algorithmic_bytes=algo, effective_achieved=algo / (ms / 1e3) / 1e9,
                     effective_frac=algo / (ms / 1e3) / 1e9 / peak, dram_bytes=dram,
