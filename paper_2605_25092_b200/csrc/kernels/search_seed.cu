@@ -539,7 +539,10 @@ __global__ void __launch_bounds__(kCons, HM_SEED_MINB) search_seed_kernel(DevInd
                     if (S.t_slot[i] < 0) ++n_es;
                     else ++n_el;
                 }
-            uint64_t tpc64 = TE ? (static_cast<uint64_t>(kHashSlots / 2) * nt) / TE : nt;
+#ifndef HM_HASH_FILL
+#define HM_HASH_FILL 2  // postings per chunk = slots * HM_HASH_FILL / 4
+#endif
+            uint64_t tpc64 = TE ? (static_cast<uint64_t>(kHashSlots * HM_HASH_FILL / 4) * nt) / TE : nt;
             if (n_el && tpc64 > (kMaxSeg - n_es) / n_el) tpc64 = (kMaxSeg - n_es) / n_el;
             const uint32_t tpc = tpc64 < 1 ? 1u : tpc64 > nt ? nt : static_cast<uint32_t>(tpc64);
             __syncthreads();  // the seeds (possibly in this area) are admitted
