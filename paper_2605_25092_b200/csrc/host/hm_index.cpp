@@ -602,9 +602,11 @@ uint32_t split_for(const hm_index* X, const hm_query_batch& hb) {
     // tiny batches one (per-slab overheads dominate thin slabs), 32-255
     // queries four, 256+ eight (LPT then evens out the heaviest queries)
     const uint64_t target = nq < 32 ? resident : nq < 256 ? 4 * resident : 8 * resident;
-    uint32_t S = static_cast<uint32_t>(std::min<uint64_t>(target / nq, 64));
+#ifndef HM_MAX_SLABS
+#define HM_MAX_SLABS 64
+#endif
+    uint32_t S = static_cast<uint32_t>(std::min<uint64_t>(target / nq, HM_MAX_SLABS));
     S = std::min<uint32_t>(S, 2048 / k);  // merge_kernel holds split x k candidates
-    S = std::min<uint32_t>(S, 64);
     S = std::min<uint32_t>(S, span / hm::kTile);  // at least a tile per slab
     return S >= 2 ? S : 1;
 }
