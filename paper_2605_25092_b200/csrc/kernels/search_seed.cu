@@ -49,7 +49,10 @@ constexpr uint64_t kProbeCost = HM_SEED_PCOST;  // seeds: a probe (short depende
 constexpr uint64_t kEMax = HM_SEED_EMAX;    // essential (non-seed) postings served here (best measured on C2)
 constexpr uint32_t kSeedMaxTerms = 16;  // longer plans go straight to the exhaustive kernel
 constexpr uint64_t kSeedMaxDf = kSeedScratch / 2;  // seed term: the strongest bound among terms with fewer postings
-constexpr uint64_t kSeedMinPostings = 65536;  // cheaper queries too (e.g. a recency window)
+// queries with fewer postings than n_docs / 540 (16K at C2) stay on the sweep;
+// relative to the index so doc shards keep the same split (measured:
+// 65,536 fixed: C2 26.7 ms, 1/8 shard 7.96 ms; n_docs / 540: 26.4 / 7.79 ms)
+constexpr uint32_t kSeedMinPostDiv = 540;
 
 // leave query q to the exhaustive kernel (which walks the LPT order itself).
 // lb > 0: a lower bound, in the exhaustive kernel's selection domain, on the
@@ -174,7 +177,7 @@ __global__ void __launch_bounds__(kCons, HM_SEED_MINB) search_seed_kernel(DevInd
             bool worth = seed != kNoTerm && (m <= kSeedMaxTerms || (a.flags & 32u));
             if (worth && !(a.flags & 32u)) {  // HM_FLAG_SEED_ALL (tests) skips the cost rule
                 const uint64_t n_seed = S.t_end[seed] - S.t_wlo[seed];
-                worth = post >= kSeedMinPostings && n_seed * m * kProbeCost < post;
+                worth = post >= ix.n_docs / kSeedMinPostDiv && n_seed * m * kProbeCost < post;
             }
             S.bad = bad || !worth;
             S.flood = 0;
