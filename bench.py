@@ -533,7 +533,12 @@ def main():
 
     def step(timing, extra=0):
         flags = (search.HM_FLAG_TIMING if timing else 0) | extra
-        tm = dev.search_batch_device(b.off, b.tid, b.out, k, flags=flags)
+        if world > 1:  # every shard's k best seed scores (seeded pass only), all-gathered: the
+            # union's k-th-score bound, then the bounded search (shard.ShardedIndex.search_device)
+            bound = shard.union_bound(sh.dev_bounds(b.off, b.tid, k, b.out, extra), k, world)
+            tm = dev.search_batch_device(b.off, b.tid, b.out, k, flags=flags, ext_bound=bound)
+        else:
+            tm = dev.search_batch_device(b.off, b.tid, b.out, k, flags=flags)
         seed = search.last_seed() if timing else None
         res = b.out
         if world > 1:
@@ -714,7 +719,8 @@ def main():
                     data="synthetic (reference generator, bit-identical native port)",
                     config=dict(workload=WORKLOAD, n_docs=C2["n_records"], n_postings_this_rank=int(len(hx.posting_rows)),
                                 n_queries=nq, k=k, exhaustive_postings_per_batch_this_rank=int(post_q.sum()),
-                                parallelism=f"doc-sharded x{world} (NCCL all-gather of k candidates)"
+                                parallelism=f"doc-sharded x{world} (NCCL all-gather of every shard's k best seed scores -> the "
+                                            f"union's k-th-score bound; NCCL all-gather of k candidates, merge)"
                                 if world > 1 else "1 GPU",
                                 l2="flushed between timed steps (256 MB write)",
                                 index_format=fmt, build_s=round(t_build, 1), exact_fallback_queries=n_exact,

@@ -80,6 +80,18 @@ typedef struct {
     double epsilon_guard;      /* CascadeConfig::epsilon_guard (1e-9) */
     uint32_t row_lo, row_hi;
     uint32_t flags;            /* HM_FLAG_* */
+    /* Doc-sharded search (optional; DEVICE pointers, hm_search_batch_device
+     * only -- NULL for the other entry points), selection domain (score *
+     * 2^-61, fp32).  With HM_FLAG_BOUND_ONLY only out_bound[n_queries * k] is
+     * written: per query the k best complete scores of the seeded pass's seed
+     * documents on this index (zeros where there are fewer).  ext_bound[i]:
+     * a lower bound on the k-th score of the UNION of the shards -- the k-th
+     * largest of all shards' out_bound values of query i: the search then
+     * returns only documents that can be in the union's top-k (possibly fewer
+     * than k) and the k-way merge of the shards' lists is the exact answer.
+     * Both disable row slabs; k <= 256. */
+    const float* ext_bound;
+    float* out_bound;
 } hm_query_batch;
 
 #define HM_FLAG_FORCE_EXACT 1u   /* run every query on the exact fp64 kernel */
@@ -98,6 +110,8 @@ typedef struct {
 #define HM_FLAG_NE_ALL 256u      /* test / measurement switch: every query the tile sweep serves
                                     goes through its essential-term variant, whatever its plan
                                     length (same results) */
+#define HM_FLAG_BOUND_ONLY 512u  /* compute only out_bound (the seeded pass's bound), see
+                                    hm_query_batch.out_bound */
 #define HM_FLAG_TIMING 4u         /* time each kernel with CUDA events on the
                                     launching stream (the call then synchronises);
                                     read back with hm_last_batch_timing */

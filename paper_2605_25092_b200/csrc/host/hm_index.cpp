@@ -588,9 +588,9 @@ void fill_w32(const hm_index* X, double k1, double b, float* w) {
 // top-k lists, merged by merge_kernel exactly like doc shards (§4).  The
 // intra-query data parallelism of PAPER.md:616.
 uint32_t split_for(const hm_index* X, const hm_query_batch& hb) {
-    if ((hb.flags & (HM_FLAG_NO_SPLIT | HM_FLAG_FORCE_EXACT)) || needs_exact(hb.k1, hb.b) || hb.n_queries == 0 ||
-        hb.k == 0)
-        return 1;  // (the fp64 fallback path keeps one CTA per query)
+    if ((hb.flags & (HM_FLAG_NO_SPLIT | HM_FLAG_FORCE_EXACT | HM_FLAG_BOUND_ONLY)) || needs_exact(hb.k1, hb.b) ||
+        hb.n_queries == 0 || hb.k == 0 || hb.ext_bound || hb.out_bound)
+        return 1;  // (the fp64 fallback path keeps one CTA per query; shard bounds are per real query)
     const uint32_t nq = hb.n_queries, k = hb.k;
     // resident sweep CTAs (launch_search runs 2 per unit of grid_search); the
     // batch is split while the heaviest query, not the total work, would set
@@ -659,6 +659,8 @@ void run_batch(hm_index* X, Workspace* w, const hm_query_batch& hb, const uint32
     a.out_conf = out.conf;
     a.out_skip = out.skip;
     a.out_post = out.postings;
+    a.ext_bound = hb.ext_bound;
+    a.out_bound = hb.out_bound;
     const uint32_t split = d_slab_row ? n_parts : split_for(X, hb);
     a.split = split;
     a.nq_real = nq;
@@ -732,6 +734,21 @@ void run_batch(hm_index* X, Workspace* w, const hm_query_batch& hb, const uint32
             ck(hm::launch_lpt_sort(w->sort_tmp, w->sort_bytes, a, w->cost_sorted, w->order_in, st), "lpt sort");
         }
         if (timing) ck(cudaEventRecord(w->ev[1], st), "event");
+        if (a.flags & HM_FLAG_BOUND_ONLY) {  // doc shards' bound pass: the seeded pass's L per query
+            if (seeded) {
+                ck(cudaMemsetAsync(w->fb_list, 0, static_cast<uint64_t>(a.nq) * sizeof(uint32_t), st), "memset");
+                ck(hm::launch_search_seed(X->dev, a, 2 * X->grid_search, st), "seeded search kernel (bounds)");
+            } else {
+                ck(cudaMemsetAsync(a.out_bound, 0, static_cast<uint64_t>(nq) * hb.k * sizeof(float), st),
+                   "memset bounds");
+            }
+            if (timing) {
+                ck(cudaEventRecord(w->ev[4], st), "event");
+                ck(cudaEventRecord(w->ev[2], st), "event");
+                ck(cudaEventRecord(w->ev[3], st), "event");
+            }
+            return;
+        }
         if (seeded) {
             ck(cudaMemsetAsync(w->fb_list, 0, static_cast<uint64_t>(a.nq) * sizeof(uint32_t), st), "memset hand-over flags");
             ck(hm::launch_search_seed(X->dev, a, 2 * X->grid_search, st), "seeded search kernel");
@@ -1043,6 +1060,8 @@ void search_host(hm_index* X, const hm_query_batch* b, hm_results* out, uint32_t
         validate(X, b);
         const uint32_t nq = b->n_queries;
         if (nq == 0) return;
+        if (b->ext_bound || b->out_bound || (b->flags & HM_FLAG_BOUND_ONLY))
+            throw std::invalid_argument("shard bounds (ext_bound / out_bound) are for hm_search_batch_device");
         if (!out->ids || !out->scores || !out->n) throw std::invalid_argument("null result buffer");
         const uint32_t ntid = b->q_off[nq];
         for (uint32_t i = 0; i < nq; ++i)
@@ -1222,6 +1241,13 @@ int hm_search_batch_device(hm_index* X, const hm_query_batch* b, hm_results* out
         ck(cudaStreamSynchronize(ust), "sync");
         const uint32_t ntid = hoff[nq];
         const bool wide_all = b->k > static_cast<uint32_t>(hm::kMaxK);
+        const bool bonly = (b->flags & HM_FLAG_BOUND_ONLY) != 0;
+        if (bonly && !b->out_bound) throw std::invalid_argument("HM_FLAG_BOUND_ONLY needs out_bound");
+        if (bonly && wide_all) {  // the wide path has no bound: none reported
+            ck(cudaMemsetAsync(b->out_bound, 0, static_cast<uint64_t>(nq) * b->k * sizeof(float), ust),
+               "memset bounds");
+            return;
+        }
         const bool long_any = max_query_len(hoff.data(), nq) > static_cast<uint32_t>(hm::kMaxTerms);
         g_last_wide = 0;
         std::shared_lock<std::shared_mutex> bake_lk;
@@ -1241,7 +1267,7 @@ int hm_search_batch_device(hm_index* X, const hm_query_batch* b, hm_results* out
                 run_wide_batch(X, w, hb, b->q_off, b->q_tid, b->tau, *out);
             } else {
                 run_batch(X, w, hb, b->q_off, b->q_tid, b->tau, *out, reinterpret_cast<float*>(w->pin));
-                if (long_any) {
+                if (long_any && !bonly) {
                     uint32_t* rc = reinterpret_cast<uint32_t*>(w->pin) + hm::kMaxCodes;
                     ck(cudaMemcpyAsync(rc, w->counters, 32, cudaMemcpyDeviceToHost, w->stream), "D2H counters");
                     ck(cudaStreamSynchronize(w->stream), "sync");

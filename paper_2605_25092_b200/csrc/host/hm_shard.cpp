@@ -12,7 +12,11 @@
 //     enabled where the devices allow it (NVLink / NVSwitch).
 //   * search: one host thread per shard uploads the batch to its device and
 //     runs the single-device launch sequence (hm_search_batch_device) with
-//     the window clipped to the shard; each leaves exact local top-k lists in
+//     the window clipped to the shard -- for batches of 256+ queries after an
+//     exchange of bounds (every shard's k best seed scores, their k-th largest
+//     per query computed on the root: bound_kth_kernel), so each shard prunes
+//     against the union's threshold; each
+//     leaves its list of the documents that can be in the union's top-k in
 //     its own HBM.  The root device then runs gather_merge_kernel
 //     (kernels/shard_merge.cu): it reads every shard's lists over peer memory
 //     and merges them by rank in the same kernel -- the all-gather and the
@@ -50,6 +54,9 @@ void rethrow_status(int st, const char* what) {
         default: throw std::runtime_error(std::string(what) + ": " + msg);
     }
 }
+
+// batches from this size on exchange the shards' bounds before the search
+constexpr uint32_t kBoundMinQueries = 256;
 
 template <typename T>
 void grow(T*& p, uint64_t& cap, uint64_t n) {
@@ -92,7 +99,11 @@ struct Shard {
     uint32_t *q_off = nullptr, *q_tid = nullptr, *n = nullptr;
     uint64_t *ids = nullptr, *post = nullptr;
     double* scores = nullptr;
-    uint64_t off_cap = 0, tid_cap = 0, n_cap = 0, ids_cap = 0, post_cap = 0, sc_cap = 0;
+    float* bound = nullptr;  // [nq][k] this shard's k best seed scores (the bound pass)
+    float* ext = nullptr;    // [nq] the union's k-th-score bound
+    uint64_t off_cap = 0, tid_cap = 0, n_cap = 0, ids_cap = 0, post_cap = 0, sc_cap = 0, bound_cap = 0, ext_cap = 0;
+    float* r_bound = nullptr;  // root-side copy of `bound` for a shard the root cannot address
+    uint64_t rbound_cap = 0;
     // root-side copies for a shard the root cannot address
     uint32_t* r_n = nullptr;
     uint64_t *r_ids = nullptr, *r_post = nullptr;
@@ -114,13 +125,14 @@ struct hm_sharded {
     uint32_t* n = nullptr;
     uint8_t* skip = nullptr;
     uint64_t* post = nullptr;
-    uint64_t tau_cap = 0, ids_cap = 0, sc_cap = 0, conf_cap = 0, n_cap = 0, skip_cap = 0, post_cap = 0;
+    float* ext = nullptr;  // the union's bounds, computed on the root
+    uint64_t tau_cap = 0, ids_cap = 0, sc_cap = 0, conf_cap = 0, n_cap = 0, skip_cap = 0, post_cap = 0, ext_cap = 0;
 
     ~hm_sharded() {
         for (auto& s : shards) {
             if (s.index) hm_index_destroy(s.index);
             cudaSetDevice(s.device);
-            void* ps[] = {s.q_off, s.q_tid, s.n, s.ids, s.post, s.scores};
+            void* ps[] = {s.q_off, s.q_tid, s.n, s.ids, s.post, s.scores, s.bound, s.ext};
             for (void* p : ps)
                 if (p) cudaFree(p);
             if (s.stream) cudaStreamDestroy(s.stream);
@@ -128,11 +140,11 @@ struct hm_sharded {
         if (!shards.empty()) {
             cudaSetDevice(shards[0].device);
             for (auto& s : shards) {
-                void* ps[] = {s.r_n, s.r_ids, s.r_post, s.r_scores};
+                void* ps[] = {s.r_n, s.r_ids, s.r_post, s.r_scores, s.r_bound};
                 for (void* p : ps)
                     if (p) cudaFree(p);
             }
-            void* ps[] = {tau, ids, scores, conf, n, skip, post};
+            void* ps[] = {tau, ids, scores, conf, n, skip, post, ext};
             for (void* p : ps)
                 if (p) cudaFree(p);
             if (root_stream) cudaStreamDestroy(root_stream);
@@ -182,6 +194,8 @@ void search(hm_sharded* H, const hm_query_batch* b, hm_results* out) {
     if (nq == 0) return;
     if (!b->q_off) throw std::invalid_argument("q_off is required");
     if (!out->ids || !out->scores || !out->n) throw std::invalid_argument("null result buffer");
+    if (b->ext_bound || b->out_bound || (b->flags & HM_FLAG_BOUND_ONLY))
+        throw std::invalid_argument("the sharded search exchanges the shards' bounds itself");
     for (uint32_t i = 0; i < nq; ++i)
         if (b->q_off[i + 1] < b->q_off[i]) throw std::invalid_argument("q_off not monotone");
     const uint32_t ntid = b->q_off[nq];
@@ -194,8 +208,16 @@ void search(hm_sharded* H, const hm_query_batch* b, hm_results* out) {
     const uint32_t G = static_cast<uint32_t>(H->shards.size());
     std::lock_guard<std::mutex> lk(H->mu);
 
-    // 1. every shard: its exact local top-k over its part of the window
-    run_parallel(G, [&](uint32_t g) {
+    // 1. every shard: its top-k over its part of the window.  Batches of
+    // kBoundMinQueries queries or more first exchange the shards' k-th-score
+    // bounds (the seeded pass's k best seed scores, HM_FLAG_BOUND_ONLY; the
+    // k-th largest over the shards on the root): each shard then prunes
+    // against the union's bound and keeps
+    // only documents that can be in the union's top-k -- the merge below is
+    // still exact, and a shard's work shrinks like its share of the corpus.
+    // (Smaller batches keep row slabs, which the bounds would disable.)
+    const bool bounded = G > 1 && nq >= kBoundMinQueries && k > 0 && k <= static_cast<uint32_t>(hm::kMaxK);
+    auto prepare = [&](uint32_t g) {
         Shard& s = H->shards[g];
         ck(cudaSetDevice(s.device), "cudaSetDevice");
         grow(s.q_off, s.off_cap, nq + 1ull);
@@ -204,21 +226,84 @@ void search(hm_sharded* H, const hm_query_batch* b, hm_results* out) {
         grow(s.scores, s.sc_cap, static_cast<uint64_t>(nq) * kk);
         grow(s.n, s.n_cap, nq);
         grow(s.post, s.post_cap, nq);
+        grow(s.bound, s.bound_cap, static_cast<uint64_t>(nq) * kk);
+        grow(s.ext, s.ext_cap, nq);
+    };
+    auto window = [&](const Shard& s, hm_query_batch& sb) {
         const uint32_t lo = std::max(row_lo, s.row0), hi = std::min(row_hi, s.row1);
-        if (lo >= hi) {  // the window misses this shard: empty lists
+        sb = *b;
+        sb.q_off = s.q_off;
+        sb.q_tid = s.q_tid;
+        sb.tau = nullptr;  // decisions are taken after the merge
+        sb.ext_bound = nullptr;
+        sb.out_bound = nullptr;
+        sb.row_lo = lo < hi ? lo - s.row0 : 0;
+        sb.row_hi = lo < hi ? hi - s.row0 : 0;
+        return lo < hi;
+    };
+    if (bounded) {
+        run_parallel(G, [&](uint32_t g) {
+            prepare(g);
+            Shard& s = H->shards[g];
+            hm_query_batch sb;
+            if (!window(s, sb)) {  // the window misses this shard: no seeds
+                ck(cudaMemsetAsync(s.bound, 0, static_cast<uint64_t>(nq) * kk * 4, s.stream), "memset");
+                ck(cudaStreamSynchronize(s.stream), "shard sync");
+                return;
+            }
+            ck(cudaMemcpyAsync(s.q_off, b->q_off, (nq + 1ull) * 4, cudaMemcpyHostToDevice, s.stream), "H2D q_off");
+            if (ntid)
+                ck(cudaMemcpyAsync(s.q_tid, b->q_tid, ntid * 4ull, cudaMemcpyHostToDevice, s.stream), "H2D q_tid");
+            sb.flags |= HM_FLAG_BOUND_ONLY;
+            sb.out_bound = s.bound;
+            hm_results r{s.ids, s.scores, s.n, nullptr, nullptr, s.post};
+            rethrow_status(hm_search_batch_device(s.index, &sb, &r, s.stream), "shard bounds");
+            ck(cudaStreamSynchronize(s.stream), "shard sync");
+        });
+        // the root: per query the k-th largest of every shard's k values (over peer
+        // memory), then the bound to every shard
+        Shard& root = H->shards[0];
+        ck(cudaSetDevice(root.device), "cudaSetDevice");
+        grow(H->ext, H->ext_cap, nq);
+        hm::BoundLists BL{};
+        BL.G = G;
+        for (uint32_t g = 0; g < G; ++g) {
+            Shard& s = H->shards[g];
+            if (s.p2p) {
+                BL.b[g] = s.bound;
+                continue;
+            }
+            grow(s.r_bound, s.rbound_cap, static_cast<uint64_t>(nq) * kk);
+            ck(cudaMemcpyPeerAsync(s.r_bound, root.device, s.bound, s.device, static_cast<uint64_t>(nq) * kk * 4,
+                                   H->root_stream),
+               "peer copy");
+            BL.b[g] = s.r_bound;
+        }
+        ck(hm::launch_bound_kth(BL, nq, kk, H->ext, H->root_stream), "bound_kth_kernel");
+        for (uint32_t g = 0; g < G; ++g) {
+            Shard& s = H->shards[g];
+            ck(cudaMemcpyPeerAsync(s.ext, s.device, H->ext, root.device, nq * 4ull, H->root_stream), "peer copy");
+        }
+        ck(cudaStreamSynchronize(H->root_stream), "bound exchange");
+    }
+    run_parallel(G, [&](uint32_t g) {
+        Shard& s = H->shards[g];
+        if (!bounded) prepare(g);
+        ck(cudaSetDevice(s.device), "cudaSetDevice");
+        hm_query_batch sb;
+        if (!window(s, sb)) {  // the window misses this shard: empty lists
             ck(cudaMemsetAsync(s.n, 0, nq * 4ull, s.stream), "memset");
             ck(cudaMemsetAsync(s.post, 0, nq * 8ull, s.stream), "memset");
             ck(cudaStreamSynchronize(s.stream), "shard sync");
             return;
         }
-        ck(cudaMemcpyAsync(s.q_off, b->q_off, (nq + 1ull) * 4, cudaMemcpyHostToDevice, s.stream), "H2D q_off");
-        if (ntid) ck(cudaMemcpyAsync(s.q_tid, b->q_tid, ntid * 4ull, cudaMemcpyHostToDevice, s.stream), "H2D q_tid");
-        hm_query_batch sb = *b;
-        sb.q_off = s.q_off;
-        sb.q_tid = s.q_tid;
-        sb.tau = nullptr;  // decisions are taken after the merge
-        sb.row_lo = lo - s.row0;
-        sb.row_hi = hi - s.row0;
+        if (bounded) {
+            sb.ext_bound = s.ext;
+        } else {
+            ck(cudaMemcpyAsync(s.q_off, b->q_off, (nq + 1ull) * 4, cudaMemcpyHostToDevice, s.stream), "H2D q_off");
+            if (ntid)
+                ck(cudaMemcpyAsync(s.q_tid, b->q_tid, ntid * 4ull, cudaMemcpyHostToDevice, s.stream), "H2D q_tid");
+        }
         hm_results r{s.ids, s.scores, s.n, nullptr, nullptr, s.post};
         rethrow_status(hm_search_batch_device(s.index, &sb, &r, s.stream), "shard search");
         ck(cudaStreamSynchronize(s.stream), "shard sync");

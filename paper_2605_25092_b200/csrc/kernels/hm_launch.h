@@ -43,6 +43,8 @@ cudaError_t launch_gather_merge(const ShardLists& lists, uint32_t nq, uint32_t k
                                 double tau_default, double eps, uint64_t* out_ids, double* out_scores,
                                 uint32_t* out_n, double* out_conf, uint8_t* out_skip, uint64_t* out_post,
                                 cudaStream_t st);
+// doc shards: per query the k-th largest of the shards' k best seed scores
+cudaError_t launch_bound_kth(const BoundLists& lists, uint32_t nq, uint32_t k, float* out, cudaStream_t st);
 // K0: bake the long-term postings into bk[] for (k1, b); *err |= 1 when an
 // impact falls outside the 7 representable binades (kernels/bake.cu)
 uint32_t bake_ks(double k1);

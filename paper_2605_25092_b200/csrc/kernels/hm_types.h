@@ -165,6 +165,9 @@ struct BatchArgs {
     uint32_t* seed_scratch;    // per-CTA seeded-pass scratch: 2 * seed_half words (scores, rows)
     uint64_t* ne_pend;         // essential-term sweep: per CTA and warp kNePendCap rows awaiting
                                // completion, (score bits << 32) | row
+    const float* ext_bound;    // [nq_real] doc shards: lower bound on the k-th selection score of the
+                               // union of the shards (MAX over the shards' out_bound), or null
+    float* out_bound;          // [nq_real] the seeded pass's bound of this index (kFlagBoundOnly: only that)
     uint32_t seed_half;        // min(kSeedScratch / 2, n_docs): the largest seed set of the index
     uint32_t stab_stride;      // words per short term (>= n_tiles + 2)
     // results (device)
@@ -211,6 +214,15 @@ struct ShardLists {
     const uint64_t* post[kMaxShards];    // [nq] or NULL
 };
 
+constexpr uint32_t kFlagBoundOnly = 512u;  // HM_FLAG_BOUND_ONLY
+// an external bound (seed or sweep domain, score * 2^-61) used as a bound of
+// the other domain: both are within delta < 2^-15 of the exact score
+constexpr float kExtSlack = 1.0f - 1e-4f;
+// doc shards' bound exchange (shard_merge.cu): every shard's [nq][k] best seed scores
+struct BoundLists {
+    uint32_t G;
+    const float* b[kMaxShards];
+};
 constexpr uint32_t kErrTooManyTerms = 1u;
 constexpr uint32_t kErrNoConverge = 2u;
 

@@ -325,6 +325,10 @@ __global__ void __launch_bounds__(kCons, 2) search_fast_kernel(DevIndex ix, Batc
             // the k-th selection score (search_seed.cu: hand_over)
             const uint32_t fbq = a.fb_list ? a.fb_list[q] & ~kFbPlain : 0u;
             if (fbq > 1u) S.Lg = max(S.Lg, fbq);
+            if (a.ext_bound) {  // doc shards: the union's bound (seed domain, slack for this one)
+                const float e = a.ext_bound[qr] * kExtSlack;
+                if (e > 0.f) S.Lg = max(S.Lg, __float_as_uint(e));
+            }
         }
         if (!(a.flags & 2u)) {
             if (tid < kConsWarps) S.n_w[tid] = 0;

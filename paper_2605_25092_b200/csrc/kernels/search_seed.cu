@@ -116,9 +116,18 @@ __global__ void __launch_bounds__(kCons, HM_SEED_MINB) search_seed_kernel(DevInd
         const uint32_t poff = a.q_off[qr];
         const uint32_t m = a.plan_len[qr];
         const uint32_t k = a.k;
+        // doc shards: ext = a bound of the union of the shards (same seed-domain
+        // scores, global statistics); HM_FLAG_BOUND_ONLY: report this shard's L only
+        const float ext = a.ext_bound ? a.ext_bound[qr] : 0.f;
+        const bool bonly = (a.flags & kFlagBoundOnly) != 0;
+        auto give_up = [&] {  // tid 0: no bound of our own -- the sweep takes the query
+            if (bonly)
+                for (uint32_t i = 0; i < k; ++i) a.out_bound[static_cast<uint64_t>(qr) * k + i] = 0.f;
+            else hand_over(a, q, ext * kExtSlack);
+        };
         // anything unusual goes to the exhaustive kernel, which routes it on
         if (m == 0 || m > kFastTerms || k == 0 || k > kmax || (a.flags & 1u) || row_hi <= row_lo) {
-            if (tid == 0) hand_over(a, q);
+            if (tid == 0) give_up();
             continue;
         }
         // ---------------- prologue: plan, window bounds, bounds
@@ -186,7 +195,7 @@ __global__ void __launch_bounds__(kCons, HM_SEED_MINB) search_seed_kernel(DevInd
         if (tid < kConsWarps) S.n_w[tid] = 0;
         __syncthreads();
         if (S.bad) {  // no short term (or a non-positive idf): the exhaustive kernel
-            if (tid == 0) hand_over(a, q);
+            if (tid == 0) give_up();
             continue;
         }
         const uint32_t n_short = S.n_short, ts = S.n_long;
@@ -441,7 +450,27 @@ __global__ void __launch_bounds__(kCons, HM_SEED_MINB) search_seed_kernel(DevInd
             seed_pass([&](uint32_t e) { return __float_as_uint(sA[e]) == kTodo; }, true, te0);
             __syncthreads();
         }
+        if (bonly) {  // the bound pass of doc-sharded search: the k best complete seed scores
+            // (the multiset {scores > L} + (k - that count) x L, L the exact k-th
+            // largest; zeros when there are fewer than k seeds): the k-th largest
+            // over every shard's k values is a k-th score of real documents
+            if (n_seed >= k) L = block_kth_largest<kCons>(sA, n_seed, k, S.hist, S.sel, [] { __syncthreads(); });
+            if (tid == 0) S.total = 0;
+            __syncthreads();
+            float* ob = a.out_bound + static_cast<uint64_t>(qr) * k;
+            for (uint32_t e = tid; e < n_seed; e += kCons)
+                if (sA[e] > L) {
+                    const uint32_t i = atomicAdd(&S.total, 1u);
+                    if (i < k) ob[i] = sA[e];
+                }
+            __syncthreads();
+            for (uint32_t i = S.total + tid; i < k; i += kCons) ob[i] = L;
+            continue;
+        }
         if (n_seed >= k) L = block_kth_largest<kCons>(sA, n_seed, k, S.hist, S.sel, [] { __syncthreads(); }, 8);
+        // the union's bound: every document of the union's top-k scores above it
+        // (a k-th score of real documents of some shard, in the same domain)
+        L = fmaxf(L, ext);
         const float te = fmaxf(L * f_slack, kFltMin);  // admission threshold (as the exhaustive kernel's)
         if (tid == 0) S.Lg = __float_as_uint(L);
 #ifdef HM_SEED_STATS

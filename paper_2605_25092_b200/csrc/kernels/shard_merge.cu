@@ -111,6 +111,31 @@ __global__ void __launch_bounds__(kGMThreads) gather_merge_kernel(ShardLists L, 
     }
 }
 
+// Doc shards' bound exchange: per query the k-th largest of the G shards' k
+// best seed scores ([G] pointers to [nq][k], read over peer memory) -- a k-th
+// score of real documents of the union, hence a lower bound on its k-th score.
+constexpr int kBKThreads = 128;
+__global__ void __launch_bounds__(kBKThreads) bound_kth_kernel(BoundLists L, uint32_t nq, uint32_t k, float* out) {
+    __shared__ float v[kMaxShards * kMaxK];
+    __shared__ uint32_t hist[256], sel[2];
+    for (uint32_t q = blockIdx.x; q < nq; q += gridDim.x) {
+        const uint32_t n = L.G * k;
+        for (uint32_t i = threadIdx.x; i < n; i += kBKThreads) v[i] = L.b[i / k][static_cast<uint64_t>(q) * k + i % k];
+        __syncthreads();
+        const float x = block_kth_largest<kBKThreads>(v, n, k, hist, sel, [] { __syncthreads(); });
+        if (threadIdx.x == 0) out[q] = x;
+        __syncthreads();
+    }
+}
+
+cudaError_t launch_bound_kth(const BoundLists& L, uint32_t nq, uint32_t k, float* out, cudaStream_t st) {
+    if (nq == 0) return cudaSuccess;
+    if (L.G == 0 || L.G > static_cast<uint32_t>(kMaxShards) || k == 0 || k > static_cast<uint32_t>(kMaxK))
+        return cudaErrorInvalidValue;
+    bound_kth_kernel<<<nq < 4096u ? nq : 4096u, kBKThreads, 0, st>>>(L, nq, k, out);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_gather_merge(const ShardLists& L, uint32_t nq, uint32_t k, const double* tau, double tau_default,
                                 double eps, uint64_t* out_ids, double* out_scores, uint32_t* out_n,
                                 double* out_conf, uint8_t* out_skip, uint64_t* out_post, cudaStream_t st) {

@@ -32,6 +32,7 @@ HM_FLAG_TIMING = 4
 HM_FLAG_EXHAUSTIVE = 16
 HM_FLAG_SEED_ALL = 32
 HM_FLAG_NO_SPLIT = 64
+HM_FLAG_BOUND_ONLY = 512
 HM_FLAG_NO_NESKIP = 128
 HM_FLAG_NE_ALL = 256
 NO_TERM = 0xFFFFFFFF
@@ -53,7 +54,8 @@ class QueryBatch(C.Structure):
                 ("k", C.c_uint32), ("k1", C.c_double), ("b", C.c_double),
                 ("tau", C.c_void_p), ("tau_default", C.c_double),
                 ("epsilon_guard", C.c_double), ("row_lo", C.c_uint32),
-                ("row_hi", C.c_uint32), ("flags", C.c_uint32)]
+                ("row_hi", C.c_uint32), ("flags", C.c_uint32),
+                ("ext_bound", C.c_void_p), ("out_bound", C.c_void_p)]
 
 
 class Results(C.Structure):
@@ -313,17 +315,21 @@ class DeviceIndex:
 
     def search_batch_device(self, q_off, q_tid, out, k, k1=1.2, b=0.75, tau=None,
                             tau_default=0.10, epsilon_guard=1e-9, row_lo=0, row_hi=0, flags=0,
-                            stream=None):
+                            stream=None, ext_bound=None, out_bound=None):
         """Device-resident batch (torch CUDA tensors), enqueued on `stream`
         (default: torch's current stream).  `out` is a dict of torch tensors
         (ids[nq,k] int64, scores[nq,k] f64, n[nq] int32, conf[nq] f64,
-        skip[nq] uint8, postings[nq] int64)."""
+        skip[nq] uint8, postings[nq] int64).  Doc shards: out_bound (float32[nq],
+        with HM_FLAG_BOUND_ONLY) receives this shard's k-th-score bound;
+        ext_bound (float32[nq]) is the MAX of the shards' bounds (hm_b200.h)."""
         import torch
         nq = q_off.numel() - 1
         st = stream if stream is not None else torch.cuda.current_stream(q_off.device)
         qb = QueryBatch(nq, q_off.data_ptr(), q_tid.data_ptr(), int(k), k1, b,
                         None if tau is None else tau.data_ptr(), tau_default, epsilon_guard,
-                        row_lo, row_hi, flags)
+                        row_lo, row_hi, flags,
+                        None if ext_bound is None else ext_bound.data_ptr(),
+                        None if out_bound is None else out_bound.data_ptr())
         r = Results(out["ids"].data_ptr(), out["scores"].data_ptr(), out["n"].data_ptr(),
                     out["conf"].data_ptr(), out["skip"].data_ptr(), out["postings"].data_ptr())
         _check(lib().hm_search_batch_device(self._h, C.byref(qb), C.byref(r), st.cuda_stream))

@@ -119,6 +119,27 @@ def gather_and_merge(local, k, world, group=None, tau=None, tau_default=0.10,
     return out
 
 
+def union_bound(seeds, k, world, group=None):
+    """All-gather every rank's k best seed scores per query (float32[nq, k])
+    and take the k-th largest of the world * k values: a k-th score of real
+    documents of the whole corpus, hence a lower bound on its k-th score."""
+    import torch
+    import torch.distributed as dist
+    nq = seeds.shape[0]
+    if world <= 1:
+        allv = seeds
+    else:
+        g = torch.empty((world, nq, k), dtype=seeds.dtype, device=seeds.device)
+        if dist.get_backend(group) == "gloo":
+            parts = [torch.empty((nq, k), dtype=seeds.dtype) for _ in range(world)]
+            dist.all_gather(parts, seeds.cpu(), group=group)
+            g.copy_(torch.stack(parts))
+        else:
+            dist.all_gather_into_tensor(g, seeds.contiguous(), group=group)
+        allv = g.permute(1, 0, 2).reshape(nq, world * k)
+    return torch.topk(allv, k, dim=1).values[:, k - 1].contiguous()
+
+
 def allreduce_postings(local_post, world, group=None):
     """postings_touched of the merged result: the shards' counts summed."""
     import torch.distributed as dist
@@ -176,16 +197,42 @@ class ShardedIndex:
         return self, hx
 
     def search_device(self, q_off, q_tid, k, local_out, **kw):
-        """Device-resident batch: local exact top-k, all-gather, merge.  The
-        merged skip decision uses the caller's per-query tau / tau_default /
-        epsilon_guard; postings_touched is summed over the shards (every
-        posting lives on exactly one shard, so the sum is the flat count)."""
-        self.dev.search_batch_device(q_off, q_tid, local_out, k, **kw)
+        """Device-resident batch: shard bounds, local top-k, all-gather, merge.
+
+        With world > 1 every rank first runs the seeded pass's bound only
+        (HM_FLAG_BOUND_ONLY: a lower bound on each query's k-th score in its
+        shard), the bounds are all-reduced with MAX -- a lower bound on the
+        k-th score of the whole corpus -- and the search proper prunes against
+        it: a shard's list keeps only documents that can be in the global
+        top-k, so the merge of the lists is the exact answer while each shard
+        works against the global threshold instead of its own (weaker) one.
+        The merged skip decision uses the caller's per-query tau /
+        tau_default / epsilon_guard; postings_touched is summed over the
+        shards (every posting lives on exactly one shard)."""
+        if self.world > 1 and 0 < k <= 256:
+            flags = kw.pop("flags", 0)
+            nq = q_off.numel() - 1
+            seeds = self.dev_bounds(q_off, q_tid, k, local_out, flags,
+                                    **{x: v for x, v in kw.items() if x not in ("tau",)})
+            bound = union_bound(seeds, k, self.world)
+            self.dev.search_batch_device(q_off, q_tid, local_out, k, flags=flags, ext_bound=bound, **kw)
+        else:
+            self.dev.search_batch_device(q_off, q_tid, local_out, k, **kw)
         out = gather_and_merge(local_out, k, self.world, tau=kw.get("tau"),
                                tau_default=kw.get("tau_default", 0.10),
                                epsilon_guard=kw.get("epsilon_guard", 1e-9))
         out["postings"] = allreduce_postings(local_out["postings"], self.world)
         return out
+
+    def dev_bounds(self, q_off, q_tid, k, scratch_out, flags=0, **kw):
+        """This shard's bound pass: float32[nq, k], the k best complete seed
+        scores of every query (HM_FLAG_BOUND_ONLY)."""
+        import torch
+        nq = q_off.numel() - 1
+        seeds = torch.zeros((nq, k), dtype=torch.float32, device=q_off.device)
+        self.dev.search_batch_device(q_off, q_tid, scratch_out, k, flags=flags | search.HM_FLAG_BOUND_ONLY,
+                                     out_bound=seeds, **kw)
+        return seeds
 
     def search_batch(self, q_off, q_tid, k, **kw):
         """Host buffers in, host results out (H2D, search, all-gather, merge, D2H)."""

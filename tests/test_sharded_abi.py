@@ -83,6 +83,68 @@ def test_sharded_row_window(gpu, c1ish):
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("k", [1, 10, 100])
+def test_sharded_bounded_any_k_and_windows(gpu, c1ish, k):
+    """Batches of 256+ queries exchange the shards' k-th-score bounds first
+    (each shard then keeps only documents that can be in the union's top-k):
+    still the unsharded answer, with and without a row window."""
+    hx, tids = c1ish
+    off, flat = _flat(tids[:300])
+    sh = search.ShardedDeviceIndex.from_host(hx, [0, 0, 0, 0])
+    dev = search.DeviceIndex.from_host(hx)
+    n = hx.n_docs
+    for lo, hi in [(0, 0), (n // 7, n - n // 5)]:
+        got = sh.search_batch(off, flat, k, row_lo=lo, row_hi=hi)
+        want = dev.search_batch(off, flat, k, row_lo=lo, row_hi=hi)
+        for key in ("n", "ids", "conf", "skip", "postings"):
+            assert (got[key] == want[key]).all(), (k, lo, hi, key)
+        assert (got["scores"].view(np.uint64) == want["scores"].view(np.uint64)).all()
+
+
+@pytest.mark.gpu
+def test_bound_pass_and_external_bound(gpu, c1ish):
+    """HM_FLAG_BOUND_ONLY reports a lower bound on every query's k-th score
+    (selection domain, score * 2^-61); searching with that bound -- or any
+    bound at or below the k-th score -- as ext_bound returns the same top-k."""
+    hx, tids = c1ish
+    off, flat = _flat(tids)
+    dev = search.DeviceIndex.from_host(hx)
+    nq, k = len(tids), 10
+    d_off = torch.from_numpy(off.view(np.int32)).cuda()
+    d_tid = torch.from_numpy(flat.view(np.int32)).cuda()
+
+    def outbuf():
+        return dict(ids=torch.zeros((nq, k), dtype=torch.int64, device="cuda"),
+                    scores=torch.zeros((nq, k), dtype=torch.float64, device="cuda"),
+                    n=torch.zeros(nq, dtype=torch.int32, device="cuda"),
+                    conf=torch.zeros(nq, dtype=torch.float64, device="cuda"),
+                    skip=torch.zeros(nq, dtype=torch.uint8, device="cuda"),
+                    postings=torch.zeros(nq, dtype=torch.int64, device="cuda"))
+    ref = outbuf()
+    dev.search_batch_device(d_off, d_tid, ref, k)
+    seeds = torch.zeros((nq, k), dtype=torch.float32, device="cuda")
+    dev.search_batch_device(d_off, d_tid, outbuf(), k, flags=search.HM_FLAG_BOUND_ONLY, out_bound=seeds)
+    torch.cuda.synchronize()
+    sc = ref["scores"].cpu().numpy()
+    nn = ref["n"].cpu().numpy()
+    sel = sc * 2.0 ** -61
+    sv = -np.sort(-seeds.cpu().numpy().astype(np.float64), axis=1)  # the k best seed scores, descending
+    for i in range(nq):  # the j-th best seed score never exceeds the j-th best score (1e-4: the domains)
+        m = int(nn[i])
+        assert (sv[i, :m] <= sel[i, :m] * (1 + 1e-4)).all(), f"query {i}: a seed score above the top-k"
+        assert (sv[i, m:] == 0).all()
+    bound = seeds.min(dim=1).values.contiguous()  # one shard: the k-th largest of its k values
+    kth = np.where(nn >= k, sc[:, k - 1], 0.0) * 2.0 ** -61
+    assert (bound.cpu().numpy() > 0).sum() > nq // 4, "the seeded pass reported almost no bounds"
+    for ext in (bound, torch.from_numpy((kth * (1 - 1e-4)).astype(np.float32)).cuda()):
+        got = outbuf()
+        dev.search_batch_device(d_off, d_tid, got, k, ext_bound=ext)
+        torch.cuda.synchronize()
+        for key in ("n", "ids", "scores", "postings"):
+            assert torch.equal(got[key], ref[key]), key
+
+
+@pytest.mark.gpu
 def test_sharded_errors(gpu, c1ish):
     hx, tids = c1ish
     sh = search.ShardedDeviceIndex.from_host(hx, [0, 0])
