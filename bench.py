@@ -689,10 +689,18 @@ def main():
                     ms.append(e0.elapsed_time(e1))
             small_lat[f"batch_{B}"] = dict(p50_ms=pct(ms, 0.5), p99_ms=max(ms), reps=len(ms))
 
-    # ---------------- parity (N=1): the full batch vs the reference's answers
+    # ---------------- parity: the full batch vs the reference's answers (N > 1: the merged
+    # answer of the doc-sharded search, bound exchange included, on rank 0)
     parity = None
     cpu = None
     configs = None
+    if world > 1:
+        _, res = step(False)
+        torch.cuda.synchronize()
+        if rank == 0:
+            got = {key: v.cpu().numpy() for key, v in res.items()}
+            got["ids"] = got["ids"].view(np.uint64)
+            parity = parity_vs_golden(got, "c2")
     if rank == 0 and world == 1:
         dev.search_batch_device(b.off, b.tid, b.out, k)
         torch.cuda.synchronize()

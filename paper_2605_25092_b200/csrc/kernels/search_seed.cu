@@ -120,6 +120,10 @@ __global__ void __launch_bounds__(kCons, HM_SEED_MINB) search_seed_kernel(DevInd
         // scores, global statistics); HM_FLAG_BOUND_ONLY: report this shard's L only
         const float ext = a.ext_bound ? a.ext_bound[qr] : 0.f;
         const bool bonly = (a.flags & kFlagBoundOnly) != 0;
+        // with the union's bound the seeds need not be scored first: L = ext and
+        // the seed term is hashed like every other essential term (its complete
+        // seed scores were the bound pass's work)
+        const bool seedless = ext > 0.f && !bonly;
         auto give_up = [&] {  // tid 0: no bound of our own -- the sweep takes the query
             if (bonly)
                 for (uint32_t i = 0; i < k; ++i) a.out_bound[static_cast<uint64_t>(qr) * k + i] = 0.f;
@@ -183,8 +187,10 @@ __global__ void __launch_bounds__(kCons, HM_SEED_MINB) search_seed_kernel(DevInd
             // serve the query here only when probing the seeds is cheaper than
             // streaming its postings (a dependent-load probe ~ 32 streamed
             // postings) and the plan is short enough for the bounds to bite
-            bool worth = seed != kNoTerm && (m <= kSeedMaxTerms || (a.flags & 32u));
-            if (worth && !(a.flags & 32u)) {  // HM_FLAG_SEED_ALL (tests) skips the cost rule
+            bool worth = (seed != kNoTerm || seedless) && (m <= kSeedMaxTerms || (a.flags & 32u));
+            if (worth && seedless) {
+                worth = post >= ix.n_docs / kSeedMinPostDiv || (a.flags & 32u);
+            } else if (worth && !(a.flags & 32u)) {  // HM_FLAG_SEED_ALL (tests) skips the cost rule
                 const uint64_t n_seed = S.t_end[seed] - S.t_wlo[seed];
                 worth = post >= ix.n_docs / kSeedMinPostDiv && n_seed * m * kProbeCost < post;
             }
@@ -198,7 +204,7 @@ __global__ void __launch_bounds__(kCons, HM_SEED_MINB) search_seed_kernel(DevInd
             if (tid == 0) give_up();
             continue;
         }
-        const uint32_t n_short = S.n_short, ts = S.n_long;
+        const uint32_t n_short = S.n_short, ts = seedless ? kNoTerm : S.n_long;
         const uint32_t j0 = row_lo >> kTileShift, j1 = (row_hi - 1) >> kTileShift;
         const uint32_t nt = j1 - j0 + 1;
         // ---------------- short-term tile tables (probes of short terms)
@@ -247,8 +253,8 @@ __global__ void __launch_bounds__(kCons, HM_SEED_MINB) search_seed_kernel(DevInd
         // row of its e-th posting; sA[e] = the row's complete score, or 0 for a
         // row proven unable to reach the admission threshold (0 never exceeds a
         // real score, so the k-th largest sA stays a valid lower bound)
-        const uint64_t sw0 = S.t_wlo[ts];
-        const uint32_t n_seed = static_cast<uint32_t>(S.t_end[ts] - sw0);
+        const uint64_t sw0 = seedless ? 0ull : S.t_wlo[ts];
+        const uint32_t n_seed = seedless ? 0u : static_cast<uint32_t>(S.t_end[ts] - sw0);
         const bool seed_sm = n_seed <= kSeedSmemMax;
         float* const sA = seed_sm ? S.acc : gA;
         uint32_t* const sR = seed_sm ? reinterpret_cast<uint32_t*>(S.acc + kSeedSmemMax)
@@ -295,7 +301,8 @@ __global__ void __launch_bounds__(kCons, HM_SEED_MINB) search_seed_kernel(DevInd
             }
             return lo;
         };
-        if (S.t_slot[ts] < 0) {
+        if (seedless) {
+        } else if (S.t_slot[ts] < 0) {
 #pragma unroll 4
             for (uint32_t e = tid; e < n_seed; e += kCons) sR[e] = __ldg(ix.post + sw0 + e) >> cb;
         } else {  // a long seed term: rows from the tile offsets, tiles as segments
@@ -419,7 +426,12 @@ __global__ void __launch_bounds__(kCons, HM_SEED_MINB) search_seed_kernel(DevInd
 #ifndef HM_SEED_FULL
 #define HM_SEED_FULL 2048
 #endif
-        const uint32_t n_full = max(static_cast<uint32_t>(HM_SEED_FULL), 8u * k);
+#ifndef HM_BOUND_FULL
+#define HM_BOUND_FULL 2048
+#endif
+        // (the bound pass of doc shards may score fewer seeds completely: its
+        // k best only need to be good, the other shards add theirs)
+        const uint32_t n_full = max(static_cast<uint32_t>(bonly ? HM_BOUND_FULL : HM_SEED_FULL), 8u * k);
         float L = 0.f;
         if (n_seed <= n_full) {  // few seeds: every one complete
             seed_pass([](uint32_t) { return true; }, false, 0.f);
@@ -495,7 +507,7 @@ __global__ void __launch_bounds__(kCons, HM_SEED_MINB) search_seed_kernel(DevInd
             // tied with t*'s bound can sort after it and stay essential).
             // The bound sum still includes t*: an over-estimate, safe.
             const uint32_t ne =
-                __reduce_or_sync(0xffffffffu, isne ? 1u << S.msorder[lane] : 0u) & ~(1u << S.n_long);
+                __reduce_or_sync(0xffffffffu, isne ? 1u << S.msorder[lane] : 0u) & (ts < 32u ? ~(1u << ts) : ~0u);
             const uint32_t bal = __ballot_sync(0xffffffffu, isne);
             const float ub = bal ? __shfl_sync(0xffffffffu, v, 31 - __clz(bal)) : 0.f;
             if (lane == 0) S.ubne_q = ub;

@@ -63,9 +63,12 @@ for G in Gs:
     t_bound = timed(lambda: devs[0].search_batch_device(b.off, b.tid, b.out, k, flags=search.HM_FLAG_BOUND_ONLY,
                                                         out_bound=bounds[0]))
     t_main = timed(lambda: devs[0].search_batch_device(b.off, b.tid, b.out, k, ext_bound=gmax))
+    tm = devs[0].search_batch_device(b.off, b.tid, b.out, k, ext_bound=gmax, flags=search.HM_FLAG_TIMING)
+    sd = search.last_seed()
     tot = t_bound + t_main
     print(f"G={G}: shard {devs[0].n_docs} docs: unbounded {plain:.2f} ms ({base / plain / G * 100:.0f} % of linear); "
-          f"bounds {t_bound:.2f} + bounded search {t_main:.2f} = {tot:.2f} ms ({base / tot / G * 100:.0f} % of linear)",
+          f"bounds {t_bound:.2f} + bounded search {t_main:.2f} = {tot:.2f} ms ({base / tot / G * 100:.0f} % of linear) "
+          f"[bounded: seeded {sd[0]:.2f} ms, {sd[1]} handed over, sweep {tm[1]:.2f} ms]",
           flush=True)
     del devs
     torch.cuda.empty_cache()
