@@ -587,6 +587,9 @@ void fill_w32(const hm_index* X, double k1, double b, float* w) {
 // split into row slabs served as separate "slab queries" -- exact per-slab
 // top-k lists, merged by merge_kernel exactly like doc shards (§4).  The
 // intra-query data parallelism of PAPER.md:616.
+// the seeded pass runs on row windows of at least this many rows (8 tiles)
+constexpr uint32_t kSeedMinRows = 1u << 17;
+
 uint32_t split_for(const hm_index* X, const hm_query_batch& hb) {
     if ((hb.flags & (HM_FLAG_NO_SPLIT | HM_FLAG_FORCE_EXACT | HM_FLAG_BOUND_ONLY)) || needs_exact(hb.k1, hb.b) ||
         hb.n_queries == 0 || hb.k == 0 || hb.ext_bound || hb.out_bound)
@@ -700,8 +703,11 @@ void run_batch(hm_index* X, Workspace* w, const hm_query_batch& hb, const uint32
     // exhaustive kernel for the rest; HM_FLAG_EXHAUSTIVE skips the seeded pass
     // (a narrow row window -- a recency window of the temporal index -- keeps
     // every query cheap on the exhaustive kernel: no seeded pass)
+    // (and an index of a few tiles -- C1's 100K docs -- sweeps every query faster
+    // than the pass's fixed per-query work: 0.58 vs 0.94 ms per 1K queries)
     const bool seeded = !(a.flags & (HM_FLAG_EXHAUSTIVE | HM_FLAG_FORCE_EXACT)) &&
-                        ((a.flags & HM_FLAG_SEED_ALL) || 4ull * (a.row_hi - a.row_lo) >= X->dev.n_docs);
+                        ((a.flags & HM_FLAG_SEED_ALL) || (4ull * (a.row_hi - a.row_lo) >= X->dev.n_docs &&
+                                                          a.row_hi - a.row_lo >= kSeedMinRows));
     if (seeded) {
         a.fb_list = w->fb_list;
         if (!w->seed_scratch) dalloc(w->seed_scratch, 2ull * X->grid_search * 2ull * a.seed_half);  // up to 2 CTAs per SM

@@ -177,7 +177,8 @@ def _gpu_worker(rank, world, port, out_q):
     off[1:] = np.cumsum([len(t) for t in tids])
     flat = np.concatenate([np.asarray(t, np.uint32) for t in tids])
     tau = np.linspace(0.0, 0.4, len(tids))
-    res = sh.search_batch(off, flat, K, tau=torch.from_numpy(tau).cuda())
+    # HM_FLAG_SEED_ALL: the seeded pass (and with it the shards' bound exchange) runs on these small shards
+    res = sh.search_batch(off, flat, K, tau=torch.from_numpy(tau).cuda(), flags=search.HM_FLAG_SEED_ALL)
     if rank == 0:
         out_q.put({k: v for k, v in res.items()})
     dist.barrier()

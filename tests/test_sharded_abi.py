@@ -84,17 +84,21 @@ def test_sharded_row_window(gpu, c1ish):
 
 @pytest.mark.gpu
 @pytest.mark.parametrize("k", [1, 10, 100])
-def test_sharded_bounded_any_k_and_windows(gpu, c1ish, k):
-    """Batches of 256+ queries exchange the shards' k-th-score bounds first
+@pytest.mark.parametrize("flags", [0, 32])
+def test_sharded_bounded_any_k_and_windows(gpu, c1ish, k, flags):
+    """Batches of 256+ queries exchange the shards' k best seed scores first
     (each shard then keeps only documents that can be in the union's top-k):
-    still the unsharded answer, with and without a row window."""
+    still the unsharded answer, with and without a row window.  flags 32 =
+    HM_FLAG_SEED_ALL: the seeded pass runs on these small shards too, so the
+    bounds are real and the shards' seeded passes run without their seed
+    phase."""
     hx, tids = c1ish
     off, flat = _flat(tids[:300])
     sh = search.ShardedDeviceIndex.from_host(hx, [0, 0, 0, 0])
     dev = search.DeviceIndex.from_host(hx)
     n = hx.n_docs
     for lo, hi in [(0, 0), (n // 7, n - n // 5)]:
-        got = sh.search_batch(off, flat, k, row_lo=lo, row_hi=hi)
+        got = sh.search_batch(off, flat, k, row_lo=lo, row_hi=hi, flags=flags)
         want = dev.search_batch(off, flat, k, row_lo=lo, row_hi=hi)
         for key in ("n", "ids", "conf", "skip", "postings"):
             assert (got[key] == want[key]).all(), (k, lo, hi, key)
@@ -123,7 +127,9 @@ def test_bound_pass_and_external_bound(gpu, c1ish):
     ref = outbuf()
     dev.search_batch_device(d_off, d_tid, ref, k)
     seeds = torch.zeros((nq, k), dtype=torch.float32, device="cuda")
-    dev.search_batch_device(d_off, d_tid, outbuf(), k, flags=search.HM_FLAG_BOUND_ONLY, out_bound=seeds)
+    # (HM_FLAG_SEED_ALL: the seeded pass also runs on this small index)
+    dev.search_batch_device(d_off, d_tid, outbuf(), k, flags=search.HM_FLAG_BOUND_ONLY | search.HM_FLAG_SEED_ALL,
+                            out_bound=seeds)
     torch.cuda.synchronize()
     sc = ref["scores"].cpu().numpy()
     nn = ref["n"].cpu().numpy()
@@ -137,11 +143,12 @@ def test_bound_pass_and_external_bound(gpu, c1ish):
     kth = np.where(nn >= k, sc[:, k - 1], 0.0) * 2.0 ** -61
     assert (bound.cpu().numpy() > 0).sum() > nq // 4, "the seeded pass reported almost no bounds"
     for ext in (bound, torch.from_numpy((kth * (1 - 1e-4)).astype(np.float32)).cuda()):
-        got = outbuf()
-        dev.search_batch_device(d_off, d_tid, got, k, ext_bound=ext)
-        torch.cuda.synchronize()
-        for key in ("n", "ids", "scores", "postings"):
-            assert torch.equal(got[key], ref[key]), key
+        for flags in (0, search.HM_FLAG_SEED_ALL):  # the sweep alone / the seeded pass without its seed phase
+            got = outbuf()
+            dev.search_batch_device(d_off, d_tid, got, k, ext_bound=ext, flags=flags)
+            torch.cuda.synchronize()
+            for key in ("n", "ids", "scores", "postings"):
+                assert torch.equal(got[key], ref[key]), (flags, key)
 
 
 @pytest.mark.gpu
