@@ -63,8 +63,23 @@ for G in Gs:
     t_bound = timed(lambda: devs[0].search_batch_device(b.off, b.tid, b.out, k, flags=search.HM_FLAG_BOUND_ONLY,
                                                         out_bound=bounds[0]))
     t_main = timed(lambda: devs[0].search_batch_device(b.off, b.tid, b.out, k, ext_bound=gmax))
+    try:  # development counters of a -DHM_SEED_STATS scratch build (HM_LIB_DIR): reset
+        import ctypes
+        from paper_2605_25092_b200 import _lib
+        _stats = _lib.load("libhm_b200.so").hm_seed_stats
+        _arr = (ctypes.c_ulonglong * 32)()
+        _stats(_arr, 1)
+    except (AttributeError, OSError):
+        _stats = None
     tm = devs[0].search_batch_device(b.off, b.tid, b.out, k, ext_bound=gmax, flags=search.HM_FLAG_TIMING)
     sd = search.last_seed()
+    if _stats:
+        _stats(_arr, 1)
+        v = list(_arr)
+        nq_s = max(v[0], 1)
+        print(f"    bounded seeded pass per query: cycles prologue {v[6] / nq_s:.0f} seeds {v[7] / nq_s:.0f} "
+              f"candidates {v[8] / max(v[11], 1):.0f} epilogue {v[9] / max(v[11], 1):.0f}; chunks {v[12] / nq_s:.1f}; "
+              f"served {v[11]}, NE probes/q {v[5] / nq_s:.0f}", flush=True)
     tot = t_bound + t_main
     print(f"G={G}: shard {devs[0].n_docs} docs: unbounded {plain:.2f} ms ({base / plain / G * 100:.0f} % of linear); "
           f"bounds {t_bound:.2f} + bounded search {t_main:.2f} = {tot:.2f} ms ({base / tot / G * 100:.0f} % of linear) "
