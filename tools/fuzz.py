@@ -5,7 +5,8 @@
 
 BM25 (random corpora, k1/b, k, row windows, duplicate/unknown terms),
 learned-sparse bridge (random vectors, quantised weights for ties), dense
-(tensor-core and fp64 paths, duplicated rows).  Stops at the first mismatch
+(tensor-core and fp64 paths, duplicated rows), doc-sharded search (2-8 shards,
+the bound exchange, windows).  Stops at the first mismatch
 with the failing case printed."""
 import os
 import sys
@@ -110,14 +111,55 @@ def fuzz_dense(rng):
          ("dense", n, dim, k, flags, search.DenseIndex.last_stats()))
 
 
+def fuzz_sharded(rng):
+    """Doc-sharded search behind the C ABI (hm_sharded_*): 2-8 shards of a
+    random corpus on cuda:0, batches large enough for the shards' bound
+    exchange (and small ones without it), the seeded pass forced or not,
+    row windows -- against the reference library query by query."""
+    n = int(rng.integers(2000, 60000))
+    V = int(rng.integers(50, 3000))
+    docs = [(int(d), " ".join("t%d" % min(V - 1, int(rng.zipf(1.3)) - 1) for _ in range(rng.integers(1, 30))))
+            for d in rng.permutation(n * 3)[:n]]
+    ri = ref.RefIndex.from_texts(docs, ref.TOK_MINIMAL)
+    e = ri.export()
+    G = int(rng.integers(2, 9))
+    sh = search.ShardedDeviceIndex(e["term_offsets"], e["posting_rows"], e["idf"], e["order_key"], e["doc_lens"],
+                                   e["doc_ids"], e["avgdl"], [0] * G, posting_weights=e["posting_weights"])
+    vocab = {t: i for i, t in enumerate(e["terms"])}
+    nq = int(rng.choice([int(rng.integers(1, 40)), int(rng.integers(256, 600))]))
+    qs = [["t%d" % min(V + 3, int(rng.zipf(1.3)) - 1) for _ in range(rng.integers(1, 7))] for _ in range(nq)]
+    tids = [[vocab.get(t, 0xFFFFFFFF) for t in q] for q in qs]
+    off = np.zeros(nq + 1, np.uint32)
+    off[1:] = np.cumsum([len(t) for t in tids])
+    flat = np.array([x for t in tids for x in t], np.uint32)
+    k = int(rng.choice([1, 3, 10, 50, 100]))
+    flags = int(rng.choice([0, search.HM_FLAG_SEED_ALL]))
+    lo = hi = 0
+    if rng.random() < 0.3:
+        lo = int(rng.integers(0, n))
+        hi = int(rng.integers(lo, n + 1))
+    got = sh.search_batch(off, flat, k, flags=flags, row_lo=lo, row_hi=hi)
+    if lo or hi:
+        orc = restate.OracleIndex(e["term_offsets"], e["posting_rows"], e["posting_weights"], e["idf"],
+                                  e["order_key"], e["doc_lens"], e["doc_ids"], e["avgdl"])
+        w = orc.topk(tids, k, row_lo=lo, row_hi=hi if hi else n)
+        same(got["ids"], got["scores"], got["n"], w[0], w[1], w[2], ("sharded window", n, V, G, k, lo, hi, flags))
+        return
+    for i, q in enumerate(qs):
+        w_ids, w_sc, w_post = ri.search(q, k)
+        same(got["ids"][i:i + 1], got["scores"][i:i + 1], got["n"][i:i + 1], [w_ids], [w_sc], [len(w_ids)],
+             ("sharded", n, V, G, k, q, flags))
+        assert int(got["postings"][i]) == w_post, ("sharded postings", q)
+
+
 def main():
     budget = float(sys.argv[1]) if len(sys.argv) > 1 else 300.0
     rng = np.random.default_rng(int(time.time()))
     t0 = time.time()
-    counts = dict(bm25=0, bridge=0, dense=0)
+    counts = dict(bm25=0, bridge=0, dense=0, sharded=0)
     while time.time() - t0 < budget:
-        which = rng.choice(["bm25", "bridge", "dense"])
-        {"bm25": fuzz_bm25, "bridge": fuzz_bridge, "dense": fuzz_dense}[which](rng)
+        which = rng.choice(["bm25", "bridge", "dense", "sharded"])
+        {"bm25": fuzz_bm25, "bridge": fuzz_bridge, "dense": fuzz_dense, "sharded": fuzz_sharded}[which](rng)
         counts[which] += 1
     print("fuzz ok:", counts)
 
