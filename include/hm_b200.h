@@ -2,10 +2,13 @@
  *
  * This is the drop-in boundary under the reference's C++ search API.  The
  * reference has no FFI of its own: its boundary is the C++
- * API in /root/reference/proj/include/hybrid/.  Each entry point below names
- * the reference interface it replaces; include/hybrid/ (this repo) keeps
- * those C++ declarations and implements them on top of this ABI, and
- * INTEGRATION.md shows the bindings (C++, ctypes) a maintainer would add.
+ * API in proj/include/hybrid/.  Each entry point below names the reference
+ * interface it replaces.  The C++ drop-in (paper_2605_25092_b200/csrc/dropin/)
+ * is compiled against the reference's own, unmodified headers -- used in
+ * place, never copied into this repo -- and defines the reference's search
+ * entry points on top of this ABI; include/hybrid_b200.hpp adds the batch
+ * extension.  INTEGRATION.md shows the bindings (C++, ctypes) a maintainer
+ * would add.
  *
  * Conventions: plain pointers and sizes only; every function returns
  * HM_OK (0) or a nonzero hm_status, with a thread-local message in
