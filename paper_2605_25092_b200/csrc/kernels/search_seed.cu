@@ -130,7 +130,10 @@ __global__ void __launch_bounds__(kCons, HM_SEED_MINB) search_seed_kernel(DevInd
             else hand_over(a, q, ext * kExtSlack);
         };
         // anything unusual goes to the exhaustive kernel, which routes it on
-        if (m == 0 || m > kFastTerms || k == 0 || k > kmax || (a.flags & 1u) || row_hi <= row_lo) {
+        // (plans longer than kSeedMaxTerms go to the sweep before the prologue's
+        // serial bound sort: C4's 24-32-term plans)
+        if (m == 0 || m > kFastTerms || k == 0 || k > kmax || (a.flags & 1u) || row_hi <= row_lo ||
+            (m > kSeedMaxTerms && !(a.flags & 32u))) {
             if (tid == 0) give_up();
             continue;
         }
