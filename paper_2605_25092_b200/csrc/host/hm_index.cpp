@@ -80,8 +80,9 @@ struct Workspace {
     // device
     uint32_t *q_off = nullptr, *q_tid = nullptr, *plan_tid = nullptr, *plan_mult = nullptr,
              *plan_len = nullptr, *order_in = nullptr, *order = nullptr, *counters = nullptr,
-             *exact_list = nullptr, *out_n = nullptr, *fb_list = nullptr, *wide_list = nullptr;
-    uint64_t *cost = nullptr, *cost_sorted = nullptr, *out_ids = nullptr, *out_post = nullptr;
+             *exact_list = nullptr, *out_n = nullptr, *fb_list = nullptr, *wide_list = nullptr,
+             *order_seed = nullptr;
+    uint64_t *cost = nullptr, *cost_sorted = nullptr, *out_ids = nullptr, *out_post = nullptr, *cost_seed = nullptr;
     double *tau = nullptr, *out_scores = nullptr, *out_conf = nullptr;
     float* w32 = nullptr;
     uint8_t* out_skip = nullptr;
@@ -128,12 +129,13 @@ struct Workspace {
         drop_graph();
         void* ps[] = {q_off, q_tid, plan_tid, plan_mult, plan_len, order_in, order, counters,
                       exact_list, fb_list, wide_list, out_n, cost, cost_sorted, out_ids, out_post, tau,
+                      order_seed, cost_seed,
                       out_scores, out_conf, w32, out_skip, sort_tmp};
         for (void* p : ps)
             if (p) cudaFree(p);
         q_off = q_tid = plan_tid = plan_mult = plan_len = order_in = order = counters = exact_list =
-            out_n = fb_list = wide_list = nullptr;
-        cost = cost_sorted = out_ids = out_post = nullptr;
+            out_n = fb_list = wide_list = order_seed = nullptr;
+        cost = cost_sorted = out_ids = out_post = cost_seed = nullptr;
         tau = out_scores = out_conf = nullptr;
         w32 = nullptr;
         out_skip = nullptr;
@@ -535,6 +537,8 @@ void ensure(Workspace* w, uint32_t nq, uint32_t ntid, uint32_t k, bool need_io) 
         dalloc(w->wide_list, NQ);
         dalloc(w->cost, NQ);
         dalloc(w->cost_sorted, NQ);
+        dalloc(w->cost_seed, NQ);
+        dalloc(w->order_seed, NQ);
         dalloc(w->tau, NQ);
         dalloc(w->w32, hm::kMaxCodes);
         dalloc(w->out_ids, static_cast<uint64_t>(NQ) * K);
@@ -708,6 +712,10 @@ void run_batch(hm_index* X, Workspace* w, const hm_query_batch& hb, const uint32
     const bool seeded = !(a.flags & (HM_FLAG_EXHAUSTIVE | HM_FLAG_FORCE_EXACT)) &&
                         ((a.flags & HM_FLAG_SEED_ALL) || (4ull * (a.row_hi - a.row_lo) >= X->dev.n_docs &&
                                                           a.row_hi - a.row_lo >= kSeedMinRows));
+    if (seeded && split == 1) {  // the seeded pass walks its own LPT order (its cost is not the sweep's)
+        a.cost_seed = w->cost_seed;
+        a.order_seed = w->order_seed;
+    }
     if (seeded) {
         a.fb_list = w->fb_list;
         if (!w->seed_scratch) dalloc(w->seed_scratch, 2ull * X->grid_search * 2ull * a.seed_half);  // up to 2 CTAs per SM
@@ -738,6 +746,10 @@ void run_batch(hm_index* X, Workspace* w, const hm_query_batch& hb, const uint32
         } else {
             ck(hm::launch_plan(X->dev, a, w->order_in, st), "plan kernel");
             ck(hm::launch_lpt_sort(w->sort_tmp, w->sort_bytes, a, w->cost_sorted, w->order_in, st), "lpt sort");
+            if (a.order_seed)  // the seeded pass's own LPT order
+                ck(hm::launch_seed_sort(w->sort_tmp, w->sort_bytes, a, w->cost_sorted, w->order_in, w->order_seed,
+                                        st),
+                   "seed lpt sort");
         }
         if (timing) ck(cudaEventRecord(w->ev[1], st), "event");
         if (a.flags & HM_FLAG_BOUND_ONLY) {  // doc shards' bound pass: the seeded pass's L per query

@@ -63,10 +63,15 @@ __global__ void plan_kernel(DevIndex ix, BatchArgs a, uint32_t* order_in) {
         pt[j + 1] = t;
         pm[j + 1] = mu;
     }
-    uint64_t c = 0;
-    for (uint32_t i = 0; i < m; ++i) c += ix.term_off[pt[i] + 1] - ix.term_off[pt[i]];
+    uint64_t c = 0, cs = 0;
+    for (uint32_t i = 0; i < m; ++i) {
+        const uint64_t df = ix.term_off[pt[i] + 1] - ix.term_off[pt[i]];
+        c += df;
+        if (df <= kSeedScratch / 2) cs += df;
+    }
     a.plan_len[q] = m;
     a.cost[q] = c;
+    if (a.cost_seed) a.cost_seed[q] = cs;
     if (m >= kNeMinTerms && m <= 32) atomicAdd(&a.counters[8], 1u);  // the essential-term sweep has work
     order_in[q] = q;
 }
@@ -421,6 +426,13 @@ cudaError_t launch_lpt_sort(void* temp, size_t bytes, const BatchArgs& a, uint64
     if (a.nq == 0) return cudaSuccess;
     return cub::DeviceRadixSort::SortPairsDescending(temp, bytes, a.cost, cost_sorted, order_in,
                                                      a.order, static_cast<int>(a.nq), 0, 64, st);
+}
+
+cudaError_t launch_seed_sort(void* temp, size_t bytes, const BatchArgs& a, uint64_t* cost_sorted,
+                             const uint32_t* order_in, uint32_t* order_seed, cudaStream_t st) {
+    if (a.nq == 0) return cudaSuccess;
+    return cub::DeviceRadixSort::SortPairsDescending(temp, bytes, a.cost_seed, cost_sorted, order_in, order_seed,
+                                                     static_cast<int>(a.nq), 0, 64, st);
 }
 
 static bool g_exact_attr = false;

@@ -149,6 +149,9 @@ struct BatchArgs {
     uint32_t* plan_len;        // [nq]
     uint64_t* cost;            // [nq] sum of df over the plan (LPT key)
     uint32_t* order;           // [nq] queries, most expensive first
+    uint64_t* cost_seed;       // [nq] the seeded pass's cost proxy: postings of the plan terms with at
+                               // most kSeedScratch / 2 postings (its seeds and essential candidates)
+    const uint32_t* order_seed;  // [nq] queries by cost_seed descending (the seeded pass's LPT), or null
     uint32_t* counters;        // [0]=work cursor (seeded or exhaustive), [1]=exact list size,
                                // [2]=work cursor exact, [3]=error flags,
                                // [4]=queries handed over, [5]=exhaustive cursor after the seeded pass,

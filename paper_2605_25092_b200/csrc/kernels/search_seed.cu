@@ -102,7 +102,7 @@ __global__ void __launch_bounds__(kCons, HM_SEED_MINB) search_seed_kernel(DevInd
         __syncthreads();
         if (tid == 0) {
             const uint32_t w = atomicAdd(&a.counters[0], 1u);
-            S.q = w < a.nq ? a.order[w] : kNoTerm;
+            S.q = w < a.nq ? (a.order_seed ? a.order_seed[w] : a.order[w]) : kNoTerm;
         }
         __syncthreads();
         const uint32_t q = S.q;
