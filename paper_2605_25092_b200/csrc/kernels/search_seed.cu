@@ -854,6 +854,16 @@ __global__ void __launch_bounds__(kCons, HM_SEED_MINB) search_seed_kernel(DevInd
         }
 #endif
     }
+#ifdef HM_SEED_STATS  // tail: CTA exit times (globaltimer, ns; tools/seed_tail.py)
+    if (tid == 0) {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        atomicMax(&g_seed_stats[20], t);
+        atomicMin(&g_seed_stats[21], t);
+        SST(22, t >> 10);
+        SST(23, 1);
+    }
+#endif
 }
 
 template <int CAPW>
@@ -894,7 +904,8 @@ cudaError_t launch_search_seed(const DevIndex& ix, const BatchArgs& a, int cap, 
 extern "C" int hm_seed_stats(unsigned long long* out, int reset) {
     if (cudaMemcpyFromSymbol(out, hm::g_seed_stats, sizeof(hm::g_seed_stats)) != cudaSuccess) return -1;
     if (reset) {
-        static const unsigned long long z[32] = {};
+        unsigned long long z[32] = {};
+        z[21] = ~0ull;  // running minimum of the CTA exit times
         cudaMemcpyToSymbol(hm::g_seed_stats, z, sizeof(z));
     }
     return 0;

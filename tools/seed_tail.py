@@ -1,3 +1,6 @@
+"""Development aid (scratch build with -DHM_SEED_STATS, HM_LIB_DIR): the
+seeded pass's tail on C2 -- the spread of its CTAs' exit times (first ->
+last, mean -> last) over three batches."""
 import sys, os, ctypes
 sys.path.insert(0, '/root/repo')
 import numpy as np, torch, bench
