@@ -5,7 +5,9 @@
 
 Builds the config's index, runs one warm-up batch (bakes the postings for
 k1=1.2 b=0.75), then one measured batch with HM_FLAG_TIMING (eager launches,
-no CUDA-graph replay).  With -s 4 ncu skips the warm-up batch's four kernels.
+no CUDA-graph replay).  A batch launches five matching kernels (plan, seeded
+pass, the essential-term sweep -- empty on C2 -- the sweep, exact): -s 5 -c 5
+captures the measured batch.
 """
 import os
 import sys
