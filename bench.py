@@ -639,33 +639,40 @@ def main():
     h2d = q_off.nbytes + tids.nbytes + 4 * 4096
     d2h = nq * k * 16 + nq * (4 + 8 + 1 + 8) + 16
 
-    # ---------------- e2e from query strings (N=1): vocabulary resolution in native threads
-    strings = None
-    if world == 1:
-        vocab = search.Vocab(hx.term_strings())
-        qtext = [" ".join(queries.terms(i)) for i in range(nq)]
-        enc = [s.encode() for s in qtext]
-        text = b"".join(enc)
-        toff = np.zeros(nq + 1, np.uint64)
-        toff[1:] = np.cumsum([len(e) for e in enc])
-        vocab.resolve_text(text, toff)
-        s_ms, r_ms = [], []
-        for _ in range(args.steps):
-            flush.zero_()
-            torch.cuda.synchronize()
-            t1 = time.perf_counter()
-            o2, t2 = vocab.resolve_text(text, toff)
-            t_res = time.perf_counter()
-            dev.search_batch(o2, t2, k)
-            t3 = time.perf_counter()
-            s_ms.append((t3 - t1) * 1e3)
-            r_ms.append((t_res - t1) * 1e3)
-        assert (o2 == q_off).all() and (t2 == tids).all(), "string resolution differs from the term ids"
-        strings = dict(value=nq * len(s_ms) / (sum(s_ms) / 1e3), unit="queries/s", p50_ms=pct(s_ms, 0.5),
-                       p99_ms=pct(s_ms, 0.99), resolve_ms_p50=pct(r_ms, 0.5),
-                       h2d_bytes_per_step=int(h2d), d2h_bytes_per_step=int(d2h),
-                       path="query strings (host) -> hm_vocab_resolve (native threads) -> hm_search_batch",
-                       text_bytes=len(text))
+    # ---------------- e2e from query strings: vocabulary resolution in native threads (N > 1:
+    # every rank resolves the batch against the global vocabulary its shard carries, then the
+    # doc-sharded search; max over ranks)
+    vocab = search.Vocab(hx.term_strings())
+    qtext = [" ".join(queries.terms(i)) for i in range(nq)]
+    enc = [s.encode() for s in qtext]
+    text = b"".join(enc)
+    toff = np.zeros(nq + 1, np.uint64)
+    toff[1:] = np.cumsum([len(e) for e in enc])
+    vocab.resolve_text(text, toff)
+    s_ms, r_ms = [], []
+    for _ in range(args.steps):
+        flush.zero_()
+        torch.cuda.synchronize()
+        barrier()
+        t1 = time.perf_counter()
+        o2, t2 = vocab.resolve_text(text, toff)
+        t_res = time.perf_counter()
+        api.search_batch(o2, t2, k)
+        t3 = time.perf_counter()
+        s_ms.append((t3 - t1) * 1e3)
+        r_ms.append((t_res - t1) * 1e3)
+    assert (o2 == q_off).all() and (t2 == tids).all(), "string resolution differs from the term ids"
+    s_tot = sum(s_ms)
+    if world > 1:
+        t = torch.tensor([s_tot], dtype=torch.float64, device=d)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        s_tot = float(t.item())
+    strings = dict(value=nq * len(s_ms) / (s_tot / 1e3), unit="queries/s", p50_ms=pct(s_ms, 0.5),
+                   p99_ms=pct(s_ms, 0.99), resolve_ms_p50=pct(r_ms, 0.5),
+                   h2d_bytes_per_step=int(h2d), d2h_bytes_per_step=int(d2h),
+                   path="query strings (host) -> hm_vocab_resolve (native threads) -> hm_search_batch"
+                        + (" on every rank's shard, NCCL merge" if world > 1 else ""),
+                   text_bytes=len(text))
 
     # ---------------- small-batch latency (N=1; device time of 1- and 10-query batches)
     small_lat = None

@@ -174,6 +174,7 @@ struct hm_index {
     uint64_t bytes = 0;
     uint32_t row_bits = 0, code_bits = 0, n_codes = 0;
     uint64_t n_escaped = 0;
+    uint64_t n_postings = 0;  // a query's cost (postings of its terms) never exceeds it: LPT key bits
     std::vector<uint32_t> code_tf, code_len;
     int grid_search = 0, grid_exact = 0;
     // baked long-term postings (kernels/bake.cu) for one (k1, b)
@@ -205,6 +206,7 @@ void build_index(const hm_csr_view* v, hm_index* X) {
     const uint32_t V = v->n_terms, N = v->n_docs;
     if (!v->term_offsets) throw std::invalid_argument("term_offsets is required");
     const uint64_t P = v->term_offsets[V];
+    X->n_postings = P;
     if ((P && !v->posting_rows) || (N && (!v->doc_lens || !v->doc_ids)) ||
         (V && (!v->term_idfs || !v->term_order_keys)))
         throw std::invalid_argument("hm_csr_view: missing array");
@@ -736,19 +738,23 @@ void run_batch(hm_index* X, Workspace* w, const hm_query_batch& hb, const uint32
            "upload w32");
         ck(cudaMemsetAsync(w->counters, 0, 16 * sizeof(uint32_t), st), "memset counters");
         if (timing) ck(cudaEventRecord(w->ev[0], st), "event");
+        // the costs are postings counts <= the index's: radix passes over those bits only
+        const int key_bits = X->n_postings ? 64 - __builtin_clzll(X->n_postings) : 1;
         if (split > 1) {  // plan + LPT over the real queries, then every slab of each
             hm::BatchArgs ap = a;
             ap.nq = nq;
             ap.order = w->exact_list;  // scratch until the sweep appends to it
             ck(hm::launch_plan(X->dev, ap, w->order_in, st), "plan kernel");
-            ck(hm::launch_lpt_sort(w->sort_tmp, w->sort_bytes, ap, w->cost_sorted, w->order_in, st), "lpt sort");
+            ck(hm::launch_lpt_sort(w->sort_tmp, w->sort_bytes, ap, w->cost_sorted, w->order_in, key_bits, st),
+               "lpt sort");
             ck(hm::launch_expand_order(nq, split, w->exact_list, w->order, st), "expand order");
         } else {
             ck(hm::launch_plan(X->dev, a, w->order_in, st), "plan kernel");
-            ck(hm::launch_lpt_sort(w->sort_tmp, w->sort_bytes, a, w->cost_sorted, w->order_in, st), "lpt sort");
+            ck(hm::launch_lpt_sort(w->sort_tmp, w->sort_bytes, a, w->cost_sorted, w->order_in, key_bits, st),
+               "lpt sort");
             if (a.order_seed)  // the seeded pass's own LPT order
                 ck(hm::launch_seed_sort(w->sort_tmp, w->sort_bytes, a, w->cost_sorted, w->order_in, w->order_seed,
-                                        st),
+                                        key_bits, st),
                    "seed lpt sort");
         }
         if (timing) ck(cudaEventRecord(w->ev[1], st), "event");

@@ -422,17 +422,17 @@ cudaError_t lpt_sort_bytes(uint32_t nq, size_t* bytes) {
 }
 
 cudaError_t launch_lpt_sort(void* temp, size_t bytes, const BatchArgs& a, uint64_t* cost_sorted,
-                            const uint32_t* order_in, cudaStream_t st) {
+                            const uint32_t* order_in, int key_bits, cudaStream_t st) {
     if (a.nq == 0) return cudaSuccess;
     return cub::DeviceRadixSort::SortPairsDescending(temp, bytes, a.cost, cost_sorted, order_in,
-                                                     a.order, static_cast<int>(a.nq), 0, 64, st);
+                                                     a.order, static_cast<int>(a.nq), 0, key_bits, st);
 }
 
 cudaError_t launch_seed_sort(void* temp, size_t bytes, const BatchArgs& a, uint64_t* cost_sorted,
-                             const uint32_t* order_in, uint32_t* order_seed, cudaStream_t st) {
+                             const uint32_t* order_in, uint32_t* order_seed, int key_bits, cudaStream_t st) {
     if (a.nq == 0) return cudaSuccess;
     return cub::DeviceRadixSort::SortPairsDescending(temp, bytes, a.cost_seed, cost_sorted, order_in, order_seed,
-                                                     static_cast<int>(a.nq), 0, 64, st);
+                                                     static_cast<int>(a.nq), 0, key_bits, st);
 }
 
 static bool g_exact_attr = false;

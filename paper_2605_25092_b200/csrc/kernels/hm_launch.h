@@ -15,10 +15,11 @@ cudaError_t launch_plan(const DevIndex& ix, const BatchArgs& a, uint32_t* order_
 cudaError_t lpt_sort_bytes(uint32_t nq, size_t* bytes);
 cudaError_t launch_lpt_sort(void* temp, size_t bytes, const BatchArgs& a,
                             uint64_t* cost_sorted, const uint32_t* order_in,
-                            cudaStream_t st);
+                            int key_bits, cudaStream_t st);
 // the seeded pass's own LPT order (cost_seed descending) into order_seed
+// (key_bits: the costs' significant bits -- radix passes over those only)
 cudaError_t launch_seed_sort(void* temp, size_t bytes, const BatchArgs& a, uint64_t* cost_sorted,
-                             const uint32_t* order_in, uint32_t* order_seed, cudaStream_t st);
+                             const uint32_t* order_in, uint32_t* order_seed, int key_bits, cudaStream_t st);
 // small batches split each query into row slabs (BatchArgs::split): slab
 // queries in the real LPT order, and their postings summed per real query
 cudaError_t launch_expand_order(uint32_t nq_real, uint32_t split, const uint32_t* order_real, uint32_t* order,

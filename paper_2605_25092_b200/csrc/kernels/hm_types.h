@@ -110,7 +110,10 @@ constexpr uint16_t kDenseEscape = 0xFFFE;
 #define HM_SEED_SCRATCH (2 * 131072)
 #endif
 constexpr uint32_t kSeedScratch = HM_SEED_SCRATCH;  // words per CTA (search_seed.cu: kSeedMaxDf scores + rows)
-constexpr uint32_t kNePendCap = 8192;     // essential-term sweep: pending rows per warp
+#ifndef HM_NE_PEND_CAP
+#define HM_NE_PEND_CAP 8192
+#endif
+constexpr uint32_t kNePendCap = HM_NE_PEND_CAP;  // essential-term sweep: pending rows per warp
 #ifndef HM_NE_MIN_TERMS
 #define HM_NE_MIN_TERMS 8
 #endif
