@@ -113,6 +113,67 @@ __device__ __forceinline__ float esc_w(const DevIndex& ix, uint64_t gidx, uint32
                     static_cast<double>(__ldg(ix.doc_lens + row)), ix.avgdl, k1, b);
 }
 
+// ---------------------------------------------------------------- short-term tile tables
+// Row tab[jj] of short term s (list[s], its window [t_wlo, t_end) with prefix
+// pref[s] in the concatenation of the short terms' windows): the offset (from
+// t_start) of its first posting in tile j0 + jj, tab[nt] the window's end.
+// Every posting f fills the entries of the tiles from its predecessor's tile
+// (exclusive) to its own; HM_SHORT_U postings per thread are loaded before any
+// entry is written (their loads in flight together).  Empty windows are filled
+// by the second loop.  Ends with the CTA barrier.
+#ifndef HM_SHORT_U
+#define HM_SHORT_U 4
+#endif
+template <class Sm>
+__device__ __forceinline__ void short_tables(const DevIndex& ix, Sm& S, const uint16_t* list, uint32_t n_short,
+                                             uint32_t* stab, uint32_t stride, uint32_t j0, uint32_t nt,
+                                             uint32_t cb) {
+    constexpr int U = HM_SHORT_U;
+    constexpr int NT = kCons;
+    const uint32_t total = S.pref[n_short];
+    for (uint32_t f0 = threadIdx.x; f0 < total; f0 += U * NT) {
+        uint64_t g[U], w0[U];
+        uint32_t sl[U], pc[U], pv[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const uint32_t f = f0 + u * NT;
+            uint32_t lo = 0, hi = n_short;  // s: pref[s] <= f < pref[s+1]
+            while (hi - lo > 1) {
+                const uint32_t mid = (lo + hi) >> 1;
+                if (S.pref[mid] <= f) lo = mid;
+                else hi = mid;
+            }
+            sl[u] = lo;
+            w0[u] = S.t_wlo[list[lo]];
+            g[u] = w0[u] + (f - S.pref[lo]);
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const bool ok = f0 + u * NT < total;
+            pc[u] = ok ? __ldg(ix.post + g[u]) : 0u;
+            pv[u] = ok && g[u] != w0[u] ? __ldg(ix.post + g[u] - 1) : 0u;
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            if (f0 + u * NT >= total) break;
+            const uint32_t i = list[sl[u]];
+            const uint64_t w1 = S.t_end[i], s0 = S.t_start[i];
+            const int jt = static_cast<int>((pc[u] >> cb) >> kTileShift) - static_cast<int>(j0);
+            const int jp = g[u] == w0[u] ? -1 : static_cast<int>((pv[u] >> cb) >> kTileShift) - static_cast<int>(j0);
+            uint32_t* tab = stab + static_cast<uint64_t>(sl[u]) * stride;
+            for (int jj = jp + 1; jj <= jt; ++jj) tab[jj] = static_cast<uint32_t>(g[u] - s0);
+            if (g[u] + 1 == w1)
+                for (int jj = jt + 1; jj <= static_cast<int>(nt); ++jj) tab[jj] = static_cast<uint32_t>(w1 - s0);
+        }
+    }
+    for (uint32_t x = threadIdx.x; x < n_short * (nt + 1); x += NT) {
+        const uint32_t s = x / (nt + 1), jj = x % (nt + 1), i = list[s];
+        if (S.t_wlo[i] == S.t_end[i])
+            stab[static_cast<uint64_t>(s) * stride + jj] = static_cast<uint32_t>(S.t_wlo[i] - S.t_start[i]);
+    }
+    __syncthreads();
+}
+
 // ---------------------------------------------------------------- per-warp list
 // Raise the warp's k-th bound from its own list (exact k-th largest by a
 // binary search over the float bit pattern, values are >= 0), keep the

@@ -211,34 +211,7 @@ __global__ void __launch_bounds__(kCons, HM_SEED_MINB) search_seed_kernel(DevInd
         const uint32_t j0 = row_lo >> kTileShift, j1 = (row_hi - 1) >> kTileShift;
         const uint32_t nt = j1 - j0 + 1;
         // ---------------- short-term tile tables (probes of short terms)
-        {
-            const uint32_t total = S.pref[n_short];
-            for (uint32_t f = tid; f < total; f += kCons) {
-                uint32_t lo = 0, hi = n_short;  // s: pref[s] <= f < pref[s+1]
-                while (hi - lo > 1) {
-                    const uint32_t mid = (lo + hi) >> 1;
-                    if (S.pref[mid] <= f) lo = mid;
-                    else hi = mid;
-                }
-                const uint32_t s = lo, i = S.order_list[s];
-                const uint64_t w0 = S.t_wlo[i], w1 = S.t_end[i], s0 = S.t_start[i];
-                const uint64_t g = w0 + (f - S.pref[s]);
-                const int jt = static_cast<int>((__ldg(ix.post + g) >> cb) >> kTileShift) - static_cast<int>(j0);
-                const int jp = g == w0 ? -1
-                                       : static_cast<int>((__ldg(ix.post + g - 1) >> cb) >> kTileShift) -
-                                             static_cast<int>(j0);
-                uint32_t* tab = stab + static_cast<uint64_t>(s) * stride;
-                for (int jj = jp + 1; jj <= jt; ++jj) tab[jj] = static_cast<uint32_t>(g - s0);
-                if (g + 1 == w1)
-                    for (int jj = jt + 1; jj <= static_cast<int>(nt); ++jj) tab[jj] = static_cast<uint32_t>(w1 - s0);
-            }
-            for (uint32_t x = tid; x < n_short * (nt + 1); x += kCons) {
-                const uint32_t s = x / (nt + 1), jj = x % (nt + 1), i = S.order_list[s];
-                if (S.t_wlo[i] == S.t_end[i])
-                    stab[static_cast<uint64_t>(s) * stride + jj] = static_cast<uint32_t>(S.t_wlo[i] - S.t_start[i]);
-            }
-        }
-        __syncthreads();
+        short_tables(ix, S, S.order_list, n_short, stab, stride, j0, nt, cb);
 #ifdef HM_SEED_STATS
         c_t1 = clock64();
 #endif
