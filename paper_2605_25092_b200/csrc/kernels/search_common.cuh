@@ -333,11 +333,53 @@ __device__ __forceinline__ void step_apply(float* __restrict__ acc, uint32_t wba
 // Margin confidence + skip (src/cascade.cpp:15-21, 79-84).  A near-tie flood
 // (> kSurvCap survivors) hands the query to the exact kernel.  Leaves the
 // accumulator area zero.
+// (tf, doc length) of plan term i in a row of the query's window, for the
+// exact rescoring: a dense term's per-row code (one load), a short term's
+// tile segment (stab row t_spos[i]), else find_posting's sub-tile search.
+template <class Sm>
+__device__ __forceinline__ bool exact_lookup(const DevIndex& ix, const Sm& S, const uint32_t* stab, uint32_t stride,
+                                             uint32_t j0, uint32_t cb, uint32_t i, uint32_t row, double* tf,
+                                             double* dl) {
+    const int32_t slot = S.t_slot[i];
+    if (slot >= 0) {
+        const int32_t d = S.t_dense[i];
+        if (d >= 0) {
+            const uint16_t code = __ldg(ix.dense + static_cast<uint64_t>(d) * ix.n_docs + row);
+            if (code == kDenseAbsent) return false;
+            if (code != kDenseEscape) {
+                *tf = ix.code_tf[code];
+                *dl = ix.code_len[code];
+                return true;
+            }
+        }
+        return find_posting(ix, slot, S.t_start[i], S.t_end[i], row, ix.code_tf, ix.code_len, tf, dl);
+    }
+    const uint32_t* tab = stab + static_cast<uint64_t>(S.t_spos[i]) * stride;
+    const uint32_t jj = (row >> kTileShift) - j0;
+    const uint64_t s0 = S.t_start[i];
+    const uint64_t lo = s0 + tab[jj], hi = s0 + tab[jj + 1];
+    const uint64_t pos = lower_bound_row(ix.post, lo, hi, row, cb);
+    if (pos >= hi) return false;
+    const uint32_t p = __ldg(ix.post + pos);
+    if ((p >> cb) != row) return false;
+    const uint32_t code = p & ix.esc_short;
+    if (code < ix.n_codes_short) {
+        *tf = ix.code_tf[code];
+        *dl = ix.code_len[code];
+    } else {
+        *tf = __ldg(ix.tf + pos);
+        *dl = __ldg(ix.doc_lens + row);
+    }
+    return true;
+}
+
 template <int CAPW, int ACC, int STG>
 __device__ __forceinline__ void finish_query(const DevIndex& ix, const BatchArgs& a, SmemT<CAPW, ACC, STG>& S, uint32_t q,
                                              uint32_t m, uint32_t k, uint32_t nw, float f_slack, double k1,
-                                             double bb) {
+                                             double bb, const uint32_t* stab, uint32_t stride, uint32_t j0,
+                                             uint32_t cb) {
     constexpr int kGatherBytes = 8 * kConsWarps * CAPW;
+    static_assert(kSurvBytes + 8 * kCons <= 4 * ACC, "survivors + the rescoring batch fit in the accumulator area");
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     auto csync = [] { __syncthreads(); };
     char* sp = reinterpret_cast<char*>(S.acc);
@@ -389,37 +431,40 @@ __device__ __forceinline__ void finish_query(const DevIndex& ix, const BatchArgs
                 reinterpret_cast<uint32_t*>(sp + 16 * kSurvCap)};
     for (uint32_t i = tid; i < ns; i += kCons) sv.row[i] = (&S.cl_row[0][0])[i];
     csync();
-    // warp per survivor, lanes over plan terms; fp64 sum in plan order
-    for (uint32_t s = warp; s < ns; s += kConsWarps) {
-        const uint32_t row = sv.row[s];
-        double E = 0.0;
-        for (uint32_t t0 = 0; t0 < m; t0 += 32) {
-            const uint32_t t = t0 + lane;
-            double val = 0.0;
-            bool present = false;
-            if (t < m) {
-                double tf, dl;
-                if (find_posting(ix, S.t_slot[t], S.t_start[t], S.t_end[t], row, ix.code_tf,
-                                 ix.code_len, &tf, &dl)) {
-                    val = bm25_exact(tf, S.t_idf[t], dl, ix.avgdl, k1, bb);
-                    present = true;
-                }
-            }
-            const uint32_t cnt = min(32u, m - t0);
-            for (uint32_t u = 0; u < cnt; ++u) {
-                const double x = __shfl_sync(0xffffffffu, val, u);
-                const bool pr = __shfl_sync(0xffffffffu, present, u);
-                if (pr) {
-                    const uint32_t mu = S.t_mult[t0 + u];
-                    for (uint32_t r = 0; r < mu; ++r) E = __dadd_rn(E, x);  // :94
-                }
-            }
+    // (survivor, term) pairs over all threads, a batch of kCons lookups in flight
+    // together; then every survivor adds its terms' exact scores in plan order
+    // (fp64, mult repeats, the reference's accumulation :87-101) -- a term
+    // absent from the row (-1) adds nothing
+    double* const pv = reinterpret_cast<double*>(sp + kSurvBytes);
+    for (uint32_t i = tid; i < ns; i += kCons) sv.E[i] = 0.0;
+    const uint32_t npair = ns * m;
+    for (uint32_t p0 = 0; p0 < npair; p0 += kCons) {
+        const uint32_t p = p0 + tid;
+        double val = -1.0;
+        if (p < npair) {
+            const uint32_t s = p / m, t = p - s * m;
+            double tf, dl;
+            if (exact_lookup(ix, S, stab, stride, j0, cb, t, sv.row[s], &tf, &dl))
+                val = bm25_exact(tf, S.t_idf[t], dl, ix.avgdl, k1, bb);
         }
-        if (lane == 0) {
+        pv[tid] = val;
+        csync();
+        const uint32_t s = p0 / m + tid;
+        if (s < ns && s * m < p0 + kCons) {
+            const uint32_t x0 = max(s * m, p0), x1 = min(min(s * m + m, p0 + kCons), npair);
+            double E = sv.E[s];
+            for (uint32_t x = x0; x < x1; ++x) {
+                const double v = pv[x - p0];
+                if (v >= 0.0) {
+                    const uint32_t mu = S.t_mult[x - s * m];
+                    for (uint32_t r = 0; r < mu; ++r) E = __dadd_rn(E, v);  // :94
+                }
+            }
             sv.E[s] = E;
-            sv.id[s] = __ldg(ix.doc_ids + row);
         }
+        csync();
     }
+    for (uint32_t i = tid; i < ns; i += kCons) sv.id[i] = __ldg(ix.doc_ids + sv.row[i]);
     csync();
     const uint32_t n2 = pow2_ceil(ns);
     for (uint32_t i = ns + tid; i < n2; i += kCons) {
@@ -442,7 +487,7 @@ __device__ __forceinline__ void finish_query(const DevIndex& ix, const BatchArgs
         write_decision(a, q, sv.E, nout);
     }
     csync();
-    for (int i = tid; i < kSurvBytes / 4; i += kCons) S.acc[i] = 0.f;
+    for (int i = tid; i < (kSurvBytes + 8 * kCons) / 4; i += kCons) S.acc[i] = 0.f;  // survivors + rescoring batch
 }
 
 }  // namespace hm

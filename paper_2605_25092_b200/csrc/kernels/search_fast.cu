@@ -244,6 +244,7 @@ __global__ void __launch_bounds__(kCons, 2) search_fast_kernel(DevIndex ix, Batc
             S.t_c32[tid] = static_cast<float>(ldexp(static_cast<double>(mult) * idf, sh));
             S.t_slot[tid] = slot;
             S.t_bkb[tid] = slot >= 0 ? ix.bk_base[slot] : 0;
+            S.t_dense[tid] = slot >= 0 ? ix.dense_of_slot[slot] : -1;  // (the exact rescoring's lookups)
         }
         if (NE && tid < static_cast<int>(m)) {  // bounds and probe weights of the essential-term mode (below)
             const uint32_t t = a.plan_tid[poff + tid];
@@ -253,7 +254,6 @@ __global__ void __launch_bounds__(kCons, 2) search_fast_kernel(DevIndex ix, Batc
             const float cu = static_cast<float>(ldexp(static_cast<double>(mult) * idf, -kScoreShift));
             S.t_cu[tid] = cu;
             S.t_ms[tid] = cu * ix.tmax[t] * 1.0000010f;  // rounded up: an upper bound
-            S.t_dense[tid] = slot >= 0 ? ix.dense_of_slot[slot] : -1;
         }
         __syncthreads();
         if (tid == 0) {
@@ -312,6 +312,7 @@ __global__ void __launch_bounds__(kCons, 2) search_fast_kernel(DevIndex ix, Batc
             for (uint32_t i = 0; i < m; ++i)
                 if (S.t_slot[i] < 0) {
                     S.order_list[nl + ns] = static_cast<uint16_t>(i);
+                    S.t_spos[i] = static_cast<uint8_t>(ns);  // stab row (the NE ranks are long terms only)
                     S.pref[ns + 1] = S.pref[ns] + static_cast<uint32_t>(S.t_end[i] - S.t_wlo[i]);
                     ++ns;
                 }
@@ -829,7 +830,7 @@ __global__ void __launch_bounds__(kCons, 2) search_fast_kernel(DevIndex ix, Batc
             continue;
         }
 
-        finish_query<CAPW>(ix, a, S, q, m, k, nw, f_slack, k1, bb);
+        finish_query<CAPW>(ix, a, S, q, m, k, nw, f_slack, k1, bb, stab, stride, j0, cb);
     }
 }
 

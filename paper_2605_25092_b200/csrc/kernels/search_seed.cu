@@ -816,7 +816,7 @@ __global__ void __launch_bounds__(kCons, HM_SEED_MINB) search_seed_kernel(DevInd
             if (tid < kConsWarps) S.n_w[tid] = 0;
             continue;
         }
-        finish_query<CAPW>(ix, a, S, q, m, k, nw, f_slack, k1, bb);
+        finish_query<CAPW>(ix, a, S, q, m, k, nw, f_slack, k1, bb, stab, stride, j0, cb);
 #ifdef HM_SEED_STATS
         if (tid == 0) {
             SST(6, c_t1 - c_t0);
