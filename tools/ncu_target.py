@@ -24,6 +24,8 @@ def main():
     name = sys.argv[1] if len(sys.argv) > 1 else "c2"
     cfg = {"c2": bench.C2, "c4": bench.C4}[name]
     extra = search.HM_FLAG_EXHAUSTIVE if "--exhaustive" in sys.argv else 0
+    if "--flags" in sys.argv:
+        extra |= int(sys.argv[sys.argv.index("--flags") + 1])
     corpus, queries = bench.gen(cfg)
     hx = synth.HostIndex(corpus)
     del corpus
