@@ -325,6 +325,28 @@ void build_index(const hm_csr_view* v, hm_index* X) {
             long_terms.push_back(t);
         }
     }
+    // short terms' tile tables (hm_types.h short_tab): one pass over each
+    // such term's rows
+    std::vector<uint32_t> stab_row(std::max<uint32_t>(V, 1), hm::kNoTabRow);
+    uint64_t n_stab = 0;
+    for (uint32_t t = 0; t < V; ++t) {
+        const uint64_t df = v->term_offsets[t + 1] - v->term_offsets[t];
+        if (slot[t] < 0 && df >= hm::kShortTabMinDf) stab_row[t] = static_cast<uint32_t>(n_stab++);
+    }
+    std::vector<uint32_t> stab_all(std::max<uint64_t>(n_stab, 1) * (n_tiles + 1));
+    par_for(V, [&](int, uint64_t a, uint64_t b) {
+        for (uint64_t t = a; t < b; ++t) {
+            if (stab_row[t] == hm::kNoTabRow) continue;
+            const uint64_t o = v->term_offsets[t], df = v->term_offsets[t + 1] - o;
+            uint32_t* T = stab_all.data() + static_cast<uint64_t>(stab_row[t]) * (n_tiles + 1);
+            uint64_t i = 0;
+            for (uint32_t j = 0; j <= n_tiles; ++j) {
+                const uint64_t r0 = static_cast<uint64_t>(j) << hm::kTileShift;
+                while (i < df && v->posting_rows[o + i] < r0) ++i;
+                T[j] = static_cast<uint32_t>(i);
+            }
+        }
+    });
     // packed postings (+8 words of padding for 16-byte bulk copies)
     std::vector<uint32_t> packed(P + 8, 0);
     std::atomic<uint64_t> escaped{0};
@@ -418,6 +440,9 @@ void build_index(const hm_csr_view* v, hm_index* X) {
     d.order_key = dev_upload(v->term_order_keys, V, A, B);
     d.long_slot = dev_upload(slot.data(), V, A, B);
     d.tile_tab = dev_upload(tab.data(), tab.size(), A, B);
+    d.short_tab = dev_upload(stab_all.data(), stab_all.size(), A, B);
+    d.short_tab_row = dev_upload(stab_row.data(), std::max<uint64_t>(V, 1), A, B);
+    std::vector<uint32_t>().swap(stab_all);
     d.long_esc = dev_upload(long_esc.data(), long_esc.size(), A, B);
     d.doc_lens = dev_upload(v->doc_lens, N, A, B);
     d.doc_ids = dev_upload(v->doc_ids, N, A, B);

@@ -62,6 +62,11 @@ constexpr int kCodeBitsLong = 32 - kLocalBits;
 constexpr uint32_t kEscLong = (1u << kCodeBitsLong) - 1;
 constexpr int kMaxK = 256;
 constexpr uint32_t kNoTerm = 0xFFFFFFFFu;
+#ifndef HM_SHORT_TAB_MIN_DF
+#define HM_SHORT_TAB_MIN_DF 256
+#endif
+constexpr uint32_t kShortTabMinDf = HM_SHORT_TAB_MIN_DF;
+constexpr uint32_t kNoTabRow = 0xFFFFFFFFu;
 constexpr int kLongFactor = 32;               // long term: df > 32 * n_tiles
 constexpr int kBakeMantBits = 16;             // baked impact: 3 exponent + 16 mantissa bits
 constexpr int kBakeBinades = 7;               // normal exponent fields 1..7
@@ -82,6 +87,12 @@ struct DevIndex {
     const int32_t* long_slot;
     const uint8_t* long_esc;   // [n_long] 1 if the long term has escaped postings
     const uint32_t* tile_tab;
+    // short terms with df >= kShortTabMinDf: the offset (from the term's start)
+    // of the first posting of every tile, [row][n_tiles + 1] (row from
+    // short_tab_row, kNoTabRow otherwise) -- the kernels' per-query short-term
+    // tables are filled from it instead of scanning the postings
+    const uint32_t* short_tab;
+    const uint32_t* short_tab_row;
     const uint32_t* doc_lens;
     const uint64_t* doc_ids;
     const uint32_t* code_tf;   // [kMaxCodes]

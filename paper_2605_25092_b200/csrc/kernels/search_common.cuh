@@ -54,6 +54,7 @@ struct __align__(16) SmemT {
     uint32_t t_mult[kFastTerms];
     float t_c32[kFastTerms];
     int32_t t_slot[kFastTerms];
+    uint32_t t_trow[kFastTerms];           // short terms: row of the index's tile table (kNoTabRow: none)
     uint4 stg[kConsWarps][STG ? FastCfg<CAPW>::kStages : 1][STG ? FastCfg<CAPW>::kC * 32 : 1];  // per-warp cp.async staging of baked postings
     uint64_t t_bkb[kFastTerms];            // long terms: start of the term's baked ranges in bk
     uint4 rdesc[kConsWarps][kFastTerms];  // per warp: the unit's nonempty long-term ranges in this tile
@@ -115,7 +116,8 @@ __device__ __forceinline__ float esc_w(const DevIndex& ix, uint64_t gidx, uint32
 
 // ---------------------------------------------------------------- short-term tile tables
 // Row tab[jj] of short term s (list[s], its window [t_wlo, t_end) with prefix
-// pref[s] in the concatenation of the short terms' windows): the offset (from
+// pref[s] in the concatenation of the scanned short terms' windows -- length 0
+// for a term with an index tile table, filled from it): the offset (from
 // t_start) of its first posting in tile j0 + jj, tab[nt] the window's end.
 // Every posting f fills the entries of the tiles from its predecessor's tile
 // (exclusive) to its own; HM_SHORT_U postings per thread are loaded before any
@@ -166,10 +168,19 @@ __device__ __forceinline__ void short_tables(const DevIndex& ix, Sm& S, const ui
                 for (int jj = jt + 1; jj <= static_cast<int>(nt); ++jj) tab[jj] = static_cast<uint32_t>(w1 - s0);
         }
     }
+    // empty windows, and the terms with an index tile table (their postings
+    // were not scanned): the table clamped to the window
     for (uint32_t x = threadIdx.x; x < n_short * (nt + 1); x += NT) {
         const uint32_t s = x / (nt + 1), jj = x % (nt + 1), i = list[s];
-        if (S.t_wlo[i] == S.t_end[i])
-            stab[static_cast<uint64_t>(s) * stride + jj] = static_cast<uint32_t>(S.t_wlo[i] - S.t_start[i]);
+        const uint32_t lo = static_cast<uint32_t>(S.t_wlo[i] - S.t_start[i]);
+        const uint32_t hi = static_cast<uint32_t>(S.t_end[i] - S.t_start[i]);
+        const uint32_t r = S.t_trow[i];
+        if (r != kNoTabRow) {
+            const uint32_t v = jj == nt ? hi : __ldg(ix.short_tab + static_cast<uint64_t>(r) * (ix.n_tiles + 1) + j0 + jj);
+            stab[static_cast<uint64_t>(s) * stride + jj] = min(max(v, lo), hi);
+        } else if (lo == hi) {
+            stab[static_cast<uint64_t>(s) * stride + jj] = lo;
+        }
     }
     __syncthreads();
 }

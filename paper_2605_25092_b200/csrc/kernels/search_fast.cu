@@ -243,6 +243,7 @@ __global__ void __launch_bounds__(kCons, 2) search_fast_kernel(DevIndex ix, Batc
             const int sh = slot >= 0 ? static_cast<int>(ix.bk_ks) - kScoreShift : -kScoreShift;
             S.t_c32[tid] = static_cast<float>(ldexp(static_cast<double>(mult) * idf, sh));
             S.t_slot[tid] = slot;
+            S.t_trow[tid] = slot < 0 ? ix.short_tab_row[t] : kNoTabRow;
             S.t_bkb[tid] = slot >= 0 ? ix.bk_base[slot] : 0;
             S.t_dense[tid] = slot >= 0 ? ix.dense_of_slot[slot] : -1;  // (the exact rescoring's lookups)
         }
@@ -313,7 +314,8 @@ __global__ void __launch_bounds__(kCons, 2) search_fast_kernel(DevIndex ix, Batc
                 if (S.t_slot[i] < 0) {
                     S.order_list[nl + ns] = static_cast<uint16_t>(i);
                     S.t_spos[i] = static_cast<uint8_t>(ns);  // stab row (the NE ranks are long terms only)
-                    S.pref[ns + 1] = S.pref[ns] + static_cast<uint32_t>(S.t_end[i] - S.t_wlo[i]);
+                    S.pref[ns + 1] =  // (a term with an index tile table is not scanned)
+                        S.pref[ns] + (S.t_trow[i] != kNoTabRow ? 0u : static_cast<uint32_t>(S.t_end[i] - S.t_wlo[i]));
                     ++ns;
                 }
             S.post = post;

@@ -152,6 +152,7 @@ __global__ void __launch_bounds__(kCons, HM_SEED_MINB) search_seed_kernel(DevInd
             S.t_idf[tid] = idf;
             S.t_mult[tid] = mult;
             S.t_slot[tid] = slot;
+            S.t_trow[tid] = slot < 0 ? ix.short_tab_row[t] : kNoTabRow;
             const float cu = static_cast<float>(ldexp(static_cast<double>(mult) * idf, -kScoreShift));
             S.t_cu[tid] = cu;
             S.t_ms[tid] = cu * ix.tmax[t] * 1.0000010f;  // rounded up: an upper bound
@@ -169,7 +170,8 @@ __global__ void __launch_bounds__(kCons, HM_SEED_MINB) search_seed_kernel(DevInd
                 if (S.t_slot[i] < 0) {
                     S.order_list[ns] = static_cast<uint16_t>(i);
                     S.t_spos[i] = static_cast<uint8_t>(ns);
-                    S.pref[ns + 1] = S.pref[ns] + static_cast<uint32_t>(S.t_end[i] - S.t_wlo[i]);
+                    S.pref[ns + 1] =  // (a term with an index tile table is not scanned)
+                        S.pref[ns] + (S.t_trow[i] != kNoTabRow ? 0u : static_cast<uint32_t>(S.t_end[i] - S.t_wlo[i]));
                     ++ns;
                 }
                 if (S.t_end[i] - S.t_wlo[i] <= kSeedMaxDf && (seed == kNoTerm || S.t_ms[i] > S.t_ms[seed]))
@@ -211,7 +213,16 @@ __global__ void __launch_bounds__(kCons, HM_SEED_MINB) search_seed_kernel(DevInd
         const uint32_t j0 = row_lo >> kTileShift, j1 = (row_hi - 1) >> kTileShift;
         const uint32_t nt = j1 - j0 + 1;
         // ---------------- short-term tile tables (probes of short terms)
+#ifdef HM_SEED_STATS
+        const long long c_tab = clock64();
+#endif
         short_tables(ix, S, S.order_list, n_short, stab, stride, j0, nt, cb);
+#ifdef HM_SEED_STATS
+        if (tid == 0) {
+            SST(24, clock64() - c_tab);
+            SST(25, S.pref[n_short]);
+        }
+#endif
 #ifdef HM_SEED_STATS
         c_t1 = clock64();
 #endif
