@@ -447,7 +447,10 @@ __device__ __forceinline__ void finish_query(const DevIndex& ix, const BatchArgs
     // (fp64, mult repeats, the reference's accumulation :87-101) -- a term
     // absent from the row (-1) adds nothing
     double* const pv = reinterpret_cast<double*>(sp + kSurvBytes);
-    for (uint32_t i = tid; i < ns; i += kCons) sv.E[i] = 0.0;
+    for (uint32_t i = tid; i < ns; i += kCons) {
+        sv.E[i] = 0.0;
+        sv.id[i] = __ldg(ix.doc_ids + sv.row[i]);  // (in flight with the first batch of lookups)
+    }
     const uint32_t npair = ns * m;
     for (uint32_t p0 = 0; p0 < npair; p0 += kCons) {
         const uint32_t p = p0 + tid;
@@ -475,8 +478,6 @@ __device__ __forceinline__ void finish_query(const DevIndex& ix, const BatchArgs
         }
         csync();
     }
-    for (uint32_t i = tid; i < ns; i += kCons) sv.id[i] = __ldg(ix.doc_ids + sv.row[i]);
-    csync();
     const uint32_t n2 = pow2_ceil(ns);
     for (uint32_t i = ns + tid; i < n2; i += kCons) {
         sv.E[i] = -INFINITY;
