@@ -414,7 +414,10 @@ __global__ void __launch_bounds__(kCons, HM_SEED_MINB) search_seed_kernel(DevInd
 #define HM_SEED_FULL 2048
 #endif
 #ifndef HM_BOUND_FULL
-#define HM_BOUND_FULL 2048
+#define HM_BOUND_FULL 512  // (2,048 / 1,024 / 256 / 128 with or without (b): profiles/r02_shard_scaling.md)
+#endif
+#ifndef HM_BOUND_SKIP_B
+#define HM_BOUND_SKIP_B 1
 #endif
         // (the bound pass of doc shards may score fewer seeds completely: its
         // k best only need to be good, the other shards add theirs)
@@ -445,9 +448,12 @@ __global__ void __launch_bounds__(kCons, HM_SEED_MINB) search_seed_kernel(DevInd
             __syncthreads();
             const float L0 = block_kth_largest<kCons>(sA, n_seed, k, S.hist, S.sel, [] { __syncthreads(); }, 8);
             const float te0 = fmaxf(L0 * f_slack, kFltMin);
-            // (b) the other seeds with early exit against te0
-            seed_pass([&](uint32_t e) { return __float_as_uint(sA[e]) == kTodo; }, true, te0);
-            __syncthreads();
+            // (b) the other seeds with early exit against te0 (the bound pass of
+            // doc shards may stop at (a): its k best need only be good)
+            if (!(bonly && HM_BOUND_SKIP_B)) {
+                seed_pass([&](uint32_t e) { return __float_as_uint(sA[e]) == kTodo; }, true, te0);
+                __syncthreads();
+            }
         }
         if (bonly) {  // the bound pass of doc-sharded search: the k best complete seed scores
             // (the multiset {scores > L} + (k - that count) x L, L the exact k-th
