@@ -31,6 +31,8 @@
 // bit-identical fp64 results -- are the same.  Queries without a short term,
 // with too many essential postings, or with more candidates than the lists can
 // hold are appended to the fallback list that the exhaustive kernel serves.
+#include <cstddef>
+
 #include "hm_device.cuh"
 #include "hm_launch.h"
 #include "hm_ptx.cuh"
@@ -324,6 +326,10 @@ __global__ void __launch_bounds__(kCons, HM_SEED_MINB) search_seed_kernel(DevInd
                 __syncthreads();
             }
         }
+#ifdef HM_SEED_STATS
+        __syncthreads();
+        if (tid == 0) SST(26, clock64() - c_t1);  // seeds collected
+#endif
         // t*'s own contribution to seed e (its posting's code, no probe)
         auto seed_imp = [&](uint32_t e) -> float {
             const uint32_t p = __ldg(ix.post + sw0 + e);
@@ -423,6 +429,9 @@ __global__ void __launch_bounds__(kCons, HM_SEED_MINB) search_seed_kernel(DevInd
         // k best only need to be good, the other shards add theirs)
         const uint32_t n_full = max(static_cast<uint32_t>(bonly ? HM_BOUND_FULL : HM_SEED_FULL), 8u * k);
         float L = 0.f;
+#ifdef HM_SEED_STATS
+        const long long c_s0 = clock64();
+#endif
         if (n_seed <= n_full) {  // few seeds: every one complete
             seed_pass([](uint32_t) { return true; }, false, 0.f);
             __syncthreads();
@@ -438,14 +447,35 @@ __global__ void __launch_bounds__(kCons, HM_SEED_MINB) search_seed_kernel(DevInd
             // score (>= n_full >= k complete rows are normal and positive), so
             // the k-th largest is the complete rows' lower bound L0
             constexpr uint32_t kTodo = 1u;
-            seed_pass(
-                [&](uint32_t e) {
-                    const bool top = sA[e] >= v0 && atomicAdd(&S.total, 1u) < 2u * n_full;
-                    if (!top) sA[e] = __uint_as_float(kTodo);
-                    return top;
-                },
-                false, 0.f);
+            // the selected seeds are compacted into a list first (the candidate
+            // lists' area, free until admission), so the probes run densely --
+            // scattered picks would keep most lanes of every probe round idle
+            uint32_t* const pick = &S.cl_row[0][0];
+            constexpr uint32_t kPickCap = 2u * kConsWarps * CAPW;  // cl_row + cl_val
+            static_assert(offsetof(Smem, cl_val) == offsetof(Smem, cl_row) + sizeof(uint32_t) * kConsWarps * CAPW,
+                          "the candidate lists are contiguous");
+            const uint32_t cap = min(2u * n_full, kPickCap);
+            for (uint32_t e = tid; e < n_seed; e += kCons) {
+                const uint32_t pos = sA[e] >= v0 ? atomicAdd(&S.total, 1u) : cap;
+                if (pos < cap) pick[pos] = e;
+                else sA[e] = __uint_as_float(kTodo);
+            }
             __syncthreads();
+            const uint32_t npick = min(S.total, cap);
+            for (uint32_t x = tid; x < npick; x += kP * kCons) {
+                uint32_t eu[kP], vm = 0;
+#pragma unroll
+                for (int u = 0; u < kP; ++u) {
+                    const uint32_t xi = x + u * kCons;
+                    eu[u] = xi < npick ? pick[xi] : 0u;
+                    vm |= (xi < npick ? 1u : 0u) << u;
+                }
+                score_seeds(eu, vm, false, 0.f);
+            }
+            __syncthreads();
+#ifdef HM_SEED_STATS
+            if (tid == 0) SST(27, clock64() - c_s0);  // (a) incl. its selection
+#endif
             const float L0 = block_kth_largest<kCons>(sA, n_seed, k, S.hist, S.sel, [] { __syncthreads(); }, 8);
             const float te0 = fmaxf(L0 * f_slack, kFltMin);
             // (b) the other seeds with early exit against te0 (the bound pass of
@@ -472,7 +502,17 @@ __global__ void __launch_bounds__(kCons, HM_SEED_MINB) search_seed_kernel(DevInd
             for (uint32_t i = S.total + tid; i < k; i += kCons) ob[i] = L;
             continue;
         }
+#ifdef HM_SEED_STATS
+        const long long c_s1 = clock64();
+        if (tid == 0) {
+            SST(28, c_s1 - c_s0);  // all seed scoring
+            SST(29, n_seed > n_full ? 1 : 0);
+        }
+#endif
         if (n_seed >= k) L = block_kth_largest<kCons>(sA, n_seed, k, S.hist, S.sel, [] { __syncthreads(); }, 8);
+#ifdef HM_SEED_STATS
+        if (tid == 0) SST(30, clock64() - c_s1);  // final selection
+#endif
         // the union's bound: every document of the union's top-k scores above it
         // (a k-th score of real documents of some shard, in the same domain)
         L = fmaxf(L, ext);

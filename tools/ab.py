@@ -76,7 +76,9 @@ def main():
                    f"cand={v[8] / max(v[11], 1):.0f} epilogue={v[9] / max(v[11], 1):.0f} "
                    f"chunks/q={v[12] / nq_seed:.1f} insert={v[13] / nq_seed:.0f} (segments {v[15] / nq_seed:.0f}) scan={v[14] / nq_seed:.0f} "
                    f"hashed_q={v[17]} TE/hq={v[16] / max(v[17], 1):.0f} seeds/hq={v[18] / max(v[17], 1):.0f} "
-                   f"short_tables_cycles/q={v[24] / nq_seed:.0f} short_postings/q={v[25] / nq_seed:.0f}")
+                   f"short_tables_cycles/q={v[24] / nq_seed:.0f} short_postings/q={v[25] / nq_seed:.0f} "
+                   f"seed_collect/q={v[26] / nq_seed:.0f} seed_a/q={v[27] / nq_seed:.0f} seed_scoring/q={v[28] / nq_seed:.0f} "
+                   f"many_seeds_q={v[29]} final_kth/q={v[30] / nq_seed:.0f}")
         except AttributeError:
             pass
         print(f"{name} flags={fl:4d}: {np.median(ts):8.2f} ms  {cfg['n_queries'] / np.median(ts) * 1e3:10.0f} q/s  "
