@@ -374,8 +374,12 @@ __global__ void __launch_bounds__(kCons, HM_SEED_MINB) search_seed_kernel(DevInd
             for (int u = 0; u < kP; ++u) rw.r[u] = (vm >> u) & 1u ? sR[eu[u]] : 0u;
             float A[kP] = {};
             uint32_t live = vm;
-            if (!early) {
+            if (!early) {  // t*'s contribution from the seed's own posting, the others probed
+#pragma unroll
+                for (int u = 0; u < kP; ++u)
+                    if ((vm >> u) & 1u) A[u] = seed_imp(eu[u]);
                 for (uint32_t i = 0; i < m; ++i) {
+                    if (i == ts) continue;
                     SCNT(c_sp, __popc(vm));
                     const ValsN<kP> x = seed_probeN<Smem, kP>(sc, i, rw, vm);
 #pragma unroll
