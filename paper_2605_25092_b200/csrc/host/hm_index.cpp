@@ -327,11 +327,14 @@ void build_index(const hm_csr_view* v, hm_index* X) {
     }
     // short terms' tile tables (hm_types.h short_tab): one pass over each
     // such term's rows
+    // (terms with fewer postings than half the tiles cost less to scan per query
+    // than their table's n_tiles + 1 entries to fill: none kept for them)
     std::vector<uint32_t> stab_row(std::max<uint32_t>(V, 1), hm::kNoTabRow);
     uint64_t n_stab = 0;
+    const uint64_t stab_min = std::max<uint64_t>(hm::kShortTabMinDf, n_tiles / 2);
     for (uint32_t t = 0; t < V; ++t) {
         const uint64_t df = v->term_offsets[t + 1] - v->term_offsets[t];
-        if (slot[t] < 0 && df >= hm::kShortTabMinDf) stab_row[t] = static_cast<uint32_t>(n_stab++);
+        if (slot[t] < 0 && df >= stab_min) stab_row[t] = static_cast<uint32_t>(n_stab++);
     }
     std::vector<uint32_t> stab_all(std::max<uint64_t>(n_stab, 1) * (n_tiles + 1));
     par_for(V, [&](int, uint64_t a, uint64_t b) {

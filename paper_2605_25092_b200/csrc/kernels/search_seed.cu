@@ -111,7 +111,7 @@ __global__ void __launch_bounds__(kCons, HM_SEED_MINB) search_seed_kernel(DevInd
         if (q == kNoTerm) break;
 #ifdef HM_SEED_STATS
         long long c_t0 = clock64(), c_t1 = 0, c_t2 = 0, c_t3 = 0;
-        uint32_t c_sp = 0, c_ep = 0, c_np = 0, c_en = 0;
+        uint32_t c_sp = 0, c_ep = 0, c_np = 0, c_en = 0, c_ns = 0;  // c_ep / c_ns: probe slots (kP per call)
 #endif
         uint32_t qr, row_lo, row_hi;  // the real query and this (slab) query's rows
         query_window(a, q, qr, row_lo, row_hi);
@@ -381,6 +381,7 @@ __global__ void __launch_bounds__(kCons, HM_SEED_MINB) search_seed_kernel(DevInd
                 for (uint32_t i = 0; i < m; ++i) {
                     if (i == ts) continue;
                     SCNT(c_sp, __popc(vm));
+                    SCNT(c_ep, kP);
                     const ValsN<kP> x = seed_probeN<Smem, kP>(sc, i, rw, vm);
 #pragma unroll
                     for (int u = 0; u < kP; ++u) A[u] += x.v[u];
@@ -398,6 +399,7 @@ __global__ void __launch_bounds__(kCons, HM_SEED_MINB) search_seed_kernel(DevInd
                         if (((live >> u) & 1u) && (A[u] + rem) * f_ub < thr) live &= ~(1u << u);
                     if (!live) break;
                     SCNT(c_sp, __popc(live));
+                    SCNT(c_ep, kP);
                     const ValsN<kP> x = seed_probeN<Smem, kP>(sc, i, rw, live);
 #pragma unroll
                     for (int u = 0; u < kP; ++u)
@@ -827,6 +829,7 @@ __global__ void __launch_bounds__(kCons, HM_SEED_MINB) search_seed_kernel(DevInd
                             if (((live >> u) & 1u) && (A[u] + rem) * f_ub < tn) live &= ~(1u << u);
                         if (!live) break;
                         SCNT(c_np, __popc(live));
+                        SCNT(c_ns, kP);
                         const ValsN<kP> xv = seed_probeN<Smem, kP>(sc, i2, rw, live);
 #pragma unroll
                         for (int u = 0; u < kP; ++u)
@@ -855,11 +858,11 @@ __global__ void __launch_bounds__(kCons, HM_SEED_MINB) search_seed_kernel(DevInd
         }
 #ifdef HM_SEED_STATS
         {
-            const uint32_t vs[4] = {c_sp, c_en, c_ep, c_np};
-            for (int z = 0; z < 4; ++z) {
+            const uint32_t vs[5] = {c_sp, c_en, c_ep, c_np, c_ns};
+            for (int z = 0; z < 5; ++z) {
                 uint32_t v = vs[z];
                 for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-                if (lane == 0) SST(2 + z, v);
+                if (lane == 0) SST(z < 4 ? 2 + z : 31, v);
             }
         }
 #endif

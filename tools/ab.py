@@ -71,7 +71,8 @@ def main():
             v = list(arr)
             nq_seed = max(v[0], 1)
             st += (f" seed: queries={v[0]} served={v[11]} emax_handover={v[10]} seeds/q={v[1] / nq_seed:.0f} "
-                   f"seed_probes/q={v[2] / nq_seed:.0f} Eposts/q={v[3] / nq_seed:.0f} Eprobes/q={v[4] / nq_seed:.0f} "
+                   f"seed_probes/q={v[2] / nq_seed:.0f} Eposts/q={v[3] / nq_seed:.0f} seed_probe_slots/q={v[4] / nq_seed:.0f} "
+                   f"NE_probe_slots/q={v[31] / nq_seed:.0f} "
                    f"NEprobes/q={v[5] / nq_seed:.0f} cycles/q prologue={v[6] / nq_seed:.0f} seeds={v[7] / nq_seed:.0f} "
                    f"cand={v[8] / max(v[11], 1):.0f} epilogue={v[9] / max(v[11], 1):.0f} "
                    f"chunks/q={v[12] / nq_seed:.1f} insert={v[13] / nq_seed:.0f} (segments {v[15] / nq_seed:.0f}) scan={v[14] / nq_seed:.0f} "
