@@ -6,6 +6,18 @@
 #include "hm_ptx.cuh"
 
 namespace hm {
+#ifdef HM_SEED_STATS  // development counters (scratch builds): [32..39] the epilogue's phases
+static __device__ unsigned long long g_seed_stats[40];
+#define FIN_T(i, t0)                                                                         \
+    do {                                                                                     \
+        if (threadIdx.x == 0) atomicAdd(&g_seed_stats[i], static_cast<unsigned long long>(clock64() - (t0))); \
+        t0 = clock64();                                                                      \
+    } while (0)
+#define FIN_CNT() atomicAdd(&g_seed_stats[38], 1ull)
+#else
+#define FIN_T(i, t0) ((void)0)
+#define FIN_CNT() ((void)0)
+#endif
 constexpr int kCons = 256;                // threads per CTA
 constexpr int kConsWarps = kCons / 32;    // 8: warp w owns unit w of a tile
 constexpr int kUnitRows = 1 << kUnitShift;  // 2048 rows per warp unit (hm_types.h)
@@ -392,6 +404,9 @@ __device__ __forceinline__ void finish_query(const DevIndex& ix, const BatchArgs
     constexpr int kGatherBytes = 8 * kConsWarps * CAPW;
     static_assert(kSurvBytes + 8 * kCons <= 4 * ACC, "survivors + the rescoring batch fit in the accumulator area");
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+#ifdef HM_SEED_STATS
+    long long ft = clock64();
+#endif
     auto csync = [] { __syncthreads(); };
     char* sp = reinterpret_cast<char*>(S.acc);
     float* gv = reinterpret_cast<float*>(sp);
@@ -415,7 +430,9 @@ __device__ __forceinline__ void finish_query(const DevIndex& ix, const BatchArgs
     csync();
     const uint32_t nc = S.total;
     float theta = 0.f;
+    FIN_T(32, ft);
     if (nc >= k) theta = block_kth_largest<kCons>(gv, nc, k, S.hist, S.sel, csync) * f_slack;
+    FIN_T(33, ft);
     if (warp == 0) {
         uint32_t w = 0;
         for (uint32_t b0 = 0; b0 < nc; b0 += 32) {
@@ -438,6 +455,7 @@ __device__ __forceinline__ void finish_query(const DevIndex& ix, const BatchArgs
         if (tid == 0) a.exact_list[atomicAdd(&a.counters[1], 1u)] = q;
         return;
     }
+    FIN_T(34, ft);
     SurvView sv{reinterpret_cast<double*>(sp), reinterpret_cast<uint64_t*>(sp + 8 * kSurvCap),
                 reinterpret_cast<uint32_t*>(sp + 16 * kSurvCap)};
     for (uint32_t i = tid; i < ns; i += kCons) sv.row[i] = (&S.cl_row[0][0])[i];
@@ -478,28 +496,41 @@ __device__ __forceinline__ void finish_query(const DevIndex& ix, const BatchArgs
         }
         csync();
     }
-    const uint32_t n2 = pow2_ceil(ns);
-    for (uint32_t i = ns + tid; i < n2; i += kCons) {
-        sv.E[i] = -INFINITY;
-        sv.id[i] = ~0ull;
-        sv.row[i] = 0;
+    FIN_T(35, ft);
+    // rank of every survivor in (score desc, DocId asc) order -- the pairs are
+    // distinct (DocIds are) -- by counting the survivors ranked before it; the
+    // top k land in rank order in the rescoring batch's area (k <= 128)
+    double* const tE = reinterpret_cast<double*>(sp + kSurvBytes);
+    uint64_t* const tI = reinterpret_cast<uint64_t*>(sp + kSurvBytes + 8 * 128);
+    static_assert(16 * 128 <= 8 * kCons, "the top-k fits in the rescoring batch's area");
+    for (uint32_t i = tid; i < ns; i += kCons) {
+        const double e = sv.E[i];
+        const uint64_t id = sv.id[i];
+        uint32_t r = 0;
+        for (uint32_t j = 0; j < ns; ++j) r += better(sv.E[j], sv.id[j], e, id) ? 1u : 0u;
+        if (r < k) {
+            tE[r] = e;
+            tI[r] = id;
+        }
     }
     csync();
-    block_bitonic<kCons>(sv.E, sv.id, sv.row, n2, csync);
+    FIN_T(36, ft);
     if (tid == 0) {
         uint32_t nout = 0;
         for (uint32_t i = 0; i < ns && nout < k; ++i) {
-            if (!(sv.E[i] > 0.0)) break;  // zero scores never emitted (:56)
-            a.out_ids[static_cast<uint64_t>(q) * k + nout] = sv.id[i];
-            a.out_scores[static_cast<uint64_t>(q) * k + nout] = sv.E[i];
+            if (!(tE[i] > 0.0)) break;  // zero scores never emitted (:56)
+            a.out_ids[static_cast<uint64_t>(q) * k + nout] = tI[i];
+            a.out_scores[static_cast<uint64_t>(q) * k + nout] = tE[i];
             ++nout;
         }
         a.out_n[q] = nout;
         if (a.out_post) a.out_post[q] = S.post;
-        write_decision(a, q, sv.E, nout);
+        write_decision(a, q, tE, nout);
     }
     csync();
     for (int i = tid; i < (kSurvBytes + 8 * kCons) / 4; i += kCons) S.acc[i] = 0.f;  // survivors + rescoring batch
+    FIN_T(37, ft);
+    if (threadIdx.x == 0) FIN_CNT();
 }
 
 }  // namespace hm

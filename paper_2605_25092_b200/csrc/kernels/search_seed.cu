@@ -66,7 +66,7 @@ __device__ __forceinline__ void hand_over(const BatchArgs& a, uint32_t q, float 
 }
 
 #ifdef HM_SEED_STATS  // development counters (scratch builds only): hm_seed_stats()
-__device__ unsigned long long g_seed_stats[32];
+// (g_seed_stats[40]: search_common.cuh, one copy per translation unit)
 #define SST(i, v) atomicAdd(&g_seed_stats[i], static_cast<unsigned long long>(v))
 #define SCNT(var, v) (var += (v))
 #else
@@ -941,7 +941,7 @@ cudaError_t launch_search_seed(const DevIndex& ix, const BatchArgs& a, int cap, 
 extern "C" int hm_seed_stats(unsigned long long* out, int reset) {
     if (cudaMemcpyFromSymbol(out, hm::g_seed_stats, sizeof(hm::g_seed_stats)) != cudaSuccess) return -1;
     if (reset) {
-        unsigned long long z[32] = {};
+        unsigned long long z[40] = {};
         z[21] = ~0ull;  // running minimum of the CTA exit times
         cudaMemcpyToSymbol(hm::g_seed_stats, z, sizeof(z));
     }

@@ -66,7 +66,7 @@ def main():
             import ctypes
             from paper_2605_25092_b200 import _lib
             fn = _lib.load("libhm_b200.so").hm_seed_stats
-            arr = (ctypes.c_ulonglong * 32)()
+            arr = (ctypes.c_ulonglong * 40)()
             fn(arr, 1)
             v = list(arr)
             nq_seed = max(v[0], 1)
@@ -79,7 +79,9 @@ def main():
                    f"hashed_q={v[17]} TE/hq={v[16] / max(v[17], 1):.0f} seeds/hq={v[18] / max(v[17], 1):.0f} "
                    f"short_tables_cycles/q={v[24] / nq_seed:.0f} short_postings/q={v[25] / nq_seed:.0f} "
                    f"seed_collect/q={v[26] / nq_seed:.0f} seed_a/q={v[27] / nq_seed:.0f} seed_scoring/q={v[28] / nq_seed:.0f} "
-                   f"many_seeds_q={v[29]} final_kth/q={v[30] / nq_seed:.0f}")
+                   f"many_seeds_q={v[29]} final_kth/q={v[30] / nq_seed:.0f} "
+                   f"epilogue(gather,kth,surv,rescore,sort,out)/fin=" +
+                   str([round(v[i] / max(v[38], 1)) for i in range(32, 38)]))
         except AttributeError:
             pass
         print(f"{name} flags={fl:4d}: {np.median(ts):8.2f} ms  {cfg['n_queries'] / np.median(ts) * 1e3:10.0f} q/s  "

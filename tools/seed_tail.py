@@ -10,7 +10,7 @@ hx = synth.HostIndex(corpus); del corpus
 dev = search.DeviceIndex.from_host(hx)
 b = bench.DevBatch(torch, torch.device("cuda", 0), queries.offsets.astype(np.uint32), hx.resolve(queries.term_ranks), 10)
 fn = _lib.load("libhm_b200.so").hm_seed_stats
-arr = (ctypes.c_ulonglong * 32)()
+arr = (ctypes.c_ulonglong * 40)()
 for r in range(3):
     dev.search_batch_device(b.off, b.tid, b.out, 10, flags=search.HM_FLAG_TIMING)
 fn(arr, 1)

@@ -67,7 +67,7 @@ for G in Gs:
         import ctypes
         from paper_2605_25092_b200 import _lib
         _stats = _lib.load("libhm_b200.so").hm_seed_stats
-        _arr = (ctypes.c_ulonglong * 32)()
+        _arr = (ctypes.c_ulonglong * 40)()
         _stats(_arr, 1)
     except (AttributeError, OSError):
         _stats = None
