@@ -308,65 +308,80 @@ __global__ void __launch_bounds__(kExactThreads, 1) exact_kernel(DevIndex ix, Ba
 constexpr int kMergeThreads = 256;
 constexpr int kMergeMax = 2048;
 
-__device__ void merge_bitonic(double* sc, uint64_t* id, uint32_t n) {
-    for (uint32_t k = 2; k <= n; k <<= 1)
-        for (uint32_t j = k >> 1; j > 0; j >>= 1) {
-            for (uint32_t i = threadIdx.x; i < n; i += kMergeThreads) {
-                uint32_t p = i ^ j;
-                if (p > i) {
-                    bool up = (i & k) == 0;
-                    bool sw = up ? better(sc[p], id[p], sc[i], id[i]) : better(sc[i], id[i], sc[p], id[p]);
-                    if (sw) {
-                        double ts = sc[i];
-                        sc[i] = sc[p];
-                        sc[p] = ts;
-                        uint64_t ti = id[i];
-                        id[i] = id[p];
-                        id[p] = ti;
-                    }
-                }
-            }
-            __syncthreads();
-        }
+// number of entries of the sorted list (s, d, n) ranked before (sa, ia)
+__device__ __forceinline__ uint32_t merge_count_before(const double* s, const uint64_t* d, uint32_t n, double sa,
+                                                       uint64_t ia) {
+    uint32_t lo = 0, hi = n;
+    while (lo < hi) {
+        const uint32_t mid = (lo + hi) >> 1;
+        if (better(s[mid], d[mid], sa, ia)) lo = mid + 1;
+        else hi = mid;
+    }
+    return lo;
 }
 
+// The G sorted lists of a query (slabs of a split batch: disjoint row ranges,
+// so every DocId appears once) staged in shared memory; every entry's rank in
+// the merged order is its index plus, per other list, the entries ranked
+// before it (binary search) -- the entries of rank < k are the top k, each
+// written straight to its slot (no sort; as gather_merge_kernel, shard_merge.cu).
 __global__ void __launch_bounds__(kMergeThreads) merge_kernel(
     uint32_t G, uint32_t nq, uint32_t k, const uint64_t* ids, const double* scores,
     const uint32_t* n, const double* tau, double tau_default, double eps, uint64_t* out_ids,
     double* out_scores, uint32_t* out_n, double* out_conf, uint8_t* out_skip) {
     __shared__ double sc[kMergeMax];
     __shared__ uint64_t id[kMergeMax];
+    __shared__ uint16_t s_n[kMergeMax + 1], s_base[kMergeMax + 2];  // G <= G * k <= kMergeMax
+    __shared__ double s_top[2];
     const uint32_t q = blockIdx.x;
-    const uint32_t tot = G * k;
-    const uint32_t n2 = pow2_ceil(tot);
-    for (uint32_t i = threadIdx.x; i < n2; i += kMergeThreads) {
-        double s = -INFINITY;
-        uint64_t d = ~0ull;
-        if (i < tot) {
-            uint32_t g = i / k, r = i % k;
-            if (r < n[static_cast<uint64_t>(g) * nq + q]) {
-                uint64_t o = (static_cast<uint64_t>(g) * nq + q) * k + r;
-                s = scores[o];
-                d = ids[o];
-            }
+    if (threadIdx.x == 0) {
+        uint32_t tot = 0;
+        for (uint32_t g = 0; g < G; ++g) {
+            const uint32_t m = min(n[static_cast<uint64_t>(g) * nq + q], k);
+            s_n[g] = static_cast<uint16_t>(m);
+            s_base[g] = static_cast<uint16_t>(tot);
+            tot += m;
         }
-        sc[i] = s;
-        id[i] = d;
+        s_base[G] = static_cast<uint16_t>(tot);
+        s_top[0] = s_top[1] = 0.0;
     }
     __syncthreads();
-    merge_bitonic(sc, id, n2);
-    if (threadIdx.x == 0) {
-        uint32_t nout = 0;
-        for (uint32_t i = 0; i < tot && nout < k; ++i) {
-            if (!(sc[i] > 0.0)) break;
-            out_ids[static_cast<uint64_t>(q) * k + nout] = id[i];
-            out_scores[static_cast<uint64_t>(q) * k + nout] = sc[i];
-            ++nout;
+    const uint32_t tot = s_base[G];
+    for (uint32_t e = threadIdx.x; e < G * k; e += kMergeThreads) {
+        const uint32_t g = e / k, r = e % k;
+        if (r < s_n[g]) {
+            const uint64_t o = (static_cast<uint64_t>(g) * nq + q) * k + r;
+            sc[s_base[g] + r] = scores[o];
+            id[s_base[g] + r] = ids[o];
         }
+    }
+    __syncthreads();
+    for (uint32_t e = threadIdx.x; e < tot; e += kMergeThreads) {
+        uint32_t g = 0, hi = G;  // the list holding e: largest g with s_base[g] <= e (and a nonempty list)
+        while (hi - g > 1) {
+            const uint32_t mid = (g + hi) >> 1;
+            if (s_base[mid] <= e) g = mid;
+            else hi = mid;
+        }
+        const uint32_t r = e - s_base[g];
+        const double sa = sc[e];
+        const uint64_t ia = id[e];
+        uint32_t rank = r;
+        for (uint32_t h = 0; h < G && rank < k; ++h)
+            if (h != g) rank += merge_count_before(sc + s_base[h], id + s_base[h], s_n[h], sa, ia);
+        if (rank < k) {
+            out_ids[static_cast<uint64_t>(q) * k + rank] = ia;
+            out_scores[static_cast<uint64_t>(q) * k + rank] = sa;
+            if (rank < 2) s_top[rank] = sa;
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const uint32_t nout = min(tot, k);  // (the lists hold positive scores only)
         out_n[q] = nout;
         double conf = 0.0;
-        if (nout >= 2 && sc[0] > 0.0) conf = __ddiv_rn(__dsub_rn(sc[0], sc[1]), fmax(sc[0], eps));
-        double t = tau ? tau[q] : tau_default;
+        if (nout >= 2 && s_top[0] > 0.0) conf = __ddiv_rn(__dsub_rn(s_top[0], s_top[1]), fmax(s_top[0], eps));
+        const double t = tau ? tau[q] : tau_default;
         if (out_conf) out_conf[q] = conf;
         if (out_skip) out_skip[q] = conf >= t ? 1 : 0;
     }
