@@ -309,12 +309,13 @@ constexpr int kMergeThreads = 256;
 constexpr int kMergeMax = 2048;
 
 // number of entries of the sorted list (s, d, n) ranked before (sa, ia)
+// (with_equal: also the entries equal to it)
 __device__ __forceinline__ uint32_t merge_count_before(const double* s, const uint64_t* d, uint32_t n, double sa,
-                                                       uint64_t ia) {
+                                                       uint64_t ia, bool with_equal) {
     uint32_t lo = 0, hi = n;
     while (lo < hi) {
         const uint32_t mid = (lo + hi) >> 1;
-        if (better(s[mid], d[mid], sa, ia)) lo = mid + 1;
+        if (with_equal ? !better(sa, ia, s[mid], d[mid]) : better(s[mid], d[mid], sa, ia)) lo = mid + 1;
         else hi = mid;
     }
     return lo;
@@ -367,8 +368,8 @@ __global__ void __launch_bounds__(kMergeThreads) merge_kernel(
         const double sa = sc[e];
         const uint64_t ia = id[e];
         uint32_t rank = r;
-        for (uint32_t h = 0; h < G && rank < k; ++h)
-            if (h != g) rank += merge_count_before(sc + s_base[h], id + s_base[h], s_n[h], sa, ia);
+        for (uint32_t h = 0; h < G && rank < k; ++h)  // (equal pairs -- a repeated DocId -- by list)
+            if (h != g) rank += merge_count_before(sc + s_base[h], id + s_base[h], s_n[h], sa, ia, h < g);
         if (rank < k) {
             out_ids[static_cast<uint64_t>(q) * k + rank] = ia;
             out_scores[static_cast<uint64_t>(q) * k + rank] = sa;

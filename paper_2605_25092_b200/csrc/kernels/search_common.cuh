@@ -503,11 +503,14 @@ __device__ __forceinline__ void finish_query(const DevIndex& ix, const BatchArgs
     double* const tE = reinterpret_cast<double*>(sp + kSurvBytes);
     uint64_t* const tI = reinterpret_cast<uint64_t*>(sp + kSurvBytes + 8 * 128);
     static_assert(16 * 128 <= 8 * kCons, "the top-k fits in the rescoring batch's area");
+    // (an index may repeat a DocId: equal pairs are then ordered by row, so the
+    // ranks stay distinct -- any order of equal pairs is the same output)
     for (uint32_t i = tid; i < ns; i += kCons) {
         const double e = sv.E[i];
         const uint64_t id = sv.id[i];
         uint32_t r = 0;
-        for (uint32_t j = 0; j < ns; ++j) r += better(sv.E[j], sv.id[j], e, id) ? 1u : 0u;
+        for (uint32_t j = 0; j < ns; ++j)
+            r += better(sv.E[j], sv.id[j], e, id) || (sv.E[j] == e && sv.id[j] == id && j < i) ? 1u : 0u;
         if (r < k) {
             tE[r] = e;
             tI[r] = id;

@@ -32,12 +32,14 @@ constexpr int kGMThreads = 256;
 constexpr uint32_t kGMStageMax = 4096;  // staged entries: 64 KB of shared memory
 
 // number of entries of list (s, d, n) ranked before (sa, ia)
+// (with_equal: also the entries equal to it -- a DocId repeated across shards)
 template <class S, class D>
-__device__ __forceinline__ uint32_t count_before(const S* s, const D* d, uint32_t n, double sa, uint64_t ia) {
+__device__ __forceinline__ uint32_t count_before(const S* s, const D* d, uint32_t n, double sa, uint64_t ia,
+                                                 bool with_equal) {
     uint32_t lo = 0, hi = n;
     while (lo < hi) {
         const uint32_t mid = (lo + hi) >> 1;
-        if (better(s[mid], d[mid], sa, ia)) lo = mid + 1;
+        if (with_equal ? !better(sa, ia, s[mid], d[mid]) : better(s[mid], d[mid], sa, ia)) lo = mid + 1;
         else hi = mid;
     }
     return lo;
@@ -89,8 +91,8 @@ __global__ void __launch_bounds__(kGMThreads) gather_merge_kernel(ShardLists L, 
             uint32_t rank = r;
             for (uint32_t h = 0; h < G && rank < k; ++h) {
                 if (h == g) continue;
-                rank += staged ? count_before(st_sc + s_base[h], st_id + s_base[h], s_n[h], sa, ia)
-                               : count_before(L.scores[h] + row, L.ids[h] + row, s_n[h], sa, ia);
+                rank += staged ? count_before(st_sc + s_base[h], st_id + s_base[h], s_n[h], sa, ia, h < g)
+                               : count_before(L.scores[h] + row, L.ids[h] + row, s_n[h], sa, ia, h < g);
             }
             if (rank < k) {
                 out_ids[row + rank] = ia;
