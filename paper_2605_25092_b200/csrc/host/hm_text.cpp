@@ -6,10 +6,14 @@
 // in one byte arena with an open-addressing hash table of (hash, tid) slots;
 // hm_vocab_resolve splits every query on the C locale's whitespace and looks
 // each token up (unknown -> 0xFFFFFFFF, which the planner drops exactly as
-// make_plan does), the batch cut into contiguous query ranges over a few
-// threads (two passes: count, then write).
+// make_plan does), the batch cut into contiguous query ranges over the
+// threads of a persistent pool (each range resolved once into a per-thread
+// buffer, then copied to its place once the offsets are known).
 #include <algorithm>
+#include <condition_variable>
 #include <cstring>
+#include <functional>
+#include <mutex>
 #include <stdexcept>
 #include <string>
 #include <thread>
@@ -76,6 +80,69 @@ inline void for_tokens(const char* text, uint64_t lo, uint64_t hi, F&& f) {
     }
 }
 
+// Persistent worker pool: run(T, f) calls f(0 .. T-1) -- f(0) on the caller
+// -- and returns when all are done; one run at a time (run_mu).  Spawning
+// threads per call cost more than the work (≈1 ms per 10K-query batch).
+class Pool {
+public:
+    explicit Pool(unsigned n) {
+        for (unsigned i = 1; i < n; ++i) th_.emplace_back([this, i] { loop(i); });
+    }
+    ~Pool() {
+        {
+            std::lock_guard<std::mutex> l(mu_);
+            stop_ = true;
+        }
+        cv_.notify_all();
+        for (auto& t : th_) t.join();
+    }
+    unsigned size() const { return static_cast<unsigned>(th_.size()) + 1; }
+    void run(unsigned T, const std::function<void(unsigned)>& f) {  // 1 <= T <= size()
+        std::lock_guard<std::mutex> one(run_mu_);
+        {
+            std::lock_guard<std::mutex> l(mu_);
+            job_ = &f;
+            job_t_ = T;
+            pending_ = T - 1;
+            ++gen_;
+        }
+        cv_.notify_all();
+        f(0);
+        std::unique_lock<std::mutex> l(mu_);
+        done_.wait(l, [&] { return pending_ == 0; });
+        job_ = nullptr;
+    }
+
+private:
+    void loop(unsigned id) {
+        uint64_t seen = 0;
+        std::unique_lock<std::mutex> l(mu_);
+        for (;;) {
+            cv_.wait(l, [&] { return stop_ || gen_ != seen; });
+            if (stop_) return;
+            seen = gen_;
+            if (id >= job_t_) continue;
+            const std::function<void(unsigned)>* f = job_;
+            l.unlock();
+            (*f)(id);
+            l.lock();
+            if (--pending_ == 0) done_.notify_all();
+        }
+    }
+    std::vector<std::thread> th_;
+    std::mutex mu_, run_mu_;
+    std::condition_variable cv_, done_;
+    const std::function<void(unsigned)>* job_ = nullptr;
+    unsigned job_t_ = 0, pending_ = 0;
+    uint64_t gen_ = 0;
+    bool stop_ = false;
+};
+
+Pool& pool() {
+    static Pool p(std::max(1u, std::min(std::thread::hardware_concurrency(), 16u)));
+    return p;
+}
+
 }  // namespace
 
 extern "C" {
@@ -122,31 +189,26 @@ int hm_vocab_resolve(const hm_vocab* v, uint32_t nq, const char* text, const uin
                      uint32_t* q_tid, uint64_t tid_cap, uint64_t* n_tids, uint32_t n_threads) {
     return hm_host::guard([&] {
         if (!v || !q_off || (nq && (!text || !text_off))) throw std::invalid_argument("null argument");
-        unsigned T = n_threads ? n_threads : std::max(1u, std::min(std::thread::hardware_concurrency(), 16u));
-        if (nq < 4096) T = 1;  // thread start-up would dominate
+        unsigned T = std::min(n_threads ? n_threads : pool().size(), pool().size());
+        if (nq < 1024) T = 1;  // a handful of queries: not worth waking the pool
         T = std::min<unsigned>(T, std::max(nq, 1u));
+        // pass 1 (parallel): every query range resolved into its own buffer
+        std::vector<std::vector<uint32_t>> loc(T);
         std::vector<uint32_t> cnt(nq + 1ull, 0);
-        auto count = [&](uint32_t a, uint32_t b) {
+        auto resolve = [&](unsigned t) {
+            const uint32_t a = static_cast<uint32_t>(static_cast<uint64_t>(nq) * t / T);
+            const uint32_t b = static_cast<uint32_t>(static_cast<uint64_t>(nq) * (t + 1) / T);
+            std::vector<uint32_t>& o = loc[t];
+            o.reserve(static_cast<size_t>(text_off[b] - text_off[a]) / 4 + 16);
             for (uint32_t q = a; q < b; ++q) {
-                uint32_t c = 0;
-                for_tokens(text, text_off[q], text_off[q + 1], [&](const char*, size_t) { ++c; });
-                cnt[q] = c;
+                const size_t before = o.size();
+                for_tokens(text, text_off[q], text_off[q + 1],
+                           [&](const char* s, size_t n) { o.push_back(lookup(*v, s, n)); });
+                cnt[q] = static_cast<uint32_t>(o.size() - before);
             }
         };
-        auto run = [&](auto&& f) {
-            if (T == 1) {
-                f(0u, nq);
-                return;
-            }
-            std::vector<std::thread> pool;
-            for (unsigned t = 0; t < T; ++t)
-                pool.emplace_back([&, t] {
-                    f(static_cast<uint32_t>(static_cast<uint64_t>(nq) * t / T),
-                      static_cast<uint32_t>(static_cast<uint64_t>(nq) * (t + 1) / T));
-                });
-            for (auto& th : pool) th.join();
-        };
-        run(count);
+        if (T == 1) resolve(0);
+        else pool().run(T, resolve);
         uint64_t tot = 0;
         for (uint32_t q = 0; q < nq; ++q) {
             q_off[q] = static_cast<uint32_t>(tot);
@@ -157,13 +219,13 @@ int hm_vocab_resolve(const hm_vocab* v, uint32_t nq, const char* text, const uin
         if (n_tids) *n_tids = tot;
         if (tot > tid_cap) throw std::out_of_range("q_tid capacity too small (needed count in n_tids)");
         if (tot && !q_tid) throw std::invalid_argument("q_tid is required");
-        run([&](uint32_t a, uint32_t b) {
-            for (uint32_t q = a; q < b; ++q) {
-                uint32_t* o = q_tid + q_off[q];
-                for_tokens(text, text_off[q], text_off[q + 1],
-                           [&](const char* s, size_t n) { *o++ = lookup(*v, s, n); });
-            }
-        });
+        // pass 2: each buffer copied to its place
+        auto place = [&](unsigned t) {
+            const uint32_t a = static_cast<uint32_t>(static_cast<uint64_t>(nq) * t / T);
+            if (!loc[t].empty()) std::memcpy(q_tid + q_off[a], loc[t].data(), loc[t].size() * sizeof(uint32_t));
+        };
+        if (T == 1) place(0);
+        else pool().run(T, place);
     });
 }
 
