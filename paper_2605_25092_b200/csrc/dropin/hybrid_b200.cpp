@@ -32,6 +32,7 @@
 #include <unordered_map>
 #include <vector>
 
+#include "../host/worker_pool.hpp"
 #include "dropin_common.hpp"
 #include "hm_b200.h"
 #include "hybrid/csr_index.hpp"
@@ -217,11 +218,7 @@ void resolve(const Vocab& vocab, const std::vector<std::vector<std::string>>& qu
                 if (it != vocab.end()) q_tid[q_off[i] + j] = it->second;
             }
     };
-    const unsigned T = n >= 4096 ? std::max(1u, std::min(std::thread::hardware_concurrency(), 16u)) : 1u;
-    if (T == 1) return work(0, n);
-    std::vector<std::thread> pool;
-    for (unsigned t = 0; t < T; ++t) pool.emplace_back(work, n * t / T, n * (t + 1) / T);
-    for (auto& th : pool) th.join();
+    hm_host::parallel_ranges(n, 4096, work);  // (the persistent host pool)
 }
 
 hm_query_batch make_batch(const std::vector<uint32_t>& q_off, const std::vector<uint32_t>& q_tid, uint32_t k,
@@ -264,12 +261,14 @@ std::vector<RankedList> bm25_topk_batch(const CsrIndex& x, const std::vector<std
     hm_results r{ids.data(), sc.data(), cnt.data(), conf.data(), skip.data(), post.data()};
     EntryPtr e = device_flat(x);
     throw_on(hm_search_batch(e->h, &b, &r));
-    for (std::size_t i = 0; i < n; ++i) {
-        if (stats) (*stats)[i].postings_touched += post[i];
-        if (decisions) (*decisions)[i] = Decision{conf[i], skip[i] != 0};
-        out[i].entries.reserve(cnt[i]);
-        for (uint32_t j = 0; j < cnt[i]; ++j) out[i].entries.emplace_back(ids[i * kk + j], sc[i * kk + j]);
-    }
+    hm_host::parallel_ranges(n, 4096, [&](std::size_t a, std::size_t z) {  // the reference's result objects
+        for (std::size_t i = a; i < z; ++i) {
+            if (stats) (*stats)[i].postings_touched += post[i];
+            if (decisions) (*decisions)[i] = Decision{conf[i], skip[i] != 0};
+            out[i].entries.reserve(cnt[i]);
+            for (uint32_t j = 0; j < cnt[i]; ++j) out[i].entries.emplace_back(ids[i * kk + j], sc[i * kk + j]);
+        }
+    });
     return out;
 }
 

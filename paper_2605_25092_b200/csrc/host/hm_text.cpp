@@ -21,6 +21,7 @@
 
 #include "hm_b200.h"
 #include "hm_host.h"
+#include "worker_pool.hpp"
 
 struct hm_vocab {
     std::vector<char> arena;
@@ -80,69 +81,6 @@ inline void for_tokens(const char* text, uint64_t lo, uint64_t hi, F&& f) {
     }
 }
 
-// Persistent worker pool: run(T, f) calls f(0 .. T-1) -- f(0) on the caller
-// -- and returns when all are done; one run at a time (run_mu).  Spawning
-// threads per call cost more than the work (≈1 ms per 10K-query batch).
-class Pool {
-public:
-    explicit Pool(unsigned n) {
-        for (unsigned i = 1; i < n; ++i) th_.emplace_back([this, i] { loop(i); });
-    }
-    ~Pool() {
-        {
-            std::lock_guard<std::mutex> l(mu_);
-            stop_ = true;
-        }
-        cv_.notify_all();
-        for (auto& t : th_) t.join();
-    }
-    unsigned size() const { return static_cast<unsigned>(th_.size()) + 1; }
-    void run(unsigned T, const std::function<void(unsigned)>& f) {  // 1 <= T <= size()
-        std::lock_guard<std::mutex> one(run_mu_);
-        {
-            std::lock_guard<std::mutex> l(mu_);
-            job_ = &f;
-            job_t_ = T;
-            pending_ = T - 1;
-            ++gen_;
-        }
-        cv_.notify_all();
-        f(0);
-        std::unique_lock<std::mutex> l(mu_);
-        done_.wait(l, [&] { return pending_ == 0; });
-        job_ = nullptr;
-    }
-
-private:
-    void loop(unsigned id) {
-        uint64_t seen = 0;
-        std::unique_lock<std::mutex> l(mu_);
-        for (;;) {
-            cv_.wait(l, [&] { return stop_ || gen_ != seen; });
-            if (stop_) return;
-            seen = gen_;
-            if (id >= job_t_) continue;
-            const std::function<void(unsigned)>* f = job_;
-            l.unlock();
-            (*f)(id);
-            l.lock();
-            if (--pending_ == 0) done_.notify_all();
-        }
-    }
-    std::vector<std::thread> th_;
-    std::mutex mu_, run_mu_;
-    std::condition_variable cv_, done_;
-    const std::function<void(unsigned)>* job_ = nullptr;
-    unsigned job_t_ = 0, pending_ = 0;
-    uint64_t gen_ = 0;
-    bool stop_ = false;
-};
-
-Pool& pool() {
-    static Pool p(std::max(1u, std::min(std::thread::hardware_concurrency(), 16u)));
-    return p;
-}
-
 }  // namespace
 
 extern "C" {
@@ -189,7 +127,7 @@ int hm_vocab_resolve(const hm_vocab* v, uint32_t nq, const char* text, const uin
                      uint32_t* q_tid, uint64_t tid_cap, uint64_t* n_tids, uint32_t n_threads) {
     return hm_host::guard([&] {
         if (!v || !q_off || (nq && (!text || !text_off))) throw std::invalid_argument("null argument");
-        unsigned T = std::min(n_threads ? n_threads : pool().size(), pool().size());
+        unsigned T = std::min(n_threads ? n_threads : hm_host::worker_pool().size(), hm_host::worker_pool().size());
         if (nq < 1024) T = 1;  // a handful of queries: not worth waking the pool
         T = std::min<unsigned>(T, std::max(nq, 1u));
         // pass 1 (parallel): every query range resolved into its own buffer
@@ -208,7 +146,7 @@ int hm_vocab_resolve(const hm_vocab* v, uint32_t nq, const char* text, const uin
             }
         };
         if (T == 1) resolve(0);
-        else pool().run(T, resolve);
+        else hm_host::worker_pool().run(T, resolve);
         uint64_t tot = 0;
         for (uint32_t q = 0; q < nq; ++q) {
             q_off[q] = static_cast<uint32_t>(tot);
@@ -225,7 +163,7 @@ int hm_vocab_resolve(const hm_vocab* v, uint32_t nq, const char* text, const uin
             if (!loc[t].empty()) std::memcpy(q_tid + q_off[a], loc[t].data(), loc[t].size() * sizeof(uint32_t));
         };
         if (T == 1) place(0);
-        else pool().run(T, place);
+        else hm_host::worker_pool().run(T, place);
     });
 }
 
