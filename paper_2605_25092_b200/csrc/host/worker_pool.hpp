@@ -12,6 +12,8 @@
 #include <thread>
 #include <vector>
 
+#include <unistd.h>
+
 namespace hm_host {
 
 class Pool {
@@ -71,9 +73,19 @@ private:
     bool stop_ = false;
 };
 
+// The process's pool, created on first use; a forked child (which inherits
+// the object but not its threads) gets a fresh one.  Never destroyed: the idle
+// workers end with the process.
 inline Pool& worker_pool() {
-    static Pool p(std::max(1u, std::min(std::thread::hardware_concurrency(), 16u)));
-    return p;
+    static std::mutex mu;
+    static Pool* p = nullptr;
+    static pid_t owner = 0;
+    std::lock_guard<std::mutex> l(mu);
+    if (!p || owner != getpid()) {
+        p = new Pool(std::max(1u, std::min(std::thread::hardware_concurrency(), 16u)));
+        owner = getpid();
+    }
+    return *p;
 }
 
 // f(a, b) over [0, n) cut into the pool's threads (serially below `min_n`)
